@@ -1,0 +1,199 @@
+/*
+ * sewald_gpu.h — C-ABI of the B200-native Spectral Ewald engine.
+ *
+ * Plain C: pointers, sizes, POD structs. No torch/CUDA types in signatures
+ * (streams are passed as void*). Every entry point returns an int status
+ * (SEWALD_OK = 0) and leaves a message in sewald_gpu_last_error(ctx) or
+ * sewald_last_error() for the context-free calls.
+ *
+ * Each entry point replaces one function of the reference C++ library
+ * (/root/reference/proj/include/sewald/...); the mapping is cited per call.
+ * Coordinates and strengths are AoS fp64, 3 doubles per point — exactly
+ * reinterpret_cast<const double*>(std::vector<std::array<double,3>>::data())
+ * of the reference's Vec3 vectors (domain.h:11, :52-70), so a C++ caller
+ * passes its vectors zero-copy.
+ */
+#ifndef SEWALD_GPU_H
+#define SEWALD_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. The drop-in C++ layer rethrows them as the reference's
+ * exception types (std::invalid_argument / std::domain_error /
+ * std::runtime_error), throw sites in /root/reference/proj/src. */
+enum {
+    SEWALD_OK = 0,
+    SEWALD_EINVAL = 1,   /* std::invalid_argument */
+    SEWALD_EDOMAIN = 2,  /* std::domain_error */
+    SEWALD_ERUNTIME = 3, /* std::runtime_error */
+    SEWALD_ECUDA = 4,
+    SEWALD_ECUFFT = 5,
+    SEWALD_ENOMEM = 6
+};
+
+/* enum class Kernel (domain.h:26) */
+enum { SEWALD_STOKESLET = 0, SEWALD_STRESSLET = 1, SEWALD_ROTLET = 2 };
+/* enum class WindowKind (window.h:9) */
+enum { SEWALD_WIN_KB = 0, SEWALD_WIN_PKB = 1, SEWALD_WIN_TG = 2 };
+
+/* POD mirror of EwaldParams (estimates.h:62-71) flattened with its
+ * GridSpec (grid.h:13-24), WindowSpec (window.h:15-29) and UpsamplingPlan
+ * (grid.h:29-35). */
+typedef struct sewald_params_c {
+    int32_t kind;
+    int32_t d;
+    double xi;
+    double rc;
+    double R;
+    /* GridSpec */
+    double h;
+    int32_t M[3];
+    int32_t M_ext[3];
+    double L[3];
+    double L_ext[3];
+    double pad[3];
+    int32_t f_m;
+    /* WindowSpec */
+    int32_t win_kind;
+    int32_t P;
+    double win_h;
+    double beta;
+    int32_t nu;
+    double alpha;
+    /* UpsamplingPlan */
+    double s0;
+    double s_star;
+    int32_t k_star[3];
+    double s0_raw;
+    double s_star_raw;
+} sewald_params_c;
+
+/* POD mirror of EstimateReport (estimates.h:73-90). */
+typedef struct sewald_report_c {
+    double tau_abs, U, kinf, fourier_trunc, realspace_trunc, window_err, h_estimate;
+    int32_t P_estimate;
+    double h_target;
+    int32_t P_target;
+    int32_t rc_clamped, kinf_clamped, window_saturated, tg_support_from_pkb;
+} sewald_report_c;
+
+/* Per-call stage timings (CUDA events, milliseconds) of the last pipeline run. */
+typedef struct sewald_timings_c {
+    double h2d_ms, sort_ms, spread_ms, fft_fwd_ms, scale_ms, fft_inv_ms, gather_ms,
+        realspace_ms, assemble_ms, d2h_ms, total_ms;
+    int64_t kernel_launches;
+    int64_t realspace_pairs;     /* accepted pairs (if counted), else -1 */
+} sewald_timings_c;
+
+typedef struct sewald_gpu_ctx sewald_gpu_ctx;
+
+/* ---- host-side parameter layer (no GPU needed) ---------------------- */
+
+/* select_parameters (estimates.h:106-107, estimates.cpp:211-268). */
+int sewald_select_parameters(int kind, int d, const double L[3], double Q, double xi,
+                             double tol_value, int tol_relative, int f_m, int window_kind,
+                             int pollution_fix, sewald_params_c* out, sewald_report_c* report);
+
+/* WindowSpec::make (window.cpp:76-86) into p->win_* fields. */
+int sewald_window_make(int window_kind, int P, double h, sewald_params_c* p);
+
+/* build_grid (grid.h:38, grid.cpp:35-77) into p's grid fields. */
+int sewald_build_grid(const double L[3], int d, double h_target, int P, int kind, int f_m,
+                      sewald_params_c* p);
+
+/* pkb_build (window.cpp:112-138): P*(nu+1) coefficients, row l+P/2. */
+int sewald_pkb_coefficients(const sewald_params_c* p, double* coef_out);
+
+/* Window::eval1d / hat1d (window.cpp:171-182), host evaluation for tests. */
+int sewald_window_eval(const sewald_params_c* p, const double* r, int64_t n, double* out);
+int sewald_window_hat(const sewald_params_c* p, const double* k, int64_t n, double* out);
+
+/* Q = source_quantity (domain.cpp:53-62). */
+double sewald_source_quantity(int kind, const double* f, const double* nu, int64_t N);
+
+const char* sewald_last_error(void);
+
+/* ---- device context -------------------------------------------------- */
+
+int sewald_gpu_create(int device, sewald_gpu_ctx** out);
+void sewald_gpu_destroy(sewald_gpu_ctx* ctx);
+const char* sewald_gpu_last_error(const sewald_gpu_ctx* ctx);
+/* Run all work on this cudaStream_t (NULL = the context's own stream). */
+int sewald_gpu_set_stream(sewald_gpu_ctx* ctx, void* stream);
+int sewald_gpu_get_timings(const sewald_gpu_ctx* ctx, sewald_timings_c* out);
+/* 1 = record per-stage CUDA events (adds event overhead), 0 = off. */
+int sewald_gpu_set_profiling(sewald_gpu_ctx* ctx, int enabled);
+
+/* ---- host-buffer entry points (drop-in path) ------------------------- */
+/* x, f: N*3 doubles; nu: N*3 (stresslet) or NULL; xt: Nt*3. When
+ * same_as_sources != 0 the targets are the sources (xt may be NULL or x).
+ * u_out: Nt*3 doubles (host). */
+
+/* full_potential (realspace.h:46-47, realspace.cpp:205-219). */
+int sewald_gpu_full_potential(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* x,
+                              const double* f, const double* nu, int64_t N, const double* xt,
+                              int64_t Nt, int same_as_sources, int precompute_0p, double* u_out);
+
+/* se_fourier_potential (fourier.h:81-82, fourier.cpp:805-852). */
+int sewald_gpu_fourier_potential(sewald_gpu_ctx* ctx, const sewald_params_c* p,
+                                 const double* x, const double* f, const double* nu, int64_t N,
+                                 const double* xt, int64_t Nt, int same_as_sources,
+                                 int precompute_0p, double* u_out);
+
+/* realspace_potential (realspace.h:40-41, realspace.cpp:166-203). */
+int sewald_gpu_realspace_potential(sewald_gpu_ctx* ctx, int kind, int d, const double L[3],
+                                   const double* x, const double* f, const double* nu, int64_t N,
+                                   const double* xt, int64_t Nt, int same_as_sources, double xi,
+                                   double rc, int starred, double* u_out);
+
+/* spread (fourier.h:59, fourier.cpp:237-274): grid_out = C * prod(M_ext)
+ * doubles, component-major, last axis fastest (RealField layout, fourier.h:15-28). */
+int sewald_gpu_spread(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* x,
+                      const double* f, const double* nu, int64_t N, double* grid_out);
+
+/* gather (fourier.h:71-72, fourier.cpp:276-309): grid = 3 * prod(M_ext). */
+int sewald_gpu_gather(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* grid,
+                      const double* xt, int64_t Nt, double* u_out);
+
+/* ---- device-resident session (time stepping / multi-GPU plumbing) ---- */
+/* A session keeps sources, targets, sort permutations, grids and cuFFT plans
+ * resident in HBM between calls. All pointers given to *_dev calls are
+ * device pointers on the context's device; work is ordered on the context
+ * stream. This is the layer bench.py times as `value` and the multi-GPU
+ * driver composes with torch.distributed collectives. */
+typedef struct sewald_gpu_session sewald_gpu_session;
+
+int sewald_gpu_session_create(sewald_gpu_ctx* ctx, const sewald_params_c* p,
+                              sewald_gpu_session** out);
+void sewald_gpu_session_destroy(sewald_gpu_session* s);
+/* Sources: device AoS arrays (N*3). Copied into session-owned sorted storage. */
+int sewald_gpu_session_set_sources(sewald_gpu_session* s, const double* x_dev,
+                                   const double* f_dev, const double* nu_dev, int64_t N);
+/* Targets: device AoS (Nt*3); same_as_sources uses the sources. */
+int sewald_gpu_session_set_targets(sewald_gpu_session* s, const double* xt_dev, int64_t Nt,
+                                   int same_as_sources);
+/* Number of doubles of the spread grid (C * prod M_ext). */
+int64_t sewald_gpu_session_grid_size(const sewald_gpu_session* s);
+/* Spread sources [i0, i1) (in the caller's original order) into grid_dev
+ * (zeroed first). grid_dev may be NULL to use the session's own grid. */
+int sewald_gpu_session_spread(sewald_gpu_session* s, int64_t i0, int64_t i1, double* grid_dev);
+/* Forward transform, k-space scaling, inverse transform: grid_dev (C comps)
+ * -> session flow field (3 comps). precompute_0p selects the D=0 table path. */
+int sewald_gpu_session_solve(sewald_gpu_session* s, const double* grid_dev, int precompute_0p);
+/* u_dev[t] = (for t in [t0,t1)) u_F (gather) + u_R (real space) + self +
+ * zero-mode terms; u_dev holds Nt*3 doubles in the caller's target order.
+ * parts: bit 1 = Fourier, bit 2 = real space, bit 4 = self/zero-mode terms. */
+int sewald_gpu_session_evaluate(sewald_gpu_session* s, int64_t t0, int64_t t1, int parts,
+                                double* u_dev);
+/* Whole pipeline on one GPU: spread all, solve, evaluate all (parts = 7). */
+int sewald_gpu_session_run(sewald_gpu_session* s, int precompute_0p, double* u_dev);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SEWALD_GPU_H */
