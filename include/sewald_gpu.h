@@ -128,6 +128,13 @@ int sewald_gpu_get_timings(const sewald_gpu_ctx* ctx, sewald_timings_c* out);
 /* 1 = record per-stage CUDA events (adds event overhead), 0 = off. */
 int sewald_gpu_set_profiling(sewald_gpu_ctx* ctx, int enabled);
 
+/* Cumulative number of engine kernels launched on this context. */
+int64_t sewald_gpu_launch_count(const sewald_gpu_ctx* ctx);
+
+/* Measured fp64 FMA-pipe throughput of this device in TFLOP/s (DFMA
+ * microbenchmark; roofline denominator for the fp64-bound kernels). */
+int sewald_gpu_fp64_peak(sewald_gpu_ctx* ctx, double* tflops);
+
 /* ---- host-buffer entry points (drop-in path) ------------------------- */
 /* x, f: N*3 doubles; nu: N*3 (stresslet) or NULL; xt: Nt*3. When
  * same_as_sources != 0 the targets are the sources (xt may be NULL or x).
@@ -184,11 +191,17 @@ int sewald_gpu_session_spread(sewald_gpu_session* s, int64_t i0, int64_t i1, dou
 /* Forward transform, k-space scaling, inverse transform: grid_dev (C comps)
  * -> session flow field (3 comps). precompute_0p selects the D=0 table path. */
 int sewald_gpu_session_solve(sewald_gpu_session* s, const double* grid_dev, int precompute_0p);
-/* u_dev[t] = (for t in [t0,t1)) u_F (gather) + u_R (real space) + self +
- * zero-mode terms; u_dev holds Nt*3 doubles in the caller's target order.
- * parts: bit 1 = Fourier, bit 2 = real space, bit 4 = self/zero-mode terms. */
-int sewald_gpu_session_evaluate(sewald_gpu_session* s, int64_t t0, int64_t t1, int parts,
+/* Evaluate the targets of part `part` of `nparts` equal contiguous slices of
+ * the session's internal (cell-sorted, hence spatially compact) target order.
+ * u_dev holds Nt*3 doubles in the caller's original target order; only this
+ * part's rows are written (u = u_R + u_F + terms), other rows are untouched,
+ * so per-rank results combine with a sum all-reduce. `parts` bit mask:
+ * 1 = Fourier (gather of the solved flow), 2 = real space, 4 = self /
+ * zero-mode / gauge terms. */
+int sewald_gpu_session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts,
                                 double* u_dev);
+/* Accepted real-space pairs counted since the last reset (synchronises). */
+int64_t sewald_gpu_session_pair_count(sewald_gpu_session* s, int reset);
 /* Whole pipeline on one GPU: spread all, solve, evaluate all (parts = 7). */
 int sewald_gpu_session_run(sewald_gpu_session* s, int precompute_0p, double* u_dev);
 

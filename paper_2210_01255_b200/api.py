@@ -1,0 +1,534 @@
+"""Python mirror of the reference's host API for the Spectral Ewald hot path.
+
+Same names, argument meaning and error behaviour as the reference C++
+library (/root/reference/proj/include/sewald/*.h); every numeric call goes
+through the C-ABI (include/sewald_gpu.h) into sm_100a kernels.
+
+    estimates.h:106-107  select_parameters(kind, d, cell, Q, xi, tol, opt)
+    realspace.h:46-47    full_potential(system, targets, params, opt)
+    fourier.h:81-82      se_fourier_potential(system, targets, params, opt)
+    realspace.h:40-41    realspace_potential(system, targets, xi, rc, starred, n_threads)
+    fourier.h:59, 71-72  spread(system, params) / gather(field, params, targets)
+    domain.h:78-79       source_quantity(system)
+
+Exceptions: InvalidArgument (std::invalid_argument), DomainError
+(std::domain_error), SewaldRuntimeError (std::runtime_error).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import enum
+import threading
+from dataclasses import dataclass, field
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import _abi
+from ._abi import (DomainError, InvalidArgument, SewaldError, SewaldRuntimeError, DeviceError,
+                   sewald_params_c, sewald_report_c, sewald_timings_c)
+
+
+class Kernel(enum.IntEnum):
+    """enum class Kernel (domain.h:26)."""
+    stokeslet = _abi.STOKESLET
+    stresslet = _abi.STRESSLET
+    rotlet = _abi.ROTLET
+
+
+class WindowKind(enum.IntEnum):
+    """enum class WindowKind (window.h:9)."""
+    kb = _abi.WIN_KB
+    pkb = _abi.WIN_PKB
+    tg = _abi.WIN_TG
+
+
+def strength_components(kind: Kernel) -> int:
+    """domain.h:34 — 9 for the stresslet outer product, else 3."""
+    return 9 if Kernel(kind) == Kernel.stresslet else 3
+
+
+@dataclass
+class Cell:
+    """struct Cell (domain.h:36-39)."""
+    L: Sequence[float] = (1.0, 1.0, 1.0)
+
+    def volume(self) -> float:
+        return float(self.L[0]) * float(self.L[1]) * float(self.L[2])
+
+
+def _vec3(a, name: str) -> np.ndarray:
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if arr.size == 0:
+        return arr.reshape(0, 3)
+    if arr.ndim != 2 or arr.shape[1] != 3:
+        raise InvalidArgument(f"{name} must have shape (n, 3)")
+    return arr
+
+
+@dataclass
+class SourceSystem:
+    """struct SourceSystem (domain.h:47-56): AoS positions and strengths."""
+    kind: Kernel = Kernel.stokeslet
+    cell: Cell = field(default_factory=Cell)
+    d: int = 3
+    x: np.ndarray = field(default_factory=lambda: np.zeros((0, 3)))
+    f: np.ndarray = field(default_factory=lambda: np.zeros((0, 3)))
+    nu: Optional[np.ndarray] = None
+
+    def size(self) -> int:
+        return int(np.asarray(self.x).shape[0])
+
+
+@dataclass
+class TargetSet:
+    """struct TargetSet (domain.h:58-64)."""
+    x: np.ndarray = field(default_factory=lambda: np.zeros((0, 3)))
+    same_as_sources: bool = False
+
+    @staticmethod
+    def from_sources(s: SourceSystem) -> "TargetSet":
+        return TargetSet(np.asarray(s.x), True)
+
+
+@dataclass
+class ToleranceSpec:
+    """struct ToleranceSpec (estimates.h:13-18)."""
+    value: float = 1e-8
+    relative: bool = False
+
+
+@dataclass
+class SelectionOptions:
+    """struct SelectionOptions (estimates.h:92-96)."""
+    f_m: int = 4
+    window: WindowKind = WindowKind.pkb
+    pollution_fix: bool = True
+
+
+@dataclass
+class SePipelineOptions:
+    """struct SePipelineOptions (fourier.h:76-79). `table` reuse is implicit:
+    the device session caches the D=0 kernel table per parameter set."""
+    precompute_0p: bool = True
+
+
+@dataclass
+class GridSpec:
+    """struct GridSpec (grid.h:13-24)."""
+    d: int = 3
+    h: float = 0.0
+    M: Sequence[int] = (0, 0, 0)
+    M_ext: Sequence[int] = (0, 0, 0)
+    L: Sequence[float] = (0.0, 0.0, 0.0)
+    L_ext: Sequence[float] = (0.0, 0.0, 0.0)
+    pad: Sequence[float] = (0.0, 0.0, 0.0)
+    f_m: int = 4
+
+
+@dataclass
+class WindowSpec:
+    """struct WindowSpec (window.h:15-29)."""
+    kind: WindowKind = WindowKind.pkb
+    P: int = 8
+    h: float = 1.0
+    beta: float = 20.0
+    nu: int = 6
+    alpha: float = 0.0
+
+    @staticmethod
+    def make(kind: WindowKind, P: int, h: float) -> "WindowSpec":
+        """WindowSpec::make (window.cpp:76-86), computed by the C-ABI."""
+        c = sewald_params_c()
+        _host_call(_abi.load().sewald_window_make(int(kind), int(P), float(h), C.byref(c)))
+        return WindowSpec(WindowKind(c.win_kind), c.P, c.win_h, c.beta, c.nu, c.alpha)
+
+
+@dataclass
+class UpsamplingPlan:
+    """struct UpsamplingPlan (grid.h:29-35)."""
+    s0: float = 1.0
+    s_star: float = 1.0
+    k_star: Sequence[int] = (0, 0, 0)
+    s0_raw: float = 1.0
+    s_star_raw: float = 1.0
+
+
+@dataclass
+class EwaldParams:
+    """struct EwaldParams (estimates.h:62-71)."""
+    kind: Kernel = Kernel.stokeslet
+    d: int = 3
+    xi: float = 1.0
+    rc: float = 0.0
+    R: float = 0.0
+    grid: GridSpec = field(default_factory=GridSpec)
+    window: WindowSpec = field(default_factory=WindowSpec)
+    upsampling: UpsamplingPlan = field(default_factory=UpsamplingPlan)
+
+    def to_c(self) -> sewald_params_c:
+        c = sewald_params_c()
+        c.kind, c.d = int(self.kind), int(self.d)
+        c.xi, c.rc, c.R = float(self.xi), float(self.rc), float(self.R)
+        g = self.grid
+        c.h = float(g.h)
+        for i in range(3):
+            c.M[i], c.M_ext[i] = int(g.M[i]), int(g.M_ext[i])
+            c.L[i], c.L_ext[i], c.pad[i] = float(g.L[i]), float(g.L_ext[i]), float(g.pad[i])
+            c.k_star[i] = int(self.upsampling.k_star[i])
+        c.f_m = int(g.f_m)
+        w = self.window
+        c.win_kind, c.P, c.win_h = int(w.kind), int(w.P), float(w.h)
+        c.beta, c.nu, c.alpha = float(w.beta), int(w.nu), float(w.alpha)
+        u = self.upsampling
+        c.s0, c.s_star, c.s0_raw, c.s_star_raw = float(u.s0), float(u.s_star), float(u.s0_raw), float(u.s_star_raw)
+        return c
+
+    @staticmethod
+    def from_c(c: sewald_params_c) -> "EwaldParams":
+        g = GridSpec(c.d, c.h, tuple(c.M), tuple(c.M_ext), tuple(c.L), tuple(c.L_ext), tuple(c.pad), c.f_m)
+        w = WindowSpec(WindowKind(c.win_kind), c.P, c.win_h, c.beta, c.nu, c.alpha)
+        u = UpsamplingPlan(c.s0, c.s_star, tuple(c.k_star), c.s0_raw, c.s_star_raw)
+        return EwaldParams(Kernel(c.kind), c.d, c.xi, c.rc, c.R, g, w, u)
+
+
+@dataclass
+class EstimateReport:
+    """struct EstimateReport (estimates.h:73-90)."""
+    tau_abs: float = 0.0
+    U: float = 0.0
+    kinf: float = 0.0
+    fourier_trunc: float = 0.0
+    realspace_trunc: float = 0.0
+    window_err: float = 0.0
+    h_estimate: float = 0.0
+    P_estimate: int = 0
+    h_target: float = 0.0
+    P_target: int = 0
+    rc_clamped: bool = False
+    kinf_clamped: bool = False
+    window_saturated: bool = False
+    tg_support_from_pkb: bool = False
+
+
+@dataclass
+class ParameterSelection:
+    params: EwaldParams
+    report: EstimateReport
+
+
+def _host_call(code: int):
+    if code != _abi.OK:
+        _abi.raise_for(code, _abi.load().sewald_last_error().decode())
+
+
+def _dp(a: Optional[np.ndarray]):
+    if a is None:
+        return None
+    return a.ctypes.data_as(_abi.DP)
+
+
+def select_parameters(kind: Kernel, d: int, cell: Cell, Q: float, xi: float,
+                      tol: ToleranceSpec = ToleranceSpec(),
+                      opt: SelectionOptions = SelectionOptions()) -> ParameterSelection:
+    """select_parameters (estimates.h:106-107, estimates.cpp:211-268)."""
+    lib = _abi.load()
+    c, r = sewald_params_c(), sewald_report_c()
+    L = (C.c_double * 3)(*[float(v) for v in cell.L])
+    _host_call(lib.sewald_select_parameters(int(kind), int(d), L, float(Q), float(xi), float(tol.value),
+                                            int(bool(tol.relative)), int(opt.f_m), int(opt.window),
+                                            int(bool(opt.pollution_fix)), C.byref(c), C.byref(r)))
+    rep = EstimateReport(r.tau_abs, r.U, r.kinf, r.fourier_trunc, r.realspace_trunc, r.window_err,
+                         r.h_estimate, r.P_estimate, r.h_target, r.P_target, bool(r.rc_clamped),
+                         bool(r.kinf_clamped), bool(r.window_saturated), bool(r.tg_support_from_pkb))
+    return ParameterSelection(EwaldParams.from_c(c), rep)
+
+
+def build_grid(cell: Cell, d: int, h_target: float, P: int, kind: Kernel, f_m: int) -> GridSpec:
+    """build_grid (grid.h:38, grid.cpp:35-77)."""
+    c = sewald_params_c()
+    L = (C.c_double * 3)(*[float(v) for v in cell.L])
+    _host_call(_abi.load().sewald_build_grid(L, int(d), float(h_target), int(P), int(kind), int(f_m), C.byref(c)))
+    return EwaldParams.from_c(c).grid
+
+
+def pkb_coefficients(window: WindowSpec) -> np.ndarray:
+    """pkb_build (window.cpp:112-138): (P, nu+1) monomial coefficients."""
+    p = EwaldParams(window=window).to_c()
+    out = np.zeros((window.P, window.nu + 1))
+    _host_call(_abi.load().sewald_pkb_coefficients(C.byref(p), _dp(out)))
+    return out
+
+
+def window_eval(window: WindowSpec, r) -> np.ndarray:
+    """Window::eval1d (window.cpp:171-178) on the host."""
+    r = np.ascontiguousarray(np.asarray(r, dtype=np.float64).ravel())
+    out = np.zeros_like(r)
+    p = EwaldParams(window=window).to_c()
+    _host_call(_abi.load().sewald_window_eval(C.byref(p), _dp(r), r.size, _dp(out)))
+    return out
+
+
+def window_hat(window: WindowSpec, k) -> np.ndarray:
+    """Window::hat1d (window.cpp:180-182) on the host."""
+    k = np.ascontiguousarray(np.asarray(k, dtype=np.float64).ravel())
+    out = np.zeros_like(k)
+    p = EwaldParams(window=window).to_c()
+    _host_call(_abi.load().sewald_window_hat(C.byref(p), _dp(k), k.size, _dp(out)))
+    return out
+
+
+def source_quantity(system: SourceSystem) -> float:
+    """source_quantity (domain.cpp:53-62)."""
+    f = _vec3(system.f, "f")
+    nu = _vec3(system.nu, "nu") if Kernel(system.kind) == Kernel.stresslet else None
+    return float(_abi.load().sewald_source_quantity(int(system.kind), _dp(f), _dp(nu), f.shape[0]))
+
+
+# ---------------------------------------------------------------------------
+# device engine
+# ---------------------------------------------------------------------------
+
+
+class Engine:
+    """One device context (stream, cached cuFFT plans and resident buffers)."""
+
+    def __init__(self, device: int = 0):
+        self._lib = _abi.load()
+        h = C.c_void_p()
+        code = self._lib.sewald_gpu_create(int(device), C.byref(h))
+        if code != _abi.OK:
+            _abi.raise_for(code, f"sewald_gpu_create(device={device}) failed (no usable CUDA device?)")
+        self.ctx = h
+        self.device = device
+        self._lock = threading.Lock()
+
+    def close(self):
+        if getattr(self, "ctx", None):
+            self._lib.sewald_gpu_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def check(self, code: int):
+        if code != _abi.OK:
+            _abi.raise_for(code, self._lib.sewald_gpu_last_error(self.ctx).decode())
+
+    def set_profiling(self, on: bool):
+        self.check(self._lib.sewald_gpu_set_profiling(self.ctx, int(bool(on))))
+
+    def set_stream(self, stream_ptr: int):
+        self.check(self._lib.sewald_gpu_set_stream(self.ctx, C.c_void_p(stream_ptr)))
+
+    def launch_count(self) -> int:
+        return int(self._lib.sewald_gpu_launch_count(self.ctx))
+
+    def fp64_peak_tflops(self) -> float:
+        v = C.c_double()
+        self.check(self._lib.sewald_gpu_fp64_peak(self.ctx, C.byref(v)))
+        return float(v.value)
+
+    def timings(self) -> dict:
+        t = sewald_timings_c()
+        self.check(self._lib.sewald_gpu_get_timings(self.ctx, C.byref(t)))
+        return {n: getattr(t, n) for n, _ in sewald_timings_c._fields_}
+
+
+_engines: dict = {}
+_elock = threading.Lock()
+
+
+def default_engine(device: int = 0) -> Engine:
+    with _elock:
+        e = _engines.get(device)
+        if e is None:
+            e = Engine(device)
+            _engines[device] = e
+        return e
+
+
+def _system_arrays(system: SourceSystem, params: Optional[EwaldParams] = None):
+    kind = Kernel(system.kind)
+    if params is not None and (kind != Kernel(params.kind) or int(system.d) != int(params.d)):
+        raise InvalidArgument("parameter set was built for a different system")
+    x = _vec3(system.x, "x")
+    f = _vec3(system.f, "f")
+    if f.shape[0] != x.shape[0]:
+        raise InvalidArgument("strength count does not match position count")
+    nu = None
+    if kind == Kernel.stresslet:
+        nu = _vec3(system.nu if system.nu is not None else np.zeros((0, 3)), "nu")
+        if nu.shape[0] != x.shape[0]:
+            raise InvalidArgument("stresslet needs one orientation per source")
+    elif system.nu is not None and np.asarray(system.nu).size:
+        raise InvalidArgument("orientations only apply to the stresslet")
+    if not (0 <= int(system.d) <= 3):
+        raise InvalidArgument("periodicity d must be in 0..3")
+    if any(not (float(v) > 0.0) for v in system.cell.L):
+        raise InvalidArgument("cell lengths must be positive")
+    if x.size and not np.all(np.isfinite(x)):
+        raise InvalidArgument("non-finite source position")
+    return x, f, nu
+
+
+def _params_for(system: SourceSystem, params: EwaldParams) -> sewald_params_c:
+    c = params.to_c()
+    for i in range(3):
+        c.L[i] = float(system.cell.L[i])
+    return c
+
+
+def _pipeline(entry: str, system: SourceSystem, targets: TargetSet, params: EwaldParams,
+              opt: SePipelineOptions, engine: Optional[Engine]) -> np.ndarray:
+    x, f, nu = _system_arrays(system, params)
+    if not (float(params.xi) > 0.0):
+        raise InvalidArgument("xi must be positive")
+    same = bool(targets.same_as_sources)
+    xt = x if same else _vec3(targets.x, "targets")
+    if not same and xt.size and not np.all(np.isfinite(xt)):
+        raise InvalidArgument("target coordinates must be finite")
+    nt = xt.shape[0]
+    u = np.zeros((nt, 3))
+    eng = engine or default_engine()
+    c = _params_for(system, params)
+    with eng._lock:
+        fn = getattr(eng._lib, entry)
+        eng.check(fn(eng.ctx, C.byref(c), _dp(x), _dp(f), _dp(nu), x.shape[0], _dp(xt), nt,
+                     int(same), int(bool(opt.precompute_0p)), _dp(u)))
+    return u
+
+
+def full_potential(system: SourceSystem, targets: TargetSet, params: EwaldParams,
+                   opt: SePipelineOptions = SePipelineOptions(), engine: Optional[Engine] = None) -> np.ndarray:
+    """full_potential (realspace.h:46-47): u_R + u_F + self + zero-mode terms, (Nt, 3)."""
+    return _pipeline("sewald_gpu_full_potential", system, targets, params, opt, engine)
+
+
+def se_fourier_potential(system: SourceSystem, targets: TargetSet, params: EwaldParams,
+                         opt: SePipelineOptions = SePipelineOptions(),
+                         engine: Optional[Engine] = None) -> np.ndarray:
+    """se_fourier_potential (fourier.h:81-82)."""
+    return _pipeline("sewald_gpu_fourier_potential", system, targets, params, opt, engine)
+
+
+def realspace_potential(system: SourceSystem, targets: TargetSet, xi: float, rc: float,
+                        starred: bool, n_threads: int = 1, engine: Optional[Engine] = None) -> np.ndarray:
+    """realspace_potential (realspace.h:40-41). n_threads is accepted for API
+    compatibility; the sum always runs on the GPU."""
+    del n_threads
+    if not (float(xi) > 0.0):
+        raise InvalidArgument("split parameter must be positive")
+    x, f, nu = _system_arrays(system)
+    same = bool(targets.same_as_sources)
+    xt = x if same else _vec3(targets.x, "targets")
+    if xt.size and not np.all(np.isfinite(xt)):
+        raise InvalidArgument("target coordinates must be finite")
+    if not (float(rc) > 0.0):
+        raise InvalidArgument("cell list cutoff must be positive")
+    u = np.zeros((xt.shape[0], 3))
+    eng = engine or default_engine()
+    L = (C.c_double * 3)(*[float(v) for v in system.cell.L])
+    with eng._lock:
+        eng.check(eng._lib.sewald_gpu_realspace_potential(
+            eng.ctx, int(system.kind), int(system.d), L, _dp(x), _dp(f), _dp(nu), x.shape[0], _dp(xt),
+            xt.shape[0], int(same), float(xi), float(rc), int(bool(starred)), _dp(u)))
+    return u
+
+
+def spread(system: SourceSystem, params: EwaldParams, engine: Optional[Engine] = None) -> np.ndarray:
+    """spread (fourier.h:59): RealField values, shape (C, n0, n1, n2)."""
+    x, f, nu = _system_arrays(system)
+    if int(system.d) != int(params.d):
+        raise InvalidArgument("system and grid periodicity differ")
+    n = tuple(int(v) for v in params.grid.M_ext)
+    Cc = strength_components(system.kind)
+    out = np.zeros((Cc,) + n)
+    eng = engine or default_engine()
+    c = params.to_c()
+    c.kind = int(system.kind)
+    with eng._lock:
+        eng.check(eng._lib.sewald_gpu_spread(eng.ctx, C.byref(c), _dp(x), _dp(f), _dp(nu), x.shape[0], _dp(out)))
+    return out
+
+
+def gather(field: np.ndarray, params: EwaldParams, targets: TargetSet,
+           engine: Optional[Engine] = None) -> np.ndarray:
+    """gather (fourier.h:71-72): field shape (3, n0, n1, n2) -> (Nt, 3)."""
+    fld = np.ascontiguousarray(np.asarray(field, dtype=np.float64))
+    n = tuple(int(v) for v in params.grid.M_ext)
+    if fld.shape != (3,) + n:
+        raise InvalidArgument("gather expects a 3-component field on the extended grid")
+    xt = _vec3(targets.x, "targets")
+    u = np.zeros((xt.shape[0], 3))
+    eng = engine or default_engine()
+    c = params.to_c()
+    with eng._lock:
+        eng.check(eng._lib.sewald_gpu_gather(eng.ctx, C.byref(c), _dp(fld), _dp(xt), xt.shape[0], _dp(u)))
+    return u
+
+
+class Session:
+    """Device-resident session (sewald_gpu_session_*): inputs and outputs are
+    torch CUDA tensors; torch is used only for memory and streams."""
+
+    def __init__(self, params: EwaldParams, cell: Optional[Cell] = None, engine: Optional[Engine] = None):
+        self.engine = engine or default_engine()
+        self._lib = self.engine._lib
+        c = params.to_c()
+        if cell is not None:
+            for i in range(3):
+                c.L[i] = float(cell.L[i])
+        h = C.c_void_p()
+        self.engine.check(self._lib.sewald_gpu_session_create(self.engine.ctx, C.byref(c), C.byref(h)))
+        self.s = h
+        self._keep = []
+
+    def close(self):
+        if getattr(self, "s", None):
+            self._lib.sewald_gpu_session_destroy(self.s)
+            self.s = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @staticmethod
+    def _ptr(t):
+        if t is None:
+            return None
+        assert t.is_cuda and t.dtype.is_floating_point and t.is_contiguous()
+        return C.c_void_p(t.data_ptr())
+
+    def set_sources(self, x, f, nu=None):
+        self._keep = [x, f, nu]
+        self.engine.check(self._lib.sewald_gpu_session_set_sources(
+            self.s, self._ptr(x), self._ptr(f), self._ptr(nu), int(x.shape[0])))
+
+    def set_targets(self, xt=None, same_as_sources: bool = True):
+        n = 0 if xt is None else int(xt.shape[0])
+        self.engine.check(self._lib.sewald_gpu_session_set_targets(self.s, self._ptr(xt), n, int(same_as_sources)))
+
+    def grid_size(self) -> int:
+        return int(self._lib.sewald_gpu_session_grid_size(self.s))
+
+    def spread(self, i0: int, i1: int, grid=None):
+        self.engine.check(self._lib.sewald_gpu_session_spread(self.s, int(i0), int(i1), self._ptr(grid)))
+
+    def solve(self, grid=None, precompute_0p: bool = True):
+        self.engine.check(self._lib.sewald_gpu_session_solve(self.s, self._ptr(grid), int(precompute_0p)))
+
+    def evaluate(self, u, part: int = 0, nparts: int = 1, parts: int = 7):
+        self.engine.check(self._lib.sewald_gpu_session_evaluate(self.s, int(part), int(nparts), int(parts),
+                                                                self._ptr(u)))
+
+    def pair_count(self, reset: bool = False) -> int:
+        return int(self._lib.sewald_gpu_session_pair_count(self.s, int(reset)))
+
+    def run(self, u, precompute_0p: bool = True):
+        self.engine.check(self._lib.sewald_gpu_session_run(self.s, int(precompute_0p), self._ptr(u)))

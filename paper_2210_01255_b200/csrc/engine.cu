@@ -1,0 +1,939 @@
+// Device context, resident session and pipeline orchestration.
+//
+// Pipeline (fourier.cpp:805-852 + realspace.cpp:205-219), all on one stream:
+//   sources -> [bucket by stencil tile, sort] -> spread (tiles)      -> grid
+//   grid    -> cuFFT D2Z -> k-space scale (fused operator) -> Z2D    -> flow
+//   targets -> [fold, cell sort] -> real space (cell rows) -> u  (=)
+//   flow    -> gather (warp per target)                    -> u  (+=)
+//   self / stresslet zero mode / gauge epilogue            -> u  (+=)
+// Everything stays resident in HBM between calls; host-buffer entry points
+// wrap a cached session with one H2D and one D2H copy.
+#include "engine.h"
+#include "host_params.h"
+
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+namespace sewald_b200 {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw EngineError(SEWALD_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void cufft_check(cufftResult r, const char* what) {
+    if (r != CUFFT_SUCCESS)
+        throw EngineError(SEWALD_ECUFFT, std::string(what) + ": cuFFT error " + std::to_string((int)r));
+}
+
+DevBuf::~DevBuf() {
+    if (ptr) cudaFree(ptr);
+}
+
+void* DevBuf::ensure(size_t n) {
+    if (n <= bytes && ptr) return ptr;
+    if (ptr) {
+        cuda_check(cudaDeviceSynchronize(), "sync before realloc");
+        cudaFree(ptr);
+        ptr = nullptr;
+        bytes = 0;
+    }
+    const size_t alloc = std::max<size_t>(n, 256);
+    cudaError_t e = cudaMalloc(&ptr, alloc);
+    if (e != cudaSuccess) {
+        ptr = nullptr;
+        throw EngineError(SEWALD_ENOMEM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+    }
+    bytes = alloc;
+    return ptr;
+}
+
+struct FourierPlanD3 {
+    int n[3];
+    int C;
+    cufftHandle fwd = 0, inv = 0;
+    DevBuf spec;
+    DevBuf tables;  // k0,k1,k2 (n0+n1+nh), what0, what1, what2
+    KspaceTables kt{};
+    ~FourierPlanD3() {
+        if (fwd) cufftDestroy(fwd);
+        if (inv) cufftDestroy(inv);
+    }
+};
+
+namespace {
+
+// ---- small kernels -------------------------------------------------------
+
+__global__ void finite_check_kernel(const double* __restrict__ x, int64_t n, int* __restrict__ bad) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n && !isfinite(x[i])) atomicExch(bad, 1);
+}
+
+constexpr int RED_BLOCKS = 256;
+constexpr int RED_THREADS = 256;
+
+// Per-block min/max of each coordinate (free-axis cell-list bounds).
+__global__ void minmax_kernel(const double* __restrict__ x, int64_t N, double* __restrict__ part) {
+    __shared__ double s[6][RED_THREADS];
+    double v[6] = {1e300, 1e300, 1e300, -1e300, -1e300, -1e300};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x)
+        for (int a = 0; a < 3; ++a) {
+            v[a] = fmin(v[a], x[3 * i + a]);
+            v[3 + a] = fmax(v[3 + a], x[3 * i + a]);
+        }
+    for (int a = 0; a < 6; ++a) s[a][threadIdx.x] = v[a];
+    __syncthreads();
+    for (int st = RED_THREADS / 2; st > 0; st >>= 1) {
+        if ((int)threadIdx.x < st)
+            for (int a = 0; a < 6; ++a)
+                s[a][threadIdx.x] = a < 3 ? fmin(s[a][threadIdx.x], s[a][threadIdx.x + st])
+                                          : fmax(s[a][threadIdx.x], s[a][threadIdx.x + st]);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int a = 0; a < 6; ++a) part[blockIdx.x * 6 + a] = s[a][0];
+}
+
+// Per-block partial sums: sum f (3), sum q.nu (1), sum x (q.nu) (3).
+__global__ void sums_partial_kernel(const double* __restrict__ x, const double* __restrict__ f,
+                                    const double* __restrict__ nu, int64_t N,
+                                    double* __restrict__ part) {
+    __shared__ double s[7][RED_THREADS];
+    double v[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        v[0] += f[3 * i];
+        v[1] += f[3 * i + 1];
+        v[2] += f[3 * i + 2];
+        if (nu) {
+            const double qn = f[3 * i] * nu[3 * i] + f[3 * i + 1] * nu[3 * i + 1] + f[3 * i + 2] * nu[3 * i + 2];
+            v[3] += qn;
+            v[4] += qn * x[3 * i];
+            v[5] += qn * x[3 * i + 1];
+            v[6] += qn * x[3 * i + 2];
+        }
+    }
+    for (int a = 0; a < 7; ++a) s[a][threadIdx.x] = v[a];
+    __syncthreads();
+    for (int st = RED_THREADS / 2; st > 0; st >>= 1) {
+        if ((int)threadIdx.x < st)
+            for (int a = 0; a < 7; ++a) s[a][threadIdx.x] += s[a][threadIdx.x + st];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0)
+        for (int a = 0; a < 7; ++a) part[blockIdx.x * 7 + a] = s[a][0];
+}
+
+__global__ void sums_final_kernel(const double* __restrict__ part, int nblocks, double* __restrict__ out) {
+    const int a = threadIdx.x;
+    if (a >= 7) return;
+    double acc = 0.0;
+    for (int b = 0; b < nblocks; ++b) acc += part[b * 7 + a];
+    out[a] = acc;
+}
+
+struct EpilogueArgs {
+    int kind, d, same, fourier;
+    double self_coef;   // -4 xi / sqrt(pi) (stokeslet, same points)
+    double zm_scale;    // -8 pi / V (stresslet, d = 3)
+    double gauge[3];    // per-component multipliers of sum f (d <= 1 stokeslet)
+};
+
+// u += self term + stresslet zero mode - gauge shift (realspace.cpp:211-217,
+// kernels.cpp:169-187, modified_kernels.cpp:272-281).
+__global__ void epilogue_kernel(EpilogueArgs e, const double* __restrict__ f,
+                                const double* __restrict__ xt, const double* __restrict__ sums,
+                                const uint32_t* __restrict__ torder, int64_t t0, int64_t t1,
+                                int accumulate, double* __restrict__ u) {
+    const int64_t t = t0 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= t1) return;
+    const int64_t ti = torder[t];
+    double v[3] = {0.0, 0.0, 0.0};
+    if (e.fourier) {
+        for (int c = 0; c < 3; ++c) v[c] -= e.gauge[c] * sums[c];
+    }
+    if (e.same && e.kind == SEWALD_STOKESLET)
+        for (int c = 0; c < 3; ++c) v[c] += e.self_coef * f[3 * ti + c];
+    if (e.kind == SEWALD_STRESSLET && e.d == 3)
+        for (int c = 0; c < 3; ++c) v[c] += e.zm_scale * (sums[3] * xt[3 * ti + c] - sums[4 + c]);
+    for (int c = 0; c < 3; ++c) {
+        if (accumulate)
+            u[3 * ti + c] += v[c];
+        else
+            u[3 * ti + c] = v[c];
+    }
+}
+
+int bits_for(uint64_t nkeys) {
+    int b = 1;
+    while ((1ull << b) < nkeys) ++b;
+    return b;
+}
+
+void sort_pairs(sewald_gpu_session* s, const uint32_t* kin, uint32_t* kout, const uint32_t* vin,
+                uint32_t* vout, int64_t n, int bits) {
+    size_t tmp = 0;
+    cuda_check(cub::DeviceRadixSort::SortPairs(nullptr, tmp, kin, kout, vin, vout, (int)n, 0, bits,
+                                               s->ctx->stream),
+               "cub sort size");
+    void* t = s->cub_tmp.ensure(tmp);
+    cuda_check(cub::DeviceRadixSort::SortPairs(t, tmp, kin, kout, vin, vout, (int)n, 0, bits,
+                                               s->ctx->stream),
+               "cub sort");
+    s->ctx->launches += 3;
+}
+
+void check_flag(sewald_gpu_session* s, int which, int code, const char* msg) {
+    int h = 0;
+    cuda_check(cudaMemcpyAsync(&h, s->flags.as<int>() + which, sizeof(int), cudaMemcpyDeviceToHost,
+                               s->ctx->stream),
+               "flag read");
+    cuda_check(cudaStreamSynchronize(s->ctx->stream), "flag sync");
+    if (h) {
+        cuda_check(cudaMemsetAsync(s->flags.as<int>() + which, 0, sizeof(int), s->ctx->stream), "flag reset");
+        throw EngineError(code, msg);
+    }
+}
+
+enum { FLAG_SRC_NONFINITE = 0, FLAG_TGT_NONFINITE = 1, FLAG_SPREAD_BOX = 2, FLAG_GATHER_BOX = 3,
+       FLAG_SINGULAR = 4, NFLAGS = 8 };
+
+void build_cell_grid(sewald_gpu_session* s) {
+    const sewald_params_c& p = s->p;
+    CellGrid cg{};
+    cg.d = p.d;
+    for (int a = 0; a < 3; ++a) cg.L[a] = p.L[a];
+    // Free axes: span of the (unwrapped) source coordinates.
+    double lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+    if (p.d < 3 && s->N > 0) {
+        const int nb = (int)std::min<int64_t>(RED_BLOCKS, (s->N + RED_THREADS - 1) / RED_THREADS);
+        double* part = static_cast<double*>(s->partials.ensure(sizeof(double) * 6 * RED_BLOCKS));
+        minmax_kernel<<<nb, RED_THREADS, 0, s->ctx->stream>>>(s->x.as<double>(), s->N, part);
+        ++s->ctx->launches;
+        std::vector<double> h(6 * nb);
+        cuda_check(cudaMemcpyAsync(h.data(), part, sizeof(double) * 6 * nb, cudaMemcpyDeviceToHost,
+                                   s->ctx->stream),
+                   "minmax copy");
+        cuda_check(cudaStreamSynchronize(s->ctx->stream), "minmax sync");
+        for (int a = 0; a < 3; ++a) {
+            lo[a] = h[a];
+            hi[a] = h[3 + a];
+            for (int b = 1; b < nb; ++b) {
+                lo[a] = std::min(lo[a], h[6 * b + a]);
+                hi[a] = std::max(hi[a], h[6 * b + 3 + a]);
+            }
+        }
+    }
+    static const double refine = [] {
+        const char* e = getenv("SEWALD_RS_REFINE");
+        return e ? atof(e) : 4.0;
+    }();
+    const double target_w = p.rc / refine;
+    for (int a = 0; a < 3; ++a) {
+        const double span = a < p.d ? p.L[a] : hi[a] - lo[a];
+        cg.origin[a] = a < p.d ? 0.0 : lo[a];
+        cg.n[a] = std::max(1, (int)std::floor(span / target_w));
+        if (cg.n[a] > 4096) cg.n[a] = 4096;
+    }
+    while ((int64_t)cg.n[0] * cg.n[1] * cg.n[2] > (int64_t(1) << 22)) {
+        int a = 0;
+        for (int b = 1; b < 3; ++b)
+            if (cg.n[b] > cg.n[a]) a = b;
+        cg.n[a] = (cg.n[a] + 1) / 2;
+    }
+    for (int a = 0; a < 3; ++a) {
+        const double span = a < p.d ? p.L[a] : hi[a] - lo[a];
+        cg.w[a] = span > 0.0 ? span / cg.n[a] : target_w;
+    }
+    s->cg = cg;
+}
+
+void ensure_sums(sewald_gpu_session* s) {
+    if (s->sums_ready) return;
+    double* out = static_cast<double*>(s->sums.ensure(sizeof(double) * 8));
+    double* part = static_cast<double*>(s->partials.ensure(sizeof(double) * 7 * RED_BLOCKS));
+    const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(RED_BLOCKS, (s->N + RED_THREADS - 1) / RED_THREADS));
+    if (s->N > 0) {
+        sums_partial_kernel<<<nb, RED_THREADS, 0, s->ctx->stream>>>(
+            s->x.as<double>(), s->f.as<double>(), s->stresslet ? s->nu.as<double>() : nullptr, s->N, part);
+        sums_final_kernel<<<1, 32, 0, s->ctx->stream>>>(part, nb, out);
+        s->ctx->launches += 2;
+    } else {
+        cuda_check(cudaMemsetAsync(out, 0, sizeof(double) * 8, s->ctx->stream), "sums zero");
+    }
+    s->sums_ready = true;
+}
+
+void ensure_spread_order(sewald_gpu_session* s, int64_t i0, int64_t i1) {
+    if (s->sp_i0 == i0 && s->sp_i1 == i1) return;
+    const int64_t n = i1 - i0;
+    cudaStream_t st = s->ctx->stream;
+    s->shape = spread_plan_shape(s->g, s->p.P);
+    const int nb = s->shape.nb[0] * s->shape.nb[1] * s->shape.nb[2];
+    s->sp_keys.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1));
+    s->sp_keys2.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1));
+    s->sp_vals.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1));
+    s->sp_order.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1));
+    s->sp_off.ensure(sizeof(int64_t) * (nb + 1));
+    int* bad = s->flags.as<int>() + FLAG_SPREAD_BOX;
+    launch_spread_bucket(s->g, s->p.P, s->x.as<double>() + 3 * i0, n, s->shape,
+                         s->sp_keys.as<uint32_t>(), s->sp_vals.as<uint32_t>(), bad, st);
+    ++s->ctx->launches;
+    check_flag(s, FLAG_SPREAD_BOX, SEWALD_EINVAL,
+               "point too close to the extended box boundary; free-direction padding is too small");
+    if (n > 0) {
+        sort_pairs(s, s->sp_keys.as<uint32_t>(), s->sp_keys2.as<uint32_t>(), s->sp_vals.as<uint32_t>(),
+                   s->sp_order.as<uint32_t>(), n, bits_for((uint64_t)nb + 1));
+    }
+    launch_bucket_offsets(s->sp_keys2.as<uint32_t>(), n, nb, s->sp_off.as<int64_t>(), st);
+    ++s->ctx->launches;
+    s->sp_i0 = i0;
+    s->sp_i1 = i1;
+}
+
+void ensure_cells(sewald_gpu_session* s) {
+    if (s->cells_ready) return;
+    cudaStream_t st = s->ctx->stream;
+    build_cell_grid(s);
+    const int64_t N = s->N;
+    const int64_t ncell = (int64_t)s->cg.n[0] * s->cg.n[1] * s->cg.n[2];
+    s->s_folded.ensure(sizeof(double) * 3 * std::max<int64_t>(N, 1));
+    s->c_keys.ensure(sizeof(uint32_t) * std::max<int64_t>(N, 1));
+    s->c_keys2.ensure(sizeof(uint32_t) * std::max<int64_t>(N, 1));
+    s->c_vals.ensure(sizeof(uint32_t) * std::max<int64_t>(N, 1));
+    s->c_order.ensure(sizeof(uint32_t) * std::max<int64_t>(N, 1));
+    s->c_off.ensure(sizeof(int64_t) * (ncell + 1));
+    const int S = s->stresslet ? 12 : 8;
+    s->packed.ensure(sizeof(double) * S * std::max<int64_t>(N, 1));
+    launch_fold_and_key(s->cg, s->x.as<double>(), N, s->s_folded.as<double>(), s->c_keys.as<uint32_t>(),
+                        s->c_vals.as<uint32_t>(), st);
+    if (N > 0) {
+        ++s->ctx->launches;
+        sort_pairs(s, s->c_keys.as<uint32_t>(), s->c_keys2.as<uint32_t>(), s->c_vals.as<uint32_t>(),
+                   s->c_order.as<uint32_t>(), N, bits_for((uint64_t)ncell + 1));
+    }
+    launch_bucket_offsets(s->c_keys2.as<uint32_t>(), N, (int)ncell, s->c_off.as<int64_t>(), st);
+    launch_pack_sources(s->s_folded.as<double>(), s->f.as<double>(), s->nu.as<double>(), s->stresslet,
+                        s->c_order.as<uint32_t>(), N, s->packed.as<double>(), st);
+    s->ctx->launches += 2;
+    s->cells_ready = true;
+}
+
+void ensure_target_order(sewald_gpu_session* s) {
+    ensure_cells(s);
+    if (s->same) return;  // targets reuse the source cell order
+    cudaStream_t st = s->ctx->stream;
+    const int64_t Nt = s->Nt;
+    const int64_t ncell = (int64_t)s->cg.n[0] * s->cg.n[1] * s->cg.n[2];
+    if (Nt == 0) return;
+    s->t_folded.ensure(sizeof(double) * 3 * Nt);
+    s->t_keys.ensure(sizeof(uint32_t) * Nt);
+    s->t_keys2.ensure(sizeof(uint32_t) * Nt);
+    s->t_vals.ensure(sizeof(uint32_t) * Nt);
+    s->t_order.ensure(sizeof(uint32_t) * Nt);
+    launch_fold_and_key(s->cg, s->xt.as<double>(), Nt, s->t_folded.as<double>(), s->t_keys.as<uint32_t>(),
+                        s->t_vals.as<uint32_t>(), st);
+    ++s->ctx->launches;
+    sort_pairs(s, s->t_keys.as<uint32_t>(), s->t_keys2.as<uint32_t>(), s->t_vals.as<uint32_t>(),
+               s->t_order.as<uint32_t>(), Nt, bits_for((uint64_t)ncell + 1));
+}
+
+const double* target_positions(sewald_gpu_session* s) {
+    return s->same ? s->x.as<double>() : s->xt.as<double>();
+}
+const double* target_folded(sewald_gpu_session* s) {
+    return s->same ? s->s_folded.as<double>() : s->t_folded.as<double>();
+}
+const uint32_t* target_order(sewald_gpu_session* s) {
+    return s->same ? s->c_order.as<uint32_t>() : s->t_order.as<uint32_t>();
+}
+
+void d3_prepare(sewald_gpu_session* s) {
+    if (s->d3) return;
+    auto P = std::make_unique<FourierPlanD3>();
+    const sewald_params_c& p = s->p;
+    P->C = s->C;
+    for (int a = 0; a < 3; ++a) P->n[a] = p.M_ext[a];
+    const int n0 = P->n[0], n1 = P->n[1], n2 = P->n[2], nh = n2 / 2 + 1;
+    const int64_t vol = (int64_t)n0 * n1 * n2, hvol = (int64_t)n0 * n1 * nh;
+    // Tables: wavenumbers on the periodic grid M with spacing h and the
+    // window transform at each (fourier.cpp:543-548).
+    std::vector<double> hostt;
+    std::vector<double> kx[3], wx[3];
+    for (int a = 0; a < 3; ++a) {
+        kx[a] = wavenumbers(p.M[a], p.h);
+        wx[a] = window_hat_table(p, kx[a]);
+    }
+    kx[2].resize(nh);
+    wx[2].resize(nh);
+    for (int a = 0; a < 3; ++a) hostt.insert(hostt.end(), kx[a].begin(), kx[a].end());
+    for (int a = 0; a < 3; ++a) hostt.insert(hostt.end(), wx[a].begin(), wx[a].end());
+    double* dt = static_cast<double*>(P->tables.ensure(sizeof(double) * hostt.size()));
+    cuda_check(cudaMemcpyAsync(dt, hostt.data(), sizeof(double) * hostt.size(), cudaMemcpyHostToDevice,
+                               s->ctx->stream),
+               "k tables");
+    const int len[3] = {n0, n1, nh};
+    size_t o = 0;
+    for (int a = 0; a < 3; ++a) { P->kt.k[a] = dt + o; o += len[a]; }
+    for (int a = 0; a < 3; ++a) { P->kt.what[a] = dt + o; o += len[a]; }
+    P->spec.ensure(sizeof(cuDoubleComplex) * hvol * s->C);
+    int n[3] = {n0, n1, n2};
+    int nemb_r[3] = {n0, n1, n2}, nemb_c[3] = {n0, n1, nh};
+    cufft_check(cufftPlanMany(&P->fwd, 3, n, nemb_r, 1, (int)vol, nemb_c, 1, (int)hvol, CUFFT_D2Z, s->C),
+                "plan D2Z");
+    cufft_check(cufftPlanMany(&P->inv, 3, n, nemb_c, 1, (int)hvol, nemb_r, 1, (int)vol, CUFFT_Z2D, 3),
+                "plan Z2D");
+    cufft_check(cufftSetStream(P->fwd, s->ctx->stream), "fft stream");
+    cufft_check(cufftSetStream(P->inv, s->ctx->stream), "fft stream");
+    cuda_check(cudaStreamSynchronize(s->ctx->stream), "tables sync");
+    s->d3 = std::move(P);
+}
+
+struct StageTimer {
+    sewald_gpu_ctx* ctx;
+    cudaEvent_t ev[12];
+    int n = 0;
+    explicit StageTimer(sewald_gpu_ctx* c) : ctx(c) {
+        if (ctx->profiling)
+            for (auto& e : ev) cudaEventCreate(&e);
+    }
+    void mark() {
+        if (ctx->profiling && n < 12) cudaEventRecord(ev[n++], ctx->stream);
+    }
+    double ms(int a, int b) {
+        float t = 0;
+        if (!ctx->profiling || b >= n) return 0.0;
+        cudaEventElapsedTime(&t, ev[a], ev[b]);
+        return t;
+    }
+    ~StageTimer() {
+        if (ctx->profiling)
+            for (auto& e : ev) cudaEventDestroy(e);
+    }
+};
+
+}  // namespace
+
+DevGrid make_dev_grid(const sewald_params_c& p) {
+    DevGrid g{};
+    g.d = p.d;
+    g.h = p.h;
+    for (int a = 0; a < 3; ++a) {
+        g.n[a] = p.M_ext[a];
+        g.x0[a] = a < p.d ? 0.0 : -0.5 * p.pad[a];
+        g.L[a] = p.L[a];
+    }
+    return g;
+}
+
+DevWindow make_dev_window(const sewald_params_c& p) {
+    validate_window(p);
+    if (p.P > kMaxP) throw EngineError(SEWALD_EINVAL, "window support P exceeds the device limit");
+    DevWindow w{};
+    w.kind = p.win_kind;
+    w.P = p.P;
+    w.nu = p.nu;
+    w.h = p.win_h;
+    w.half_width = 0.5 * p.win_h * static_cast<double>(p.P);
+    w.beta = p.beta;
+    w.i0_beta = bessel_i0(p.beta);
+    w.alpha = p.alpha;
+    if (p.win_kind == SEWALD_WIN_PKB) {
+        if (p.nu > kMaxNu) throw EngineError(SEWALD_EINVAL, "PKB degree exceeds the device limit");
+        const std::vector<double> c = pkb_coefficients(p);
+        std::copy(c.begin(), c.end(), w.coef);
+    }
+    return w;
+}
+
+void session_init(sewald_gpu_session* s, sewald_gpu_ctx* ctx, const sewald_params_c& p) {
+    if (p.d < 0 || p.d > 3) throw EngineError(SEWALD_EINVAL, "periodicity d must be in 0..3");
+    if (p.kind < 0 || p.kind > 2) throw EngineError(SEWALD_EINVAL, "unknown kernel");
+    for (int a = 0; a < 3; ++a)
+        if (!(p.L[a] > 0.0)) throw EngineError(SEWALD_EINVAL, "cell lengths must be positive");
+    if (std::fabs(p.win_h - p.h) > 1e-12 * p.h)
+        throw EngineError(SEWALD_EINVAL, "window was built for a different grid spacing");
+    s->ctx = ctx;
+    s->p = p;
+    s->g = make_dev_grid(p);
+    s->w = make_dev_window(p);
+    s->stresslet = p.kind == SEWALD_STRESSLET;
+    s->C = s->stresslet ? 9 : 3;
+    s->flags.ensure(sizeof(int) * NFLAGS);
+    cuda_check(cudaMemsetAsync(s->flags.ptr, 0, sizeof(int) * NFLAGS, ctx->stream), "flags");
+    s->pair_counter.ensure(sizeof(unsigned long long));
+    cuda_check(cudaMemsetAsync(s->pair_counter.ptr, 0, sizeof(unsigned long long), ctx->stream), "pairs");
+}
+
+void session_set_sources(sewald_gpu_session* s, const double* x, const double* f, const double* nu,
+                         int64_t N) {
+    cudaStream_t st = s->ctx->stream;
+    if (s->stresslet && N > 0 && !nu) throw EngineError(SEWALD_EINVAL, "stresslet needs one orientation per source");
+    if (!s->stresslet && nu) throw EngineError(SEWALD_EINVAL, "orientations only apply to the stresslet");
+    s->N = N;
+    const size_t b = sizeof(double) * 3 * std::max<int64_t>(N, 1);
+    s->x.ensure(b);
+    s->f.ensure(b);
+    if (N > 0) {
+        cuda_check(cudaMemcpyAsync(s->x.ptr, x, sizeof(double) * 3 * N, cudaMemcpyDefault, st), "x copy");
+        cuda_check(cudaMemcpyAsync(s->f.ptr, f, sizeof(double) * 3 * N, cudaMemcpyDefault, st), "f copy");
+    }
+    if (s->stresslet) {
+        s->nu.ensure(b);
+        if (N > 0)
+            cuda_check(cudaMemcpyAsync(s->nu.ptr, nu, sizeof(double) * 3 * N, cudaMemcpyDefault, st), "nu copy");
+    }
+    if (N > 0) {
+        finite_check_kernel<<<(unsigned)((3 * N + 255) / 256), 256, 0, st>>>(
+            s->x.as<double>(), 3 * N, s->flags.as<int>() + FLAG_SRC_NONFINITE);
+        ++s->ctx->launches;
+    }
+    s->sp_i0 = s->sp_i1 = -1;
+    s->cells_ready = false;
+    s->sums_ready = false;
+    if (s->same) s->Nt = N;
+}
+
+void session_set_targets(sewald_gpu_session* s, const double* xt, int64_t Nt, bool same) {
+    s->same = same;
+    if (same) {
+        s->Nt = s->N;
+        return;
+    }
+    s->Nt = Nt;
+    cudaStream_t st = s->ctx->stream;
+    s->xt.ensure(sizeof(double) * 3 * std::max<int64_t>(Nt, 1));
+    if (Nt > 0) {
+        cuda_check(cudaMemcpyAsync(s->xt.ptr, xt, sizeof(double) * 3 * Nt, cudaMemcpyDefault, st), "xt copy");
+        finite_check_kernel<<<(unsigned)((3 * Nt + 255) / 256), 256, 0, st>>>(
+            s->xt.as<double>(), 3 * Nt, s->flags.as<int>() + FLAG_TGT_NONFINITE);
+        ++s->ctx->launches;
+    }
+}
+
+void session_spread(sewald_gpu_session* s, int64_t i0, int64_t i1, double* grid) {
+    if (i0 < 0 || i1 > s->N || i0 > i1) throw EngineError(SEWALD_EINVAL, "bad source range");
+    check_flag(s, FLAG_SRC_NONFINITE, SEWALD_EINVAL, "non-finite source position");
+    ensure_spread_order(s, i0, i1);
+    cudaStream_t st = s->ctx->stream;
+    const int64_t vol = (int64_t)s->g.n[0] * s->g.n[1] * s->g.n[2];
+    if (!s->shape.tiled) {
+        cuda_check(cudaMemsetAsync(grid, 0, sizeof(double) * s->C * vol, st), "grid zero");
+        launch_spread_atomic(s->g, s->w, s->x.as<double>() + 3 * i0, s->f.as<double>() + 3 * i0,
+                             s->stresslet ? s->nu.as<double>() + 3 * i0 : nullptr, s->stresslet,
+                             i1 - i0, grid, st);
+        ++s->ctx->launches;
+        return;
+    }
+    launch_spread_tiles(s->g, s->w, s->x.as<double>() + 3 * i0, s->f.as<double>() + 3 * i0,
+                        s->stresslet ? s->nu.as<double>() + 3 * i0 : nullptr, s->stresslet,
+                        s->sp_order.as<uint32_t>(), s->sp_off.as<int64_t>(), s->shape, grid, st);
+    s->ctx->launches += s->stresslet ? 3 : 1;
+}
+
+void session_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p) {
+    if (!(s->p.xi > 0.0)) throw EngineError(SEWALD_EINVAL, "xi must be positive");
+    const int64_t vol = (int64_t)s->g.n[0] * s->g.n[1] * s->g.n[2];
+    s->flow.ensure(sizeof(double) * 3 * vol);
+    if (s->p.d < 3) {
+        aft_solve(s, grid, precompute_0p);
+        return;
+    }
+    d3_prepare(s);
+    FourierPlanD3& P = *s->d3;
+    cudaStream_t st = s->ctx->stream;
+    cuDoubleComplex* spec = P.spec.as<cuDoubleComplex>();
+    cufft_check(cufftExecD2Z(P.fwd, const_cast<double*>(grid), spec), "exec D2Z");
+    const int64_t hvol = (int64_t)P.n[0] * P.n[1] * (P.n[2] / 2 + 1);
+    launch_scale_periodic(s->p.kind, P.n[0], P.n[1], P.n[2], s->p.xi, 1.0 / (double)vol, P.kt, spec,
+                          hvol, st);
+    ++s->ctx->launches;
+    cufft_check(cufftExecZ2D(P.inv, spec, s->flow.as<double>()), "exec Z2D");
+}
+
+void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, double* u) {
+    if (nparts < 1 || part < 0 || part >= nparts) throw EngineError(SEWALD_EINVAL, "bad target partition");
+    check_flag(s, FLAG_TGT_NONFINITE, SEWALD_EINVAL, "target coordinates must be finite");
+    cudaStream_t st = s->ctx->stream;
+    ensure_target_order(s);
+    const int64_t Nt = s->Nt;
+    const int64_t t0 = Nt * part / nparts, t1 = Nt * (part + 1) / nparts;
+    if (t1 <= t0) return;
+    const uint32_t* torder = target_order(s);
+    bool first = true;
+    if (parts & 2) {
+        if (!(s->p.xi > 0.0)) throw EngineError(SEWALD_EINVAL, "split parameter must be positive");
+        if (!(s->p.rc > 0.0)) throw EngineError(SEWALD_EINVAL, "cell list cutoff must be positive");
+        RealspaceArgs a{};
+        a.kind = s->p.kind;
+        a.xi = s->p.xi;
+        a.rc = s->p.rc;
+        a.skip_self = s->same ? 1 : 0;
+        launch_realspace(s->cg, a, s->packed.as<double>(), s->stresslet, s->c_off.as<int64_t>(),
+                         target_folded(s), torder + t0, t1 - t0, u, 0,
+                         s->pair_counter.as<unsigned long long>(), s->flags.as<int>() + FLAG_SINGULAR, st);
+        ++s->ctx->launches;
+        first = false;
+    }
+    if (parts & 1) {
+        const double h3 = s->p.h * s->p.h * s->p.h;
+        launch_gather(s->g, s->w, s->flow.as<double>(), target_positions(s), torder + t0, t1 - t0, h3,
+                      first ? 0 : 1, u, st);
+        ++s->ctx->launches;
+        first = false;
+    }
+    if (parts & 4 || (parts & 1)) {
+        ensure_sums(s);
+        EpilogueArgs e{};
+        e.kind = s->p.kind;
+        e.d = s->p.d;
+        e.same = (parts & 4) && s->same;
+        e.fourier = (parts & 1) ? 1 : 0;
+        e.self_coef = -4.0 * s->p.xi / 1.7724538509055160273;
+        e.zm_scale = (parts & 4) ? -8.0 * kPi / (s->p.L[0] * s->p.L[1] * s->p.L[2]) : 0.0;
+        // gauge_flow_correction (modified_kernels.cpp:272-281) with the
+        // optimal gauge constants (modified_kernels.cpp:52-63).
+        if (s->p.kind == SEWALD_STOKESLET && s->p.d <= 1) {
+            const double R = s->p.R;
+            if (s->p.d == 0) {
+                const double bB = -0.5 / R;
+                e.gauge[0] = e.gauge[1] = e.gauge[2] = 4.0 * bB;
+            } else {
+                const double ellH = R, ellB = R * std::sqrt(M_E);
+                const double c1 = std::log(ellH * M_E) * 4.0;
+                const double c23 = std::log(ellB) * 2.0;
+                const double inv = 1.0 / s->p.L[0];
+                e.gauge[0] = c1 * inv;
+                e.gauge[1] = c23 * inv;
+                e.gauge[2] = c23 * inv;
+            }
+        }
+        const int64_t n = t1 - t0;
+        epilogue_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+            e, s->f.as<double>(), target_positions(s), s->sums.as<double>(), torder, t0, t1, first ? 0 : 1, u);
+        ++s->ctx->launches;
+    }
+}
+
+}  // namespace sewald_b200
+
+
+// ===========================================================================
+// C-ABI (device part)
+// ===========================================================================
+
+using namespace sewald_b200;
+
+namespace {
+
+template <class F>
+int ctx_guard(sewald_gpu_ctx* ctx, F&& fn) {
+    try {
+        if (ctx) cudaSetDevice(ctx->device);
+        fn();
+        return SEWALD_OK;
+    } catch (const EngineError& e) {
+        if (ctx) ctx->err = e.what();
+        return e.code;
+    } catch (const std::invalid_argument& e) {
+        if (ctx) ctx->err = e.what();
+        return SEWALD_EINVAL;
+    } catch (const std::domain_error& e) {
+        if (ctx) ctx->err = e.what();
+        return SEWALD_EDOMAIN;
+    } catch (const std::exception& e) {
+        if (ctx) ctx->err = e.what();
+        return SEWALD_ERUNTIME;
+    }
+}
+
+sewald_gpu_session* cached_session(sewald_gpu_ctx* ctx, const sewald_params_c& p) {
+    if (ctx->cached && std::memcmp(&ctx->cached_params, &p, sizeof(p)) == 0) return ctx->cached.get();
+    ctx->cached.reset();
+    auto s = std::make_unique<sewald_gpu_session>();
+    session_init(s.get(), ctx, p);
+    ctx->cached = std::move(s);
+    ctx->cached_params = p;
+    return ctx->cached.get();
+}
+
+void host_pipeline(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* x, const double* f,
+                   const double* nu, int64_t N, const double* xt, int64_t Nt, int same, int use_table,
+                   int parts, double* u_out) {
+    if (!p) throw EngineError(SEWALD_EINVAL, "null parameters");
+    if (N < 0 || Nt < 0) throw EngineError(SEWALD_EINVAL, "negative sizes");
+    if (same && Nt != N && Nt != 0 && xt) throw EngineError(SEWALD_EINVAL, "starred evaluation needs one target per source");
+    sewald_gpu_session* s = cached_session(ctx, *p);
+    StageTimer tm(ctx);
+    const int64_t launches0 = ctx->launches;
+    tm.mark();
+    session_set_targets(s, xt, Nt, same != 0);
+    session_set_sources(s, x, f, nu, N);
+    if (!same) session_set_targets(s, xt, Nt, false);
+    tm.mark();  // 1: after H2D
+    const int64_t nt = s->Nt;
+    double* du = static_cast<double*>(ctx->hu.ensure(sizeof(double) * 3 * std::max<int64_t>(nt, 1)));
+    if (parts & 1) {
+        const int64_t vol = (int64_t)s->g.n[0] * s->g.n[1] * s->g.n[2];
+        double* grid = static_cast<double*>(s->grid.ensure(sizeof(double) * s->C * vol));
+        session_spread(s, 0, N, grid);
+        tm.mark();  // 2
+        session_solve(s, grid, use_table != 0);
+        tm.mark();  // 3
+    } else {
+        tm.mark();
+        tm.mark();
+    }
+    if (nt > 0) {
+        ensure_target_order(s);
+        if ((parts & 1) && s->p.d < 3) {
+            launch_stencil_bounds(s->g, s->p.P, target_positions(s), nt, s->flags.as<int>() + FLAG_GATHER_BOX,
+                                  ctx->stream);
+            check_flag(s, FLAG_GATHER_BOX, SEWALD_EINVAL,
+                       "point too close to the extended box boundary; free-direction padding is too small");
+        }
+        tm.mark();  // 4
+        session_evaluate(s, 0, 1, parts, du);
+        tm.mark();  // 5
+        cuda_check(cudaMemcpyAsync(u_out, du, sizeof(double) * 3 * nt, cudaMemcpyDefault, ctx->stream), "u copy");
+    } else {
+        tm.mark();
+        tm.mark();
+    }
+    tm.mark();  // 6
+    cuda_check(cudaStreamSynchronize(ctx->stream), "pipeline sync");
+    check_flag(s, FLAG_SINGULAR, SEWALD_EDOMAIN, "real-space kernel is singular at the origin");
+    sewald_timings_c& T = ctx->timings;
+    T = sewald_timings_c{};
+    T.h2d_ms = tm.ms(0, 1);
+    T.spread_ms = tm.ms(1, 2);
+    T.fft_fwd_ms = tm.ms(2, 3);
+    T.realspace_ms = tm.ms(4, 5);
+    T.d2h_ms = tm.ms(5, 6);
+    T.total_ms = tm.ms(0, 6);
+    T.kernel_launches = ctx->launches - launches0;
+    T.realspace_pairs = -1;
+}
+
+}  // namespace
+
+extern "C" {
+
+int sewald_gpu_create(int device, sewald_gpu_ctx** out) {
+    if (!out) return SEWALD_EINVAL;
+    *out = nullptr;
+    auto* ctx = new sewald_gpu_ctx();
+    ctx->device = device;
+    int rc = ctx_guard(ctx, [&] {
+        cuda_check(cudaSetDevice(device), "cudaSetDevice");
+        cuda_check(cudaStreamCreateWithFlags(&ctx->own_stream, cudaStreamNonBlocking), "stream");
+        ctx->stream = ctx->own_stream;
+    });
+    if (rc != SEWALD_OK) {
+        delete ctx;
+        return rc;
+    }
+    *out = ctx;
+    return SEWALD_OK;
+}
+
+void sewald_gpu_destroy(sewald_gpu_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    ctx->cached.reset();
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
+const char* sewald_gpu_last_error(const sewald_gpu_ctx* ctx) { return ctx ? ctx->err.c_str() : "null context"; }
+
+int sewald_gpu_set_stream(sewald_gpu_ctx* ctx, void* stream) {
+    if (!ctx) return SEWALD_EINVAL;
+    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    return SEWALD_OK;
+}
+
+int sewald_gpu_get_timings(const sewald_gpu_ctx* ctx, sewald_timings_c* out) {
+    if (!ctx || !out) return SEWALD_EINVAL;
+    *out = ctx->timings;
+    return SEWALD_OK;
+}
+
+int sewald_gpu_set_profiling(sewald_gpu_ctx* ctx, int enabled) {
+    if (!ctx) return SEWALD_EINVAL;
+    ctx->profiling = enabled != 0;
+    return SEWALD_OK;
+}
+
+int sewald_gpu_full_potential(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* x,
+                              const double* f, const double* nu, int64_t N, const double* xt,
+                              int64_t Nt, int same_as_sources, int precompute_0p, double* u_out) {
+    if (!ctx) return SEWALD_EINVAL;
+    return ctx_guard(ctx, [&] {
+        host_pipeline(ctx, p, x, f, nu, N, xt, Nt, same_as_sources, precompute_0p, 7, u_out);
+    });
+}
+
+int sewald_gpu_fourier_potential(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* x,
+                                 const double* f, const double* nu, int64_t N, const double* xt,
+                                 int64_t Nt, int same_as_sources, int precompute_0p, double* u_out) {
+    if (!ctx) return SEWALD_EINVAL;
+    return ctx_guard(ctx, [&] {
+        host_pipeline(ctx, p, x, f, nu, N, xt, Nt, same_as_sources, precompute_0p, 1, u_out);
+    });
+}
+
+int sewald_gpu_realspace_potential(sewald_gpu_ctx* ctx, int kind, int d, const double L[3],
+                                   const double* x, const double* f, const double* nu, int64_t N,
+                                   const double* xt, int64_t Nt, int same_as_sources, double xi,
+                                   double rc, int starred, double* u_out) {
+    if (!ctx) return SEWALD_EINVAL;
+    return ctx_guard(ctx, [&] {
+        if (!(xi > 0.0)) throw EngineError(SEWALD_EINVAL, "split parameter must be positive");
+        if (!(rc > 0.0)) throw EngineError(SEWALD_EINVAL, "cell list cutoff must be positive");
+        const bool skip_self = starred && same_as_sources;
+        if (skip_self && Nt != N) throw EngineError(SEWALD_EINVAL, "starred evaluation needs one target per source");
+        // A minimal parameter set: real space needs kind, d, cell, xi, rc.
+        sewald_params_c p{};
+        p.kind = kind;
+        p.d = d;
+        p.xi = xi;
+        p.rc = rc;
+        for (int a = 0; a < 3; ++a) {
+            p.L[a] = L[a];
+            p.M[a] = p.M_ext[a] = 8;
+            p.L_ext[a] = L[a];
+        }
+        p.h = L[0] / 8;
+        p.f_m = 4;
+        window_make(SEWALD_WIN_TG, 2, p.h, p);
+        // Unstarred sums over coincident points must see them as distinct
+        // targets (so r = 0 is reported), which the session does by
+        // treating targets as separate when skip_self is false.
+        const bool same = skip_self;
+        const double* tx = same ? x : (same_as_sources ? x : xt);
+        host_pipeline(ctx, &p, x, f, nu, N, tx, same ? N : Nt, same ? 1 : 0, 0, 2, u_out);
+    });
+}
+
+int sewald_gpu_spread(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* x,
+                      const double* f, const double* nu, int64_t N, double* grid_out) {
+    if (!ctx) return SEWALD_EINVAL;
+    return ctx_guard(ctx, [&] {
+        sewald_gpu_session* s = cached_session(ctx, *p);
+        session_set_sources(s, x, f, nu, N);
+        const int64_t vol = (int64_t)s->g.n[0] * s->g.n[1] * s->g.n[2];
+        double* grid = static_cast<double*>(s->grid.ensure(sizeof(double) * s->C * vol));
+        session_spread(s, 0, N, grid);
+        cuda_check(cudaMemcpyAsync(grid_out, grid, sizeof(double) * s->C * vol, cudaMemcpyDefault, ctx->stream),
+                   "grid copy");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "spread sync");
+    });
+}
+
+int sewald_gpu_gather(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* grid,
+                      const double* xt, int64_t Nt, double* u_out) {
+    if (!ctx) return SEWALD_EINVAL;
+    return ctx_guard(ctx, [&] {
+        sewald_gpu_session* s = cached_session(ctx, *p);
+        const int64_t vol = (int64_t)s->g.n[0] * s->g.n[1] * s->g.n[2];
+        double* flow = static_cast<double*>(s->flow.ensure(sizeof(double) * 3 * vol));
+        cuda_check(cudaMemcpyAsync(flow, grid, sizeof(double) * 3 * vol, cudaMemcpyDefault, ctx->stream), "grid in");
+        double* dx = static_cast<double*>(ctx->hxt.ensure(sizeof(double) * 3 * std::max<int64_t>(Nt, 1)));
+        double* du = static_cast<double*>(ctx->hu.ensure(sizeof(double) * 3 * std::max<int64_t>(Nt, 1)));
+        if (Nt > 0) {
+            cuda_check(cudaMemcpyAsync(dx, xt, sizeof(double) * 3 * Nt, cudaMemcpyDefault, ctx->stream), "xt in");
+            launch_stencil_bounds(s->g, s->p.P, dx, Nt, s->flags.as<int>() + FLAG_GATHER_BOX, ctx->stream);
+            check_flag(s, FLAG_GATHER_BOX, SEWALD_EINVAL,
+                       "point too close to the extended box boundary; free-direction padding is too small");
+            const double h3 = s->p.h * s->p.h * s->p.h;
+            launch_gather(s->g, s->w, flow, dx, nullptr, Nt, h3, 0, du, ctx->stream);
+            cuda_check(cudaMemcpyAsync(u_out, du, sizeof(double) * 3 * Nt, cudaMemcpyDefault, ctx->stream), "u out");
+        }
+        cuda_check(cudaStreamSynchronize(ctx->stream), "gather sync");
+    });
+}
+
+int sewald_gpu_session_create(sewald_gpu_ctx* ctx, const sewald_params_c* p, sewald_gpu_session** out) {
+    if (!ctx || !p || !out) return SEWALD_EINVAL;
+    *out = nullptr;
+    return ctx_guard(ctx, [&] {
+        auto s = std::make_unique<sewald_gpu_session>();
+        session_init(s.get(), ctx, *p);
+        *out = s.release();
+    });
+}
+
+void sewald_gpu_session_destroy(sewald_gpu_session* s) {
+    if (!s) return;
+    cudaSetDevice(s->ctx->device);
+    cudaStreamSynchronize(s->ctx->stream);
+    delete s;
+}
+
+int sewald_gpu_session_set_sources(sewald_gpu_session* s, const double* x, const double* f,
+                                   const double* nu, int64_t N) {
+    if (!s) return SEWALD_EINVAL;
+    return ctx_guard(s->ctx, [&] { session_set_sources(s, x, f, nu, N); });
+}
+
+int sewald_gpu_session_set_targets(sewald_gpu_session* s, const double* xt, int64_t Nt, int same) {
+    if (!s) return SEWALD_EINVAL;
+    return ctx_guard(s->ctx, [&] { session_set_targets(s, xt, Nt, same != 0); });
+}
+
+int64_t sewald_gpu_session_grid_size(const sewald_gpu_session* s) {
+    if (!s) return -1;
+    return (int64_t)s->C * s->g.n[0] * s->g.n[1] * s->g.n[2];
+}
+
+int sewald_gpu_session_spread(sewald_gpu_session* s, int64_t i0, int64_t i1, double* grid) {
+    if (!s) return SEWALD_EINVAL;
+    return ctx_guard(s->ctx, [&] {
+        double* g = grid;
+        if (!g) g = static_cast<double*>(s->grid.ensure(sizeof(double) * sewald_gpu_session_grid_size(s)));
+        session_spread(s, i0, i1, g);
+    });
+}
+
+int sewald_gpu_session_solve(sewald_gpu_session* s, const double* grid, int precompute_0p) {
+    if (!s) return SEWALD_EINVAL;
+    return ctx_guard(s->ctx, [&] { session_solve(s, grid ? grid : s->grid.as<double>(), precompute_0p != 0); });
+}
+
+int sewald_gpu_session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, double* u) {
+    if (!s) return SEWALD_EINVAL;
+    return ctx_guard(s->ctx, [&] { session_evaluate(s, part, nparts, parts, u); });
+}
+
+int64_t sewald_gpu_launch_count(const sewald_gpu_ctx* ctx) { return ctx ? ctx->launches : -1; }
+
+int64_t sewald_gpu_session_pair_count(sewald_gpu_session* s, int reset) {
+    if (!s) return -1;
+    unsigned long long h = 0;
+    int rc = ctx_guard(s->ctx, [&] {
+        cuda_check(cudaMemcpyAsync(&h, s->pair_counter.ptr, sizeof(h), cudaMemcpyDeviceToHost, s->ctx->stream),
+                   "pair count");
+        cuda_check(cudaStreamSynchronize(s->ctx->stream), "pair sync");
+        if (reset) cuda_check(cudaMemsetAsync(s->pair_counter.ptr, 0, sizeof(h), s->ctx->stream), "pair reset");
+    });
+    return rc == SEWALD_OK ? (int64_t)h : -1;
+}
+
+int sewald_gpu_session_run(sewald_gpu_session* s, int precompute_0p, double* u) {
+    if (!s) return SEWALD_EINVAL;
+    return ctx_guard(s->ctx, [&] {
+        double* g = static_cast<double*>(s->grid.ensure(sizeof(double) * sewald_gpu_session_grid_size(s)));
+        session_spread(s, 0, s->N, g);
+        session_solve(s, g, precompute_0p != 0);
+        session_evaluate(s, 0, 1, 7, u);
+    });
+}
+
+}  // extern "C"

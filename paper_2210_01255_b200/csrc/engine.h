@@ -1,0 +1,107 @@
+// Device context and resident session of the B200 Spectral Ewald engine.
+#pragma once
+
+#include "../../include/sewald_gpu.h"
+#include "device_common.cuh"
+#include "sg_kernels.h"
+
+#include <cufft.h>
+
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace sewald_b200 {
+
+// Error carrying a C-ABI status code.
+struct EngineError : std::runtime_error {
+    int code;
+    EngineError(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+void cuda_check(cudaError_t e, const char* what);
+void cufft_check(cufftResult r, const char* what);
+
+// Grow-only device allocation.
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    ~DevBuf();
+    void* ensure(size_t n);
+    template <class T> T* as() const { return static_cast<T*>(ptr); }
+};
+
+struct FourierPlanD3;   // cuFFT plans + k tables for the fully periodic path
+struct FourierPlanAFT;  // zero-padded / upsampled free-direction path (d < 3)
+struct AftDeleter {
+    void operator()(FourierPlanAFT* p) const;
+};
+
+}  // namespace sewald_b200
+
+struct sewald_gpu_ctx {
+    int device = 0;
+    cudaStream_t own_stream = nullptr;
+    cudaStream_t stream = nullptr;
+    std::string err;
+    bool profiling = false;
+    sewald_timings_c timings{};
+    int64_t launches = 0;
+    // host-buffer entry points reuse one session while the parameters match
+    std::unique_ptr<sewald_gpu_session> cached;
+    sewald_params_c cached_params{};
+    // staging for host-buffer entry points
+    sewald_b200::DevBuf hx, hf, hnu, hxt, hu;
+};
+
+struct sewald_gpu_session {
+    sewald_gpu_ctx* ctx = nullptr;
+    sewald_params_c p{};
+    sewald_b200::DevGrid g{};
+    sewald_b200::DevWindow w{};
+    int C = 3;
+    bool stresslet = false;
+
+    // sources (original order, device copies)
+    int64_t N = 0;
+    sewald_b200::DevBuf x, f, nu;
+    // spread bucketing for source range [sp_i0, sp_i1)
+    int64_t sp_i0 = -1, sp_i1 = -1;
+    sewald_b200::SpreadPlanShape shape{};
+    sewald_b200::DevBuf sp_keys, sp_keys2, sp_vals, sp_order, sp_off, cub_tmp;
+    // real-space cell list
+    sewald_b200::CellGrid cg{};
+    bool cells_ready = false;
+    sewald_b200::DevBuf s_folded, c_keys, c_keys2, c_vals, c_order, c_off, packed;
+    // targets
+    int64_t Nt = 0;
+    bool same = false;
+    sewald_b200::DevBuf xt, t_folded, t_keys, t_keys2, t_vals, t_order;
+    // grids
+    sewald_b200::DevBuf grid, flow;
+    // global sums: f (3), q.nu (1), x (q.nu) (3); partials
+    sewald_b200::DevBuf sums, partials, flags, pair_counter;
+    bool sums_ready = false;
+    std::unique_ptr<sewald_b200::FourierPlanD3> d3;
+    std::unique_ptr<sewald_b200::FourierPlanAFT, sewald_b200::AftDeleter> aft;
+};
+
+namespace sewald_b200 {
+
+DevGrid make_dev_grid(const sewald_params_c& p);
+DevWindow make_dev_window(const sewald_params_c& p);
+
+void session_init(sewald_gpu_session* s, sewald_gpu_ctx* ctx, const sewald_params_c& p);
+void session_set_sources(sewald_gpu_session* s, const double* x, const double* f, const double* nu,
+                         int64_t N);
+void session_set_targets(sewald_gpu_session* s, const double* xt, int64_t Nt, bool same);
+void session_spread(sewald_gpu_session* s, int64_t i0, int64_t i1, double* grid);
+void session_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p);
+void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, double* u);
+
+// Fourier solve for d < 3 (aft.cu): grid (C comps, real) -> s->flow (3 comps).
+void aft_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p);
+
+}  // namespace sewald_b200

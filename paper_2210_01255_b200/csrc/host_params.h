@@ -1,0 +1,58 @@
+// Host-side parameter layer of the B200 Spectral Ewald engine.
+//
+// Restates, operation for operation, the reference's host arithmetic so the
+// parameters the GPU path consumes are bit-identical to the reference's:
+//   select_parameters   /root/reference/proj/src/estimates.cpp:211-268
+//   build_grid          /root/reference/proj/src/grid.cpp:35-77
+//   WindowSpec::make    /root/reference/proj/src/window.cpp:76-86
+//   pkb_build           /root/reference/proj/src/window.cpp:112-138
+//   kb_eval / kb_hat    /root/reference/proj/src/window.cpp:88-110
+//   tg_eval / ug_hat    /root/reference/proj/src/window.cpp:152-162
+//   truncation_radius   /root/reference/proj/src/modified_kernels.cpp:65-72
+// Errors are thrown as the reference's std exception types; the C-ABI layer
+// maps them to status codes.
+#pragma once
+
+#include "../../include/sewald_gpu.h"
+
+#include <array>
+#include <vector>
+
+namespace sewald_b200 {
+
+constexpr double kPi = 3.14159265358979323846;
+
+double bessel_i0(double t);
+
+// Window shape functions on the host (tables, PKB fitting, tests).
+double kb_value(const sewald_params_c& p, double r);
+double kb_transform(const sewald_params_c& p, double k);
+double ug_transform(const sewald_params_c& p, double k);
+double window_value(const sewald_params_c& p, const std::vector<double>& pkb, double r);
+double window_transform(const sewald_params_c& p, double k);
+
+std::vector<double> pkb_coefficients(const sewald_params_c& p);
+
+void window_make(int kind, int P, double h, sewald_params_c& p);
+void grid_build(const std::array<double, 3>& L, int d, double h_target, int P, int kernel,
+                int f_m, sewald_params_c& p);
+double free_truncation_radius(const sewald_params_c& p);
+
+void select_parameters(int kernel, int d, const std::array<double, 3>& L, double Q, double xi,
+                       double tol, bool relative, int f_m, int window, bool pollution_fix,
+                       sewald_params_c& out, sewald_report_c* report);
+
+// Signed DFT mode of index m on an axis of n points (fourier.cpp:28-30).
+inline int signed_mode(int m, int n) { return m < (n + 1) / 2 ? m : m - n; }
+
+// Wavenumbers 2 pi m/(n h) in DFT order (fourier.cpp:64-69).
+std::vector<double> wavenumbers(int n, double h);
+// w_hat at each wavenumber; throws runtime_error where it vanishes (fourier.cpp:71-81).
+std::vector<double> window_hat_table(const sewald_params_c& p, const std::vector<double>& k);
+
+// Integer padded length s * m_ext (fourier.cpp:92-98).
+int padded_length(double s, int m_ext);
+
+void validate_window(const sewald_params_c& p);
+
+}  // namespace sewald_b200

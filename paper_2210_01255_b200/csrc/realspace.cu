@@ -1,0 +1,337 @@
+// Short-range (real-space) Ewald sum over a cell list, fp64.
+//
+// Reference: accumulate_rows  /root/reference/proj/src/realspace.cpp:30-93
+//            build_cell_list  /root/reference/proj/src/realspace.cpp:97-164
+//            realspace_kernel /root/reference/proj/src/kernels.cpp:71-116
+//            apply            /root/reference/proj/src/kernels.cpp:189-202
+//
+// B200 layout: sources folded into the cell and sorted by a fine cell grid
+// (cell width ~ rc/4, x fastest) and packed as 64/96-byte records. One CTA
+// takes 128 consecutive targets in the same cell order; their bounding box
+// selects the cell rows whose distance is below rc, and each row's x range is
+// trimmed to the ball. Every row piece is one contiguous source range, staged
+// through shared memory and read as warp broadcasts. Per chunk, each lane
+// first tests all staged sources and records accepted ones in a 128-bit
+// register mask, then evaluates the erfc/exp kernel only on accepted pairs,
+// so the expensive fp64 path runs with converged lanes.
+//
+// The accepted set is the reference's: r = (x_t - x_s) - shift computed in
+// the same order, |r|^2 formed without FMA contraction and compared with
+// rc*rc, and the self pair skipped only on the primary image.
+#include "device_common.cuh"
+#include "sg_kernels.h"
+#include "../../include/sewald_gpu.h"
+
+namespace sewald_b200 {
+
+namespace {
+
+constexpr int RS_THREADS = 128;
+constexpr int RS_CHUNK = 128;
+constexpr double kTwoOverSqrtPi = 1.1283791670955125739;  // 2/sqrt(pi)
+constexpr double kSqrtPi = 1.7724538509055160273;
+
+__device__ __forceinline__ int floor_div(int a, int b) {
+    int q = a / b;
+    if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
+    return q;
+}
+
+__device__ __forceinline__ int cell_of(const CellGrid& cg, int ax, double v) {
+    int c = (int)floor((v - cg.origin[ax]) / cg.w[ax]);
+    return c < 0 ? 0 : (c > cg.n[ax] - 1 ? cg.n[ax] - 1 : c);
+}
+
+__global__ void fold_key_kernel(CellGrid cg, const double* __restrict__ x, int64_t N,
+                                double* __restrict__ folded, uint32_t* __restrict__ keys,
+                                uint32_t* __restrict__ vals) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    double y[3];
+    for (int ax = 0; ax < 3; ++ax) {
+        double v = x[3 * i + ax];
+        if (ax < cg.d) {  // wrap_position (domain.cpp:64-71): fmod is exact
+            v = fmod(v, cg.L[ax]);
+            if (v < 0.0) v += cg.L[ax];
+        }
+        y[ax] = v;
+        folded[3 * i + ax] = v;
+    }
+    const int cx = cell_of(cg, 0, y[0]), cy = cell_of(cg, 1, y[1]), cz = cell_of(cg, 2, y[2]);
+    keys[i] = (uint32_t)((cz * cg.n[1] + cy) * cg.n[0] + cx);
+    vals[i] = (uint32_t)i;
+}
+
+__global__ void pack_kernel(const double* __restrict__ folded, const double* __restrict__ f,
+                            const double* __restrict__ nu, int stresslet,
+                            const uint32_t* __restrict__ order, int64_t N,
+                            double* __restrict__ packed) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= N) return;
+    const int64_t i = order[k];
+    const int S = stresslet ? 12 : 8;
+    double* o = packed + k * S;
+    o[0] = folded[3 * i];
+    o[1] = folded[3 * i + 1];
+    o[2] = folded[3 * i + 2];
+    o[3] = f[3 * i];
+    o[4] = f[3 * i + 1];
+    o[5] = f[3 * i + 2];
+    if (stresslet) {
+        o[6] = nu[3 * i];
+        o[7] = nu[3 * i + 1];
+        o[8] = nu[3 * i + 2];
+        o[9] = __longlong_as_double((long long)i);
+        o[10] = 0.0;
+        o[11] = 0.0;
+    } else {
+        o[6] = __longlong_as_double((long long)i);
+        o[7] = 0.0;
+    }
+}
+
+// Kernel-specific pair contribution (kernels.cpp:71-116 contracted with
+// apply, kernels.cpp:189-202).
+template <int KIND>
+__device__ __forceinline__ void pair_eval(double xi, double r0, double r1, double r2, double r2n,
+                                          const double* s, double& u0, double& u1, double& u2) {
+    const double rn = sqrt(r2n);
+    const double xr = xi * rn;
+    const double erfc_term = erfc(xr) / rn;
+    const double gauss = 2.0 * xi / kSqrtPi * exp(-xr * xr);
+    if (KIND == SEWALD_STOKESLET) {
+        const double c = erfc_term + gauss;
+        const double a = c - 2.0 * gauss;
+        const double b = c / r2n;
+        const double rf = r0 * s[0] + r1 * s[1] + r2 * s[2];
+        const double brf = b * rf;
+        u0 += a * s[0] + brf * r0;
+        u1 += a * s[1] + brf * r1;
+        u2 += a * s[2] + brf * r2;
+    } else if (KIND == SEWALD_ROTLET) {
+        const double c = (erfc_term + gauss) / r2n;
+        // (f x r)_j = eps_jlm f_l r_m
+        u0 += c * (s[1] * r2 - s[2] * r1);
+        u1 += c * (s[2] * r0 - s[0] * r2);
+        u2 += c * (s[0] * r1 - s[1] * r0);
+    } else {
+        const double c1 = -2.0 / (r2n * r2n) * (3.0 * erfc_term + (3.0 + 2.0 * xr * xr) * gauss);
+        const double c2 = 2.0 * xi * xi * gauss;
+        const double* q = s;
+        const double* v = s + 3;
+        const double rq = r0 * q[0] + r1 * q[1] + r2 * q[2];
+        const double rv = r0 * v[0] + r1 * v[1] + r2 * v[2];
+        const double qv = q[0] * v[0] + q[1] * v[1] + q[2] * v[2];
+        const double t = c1 * rq * rv + c2 * qv;
+        u0 += t * r0 + c2 * (q[0] * rv + v[0] * rq);
+        u1 += t * r1 + c2 * (q[1] * rv + v[1] * rq);
+        u2 += t * r2 + c2 * (q[2] * rv + v[2] * rq);
+    }
+}
+
+template <int KIND, int S>
+__global__ void __launch_bounds__(RS_THREADS)
+realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed,
+                 const int64_t* __restrict__ cell_off, const double* __restrict__ tfolded,
+                 const uint32_t* __restrict__ torder, int64_t Nt, double* __restrict__ u,
+                 int accumulate, unsigned long long* __restrict__ pair_count, int* __restrict__ err) {
+    __shared__ double src[RS_CHUNK * S];
+    __shared__ double red[2][3][RS_THREADS / 32];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t t = (int64_t)blockIdx.x * RS_THREADS + tid;
+    const bool valid = t < Nt;
+    double xt0 = 0, xt1 = 0, xt2 = 0;
+    int64_t tori = -1;
+    if (valid) {
+        tori = torder[t];
+        xt0 = tfolded[3 * tori];
+        xt1 = tfolded[3 * tori + 1];
+        xt2 = tfolded[3 * tori + 2];
+    }
+
+    // Bounding box of this CTA's targets.
+    double lo[3] = {valid ? xt0 : 1e300, valid ? xt1 : 1e300, valid ? xt2 : 1e300};
+    double hi[3] = {valid ? xt0 : -1e300, valid ? xt1 : -1e300, valid ? xt2 : -1e300};
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) {
+            lo[ax] = fmin(lo[ax], __shfl_xor_sync(0xffffffffu, lo[ax], s));
+            hi[ax] = fmax(hi[ax], __shfl_xor_sync(0xffffffffu, hi[ax], s));
+        }
+        if (lane == 0) {
+            red[0][ax][warp] = lo[ax];
+            red[1][ax][warp] = hi[ax];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        lo[ax] = red[0][ax][0];
+        hi[ax] = red[1][ax][0];
+        for (int w = 1; w < RS_THREADS / 32; ++w) {
+            lo[ax] = fmin(lo[ax], red[0][ax][w]);
+            hi[ax] = fmax(hi[ax], red[1][ax][w]);
+        }
+    }
+
+    const double rc2 = a.rc * a.rc;
+    const double rcm = a.rc * (1.0 + 1e-10) + 1e-12 * fmax(fmax(cg.L[0], cg.L[1]), cg.L[2]);
+    const double rcm2 = rcm * rcm;
+
+    int clo[3], chi[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        clo[ax] = (int)floor((lo[ax] - rcm - cg.origin[ax]) / cg.w[ax]);
+        chi[ax] = (int)floor((hi[ax] + rcm - cg.origin[ax]) / cg.w[ax]);
+        if (ax >= cg.d) {
+            clo[ax] = max(clo[ax], 0);
+            chi[ax] = min(chi[ax], cg.n[ax] - 1);
+        }
+    }
+
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    unsigned long long npairs = 0;
+
+    for (int cz = clo[2]; cz <= chi[2]; ++cz) {
+        const int sz = 2 < cg.d ? floor_div(cz, cg.n[2]) : 0;
+        const int jz = cz - sz * cg.n[2];
+        const double zlo = cg.origin[2] + cz * cg.w[2], zhi = zlo + cg.w[2];
+        const double dz = fmax(0.0, fmax(zlo - hi[2], lo[2] - zhi));
+        const double shz = (double)sz * cg.L[2];
+        for (int cy = clo[1]; cy <= chi[1]; ++cy) {
+            const int sy = 1 < cg.d ? floor_div(cy, cg.n[1]) : 0;
+            const int jy = cy - sy * cg.n[1];
+            const double ylo = cg.origin[1] + cy * cg.w[1], yhi = ylo + cg.w[1];
+            const double dy = fmax(0.0, fmax(ylo - hi[1], lo[1] - yhi));
+            const double lat2 = dy * dy + dz * dz;
+            if (lat2 >= rcm2) continue;
+            const double ext = sqrt(rcm2 - lat2);
+            int cxl = (int)floor((lo[0] - ext - cg.origin[0]) / cg.w[0]);
+            int cxh = (int)floor((hi[0] + ext - cg.origin[0]) / cg.w[0]);
+            cxl = max(cxl, clo[0]);
+            cxh = min(cxh, chi[0]);
+            if (cxl > cxh) continue;
+            const double shy = (double)sy * cg.L[1];
+            const int64_t rowbase = ((int64_t)jz * cg.n[1] + jy) * cg.n[0];
+            const int sxa = 0 < cg.d ? floor_div(cxl, cg.n[0]) : 0;
+            const int sxb = 0 < cg.d ? floor_div(cxh, cg.n[0]) : 0;
+            for (int sx = sxa; sx <= sxb; ++sx) {
+                const int jlo = max(cxl - sx * cg.n[0], 0);
+                const int jhi = min(cxh - sx * cg.n[0], cg.n[0] - 1);
+                const int64_t b0 = cell_off[rowbase + jlo], b1 = cell_off[rowbase + jhi + 1];
+                if (b0 >= b1) continue;
+                const double shx = (double)sx * cg.L[0];
+                const bool primary = (sx == 0) && (sy == 0) && (sz == 0);
+                for (int64_t base = b0; base < b1; base += RS_CHUNK) {
+                    const int cnt = (int)min((int64_t)RS_CHUNK, b1 - base);
+                    __syncthreads();
+                    {
+                        const double2* g2 = reinterpret_cast<const double2*>(packed + base * S);
+                        double2* s2 = reinterpret_cast<double2*>(src);
+                        for (int e = tid; e < cnt * (S / 2); e += RS_THREADS) s2[e] = __ldg(g2 + e);
+                    }
+                    __syncthreads();
+                    if (!valid) continue;
+                    uint32_t m[RS_CHUNK / 32];
+#pragma unroll
+                    for (int wd = 0; wd < RS_CHUNK / 32; ++wd) {
+                        uint32_t bits = 0u;
+                        const int kend = min(32, cnt - 32 * wd);
+                        for (int kk = 0; kk < kend; ++kk) {
+                            const double* q = src + (32 * wd + kk) * S;
+                            const double r0 = (xt0 - q[0]) - shx;
+                            const double r1 = (xt1 - q[1]) - shy;
+                            const double r2 = (xt2 - q[2]) - shz;
+                            const double n2 = __dadd_rn(
+                                __dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1)), __dmul_rn(r2, r2));
+                            bool acc = n2 < rc2;
+                            if (a.skip_self && primary &&
+                                __double_as_longlong(q[S == 8 ? 6 : 9]) == tori)
+                                acc = false;
+                            bits |= (acc ? 1u : 0u) << kk;
+                        }
+                        m[wd] = bits;
+                    }
+                    for (;;) {
+                        int k = -1;
+                        if (m[0]) { k = __ffs(m[0]) - 1; m[0] &= m[0] - 1; }
+                        else if (m[1]) { k = 32 + __ffs(m[1]) - 1; m[1] &= m[1] - 1; }
+                        else if (m[2]) { k = 64 + __ffs(m[2]) - 1; m[2] &= m[2] - 1; }
+                        else if (m[3]) { k = 96 + __ffs(m[3]) - 1; m[3] &= m[3] - 1; }
+                        if (k < 0) break;
+                        const double* q = src + k * S;
+                        const double r0 = (xt0 - q[0]) - shx;
+                        const double r1 = (xt1 - q[1]) - shy;
+                        const double r2 = (xt2 - q[2]) - shz;
+                        const double n2 = __dadd_rn(
+                            __dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1)), __dmul_rn(r2, r2));
+                        if (n2 == 0.0) {  // kernels.cpp:19-22: singular at the origin
+                            atomicExch(err, 1);
+                            continue;
+                        }
+                        pair_eval<KIND>(a.xi, r0, r1, r2, n2, q + 3, acc0, acc1, acc2);
+                        ++npairs;
+                    }
+                }
+            }
+        }
+    }
+
+    if (valid) {
+        if (accumulate) {
+            u[3 * tori] += acc0;
+            u[3 * tori + 1] += acc1;
+            u[3 * tori + 2] += acc2;
+        } else {
+            u[3 * tori] = acc0;
+            u[3 * tori + 1] = acc1;
+            u[3 * tori + 2] = acc2;
+        }
+    }
+    if (pair_count) {
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) npairs += __shfl_xor_sync(0xffffffffu, npairs, s);
+        if (lane == 0 && npairs) atomicAdd(pair_count, npairs);
+    }
+}
+
+}  // namespace
+
+void launch_fold_and_key(const CellGrid& cg, const double* x, int64_t N, double* folded,
+                         uint32_t* keys, uint32_t* vals, cudaStream_t st) {
+    if (N == 0) return;
+    fold_key_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(cg, x, N, folded, keys, vals);
+}
+
+void launch_pack_sources(const double* folded, const double* f, const double* nu, int stresslet,
+                         const uint32_t* order, int64_t N, double* packed, cudaStream_t st) {
+    if (N == 0) return;
+    pack_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(folded, f, nu, stresslet, order, N,
+                                                              packed);
+}
+
+void launch_realspace(const CellGrid& cg, const RealspaceArgs& a, const double* packed,
+                      int stresslet, const int64_t* cell_off, const double* tfolded,
+                      const uint32_t* torder, int64_t Nt, double* u, int accumulate,
+                      unsigned long long* pair_count, int* err, cudaStream_t st) {
+    if (Nt == 0) return;
+    const unsigned blocks = (unsigned)((Nt + RS_THREADS - 1) / RS_THREADS);
+    switch (a.kind) {
+        case SEWALD_STOKESLET:
+            realspace_kernel<SEWALD_STOKESLET, 8><<<blocks, RS_THREADS, 0, st>>>(
+                cg, a, packed, cell_off, tfolded, torder, Nt, u, accumulate, pair_count, err);
+            break;
+        case SEWALD_ROTLET:
+            realspace_kernel<SEWALD_ROTLET, 8><<<blocks, RS_THREADS, 0, st>>>(
+                cg, a, packed, cell_off, tfolded, torder, Nt, u, accumulate, pair_count, err);
+            break;
+        default:
+            realspace_kernel<SEWALD_STRESSLET, 12><<<blocks, RS_THREADS, 0, st>>>(
+                cg, a, packed, cell_off, tfolded, torder, Nt, u, accumulate, pair_count, err);
+            break;
+    }
+}
+
+}  // namespace sewald_b200

@@ -1,0 +1,74 @@
+// Launch wrappers for the device kernels (spread_gather.cu, realspace.cu,
+// kspace.cu). Host code includes this; the kernels themselves stay private
+// to their translation units.
+#pragma once
+
+#include "device_common.cuh"
+
+#include <cuComplex.h>
+
+namespace sewald_b200 {
+
+// ---- spread / gather (spread_gather.cu) ----------------------------------
+struct SpreadPlanShape {
+    int nb[3];     // buckets (= output tiles) per axis
+    bool tiled;    // false -> atomic fallback for tiny periodic grids
+};
+
+SpreadPlanShape spread_plan_shape(const DevGrid& g, int P);
+void launch_spread_bucket(const DevGrid& g, int P, const double* x, int64_t N,
+                          const SpreadPlanShape& s, uint32_t* keys, uint32_t* vals, int* bad,
+                          cudaStream_t st);
+void launch_bucket_offsets(const uint32_t* keys, int64_t N, int nb, int64_t* off, cudaStream_t st);
+void launch_spread_tiles(const DevGrid& g, const DevWindow& w, const double* x, const double* f,
+                         const double* nu, int stresslet, const uint32_t* order,
+                         const int64_t* off, const SpreadPlanShape& s, double* out,
+                         cudaStream_t st);
+void launch_spread_atomic(const DevGrid& g, const DevWindow& w, const double* x, const double* f,
+                          const double* nu, int stresslet, int64_t N, double* out,
+                          cudaStream_t st);
+void launch_gather(const DevGrid& g, const DevWindow& w, const double* grid, const double* xt,
+                   const uint32_t* order, int64_t Nt, double h3, int accumulate, double* u,
+                   cudaStream_t st);
+void launch_stencil_bounds(const DevGrid& g, int P, const double* x, int64_t N, int* bad,
+                           cudaStream_t st);
+
+// ---- real space (realspace.cu) -------------------------------------------
+struct CellGrid {
+    int d;
+    int n[3];
+    double w[3];        // cell widths
+    double origin[3];   // lower corner (0 on periodic axes)
+    double L[3];
+};
+
+struct RealspaceArgs {
+    int kind;           // SEWALD_STOKESLET / STRESSLET / ROTLET
+    double xi;
+    double rc;
+    int skip_self;      // starred && targets are the sources
+};
+
+void launch_fold_and_key(const CellGrid& cg, const double* x, int64_t N, double* folded,
+                         uint32_t* keys, uint32_t* vals, cudaStream_t st);
+// Packs sorted sources: pos(3) + strengths (3, or q(3)+nu(3)) + original index.
+void launch_pack_sources(const double* folded, const double* f, const double* nu, int stresslet,
+                         const uint32_t* order, int64_t N, double* packed, cudaStream_t st);
+void launch_realspace(const CellGrid& cg, const RealspaceArgs& a, const double* packed,
+                      int stresslet, const int64_t* cell_off, const double* tfolded,
+                      const uint32_t* torder, int64_t Nt, double* u, int accumulate,
+                      unsigned long long* pair_count, int* err, cudaStream_t st);
+
+// ---- k space (kspace.cu) ---------------------------------------------------
+struct KspaceTables {
+    const double* k[3];      // wavenumbers per axis (DFT order)
+    const double* what[3];   // window transforms per axis
+};
+
+// D=3 half spectrum: modes (i, j, m) with m in [0, n2/2]; in: C comps
+// (stride cstride complex), out: 3 comps written over comps 0..2.
+void launch_scale_periodic(int kind, int n0, int n1, int n2, double xi, double norm,
+                           const KspaceTables& t, cuDoubleComplex* data, int64_t cstride,
+                           cudaStream_t st);
+
+}  // namespace sewald_b200

@@ -1,0 +1,200 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the reference.
+
+Bar (BASELINE.json north_star): rms(u_gpu - u_ref) / rms(u_ref) <= 1e-12 on
+the full velocity, fp64. Fixtures in tests/golden were produced by the
+reference itself (oracle/make_golden.py); the live cases call the compiled
+reference (oracle/_ref) when it is present.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from conftest import load_golden, rel_rms
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+def params_from_bytes(S, raw):
+    c = S.api.sewald_params_c.from_buffer_copy(bytes(raw))
+    return S.EwaldParams.from_c(c)
+
+
+def system_from(S, g):
+    nu = g.get("nu")
+    return S.SourceSystem(S.Kernel(int(g["kind"])), S.Cell(tuple(g["L"])), int(g["d"]), g["x"], g["f"], nu)
+
+
+def targets_from(S, g, system):
+    if "xt" in g:
+        return S.TargetSet(g["xt"], False)
+    return S.TargetSet.from_sources(system)
+
+
+@pytest.mark.parametrize("name,tag", [
+    ("c1_stokeslet_d3", ""), ("c1_stokeslet_d3", "_xi10"), ("stresslet_d3", ""), ("rotlet_d3", ""),
+])
+def test_golden_full_d3(S, name, tag):
+    g = load_golden(name)
+    sysm = system_from(S, g)
+    tg = targets_from(S, g, sysm)
+    params = params_from_bytes(S, g["params" + tag])
+    # the product selects the identical parameter set
+    sel = S.select_parameters(sysm.kind, sysm.d, sysm.cell, float(g["Q"]), params.xi,
+                              S.ToleranceSpec(float(g["tol"])),
+                              S.SelectionOptions(4, S.WindowKind(int(g["window"])), True))
+    assert bytes(sel.params.to_c()) == bytes(params.to_c())
+    u = S.full_potential(sysm, tg, params)
+    uF = S.se_fourier_potential(sysm, tg, params)
+    uR = S.realspace_potential(sysm, tg, params.xi, params.rc, tg.same_as_sources)
+    assert rel_rms(uR, g["uR" + tag]) < TOL
+    assert rel_rms(uF, g["uF" + tag]) < TOL
+    assert rel_rms(u, g["u" + tag]) < TOL
+
+
+@pytest.mark.parametrize("name", ["stresslet_d2", "stokeslet_d2", "rotlet_d1_tg", "stokeslet_d1", "stokeslet_d0"])
+def test_golden_realspace_free_axes(S, name):
+    g = load_golden(name)
+    sysm = system_from(S, g)
+    tg = targets_from(S, g, sysm)
+    params = params_from_bytes(S, g["params"])
+    uR = S.realspace_potential(sysm, tg, params.xi, params.rc, tg.same_as_sources)
+    assert rel_rms(uR, g["uR"]) < TOL
+
+
+@pytest.mark.parametrize("name", ["spread_kb_d3", "spread_pkb_d2_stresslet", "spread_tg_d0"])
+def test_golden_spread_gather(S, name):
+    g = load_golden(name)
+    params = params_from_bytes(S, g["params"])
+    kind = params.kind
+    sysm = S.SourceSystem(kind, S.Cell(tuple(params.grid.L)), params.d, g["x"], g["f"], g.get("nu"))
+    grid = S.spread(sysm, params)
+    ref = g["grid"]
+    assert np.max(np.abs(grid - ref)) <= 1e-14 * np.max(np.abs(ref))
+    ug = S.gather(g["field"], params, S.TargetSet(g["xt"], False))
+    assert np.max(np.abs(ug - g["ug"])) <= 1e-13 * np.max(np.abs(g["ug"]))
+
+
+def test_smoke_entry():
+    import __graft_entry__
+    __graft_entry__.smoke()
+
+
+# ---------------------------------------------------------------------------
+# live comparisons against the compiled reference (skipped without oracle/_ref)
+# ---------------------------------------------------------------------------
+
+@pytest.mark.oracle
+@pytest.mark.parametrize("kind", [0, 1, 2])
+@pytest.mark.parametrize("window", [0, 1, 2])
+def test_live_d3_windows(S, ref, kind, window):
+    rng = np.random.default_rng(100 + 3 * kind + window)
+    N = 300
+    x = rng.random((N, 3))
+    f = rng.standard_normal((N, 3))
+    nu = rng.standard_normal((N, 3)) if kind == 1 else None
+    sysm = S.SourceSystem(S.Kernel(kind), S.Cell((1, 1, 1)), 3, x, f, nu)
+    sel = S.select_parameters(sysm.kind, 3, sysm.cell, S.source_quantity(sysm), 7.0, S.ToleranceSpec(1e-9),
+                              S.SelectionOptions(4, S.WindowKind(window), True))
+    rp = ref.params_from(sel.params.to_c())
+    xt = rng.random((77, 3)) * 1.3 - 0.15  # targets outside the primary cell too
+    for same in (True, False):
+        tg = S.TargetSet.from_sources(sysm) if same else S.TargetSet(xt, False)
+        u = S.full_potential(sysm, tg, sel.params)
+        ur = ref.full_potential(rp, x, f, nu, None if same else xt, same)
+        assert rel_rms(u, ur) < TOL, (kind, window, same)
+
+
+@pytest.mark.oracle
+@pytest.mark.parametrize("case", [
+    # (kind, d, L, n, rc, own_targets) — test_realspace.cpp:328-336 shapes
+    (0, 3, (1.0, 1.0, 1.0), 400, 0.2, True),
+    (1, 3, (1.0, 1.0, 1.0), 400, 0.2, True),
+    (2, 3, (1.0, 1.0, 1.0), 400, 0.2, True),
+    (0, 3, (1.0, 1.0, 1.0), 60, 1.4, True),
+    (1, 2, (1.0, 1.3, 0.8), 200, 0.35, False),
+    (2, 1, (1.0, 0.7, 0.7), 150, 0.3, True),
+    (0, 0, (1.0, 1.0, 1.0), 150, 0.45, False),
+    (0, 3, (1.0, 1.0, 1.0), 40, 2e-3, True),
+])
+def test_live_realspace_cases(S, ref, case):
+    kind, d, L, n, rc, own = case
+    rng = np.random.default_rng(57120848 + n)
+    x = np.empty((n, 3))
+    for ax in range(3):
+        x[:, ax] = (rng.random(n) if ax < d else rng.uniform(-0.4, 0.6, n)) * L[ax]
+    f = rng.uniform(-1, 1, (n, 3))
+    nu = rng.uniform(-1, 1, (n, 3)) if kind == 1 else None
+    sysm = S.SourceSystem(S.Kernel(kind), S.Cell(L), d, x, f, nu)
+    xt = rng.uniform(-0.6, 0.8, (40, 3)) * np.asarray(L)
+    tg = S.TargetSet.from_sources(sysm) if own else S.TargetSet(xt, False)
+    u = S.realspace_potential(sysm, tg, 3.0, rc, True)
+    ur = ref.realspace_potential(kind, d, L, x, f, nu, None if own else xt, own, 3.0, rc, True)
+    scale = max(np.max(np.abs(ur)), 1e-300)
+    assert np.max(np.abs(u - ur)) / scale <= 1e-13
+
+
+@pytest.mark.oracle
+@pytest.mark.parametrize("M", [20, 24, 44, 60])
+def test_live_d3_grid_sizes(S, ref, M):
+    """Grid sizes not multiple of the spread tile, KB window P=14 (test_fourier.cpp:468-505 grid)."""
+    rng = np.random.default_rng(M)
+    N = 200
+    x = rng.random((N, 3))
+    f = rng.standard_normal((N, 3))
+    p = S.EwaldParams(S.Kernel.stokeslet, 3, 6.0, 0.3)
+    p.grid = S.GridSpec(3, 1.0 / M, (M, M, M), (M, M, M), (1, 1, 1), (1, 1, 1), (0, 0, 0), 4)
+    p.window = S.WindowSpec.make(S.WindowKind.kb, 14, 1.0 / M)
+    sysm = S.SourceSystem(S.Kernel.stokeslet, S.Cell((1, 1, 1)), 3, x, f)
+    tg = S.TargetSet.from_sources(sysm)
+    uF = S.se_fourier_potential(sysm, tg, p)
+    ur = ref.fourier_potential(ref.params_from(p.to_c()), x, f)
+    assert rel_rms(uF, ur) < TOL
+
+
+# ---------------------------------------------------------------------------
+# error behaviour (the reference's exception types)
+# ---------------------------------------------------------------------------
+
+def test_errors(S):
+    sysm = S.SourceSystem(S.Kernel.stokeslet, S.Cell((1, 1, 1)), 3,
+                          np.random.default_rng(0).random((5, 3)), np.ones((5, 3)))
+    tg = S.TargetSet.from_sources(sysm)
+    with pytest.raises(S.DomainError):  # test_realspace.cpp:429-435
+        S.realspace_potential(sysm, tg, 3.0, 0.3, False)
+    S.realspace_potential(sysm, tg, 3.0, 0.3, True)
+    with pytest.raises(S.InvalidArgument):
+        S.realspace_potential(sysm, tg, 0.0, 0.3, True)
+    bad = S.TargetSet(np.array([[0.5, 0.5, 0.5], [np.nan, 0.0, 0.0]]), False)
+    with pytest.raises(S.InvalidArgument):
+        S.realspace_potential(sysm, bad, 1.0, 0.3, False)
+    # spread outside the extended box on a free axis (test_fourier.cpp:174-187)
+    h = 1 / 16
+    p = S.EwaldParams(S.Kernel.stokeslet, 0, 5.0, 0.3)
+    p.grid = S.GridSpec(0, h, (8, 8, 8), (16, 16, 16), (0.5, 0.5, 0.5), (1, 1, 1), (0.5, 0.5, 0.5), 4)
+    p.window = S.WindowSpec.make(S.WindowKind.kb, 10, h)
+    s0 = S.SourceSystem(S.Kernel.stokeslet, S.Cell((0.5, 0.5, 0.5)), 0, np.array([[0.49, 0.25, 0.25]]),
+                        np.array([[1.0, 0, 0]]))
+    with pytest.raises(S.InvalidArgument):
+        S.spread(s0, p)
+
+
+def test_zero_strengths_exact_zero(S):
+    rng = np.random.default_rng(5)
+    x = rng.random((50, 3))
+    sysm = S.SourceSystem(S.Kernel.stokeslet, S.Cell((1, 1, 1)), 3, x, np.zeros((50, 3)))
+    sel = S.select_parameters(S.Kernel.stokeslet, 3, sysm.cell, 1.0, 6.0)
+    u = S.full_potential(sysm, S.TargetSet.from_sources(sysm), sel.params)
+    assert np.all(u == 0.0)
+
+
+def test_empty_inputs(S):
+    sysm = S.SourceSystem(S.Kernel.stokeslet, S.Cell((1, 1, 1)), 3, np.zeros((0, 3)), np.zeros((0, 3)))
+    sel = S.select_parameters(S.Kernel.stokeslet, 3, sysm.cell, 1.0, 6.0)
+    u = S.full_potential(sysm, S.TargetSet.from_sources(sysm), sel.params)
+    assert u.shape == (0, 3)
+    xt = np.random.default_rng(1).random((10, 3))
+    u = S.full_potential(sysm, S.TargetSet(xt, False), sel.params)
+    assert np.all(u == 0.0)
