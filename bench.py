@@ -250,7 +250,10 @@ def run_ours(args, cfg):
     Nt = N if same else xt.shape[0]
 
     engine = S.Engine(local)
-    stream = torch.cuda.current_stream()
+    # A dedicated (non-default) torch stream shared with the engine, so CUDA
+    # events, NCCL collectives and the engine's kernels are stream-ordered.
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
     engine.set_stream(stream.cuda_stream)
     sess = S.Session(params, S.Cell(cfg.L), engine)
     dx = torch.from_numpy(x).to(dev)

@@ -534,6 +534,7 @@ void session_spread(sewald_gpu_session* s, int64_t i0, int64_t i1, double* grid)
                         s->stresslet ? s->nu.as<double>() + 3 * i0 : nullptr, s->stresslet,
                         s->sp_order.as<uint32_t>(), s->sp_off.as<int64_t>(), s->shape, grid, st);
     s->ctx->launches += s->stresslet ? 3 : 1;
+    cuda_check(cudaGetLastError(), "spread launch");
 }
 
 void session_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p) {
@@ -554,6 +555,7 @@ void session_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p
                           hvol, st);
     ++s->ctx->launches;
     cufft_check(cufftExecZ2D(P.inv, spec, s->flow.as<double>()), "exec Z2D");
+    cuda_check(cudaGetLastError(), "solve launch");
 }
 
 void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, double* u) {
@@ -618,6 +620,7 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
             e, s->f.as<double>(), target_positions(s), s->sums.as<double>(), torder, t0, t1, first ? 0 : 1, u);
         ++s->ctx->launches;
     }
+    cuda_check(cudaGetLastError(), "evaluate launch");
 }
 
 }  // namespace sewald_b200
