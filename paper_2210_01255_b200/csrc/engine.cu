@@ -310,6 +310,7 @@ void ensure_cells(sewald_gpu_session* s) {
     s->c_off.ensure(sizeof(int64_t) * (ncell + 1));
     const int S = s->stresslet ? 12 : 8;
     s->packed.ensure(sizeof(double) * S * std::max<int64_t>(N, 1));
+    s->packedf.ensure(sizeof(float4) * std::max<int64_t>(N, 1));
     launch_fold_and_key(s->cg, s->x.as<double>(), N, s->s_folded.as<double>(), s->c_keys.as<uint32_t>(),
                         s->c_vals.as<uint32_t>(), st);
     if (N > 0) {
@@ -319,7 +320,7 @@ void ensure_cells(sewald_gpu_session* s) {
     }
     launch_bucket_offsets(s->c_keys2.as<uint32_t>(), N, (int)ncell, s->c_off.as<int64_t>(), st);
     launch_pack_sources(s->s_folded.as<double>(), s->f.as<double>(), s->nu.as<double>(), s->stresslet,
-                        s->c_order.as<uint32_t>(), N, s->packed.as<double>(), st);
+                        s->c_order.as<uint32_t>(), N, s->packed.as<double>(), s->packedf.as<float4>(), st);
     s->ctx->launches += 2;
     s->cells_ready = true;
 }
@@ -576,7 +577,15 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
         a.xi = s->p.xi;
         a.rc = s->p.rc;
         a.skip_self = s->same ? 1 : 0;
-        launch_realspace(s->cg, a, s->packed.as<double>(), s->stresslet, s->c_off.as<int64_t>(),
+        // fp32 candidate bound: coordinates (targets folded or inside the
+        // free-axis span, +-shift) are O(ext); fp32 differences carry at
+        // most a few ulp(ext) error per axis, so pad rc by 2^-18 ext.
+        double ext = a.rc;
+        for (int ax = 0; ax < 3; ++ax)
+            ext = std::max(ext, std::fabs(s->cg.origin[ax]) + s->cg.n[ax] * s->cg.w[ax] + s->cg.L[ax] + 2.0 * a.rc);
+        const double rpad = a.rc + std::ldexp(ext, -18);
+        a.thresh_f = (float)(rpad * rpad * (1.0 + std::ldexp(1.0, -16)));
+        launch_realspace(s->cg, a, s->packed.as<double>(), s->packedf.as<float4>(), s->stresslet, s->c_off.as<int64_t>(),
                          target_folded(s), torder + t0, t1 - t0, u, 0,
                          s->pair_counter.as<unsigned long long>(), s->flags.as<int>() + FLAG_SINGULAR, st);
         ++s->ctx->launches;

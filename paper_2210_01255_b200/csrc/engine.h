@@ -74,7 +74,7 @@ struct sewald_gpu_session {
     // real-space cell list
     sewald_b200::CellGrid cg{};
     bool cells_ready = false;
-    sewald_b200::DevBuf s_folded, c_keys, c_keys2, c_vals, c_order, c_off, packed;
+    sewald_b200::DevBuf s_folded, c_keys, c_keys2, c_vals, c_order, c_off, packed, packedf;
     // targets
     int64_t Nt = 0;
     bool same = false;

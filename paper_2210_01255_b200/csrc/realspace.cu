@@ -21,6 +21,7 @@
 #include "device_common.cuh"
 #include "sg_kernels.h"
 #include "../../include/sewald_gpu.h"
+#include "screened_math.cuh"
 
 namespace sewald_b200 {
 
@@ -28,8 +29,6 @@ namespace {
 
 constexpr int RS_THREADS = 128;
 constexpr int RS_CHUNK = 128;
-constexpr double kTwoOverSqrtPi = 1.1283791670955125739;  // 2/sqrt(pi)
-constexpr double kSqrtPi = 1.7724538509055160273;
 
 __device__ __forceinline__ int floor_div(int a, int b) {
     int q = a / b;
@@ -65,58 +64,60 @@ __global__ void fold_key_kernel(CellGrid cg, const double* __restrict__ x, int64
 __global__ void pack_kernel(const double* __restrict__ folded, const double* __restrict__ f,
                             const double* __restrict__ nu, int stresslet,
                             const uint32_t* __restrict__ order, int64_t N,
-                            double* __restrict__ packed) {
+                            double* __restrict__ packed, float4* __restrict__ packedf) {
     const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (k >= N) return;
     const int64_t i = order[k];
     const int S = stresslet ? 12 : 8;
     double* o = packed + k * S;
-    o[0] = folded[3 * i];
-    o[1] = folded[3 * i + 1];
-    o[2] = folded[3 * i + 2];
-    o[3] = f[3 * i];
-    o[4] = f[3 * i + 1];
-    o[5] = f[3 * i + 2];
+    const double x0 = folded[3 * i], x1 = folded[3 * i + 1], x2 = folded[3 * i + 2];
+    o[0] = x0;
+    o[1] = x1;
+    o[2] = x2;
+    o[3] = __longlong_as_double((long long)i);
+    o[4] = f[3 * i];
+    o[5] = f[3 * i + 1];
+    o[6] = f[3 * i + 2];
     if (stresslet) {
-        o[6] = nu[3 * i];
-        o[7] = nu[3 * i + 1];
-        o[8] = nu[3 * i + 2];
-        o[9] = __longlong_as_double((long long)i);
+        o[7] = nu[3 * i];
+        o[8] = nu[3 * i + 1];
+        o[9] = nu[3 * i + 2];
         o[10] = 0.0;
         o[11] = 0.0;
     } else {
-        o[6] = __longlong_as_double((long long)i);
         o[7] = 0.0;
     }
+    packedf[k] = make_float4((float)x0, (float)x1, (float)x2, 0.0f);
 }
 
-// Kernel-specific pair contribution (kernels.cpp:71-116 contracted with
-// apply, kernels.cpp:189-202).
+// Pair contribution given the shared screened factors (kernels.cpp:71-116
+// contracted with apply, kernels.cpp:189-202). s points at the strength
+// block of the packed record: f (3) or q (3) followed by nu (3).
 template <int KIND>
-__device__ __forceinline__ void pair_eval(double xi, double r0, double r1, double r2, double r2n,
-                                          const double* s, double& u0, double& u1, double& u2) {
-    const double rn = sqrt(r2n);
-    const double xr = xi * rn;
-    const double erfc_term = erfc(xr) / rn;
-    const double gauss = 2.0 * xi / kSqrtPi * exp(-xr * xr);
+__device__ __forceinline__ void pair_accumulate(const Screened& sc, double xi2, double n2, double r0,
+                                                double r1, double r2, const double* s, double& u0,
+                                                double& u1, double& u2) {
     if (KIND == SEWALD_STOKESLET) {
-        const double c = erfc_term + gauss;
-        const double a = c - 2.0 * gauss;
-        const double b = c / r2n;
+        // m_jl = (d_jl + r_j r_l / r^2)(erfc/r + g) - 2 g d_jl
+        const double a = sc.Ey * (sc.R - sc.cx);
+        const double b = sc.Ey * (sc.iy * sc.iy) * (sc.R + sc.cx);
         const double rf = r0 * s[0] + r1 * s[1] + r2 * s[2];
         const double brf = b * rf;
-        u0 += a * s[0] + brf * r0;
-        u1 += a * s[1] + brf * r1;
-        u2 += a * s[2] + brf * r2;
+        u0 = fma(a, s[0], fma(brf, r0, u0));
+        u1 = fma(a, s[1], fma(brf, r1, u1));
+        u2 = fma(a, s[2], fma(brf, r2, u2));
     } else if (KIND == SEWALD_ROTLET) {
-        const double c = (erfc_term + gauss) / r2n;
-        // (f x r)_j = eps_jlm f_l r_m
-        u0 += c * (s[1] * r2 - s[2] * r1);
-        u1 += c * (s[2] * r0 - s[0] * r2);
-        u2 += c * (s[0] * r1 - s[1] * r0);
+        // m_jl = eps_jlm r_m (erfc/r + g) / r^2  ->  c (f x r)
+        const double c = sc.Ey * (sc.iy * sc.iy) * (sc.R + sc.cx);
+        u0 = fma(c, s[1] * r2 - s[2] * r1, u0);
+        u1 = fma(c, s[2] * r0 - s[0] * r2, u1);
+        u2 = fma(c, s[0] * r1 - s[1] * r0, u2);
     } else {
-        const double c1 = -2.0 / (r2n * r2n) * (3.0 * erfc_term + (3.0 + 2.0 * xr * xr) * gauss);
-        const double c2 = 2.0 * xi * xi * gauss;
+        // t_jlm = c1 r_j r_l r_m + c2 (d_jl r_m + d_mj r_l + d_lm r_j)
+        const double iy2 = sc.iy * sc.iy;
+        const double x2 = xi2 * n2;
+        const double c1 = -2.0 * sc.Ey * (iy2 * iy2) * (3.0 * sc.R + (3.0 + 2.0 * x2) * sc.cx);
+        const double c2 = 2.0 * xi2 * sc.Ey * sc.cx;
         const double* q = s;
         const double* v = s + 3;
         const double rq = r0 * q[0] + r1 * q[1] + r2 * q[2];
@@ -130,12 +131,15 @@ __device__ __forceinline__ void pair_eval(double xi, double r0, double r1, doubl
 }
 
 template <int KIND, int S>
-__global__ void __launch_bounds__(RS_THREADS)
+__global__ void __launch_bounds__(RS_THREADS, 4)
 realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed,
-                 const int64_t* __restrict__ cell_off, const double* __restrict__ tfolded,
-                 const uint32_t* __restrict__ torder, int64_t Nt, double* __restrict__ u,
-                 int accumulate, unsigned long long* __restrict__ pair_count, int* __restrict__ err) {
-    __shared__ double src[RS_CHUNK * S];
+                 const float4* __restrict__ packedf, const int64_t* __restrict__ cell_off,
+                 const double* __restrict__ tfolded, const uint32_t* __restrict__ torder, int64_t Nt,
+                 double* __restrict__ u, int accumulate, unsigned long long* __restrict__ pair_count,
+                 int* __restrict__ err) {
+    __shared__ __align__(16) double src[RS_CHUNK * S];
+    __shared__ float4 srcf[RS_CHUNK];
+    __shared__ uint8_t queue[RS_CHUNK][RS_THREADS];
     __shared__ double red[2][3][RS_THREADS / 32];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -177,6 +181,7 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
     }
 
     const double rc2 = a.rc * a.rc;
+    const double xi2 = a.xi * a.xi;
     const double rcm = a.rc * (1.0 + 1e-10) + 1e-12 * fmax(fmax(cg.L[0], cg.L[1]), cg.L[2]);
     const double rcm2 = rcm * rcm;
 
@@ -224,6 +229,8 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
                 if (b0 >= b1) continue;
                 const double shx = (double)sx * cg.L[0];
                 const bool primary = (sx == 0) && (sy == 0) && (sz == 0);
+                // fp32 image of this target relative to the row piece's shift
+                const float tf0 = (float)(xt0 - shx), tf1 = (float)(xt1 - shy), tf2 = (float)(xt2 - shz);
                 for (int64_t base = b0; base < b1; base += RS_CHUNK) {
                     const int cnt = (int)min((int64_t)RS_CHUNK, b1 - base);
                     __syncthreads();
@@ -231,47 +238,35 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
                         const double2* g2 = reinterpret_cast<const double2*>(packed + base * S);
                         double2* s2 = reinterpret_cast<double2*>(src);
                         for (int e = tid; e < cnt * (S / 2); e += RS_THREADS) s2[e] = __ldg(g2 + e);
+                        if (tid < cnt) srcf[tid] = __ldg(packedf + base + tid);
                     }
                     __syncthreads();
                     if (!valid) continue;
-                    uint32_t m[RS_CHUNK / 32];
-#pragma unroll
-                    for (int wd = 0; wd < RS_CHUNK / 32; ++wd) {
-                        uint32_t bits = 0u;
-                        const int kend = min(32, cnt - 32 * wd);
-                        for (int kk = 0; kk < kend; ++kk) {
-                            const double* q = src + (32 * wd + kk) * S;
-                            const double r0 = (xt0 - q[0]) - shx;
-                            const double r1 = (xt1 - q[1]) - shy;
-                            const double r2 = (xt2 - q[2]) - shz;
-                            const double n2 = __dadd_rn(
-                                __dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1)), __dmul_rn(r2, r2));
-                            bool acc = n2 < rc2;
-                            if (a.skip_self && primary &&
-                                __double_as_longlong(q[S == 8 ? 6 : 9]) == tori)
-                                acc = false;
-                            bits |= (acc ? 1u : 0u) << kk;
-                        }
-                        m[wd] = bits;
+                    // Pass 1 (fp32, conservative): queue candidate sources.
+                    int nq = 0;
+                    for (int k = 0; k < cnt; ++k) {
+                        const float4 q = srcf[k];
+                        const float d0 = tf0 - q.x, d1 = tf1 - q.y, d2 = tf2 - q.z;
+                        const float dd = fmaf(d2, d2, fmaf(d1, d1, d0 * d0));
+                        if (dd < a.thresh_f) queue[nq++][tid] = (uint8_t)k;
                     }
-                    for (;;) {
-                        int k = -1;
-                        if (m[0]) { k = __ffs(m[0]) - 1; m[0] &= m[0] - 1; }
-                        else if (m[1]) { k = 32 + __ffs(m[1]) - 1; m[1] &= m[1] - 1; }
-                        else if (m[2]) { k = 64 + __ffs(m[2]) - 1; m[2] &= m[2] - 1; }
-                        else if (m[3]) { k = 96 + __ffs(m[3]) - 1; m[3] &= m[3] - 1; }
-                        if (k < 0) break;
+                    // Pass 2 (fp64, exact reference test + kernel) on queued pairs.
+                    for (int j = 0; j < nq; ++j) {
+                        const int k = queue[j][tid];
                         const double* q = src + k * S;
                         const double r0 = (xt0 - q[0]) - shx;
                         const double r1 = (xt1 - q[1]) - shy;
                         const double r2 = (xt2 - q[2]) - shz;
-                        const double n2 = __dadd_rn(
-                            __dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1)), __dmul_rn(r2, r2));
-                        if (n2 == 0.0) {  // kernels.cpp:19-22: singular at the origin
-                            atomicExch(err, 1);
+                        const double n2 = __dadd_rn(__dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1)),
+                                                    __dmul_rn(r2, r2));
+                        if (!(n2 < rc2)) continue;
+                        if (n2 == 0.0) {  // self pair (skipped) or coincident points (kernels.cpp:19-22)
+                            if (!(a.skip_self && primary && __double_as_longlong(q[3]) == tori))
+                                atomicExch(err, 1);
                             continue;
                         }
-                        pair_eval<KIND>(a.xi, r0, r1, r2, n2, q + 3, acc0, acc1, acc2);
+                        const Screened sc = screened(n2, a.xi, xi2);
+                        pair_accumulate<KIND>(sc, xi2, n2, r0, r1, r2, q + 4, acc0, acc1, acc2);
                         ++npairs;
                     }
                 }
@@ -306,14 +301,15 @@ void launch_fold_and_key(const CellGrid& cg, const double* x, int64_t N, double*
 }
 
 void launch_pack_sources(const double* folded, const double* f, const double* nu, int stresslet,
-                         const uint32_t* order, int64_t N, double* packed, cudaStream_t st) {
+                         const uint32_t* order, int64_t N, double* packed, float4* packedf,
+                         cudaStream_t st) {
     if (N == 0) return;
     pack_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(folded, f, nu, stresslet, order, N,
-                                                              packed);
+                                                              packed, packedf);
 }
 
 void launch_realspace(const CellGrid& cg, const RealspaceArgs& a, const double* packed,
-                      int stresslet, const int64_t* cell_off, const double* tfolded,
+                      const float4* packedf, int stresslet, const int64_t* cell_off, const double* tfolded,
                       const uint32_t* torder, int64_t Nt, double* u, int accumulate,
                       unsigned long long* pair_count, int* err, cudaStream_t st) {
     if (Nt == 0) return;
@@ -321,15 +317,15 @@ void launch_realspace(const CellGrid& cg, const RealspaceArgs& a, const double* 
     switch (a.kind) {
         case SEWALD_STOKESLET:
             realspace_kernel<SEWALD_STOKESLET, 8><<<blocks, RS_THREADS, 0, st>>>(
-                cg, a, packed, cell_off, tfolded, torder, Nt, u, accumulate, pair_count, err);
+                cg, a, packed, packedf, cell_off, tfolded, torder, Nt, u, accumulate, pair_count, err);
             break;
         case SEWALD_ROTLET:
             realspace_kernel<SEWALD_ROTLET, 8><<<blocks, RS_THREADS, 0, st>>>(
-                cg, a, packed, cell_off, tfolded, torder, Nt, u, accumulate, pair_count, err);
+                cg, a, packed, packedf, cell_off, tfolded, torder, Nt, u, accumulate, pair_count, err);
             break;
         default:
             realspace_kernel<SEWALD_STRESSLET, 12><<<blocks, RS_THREADS, 0, st>>>(
-                cg, a, packed, cell_off, tfolded, torder, Nt, u, accumulate, pair_count, err);
+                cg, a, packed, packedf, cell_off, tfolded, torder, Nt, u, accumulate, pair_count, err);
             break;
     }
 }

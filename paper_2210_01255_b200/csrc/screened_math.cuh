@@ -1,0 +1,107 @@
+// fp64 building blocks of the real-space (Hasimoto / Ewald screened) kernels,
+// written for the B200 fp64 pipe instead of the general libdevice routines:
+//
+//   erfc(x) / r  and  (2 xi / sqrt(pi)) e^{-x^2},  x = xi r
+//
+// both share E = e^{-x^2}: erfc(x) = E * erfcx(x), and erfcx is smooth on
+// [0, inf) so one branch-free rational P9/Q9 (tools/fit_erfcx.py, max rel.
+// error 7e-16 on [0,10]) covers every pair; beyond x = 10 the product with
+// E (< 4e-44) is negligible. exp uses a Cody-Waite reduction and a degree-13
+// polynomial; 1/r and 1/Q start from the MUFU approximations and take Newton
+// steps. Together ~60 fp64 instructions per pair instead of ~600 for
+// erfc() + exp() + sqrt() + two divisions from libdevice.
+//
+// Reference formulas: /root/reference/proj/src/kernels.cpp:71-116.
+#pragma once
+
+#include "erfcx_coeffs.h"
+
+namespace sewald_b200 {
+
+constexpr double kTwoOverSqrtPiD = 1.12837916709551257390;  // 2 / sqrt(pi)
+
+__device__ __forceinline__ double rcp_approx(double a) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+    return r;
+}
+
+__device__ __forceinline__ double rsqrt_approx(double a) {
+    double r;
+    asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(a));
+    return r;
+}
+
+// 1/sqrt(a), a > 0 normal: MUFU seed + two Newton steps (~1 ulp).
+__device__ __forceinline__ double rsqrt_nr(double a) {
+    double y = rsqrt_approx(a);
+    double e = fma(-a * y, y, 1.0);
+    y = fma(0.5 * y, e, y);
+    e = fma(-a * y, y, 1.0);
+    return fma(0.5 * y, e, y);
+}
+
+// e^{-y} for y >= 0 (clamped at 708 where the result is < 1e-307).
+__device__ __forceinline__ double exp_neg(double y) {
+    y = fmin(y, 708.0);
+    const double shifter = 6755399441055744.0;  // 1.5 * 2^52
+    const double t = fma(-y, 1.4426950408889634074, shifter);
+    const int n = __double2loint(t);
+    const double dn = t - shifter;
+    double f = fma(dn, -6.93147180559945286227e-01, -y);
+    f = fma(dn, -2.31904681384629955842e-17, f);
+    double p = 1.6059043836821614599e-10;  // 1/13!
+    p = fma(p, f, 2.0876756987868098979e-09);
+    p = fma(p, f, 2.5052108385441718775e-08);
+    p = fma(p, f, 2.7557319223985890653e-07);
+    p = fma(p, f, 2.7557319223985890653e-06);
+    p = fma(p, f, 2.4801587301587301587e-05);
+    p = fma(p, f, 1.9841269841269841270e-04);
+    p = fma(p, f, 1.3888888888888888889e-03);
+    p = fma(p, f, 8.3333333333333333333e-03);
+    p = fma(p, f, 4.1666666666666666667e-02);
+    p = fma(p, f, 1.6666666666666666667e-01);
+    p = fma(p, f, 0.5);
+    p = fma(p, f, 1.0);
+    p = fma(p, f, 1.0);
+    return p * __hiloint2double((n + 1023) << 20, 0);
+}
+
+// erfcx(x) = e^{x^2} erfc(x) for x >= 0 (rational P9/Q9).
+__device__ __forceinline__ double erfcx_rat(double x) {
+    constexpr double P[10] = SEWALD_ERFCX_P;
+    constexpr double Q[10] = SEWALD_ERFCX_Q;
+    double p = P[9], q = Q[9];
+#pragma unroll
+    for (int i = 8; i >= 0; --i) {
+        p = fma(p, x, P[i]);
+        q = fma(q, x, Q[i]);
+    }
+    double y = rcp_approx(q);
+    y = fma(y, fma(-q, y, 1.0), y);
+    const double r = p * y;
+    return fma(y, fma(-q, r, p), r);
+}
+
+// Shared screened factors for one pair at squared distance n2:
+//   iy   = 1/r
+//   Ey   = e^{-x^2} / r
+//   R    = erfcx(x), cx = (2/sqrt(pi)) x
+// so that erfc(x)/r = Ey R and the Gaussian term g = (2 xi/sqrt(pi)) e^{-x^2} = Ey cx.
+struct Screened {
+    double iy, Ey, R, cx, E;
+};
+
+__device__ __forceinline__ Screened screened(double n2, double xi, double xi2) {
+    Screened s;
+    s.iy = rsqrt_nr(n2);
+    const double r = n2 * s.iy;
+    const double x = xi * r;
+    s.E = exp_neg(xi2 * n2);
+    s.Ey = s.E * s.iy;
+    s.R = erfcx_rat(x);
+    s.cx = kTwoOverSqrtPiD * x;
+    return s;
+}
+
+}  // namespace sewald_b200

@@ -47,15 +47,18 @@ struct RealspaceArgs {
     double xi;
     double rc;
     int skip_self;      // starred && targets are the sources
+    float thresh_f;     // conservative fp32 bound on rc^2 for the candidate pass
 };
 
 void launch_fold_and_key(const CellGrid& cg, const double* x, int64_t N, double* folded,
                          uint32_t* keys, uint32_t* vals, cudaStream_t st);
-// Packs sorted sources: pos(3) + strengths (3, or q(3)+nu(3)) + original index.
+// Packs sorted sources: pos(3) + original index + strengths (3, or q(3)+nu(3)),
+// plus an fp32 position copy for the candidate pass.
 void launch_pack_sources(const double* folded, const double* f, const double* nu, int stresslet,
-                         const uint32_t* order, int64_t N, double* packed, cudaStream_t st);
+                         const uint32_t* order, int64_t N, double* packed, float4* packedf,
+                         cudaStream_t st);
 void launch_realspace(const CellGrid& cg, const RealspaceArgs& a, const double* packed,
-                      int stresslet, const int64_t* cell_off, const double* tfolded,
+                      const float4* packedf, int stresslet, const int64_t* cell_off, const double* tfolded,
                       const uint32_t* torder, int64_t Nt, double* u, int accumulate,
                       unsigned long long* pair_count, int* err, cudaStream_t st);
 
