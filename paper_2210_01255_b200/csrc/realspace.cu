@@ -28,7 +28,8 @@ namespace sewald_b200 {
 namespace {
 
 constexpr int RS_THREADS = 128;
-constexpr int RS_CHUNK = 128;
+constexpr int RS_WARPS = 4;
+constexpr int WCHUNK = 64;
 
 __device__ __forceinline__ int floor_div(int a, int b) {
     int q = a / b;
@@ -130,6 +131,9 @@ __device__ __forceinline__ void pair_accumulate(const Screened& sc, double xi2, 
     }
 }
 
+// One WARP = one independent work unit: 32 consecutive targets in cell
+// order (spatially compact), their bounding box, the cell rows within rc of
+// it, and a private shared-memory staging area. No block-wide barriers.
 template <int KIND, int S>
 __global__ void __launch_bounds__(RS_THREADS, 4)
 realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed,
@@ -137,13 +141,17 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
                  const double* __restrict__ tfolded, const uint32_t* __restrict__ torder, int64_t Nt,
                  double* __restrict__ u, int accumulate, unsigned long long* __restrict__ pair_count,
                  int* __restrict__ err) {
-    __shared__ __align__(16) double src[RS_CHUNK * S];
-    __shared__ float4 srcf[RS_CHUNK];
-    __shared__ uint8_t queue[RS_CHUNK][RS_THREADS];
-    __shared__ double red[2][3][RS_THREADS / 32];
+    __shared__ __align__(16) double src_all[RS_WARPS][WCHUNK * S];
+    __shared__ float4 srcf_all[RS_WARPS][WCHUNK];
+    __shared__ uint8_t queue_all[RS_WARPS][WCHUNK][32];
 
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t t = (int64_t)blockIdx.x * RS_THREADS + tid;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    double* src = src_all[warp];
+    float4* srcf = srcf_all[warp];
+    uint8_t(*queue)[32] = queue_all[warp];
+
+    const int64_t t = ((int64_t)blockIdx.x * RS_WARPS + warp) * 32 + lane;
+    if (((int64_t)blockIdx.x * RS_WARPS + warp) * 32 >= Nt) return;  // whole warp idle
     const bool valid = t < Nt;
     double xt0 = 0, xt1 = 0, xt2 = 0;
     int64_t tori = -1;
@@ -154,7 +162,7 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
         xt2 = tfolded[3 * tori + 2];
     }
 
-    // Bounding box of this CTA's targets.
+    // Bounding box of this warp's targets.
     double lo[3] = {valid ? xt0 : 1e300, valid ? xt1 : 1e300, valid ? xt2 : 1e300};
     double hi[3] = {valid ? xt0 : -1e300, valid ? xt1 : -1e300, valid ? xt2 : -1e300};
 #pragma unroll
@@ -163,20 +171,6 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
         for (int s = 16; s > 0; s >>= 1) {
             lo[ax] = fmin(lo[ax], __shfl_xor_sync(0xffffffffu, lo[ax], s));
             hi[ax] = fmax(hi[ax], __shfl_xor_sync(0xffffffffu, hi[ax], s));
-        }
-        if (lane == 0) {
-            red[0][ax][warp] = lo[ax];
-            red[1][ax][warp] = hi[ax];
-        }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int ax = 0; ax < 3; ++ax) {
-        lo[ax] = red[0][ax][0];
-        hi[ax] = red[1][ax][0];
-        for (int w = 1; w < RS_THREADS / 32; ++w) {
-            lo[ax] = fmin(lo[ax], red[0][ax][w]);
-            hi[ax] = fmax(hi[ax], red[1][ax][w]);
         }
     }
 
@@ -231,16 +225,16 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
                 const bool primary = (sx == 0) && (sy == 0) && (sz == 0);
                 // fp32 image of this target relative to the row piece's shift
                 const float tf0 = (float)(xt0 - shx), tf1 = (float)(xt1 - shy), tf2 = (float)(xt2 - shz);
-                for (int64_t base = b0; base < b1; base += RS_CHUNK) {
-                    const int cnt = (int)min((int64_t)RS_CHUNK, b1 - base);
-                    __syncthreads();
+                for (int64_t base = b0; base < b1; base += WCHUNK) {
+                    const int cnt = (int)min((int64_t)WCHUNK, b1 - base);
+                    __syncwarp();
                     {
                         const double2* g2 = reinterpret_cast<const double2*>(packed + base * S);
                         double2* s2 = reinterpret_cast<double2*>(src);
-                        for (int e = tid; e < cnt * (S / 2); e += RS_THREADS) s2[e] = __ldg(g2 + e);
-                        if (tid < cnt) srcf[tid] = __ldg(packedf + base + tid);
+                        for (int e = lane; e < cnt * (S / 2); e += 32) s2[e] = __ldg(g2 + e);
+                        for (int e = lane; e < cnt; e += 32) srcf[e] = __ldg(packedf + base + e);
                     }
-                    __syncthreads();
+                    __syncwarp();
                     if (!valid) continue;
                     // Pass 1 (fp32, conservative): queue candidate sources.
                     int nq = 0;
@@ -248,11 +242,11 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
                         const float4 q = srcf[k];
                         const float d0 = tf0 - q.x, d1 = tf1 - q.y, d2 = tf2 - q.z;
                         const float dd = fmaf(d2, d2, fmaf(d1, d1, d0 * d0));
-                        if (dd < a.thresh_f) queue[nq++][tid] = (uint8_t)k;
+                        if (dd < a.thresh_f) queue[nq++][lane] = (uint8_t)k;
                     }
                     // Pass 2 (fp64, exact reference test + kernel) on queued pairs.
                     for (int j = 0; j < nq; ++j) {
-                        const int k = queue[j][tid];
+                        const int k = queue[j][lane];
                         const double* q = src + k * S;
                         const double r0 = (xt0 - q[0]) - shx;
                         const double r1 = (xt1 - q[1]) - shy;

@@ -18,7 +18,19 @@
 
 namespace sewald_b200 {
 
-constexpr double kTwoOverSqrtPiD = 1.12837916709551257390;  // 2 / sqrt(pi)
+// Polynomial coefficients live in the constant bank so DFMA takes them as
+// c[][] operands (as literals they are rebuilt with UMOVs on every use).
+__constant__ double c_erfcx_p[10] = SEWALD_ERFCX_P;
+__constant__ double c_erfcx_q[10] = SEWALD_ERFCX_Q;
+__constant__ double c_exp_poly[14] = {
+    1.0, 1.0, 0.5, 1.6666666666666666667e-01, 4.1666666666666666667e-02, 8.3333333333333333333e-03,
+    1.3888888888888888889e-03, 1.9841269841269841270e-04, 2.4801587301587301587e-05,
+    2.7557319223985890653e-06, 2.7557319223985890653e-07, 2.5052108385441718775e-08,
+    2.0876756987868098979e-09, 1.6059043836821614599e-10};
+
+// exp reduction constants: shifter (1.5 * 2^52), log2(e), -ln2 hi/lo, 2/sqrt(pi)
+__constant__ double c_misc[5] = {6755399441055744.0, 1.4426950408889634074, -6.93147180559945286227e-01,
+                                 -2.31904681384629955842e-17, 1.12837916709551257390};
 
 __device__ __forceinline__ double rcp_approx(double a) {
     double r;
@@ -44,38 +56,25 @@ __device__ __forceinline__ double rsqrt_nr(double a) {
 // e^{-y} for y >= 0 (clamped at 708 where the result is < 1e-307).
 __device__ __forceinline__ double exp_neg(double y) {
     y = fmin(y, 708.0);
-    const double shifter = 6755399441055744.0;  // 1.5 * 2^52
-    const double t = fma(-y, 1.4426950408889634074, shifter);
+    const double shifter = c_misc[0];
+    const double t = fma(-y, c_misc[1], shifter);
     const int n = __double2loint(t);
     const double dn = t - shifter;
-    double f = fma(dn, -6.93147180559945286227e-01, -y);
-    f = fma(dn, -2.31904681384629955842e-17, f);
-    double p = 1.6059043836821614599e-10;  // 1/13!
-    p = fma(p, f, 2.0876756987868098979e-09);
-    p = fma(p, f, 2.5052108385441718775e-08);
-    p = fma(p, f, 2.7557319223985890653e-07);
-    p = fma(p, f, 2.7557319223985890653e-06);
-    p = fma(p, f, 2.4801587301587301587e-05);
-    p = fma(p, f, 1.9841269841269841270e-04);
-    p = fma(p, f, 1.3888888888888888889e-03);
-    p = fma(p, f, 8.3333333333333333333e-03);
-    p = fma(p, f, 4.1666666666666666667e-02);
-    p = fma(p, f, 1.6666666666666666667e-01);
-    p = fma(p, f, 0.5);
-    p = fma(p, f, 1.0);
-    p = fma(p, f, 1.0);
+    double f = fma(dn, c_misc[2], -y);
+    f = fma(dn, c_misc[3], f);
+    double p = c_exp_poly[13];
+#pragma unroll
+    for (int i = 12; i >= 0; --i) p = fma(p, f, c_exp_poly[i]);
     return p * __hiloint2double((n + 1023) << 20, 0);
 }
 
 // erfcx(x) = e^{x^2} erfc(x) for x >= 0 (rational P9/Q9).
 __device__ __forceinline__ double erfcx_rat(double x) {
-    constexpr double P[10] = SEWALD_ERFCX_P;
-    constexpr double Q[10] = SEWALD_ERFCX_Q;
-    double p = P[9], q = Q[9];
+    double p = c_erfcx_p[9], q = c_erfcx_q[9];
 #pragma unroll
     for (int i = 8; i >= 0; --i) {
-        p = fma(p, x, P[i]);
-        q = fma(q, x, Q[i]);
+        p = fma(p, x, c_erfcx_p[i]);
+        q = fma(q, x, c_erfcx_q[i]);
     }
     double y = rcp_approx(q);
     y = fma(y, fma(-q, y, 1.0), y);
@@ -100,7 +99,7 @@ __device__ __forceinline__ Screened screened(double n2, double xi, double xi2) {
     s.E = exp_neg(xi2 * n2);
     s.Ey = s.E * s.iy;
     s.R = erfcx_rat(x);
-    s.cx = kTwoOverSqrtPiD * x;
+    s.cx = c_misc[4] * x;
     return s;
 }
 
