@@ -198,3 +198,88 @@ def test_empty_inputs(S):
     xt = np.random.default_rng(1).random((10, 3))
     u = S.full_potential(sysm, S.TargetSet(xt, False), sel.params)
     assert np.all(u == 0.0)
+
+
+# ---------------------------------------------------------------------------
+# free directions (d = 2, 1, 0): mode classes, truncated kernels, D=0 table
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("name", ["stresslet_d2", "stokeslet_d2", "rotlet_d1_tg", "stokeslet_d1", "stokeslet_d0"])
+def test_golden_full_free_axes(S, name):
+    g = load_golden(name)
+    sysm = system_from(S, g)
+    tg = targets_from(S, g, sysm)
+    params = params_from_bytes(S, g["params"])
+    uF = S.se_fourier_potential(sysm, tg, params)
+    assert rel_rms(uF, g["uF"]) < TOL
+    if "uF_direct" in g:
+        uFd = S.se_fourier_potential(sysm, tg, params, S.SePipelineOptions(precompute_0p=False))
+        assert rel_rms(uFd, g["uF_direct"]) < TOL
+    u = S.full_potential(sysm, tg, params)
+    assert rel_rms(u, g["u"]) < TOL
+
+
+def _test_grid(S, d, h, M, Mext):
+    L = tuple(h * m for m in M)
+    Le = tuple(h * m for m in Mext)
+    return S.GridSpec(d, h, M, Mext, L, Le, tuple(a - b for a, b in zip(Le, L)), 4)
+
+
+@pytest.mark.oracle
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_live_reference_test_grids(S, ref, kind):
+    """The reference's own hand-built grids (test_fourier.cpp:507-724)."""
+    cases = []
+    # planar periodic: M=(8,8,4), M_ext=(8,8,12), s0=2, s*=1.5, k*=(2,2,0)
+    g2 = _test_grid(S, 2, 1 / 8, (8, 8, 4), (8, 8, 12))
+    cases.append((2, g2, (1.0, 1.0, 0.5), 2.5, 10, S.UpsamplingPlan(2.0, 1.5, (2, 2, 0)), 1.5, (0.2, 0.7), True))
+    # singly periodic: M=(8,4,4), M_ext=(8,12,12), s0=8/3, s*=1.5, k*=(2,0,0)
+    g1 = _test_grid(S, 1, 1 / 8, (8, 4, 4), (8, 12, 12))
+    cases.append((1, g1, (1.0, 0.5, 0.5), 3.0, 10, S.UpsamplingPlan(8 / 3, 1.5, (2, 0, 0)), 1.5 * np.sqrt(2), (0.2, 0.7), True))
+    # free space: M=(8,8,8), M_ext=(16,16,16), s0=3 (direct) and table path
+    g0 = _test_grid(S, 0, 1 / 16, (8, 8, 8), (16, 16, 16))
+    cases.append((0, g0, (0.5, 0.5, 0.5), 5.0, 12, S.UpsamplingPlan(3.0), np.sqrt(3.0), (0.3, 0.7), False))
+    cases.append((0, g0, (0.5, 0.5, 0.5), 5.0, 12, S.UpsamplingPlan(3.0), np.sqrt(3.0), (0.3, 0.7), True))
+    g0b = _test_grid(S, 0, 1 / 16, (8, 8, 8), (32, 32, 32))
+    cases.append((0, g0b, (0.5, 0.5, 0.5), 5.0, 12, S.UpsamplingPlan(2.75), 2 * np.sqrt(3.0), (0.3, 0.7), True))
+    rng = np.random.default_rng(71 + kind)
+    for d, grid, L, xi, P, plan, R, (lo, hi), table in cases:
+        if d == 1 and kind == 1:
+            continue  # the reference's singly periodic test covers stokeslet and rotlet
+        n = 6
+        x = np.empty((n, 3))
+        for ax in range(3):
+            x[:, ax] = (rng.random(n) if ax < d else rng.uniform(lo, hi, n)) * L[ax]
+        f = rng.uniform(-1, 1, (n, 3))
+        nu = rng.uniform(-1, 1, (n, 3)) if kind == 1 else None
+        p = S.EwaldParams(S.Kernel(kind), d, xi, 0.3, R, grid, S.WindowSpec.make(S.WindowKind.kb, P, grid.h), plan)
+        sysm = S.SourceSystem(S.Kernel(kind), S.Cell(L), d, x, f, nu)
+        tg = S.TargetSet.from_sources(sysm)
+        opt = S.SePipelineOptions(precompute_0p=table)
+        u = S.se_fourier_potential(sysm, tg, p, opt)
+        rp = ref.params_from(p.to_c())
+        ur = ref.fourier_potential(rp, x, f, nu, None, True, precompute_0p=table)
+        assert rel_rms(u, ur) < TOL, (d, table)
+
+
+@pytest.mark.oracle
+@pytest.mark.parametrize("d", [0, 1, 2])
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_live_free_axes_selected(S, ref, d, kind):
+    rng = np.random.default_rng(1000 + 10 * d + kind)
+    N = 120
+    L = (1.0, 1.0, 1.0) if d else (2.0, 1.0, 1.0)
+    x = rng.random((N, 3)) * np.asarray(L)
+    f = rng.standard_normal((N, 3))
+    nu = rng.standard_normal((N, 3)) if kind == 1 else None
+    sysm = S.SourceSystem(S.Kernel(kind), S.Cell(L), d, x, f, nu)
+    window = S.WindowKind.tg if (d == 1 and kind == 2) else S.WindowKind.pkb
+    sel = S.select_parameters(sysm.kind, d, sysm.cell, S.source_quantity(sysm), 6.0, S.ToleranceSpec(1e-8),
+                              S.SelectionOptions(4, window, True))
+    rp = ref.params_from(sel.params.to_c())
+    xt = rng.random((50, 3)) * np.asarray(L)
+    for same in (True, False):
+        tg = S.TargetSet.from_sources(sysm) if same else S.TargetSet(xt, False)
+        u = S.full_potential(sysm, tg, sel.params)
+        ur = ref.full_potential(rp, x, f, nu, None if same else xt, same)
+        assert rel_rms(u, ur) < TOL, (d, kind, same)
