@@ -37,7 +37,7 @@ CONFIGS = {
     2: Config(2, "c2_stokeslet_d3_N1e6", Kernel.stokeslet, 3, (1.0, 1.0, 1.0), 1_000_000, None, 1e-8, 37.0, WindowKind.pkb),
     3: Config(3, "c3_stresslet_d2_N1e6", Kernel.stresslet, 2, (1.0, 1.0, 1.0), 1_000_000, None, 1e-8, 33.5, WindowKind.pkb),
     4: Config(4, "c4_rotlet_d1_N5e5", Kernel.rotlet, 1, (1.0, 1.0, 1.0), 500_000, 500_000, 1e-10, 34.0, WindowKind.tg),
-    5: Config(5, "c5_stokeslet_d0_N4e6", Kernel.stokeslet, 0, (2.0, 1.0, 1.0), 4_000_000, None, 1e-6, 19.5, WindowKind.pkb),
+    5: Config(5, "c5_stokeslet_d0_N4e6", Kernel.stokeslet, 0, (2.0, 1.0, 1.0), 4_000_000, None, 1e-6, 68.5, WindowKind.pkb),
 }
 
 
