@@ -265,14 +265,12 @@ def run_ours(args, cfg):
     l2 = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
     i0, i1 = N * rank // ws, N * (rank + 1) // ws
 
+    from paper_2210_01255_b200.parallel import sharded_step
+
     def step():
         sess.set_sources(dx, df, dnu)
         sess.set_targets(dxt, same)
-        sess.spread(i0, i1, grid)
-        if ws > 1:
-            dist.all_reduce(grid)
-        sess.solve(grid, True)
-        sess.evaluate(u, rank, ws, 7)
+        sharded_step(sess, N, grid, u, rank, ws, all_reduce=dist.all_reduce if ws > 1 else None)
 
     def barrier():
         if ws > 1:

@@ -287,6 +287,32 @@ int ref_flow_field(const sewald_params_c* p, const double* x, const double* f, c
     });
 }
 
+// aft_forward -> scale -> aft_inverse on a given spread grid (C comps) ->
+// 3-component flow field (the stage sequence of se_fourier_potential,
+// fourier.cpp:816-840, starting from an existing RealField).
+int ref_solve_grid(const sewald_params_c* p, const double* grid, int use_table, double* flow_out) {
+    return guarded([&] {
+        EwaldParams e = from_c(p);
+        const Window window(e.window);
+        const ModifiedKernelSpec spec = ModifiedKernelSpec::optimal(e.kind, e.d, e.d == 3 ? 1.0 : e.R);
+        RealField phi = RealField::zeros(e.grid.M_ext, strength_components(e.kind));
+        std::memcpy(phi.v.data(), grid, sizeof(double) * phi.v.size());
+        UpsamplingPlan plan = e.upsampling;
+        FourierField scaled;
+        if (e.d == 0 && use_table) {
+            plan.s0 = 2.0;
+            FourierField modes = aft_forward(phi, e.grid, plan);
+            PrecomputedKernel0P table = precompute_0p(e.kind, e.grid, e.R);
+            scaled = scale(modes, table, e.xi, window, e.grid);
+        } else {
+            FourierField modes = aft_forward(phi, e.grid, plan);
+            scaled = scale(modes, spec, e.xi, window, e.grid);
+        }
+        RealField flow = aft_inverse(scaled, e.grid, plan);
+        std::memcpy(flow_out, flow.v.data(), sizeof(double) * flow.v.size());
+    });
+}
+
 int ref_fourier_potential(const sewald_params_c* p, const double* x, const double* f,
                           const double* nu, int64_t N, const double* xt, int64_t Nt, int same,
                           int precompute_0p, double* u_out) {

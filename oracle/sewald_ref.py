@@ -62,6 +62,7 @@ _SIGS = {
     "ref_spread": (C.c_int, [PP, DP, DP, DP, I64, DP]),
     "ref_gather": (C.c_int, [PP, DP, DP, I64, DP]),
     "ref_flow_field": (C.c_int, [PP, DP, DP, DP, I64, C.c_int, DP]),
+    "ref_solve_grid": (C.c_int, [PP, DP, C.c_int, DP]),
     "ref_fourier_potential": (C.c_int, [PP, DP, DP, DP, I64, DP, I64, C.c_int, C.c_int, DP]),
     "ref_realspace_potential": (C.c_int, [C.c_int, C.c_int, DP, DP, DP, DP, I64, DP, I64, C.c_int,
                                           C.c_double, C.c_double, C.c_int, C.c_int, DP]),
@@ -191,6 +192,13 @@ def flow_field(p: RefParams, x, f, nu=None, use_table=True) -> np.ndarray:
     x, f, nu = _v3(x), _v3(f), _v3(nu)
     out = np.zeros((3, p.M_ext[0], p.M_ext[1], p.M_ext[2]))
     _chk(lib().ref_flow_field(C.byref(p), _dp(x), _dp(f), _dp(nu), x.shape[0], int(use_table), _dp(out)))
+    return out
+
+
+def solve_grid(p: RefParams, grid, use_table=True) -> np.ndarray:
+    grid = np.ascontiguousarray(grid, dtype=np.float64)
+    out = np.zeros((3, p.M_ext[0], p.M_ext[1], p.M_ext[2]))
+    _chk(lib().ref_solve_grid(C.byref(p), _dp(grid), int(use_table), _dp(out)))
     return out
 
 
