@@ -191,11 +191,13 @@ int sewald_gpu_session_spread(sewald_gpu_session* s, int64_t i0, int64_t i1, dou
 /* Forward transform, k-space scaling, inverse transform: grid_dev (C comps)
  * -> session flow field (3 comps). precompute_0p selects the D=0 table path. */
 int sewald_gpu_session_solve(sewald_gpu_session* s, const double* grid_dev, int precompute_0p);
-/* Evaluate the targets of part `part` of `nparts` equal contiguous slices of
- * the session's internal (cell-sorted, hence spatially compact) target order.
- * u_dev holds Nt*3 doubles in the caller's original target order; only this
- * part's rows are written (u = u_R + u_F + terms), other rows are untouched,
- * so per-rank results combine with a sum all-reduce. `parts` bit mask:
+/* Evaluate the targets of part `part` of `nparts` cluster-aligned contiguous
+ * slices of the session's internal (cell-sorted, hence spatially compact)
+ * target order. u_dev holds Nt*3 doubles in the caller's original target
+ * order. With nparts == 1 it receives the full result. With nparts > 1 (or
+ * when the pair-symmetric real-space sum is used, targets == sources) the
+ * whole array is zeroed first and this part's contributions are
+ * accumulated, so per-rank outputs combine with a sum all-reduce. `parts` bit mask:
  * 1 = Fourier (gather of the solved flow), 2 = real space, 4 = self /
  * zero-mode / gauge terms. */
 int sewald_gpu_session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts,

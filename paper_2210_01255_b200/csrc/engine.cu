@@ -565,10 +565,25 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
     cudaStream_t st = s->ctx->stream;
     ensure_target_order(s);
     const int64_t Nt = s->Nt;
-    const int64_t t0 = Nt * part / nparts, t1 = Nt * (part + 1) / nparts;
+    // Cluster-aligned partition of the cell-ordered targets (32 per cluster).
+    const int64_t ncl = (Nt + 31) / 32;
+    const int64_t c0 = ncl * part / nparts, c1 = ncl * (part + 1) / nparts;
+    const int64_t t0 = std::min<int64_t>(32 * c0, Nt), t1 = std::min<int64_t>(32 * c1, Nt);
     if (t1 <= t0) return;
     const uint32_t* torder = target_order(s);
+    static const bool sym_enabled = [] {
+        const char* e = getenv("SEWALD_RS_SYM");
+        return !(e && e[0] == '0');
+    }();
+    const bool use_sym = (parts & 2) && s->same && sym_enabled;
+    // The pair-symmetric real-space sum adds reactions to any particle, and
+    // multi-part evaluation is combined by summing the per-part outputs: in
+    // both cases the whole output is zeroed here and every stage accumulates.
     bool first = true;
+    if (use_sym || nparts > 1) {
+        cuda_check(cudaMemsetAsync(u, 0, sizeof(double) * 3 * Nt, st), "u zero");
+        first = false;
+    }
     if (parts & 2) {
         if (!(s->p.xi > 0.0)) throw EngineError(SEWALD_EINVAL, "split parameter must be positive");
         if (!(s->p.rc > 0.0)) throw EngineError(SEWALD_EINVAL, "cell list cutoff must be positive");
@@ -577,17 +592,22 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
         a.xi = s->p.xi;
         a.rc = s->p.rc;
         a.skip_self = s->same ? 1 : 0;
-        // fp32 candidate bound: coordinates (targets folded or inside the
-        // free-axis span, +-shift) are O(ext); fp32 differences carry at
-        // most a few ulp(ext) error per axis, so pad rc by 2^-18 ext.
-        double ext = a.rc;
-        for (int ax = 0; ax < 3; ++ax)
-            ext = std::max(ext, std::fabs(s->cg.origin[ax]) + s->cg.n[ax] * s->cg.w[ax] + s->cg.L[ax] + 2.0 * a.rc);
-        const double rpad = a.rc + std::ldexp(ext, -18);
-        a.thresh_f = (float)(rpad * rpad * (1.0 + std::ldexp(1.0, -16)));
-        launch_realspace(s->cg, a, s->packed.as<double>(), s->packedf.as<float4>(), s->stresslet, s->c_off.as<int64_t>(),
-                         target_folded(s), torder + t0, t1 - t0, u, 0,
-                         s->pair_counter.as<unsigned long long>(), s->flags.as<int>() + FLAG_SINGULAR, st);
+        if (use_sym) {
+            launch_realspace_sym(s->cg, a, s->packed.as<double>(), Nt, s->c_off.as<int64_t>(), c0, c1, u,
+                                 s->pair_counter.as<unsigned long long>(), s->flags.as<int>() + FLAG_SINGULAR, st);
+        } else {
+            // fp32 candidate bound: coordinates (targets folded or inside the
+            // free-axis span, +-shift) are O(ext); fp32 differences carry at
+            // most a few ulp(ext) error per axis, so pad rc by 2^-18 ext.
+            double ext = a.rc;
+            for (int ax = 0; ax < 3; ++ax)
+                ext = std::max(ext, std::fabs(s->cg.origin[ax]) + s->cg.n[ax] * s->cg.w[ax] + s->cg.L[ax] + 2.0 * a.rc);
+            const double rpad = a.rc + std::ldexp(ext, -18);
+            a.thresh_f = (float)(rpad * rpad * (1.0 + std::ldexp(1.0, -16)));
+            launch_realspace(s->cg, a, s->packed.as<double>(), s->packedf.as<float4>(), s->stresslet,
+                             s->c_off.as<int64_t>(), target_folded(s), torder + t0, t1 - t0, u, first ? 0 : 1,
+                             s->pair_counter.as<unsigned long long>(), s->flags.as<int>() + FLAG_SINGULAR, st);
+        }
         ++s->ctx->launches;
         first = false;
     }

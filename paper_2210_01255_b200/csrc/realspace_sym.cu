@@ -1,0 +1,303 @@
+// Real-space sum for targets == sources (the starred sum of full_potential),
+// using pair symmetry: each unordered pair {a, b + shift} within rc is
+// evaluated ONCE and applied to both particles (the kernels are even
+// (stokeslet) or odd (rotlet, stresslet) in r, and the reference's
+// r_ba = (x_b - x_a) - (-shift) is exactly -r_ab in IEEE arithmetic, so the
+// accepted set and every term match the reference's two directed sums).
+//
+// Reference: accumulate_rows /root/reference/proj/src/realspace.cpp:30-93,
+//            realspace_kernel /root/reference/proj/src/kernels.cpp:71-116.
+//
+// Work unit = one warp = one i-cluster of 32 consecutive particles in cell
+// order. Its bounding box selects the cell rows within rc; each row piece is
+// streamed as j-blocks of up to 32 particles into warp-private shared
+// memory. The 32 x 32 block is swept in 32 lock-step rotations (lane l pairs
+// with j = (l + s) mod 32), so the j particles touched in one step are all
+// distinct: reactions accumulate in shared memory without atomics and are
+// flushed once per j-block with fp64 RED to global memory. Steps with no
+// accepted lane are skipped (warp vote). Half rule: a pair (a, b, shift) is
+// evaluated iff b > a, or b == a with shift > 0 lexicographically (the self
+// pair, b == a with zero shift, is the starred exclusion).
+#include "device_common.cuh"
+#include "sg_kernels.h"
+#include "screened_math.cuh"
+#include "../../include/sewald_gpu.h"
+
+namespace sewald_b200 {
+
+namespace {
+
+constexpr int SYM_WARPS = 4;
+constexpr int SYM_THREADS = 32 * SYM_WARPS;
+
+__device__ __forceinline__ int fdiv(int a, int b) {
+    int q = a / b;
+    if ((a % b != 0) && ((a < 0) != (b < 0))) --q;
+    return q;
+}
+
+template <int KIND>
+struct Strength;
+template <>
+struct Strength<SEWALD_STOKESLET> {
+    static constexpr int n = 3;
+};
+template <>
+struct Strength<SEWALD_ROTLET> {
+    static constexpr int n = 3;
+};
+template <>
+struct Strength<SEWALD_STRESSLET> {
+    static constexpr int n = 6;
+};
+
+// Contribution of source strength s at separation r (target - source) and
+// its reaction on the source from the target strength t (separation -r).
+template <int KIND>
+__device__ __forceinline__ void pair_both(const Screened& sc, double xi2, double n2, double r0, double r1,
+                                          double r2, const double* s, const double* t, double* ua, double* ub) {
+    if (KIND == SEWALD_STOKESLET) {
+        const double a = sc.Ey * (sc.R - sc.cx);
+        const double b = sc.Ey * (sc.iy * sc.iy) * (sc.R + sc.cx);
+        const double bs = b * (r0 * s[0] + r1 * s[1] + r2 * s[2]);
+        const double bt = b * (r0 * t[0] + r1 * t[1] + r2 * t[2]);
+        ua[0] = fma(a, s[0], fma(bs, r0, ua[0]));
+        ua[1] = fma(a, s[1], fma(bs, r1, ua[1]));
+        ua[2] = fma(a, s[2], fma(bs, r2, ua[2]));
+        ub[0] = fma(a, t[0], bt * r0);
+        ub[1] = fma(a, t[1], bt * r1);
+        ub[2] = fma(a, t[2], bt * r2);
+    } else if (KIND == SEWALD_ROTLET) {
+        const double c = sc.Ey * (sc.iy * sc.iy) * (sc.R + sc.cx);
+        ua[0] = fma(c, s[1] * r2 - s[2] * r1, ua[0]);
+        ua[1] = fma(c, s[2] * r0 - s[0] * r2, ua[1]);
+        ua[2] = fma(c, s[0] * r1 - s[1] * r0, ua[2]);
+        ub[0] = -c * (t[1] * r2 - t[2] * r1);
+        ub[1] = -c * (t[2] * r0 - t[0] * r2);
+        ub[2] = -c * (t[0] * r1 - t[1] * r0);
+    } else {
+        const double iy2 = sc.iy * sc.iy;
+        const double x2 = xi2 * n2;
+        const double c1 = -2.0 * sc.Ey * (iy2 * iy2) * (3.0 * sc.R + (3.0 + 2.0 * x2) * sc.cx);
+        const double c2 = 2.0 * xi2 * sc.Ey * sc.cx;
+        {
+            const double* q = s;
+            const double* v = s + 3;
+            const double rq = r0 * q[0] + r1 * q[1] + r2 * q[2];
+            const double rv = r0 * v[0] + r1 * v[1] + r2 * v[2];
+            const double qv = q[0] * v[0] + q[1] * v[1] + q[2] * v[2];
+            const double w = c1 * rq * rv + c2 * qv;
+            ua[0] += w * r0 + c2 * (q[0] * rv + v[0] * rq);
+            ua[1] += w * r1 + c2 * (q[1] * rv + v[1] * rq);
+            ua[2] += w * r2 + c2 * (q[2] * rv + v[2] * rq);
+        }
+        {
+            const double* q = t;
+            const double* v = t + 3;
+            const double rq = r0 * q[0] + r1 * q[1] + r2 * q[2];
+            const double rv = r0 * v[0] + r1 * v[1] + r2 * v[2];
+            const double qv = q[0] * v[0] + q[1] * v[1] + q[2] * v[2];
+            const double w = c1 * rq * rv + c2 * qv;
+            ub[0] = -(w * r0 + c2 * (q[0] * rv + v[0] * rq));
+            ub[1] = -(w * r1 + c2 * (q[1] * rv + v[1] * rq));
+            ub[2] = -(w * r2 + c2 * (q[2] * rv + v[2] * rq));
+        }
+    }
+}
+
+template <int KIND, int S>
+__global__ void __launch_bounds__(SYM_THREADS, 4)
+realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed,
+                     const int64_t* __restrict__ cell_off, int64_t N, int64_t c0, int64_t c1,
+                     double* __restrict__ u, unsigned long long* __restrict__ pair_count, int* __restrict__ err) {
+    constexpr int NS = Strength<KIND>::n;
+    __shared__ double jx_all[SYM_WARPS][3][32];
+    __shared__ double js_all[SYM_WARPS][NS][32];
+    __shared__ double racc_all[SYM_WARPS][3][32];
+    __shared__ long long jid_all[SYM_WARPS][32];
+
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t cl = c0 + (int64_t)blockIdx.x * SYM_WARPS + warp;
+    if (cl >= c1) return;
+    double(*jx)[32] = jx_all[warp];
+    double(*js)[32] = js_all[warp];
+    double(*racc)[32] = racc_all[warp];
+    long long* jid = jid_all[warp];
+
+    const int64_t istart = cl * 32;
+    const int64_t ia = istart + lane;
+    const bool valid = ia < N;
+    double xa0 = 0, xa1 = 0, xa2 = 0, fa[NS];
+    long long ida = -1;
+#pragma unroll
+    for (int c = 0; c < NS; ++c) fa[c] = 0.0;
+    if (valid) {
+        const double* q = packed + ia * S;
+        xa0 = q[0];
+        xa1 = q[1];
+        xa2 = q[2];
+        ida = __double_as_longlong(q[3]);
+#pragma unroll
+        for (int c = 0; c < NS; ++c) fa[c] = q[4 + c];
+    }
+
+    double lo[3] = {valid ? xa0 : 1e300, valid ? xa1 : 1e300, valid ? xa2 : 1e300};
+    double hi[3] = {valid ? xa0 : -1e300, valid ? xa1 : -1e300, valid ? xa2 : -1e300};
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax)
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) {
+            lo[ax] = fmin(lo[ax], __shfl_xor_sync(0xffffffffu, lo[ax], s));
+            hi[ax] = fmax(hi[ax], __shfl_xor_sync(0xffffffffu, hi[ax], s));
+        }
+
+    const double rc2 = a.rc * a.rc;
+    const double xi2 = a.xi * a.xi;
+    const double rcm = a.rc * (1.0 + 1e-10) + 1e-12 * fmax(fmax(cg.L[0], cg.L[1]), cg.L[2]);
+    const double rcm2 = rcm * rcm;
+    int clo[3], chi[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ++ax) {
+        clo[ax] = (int)floor((lo[ax] - rcm - cg.origin[ax]) / cg.w[ax]);
+        chi[ax] = (int)floor((hi[ax] + rcm - cg.origin[ax]) / cg.w[ax]);
+        if (ax >= cg.d) {
+            clo[ax] = max(clo[ax], 0);
+            chi[ax] = min(chi[ax], cg.n[ax] - 1);
+        }
+    }
+
+    double ua[3] = {0.0, 0.0, 0.0};
+    unsigned long long npairs = 0;
+
+    for (int cz = clo[2]; cz <= chi[2]; ++cz) {
+        const int sz = 2 < cg.d ? fdiv(cz, cg.n[2]) : 0;
+        const int jz = cz - sz * cg.n[2];
+        const double zlo = cg.origin[2] + cz * cg.w[2], zhi = zlo + cg.w[2];
+        const double dz = fmax(0.0, fmax(zlo - hi[2], lo[2] - zhi));
+        const double shz = (double)sz * cg.L[2];
+        for (int cy = clo[1]; cy <= chi[1]; ++cy) {
+            const int sy = 1 < cg.d ? fdiv(cy, cg.n[1]) : 0;
+            const int jy = cy - sy * cg.n[1];
+            const double ylo = cg.origin[1] + cy * cg.w[1], yhi = ylo + cg.w[1];
+            const double dy = fmax(0.0, fmax(ylo - hi[1], lo[1] - yhi));
+            const double lat2 = dy * dy + dz * dz;
+            if (lat2 >= rcm2) continue;
+            const double ext = sqrt(rcm2 - lat2);
+            int cxl = (int)floor((lo[0] - ext - cg.origin[0]) / cg.w[0]);
+            int cxh = (int)floor((hi[0] + ext - cg.origin[0]) / cg.w[0]);
+            cxl = max(cxl, clo[0]);
+            cxh = min(cxh, chi[0]);
+            if (cxl > cxh) continue;
+            const double shy = (double)sy * cg.L[1];
+            const int64_t rowbase = ((int64_t)jz * cg.n[1] + jy) * cg.n[0];
+            const int sxa = 0 < cg.d ? fdiv(cxl, cg.n[0]) : 0;
+            const int sxb = 0 < cg.d ? fdiv(cxh, cg.n[0]) : 0;
+            for (int sx = sxa; sx <= sxb; ++sx) {
+                const int jlo = max(cxl - sx * cg.n[0], 0);
+                const int jhi = min(cxh - sx * cg.n[0], cg.n[0] - 1);
+                int64_t b0 = cell_off[rowbase + jlo];
+                const int64_t b1 = cell_off[rowbase + jhi + 1];
+                // half rule: partners with a smaller sorted index than every
+                // particle of this cluster are evaluated by their own warp
+                if (b0 < istart) b0 = istart;
+                if (b0 >= b1) continue;
+                const double shx = (double)sx * cg.L[0];
+                const bool pos_shift = sx > 0 || (sx == 0 && (sy > 0 || (sy == 0 && sz > 0)));
+                for (int64_t jb = b0; jb < b1; jb += 32) {
+                    const int cnt = (int)min((int64_t)32, b1 - jb);
+                    __syncwarp();
+                    if (lane < cnt) {
+                        const double* q = packed + (jb + lane) * S;
+                        jx[0][lane] = q[0];
+                        jx[1][lane] = q[1];
+                        jx[2][lane] = q[2];
+                        jid[lane] = __double_as_longlong(q[3]);
+#pragma unroll
+                        for (int c = 0; c < NS; ++c) js[c][lane] = q[4 + c];
+                    }
+                    racc[0][lane] = 0.0;
+                    racc[1][lane] = 0.0;
+                    racc[2][lane] = 0.0;
+                    __syncwarp();
+                    const bool overlap = jb < istart + 32;  // j-block meets this cluster
+                    for (int s = 0; s < 32; ++s) {
+                        const int j = (lane + s) & 31;
+                        bool acc = valid && j < cnt;
+                        if (overlap) {
+                            const int64_t gj = jb + j;
+                            acc = acc && (gj > ia || (gj == ia && pos_shift));
+                        }
+                        double r0 = 0, r1 = 0, r2 = 0, n2 = 0;
+                        if (acc) {
+                            r0 = (xa0 - jx[0][j]) - shx;
+                            r1 = (xa1 - jx[1][j]) - shy;
+                            r2 = (xa2 - jx[2][j]) - shz;
+                            n2 = __dadd_rn(__dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1)), __dmul_rn(r2, r2));
+                            acc = n2 < rc2;
+                        }
+                        if (!__any_sync(0xffffffffu, acc)) continue;
+                        if (acc) {
+                            if (n2 == 0.0) {  // coincident distinct points (kernels.cpp:19-22)
+                                atomicExch(err, 1);
+                            } else {
+                                double sj[NS];
+#pragma unroll
+                                for (int c = 0; c < NS; ++c) sj[c] = js[c][j];
+                                const Screened sc = screened(n2, a.xi, xi2);
+                                double ub[3];
+                                pair_both<KIND>(sc, xi2, n2, r0, r1, r2, sj, fa, ua, ub);
+                                racc[0][j] += ub[0];
+                                racc[1][j] += ub[1];
+                                racc[2][j] += ub[2];
+                                npairs += 2;
+                            }
+                        }
+                    }
+                    __syncwarp();
+                    if (lane < cnt) {
+                        double* dst = u + 3 * jid[lane];
+                        atomicAdd(dst, racc[0][lane]);
+                        atomicAdd(dst + 1, racc[1][lane]);
+                        atomicAdd(dst + 2, racc[2][lane]);
+                    }
+                }
+            }
+        }
+    }
+    if (valid) {
+        double* dst = u + 3 * ida;
+        atomicAdd(dst, ua[0]);
+        atomicAdd(dst + 1, ua[1]);
+        atomicAdd(dst + 2, ua[2]);
+    }
+    if (pair_count) {
+#pragma unroll
+        for (int s = 16; s > 0; s >>= 1) npairs += __shfl_xor_sync(0xffffffffu, npairs, s);
+        if (lane == 0 && npairs) atomicAdd(pair_count, npairs);
+    }
+}
+
+}  // namespace
+
+void launch_realspace_sym(const CellGrid& cg, const RealspaceArgs& a, const double* packed, int64_t N,
+                          const int64_t* cell_off, int64_t c0, int64_t c1, double* u,
+                          unsigned long long* pair_count, int* err, cudaStream_t st) {
+    if (c1 <= c0) return;
+    const unsigned blocks = (unsigned)((c1 - c0 + SYM_WARPS - 1) / SYM_WARPS);
+    switch (a.kind) {
+        case SEWALD_STOKESLET:
+            realspace_sym_kernel<SEWALD_STOKESLET, 8><<<blocks, SYM_THREADS, 0, st>>>(cg, a, packed, cell_off, N, c0,
+                                                                                       c1, u, pair_count, err);
+            break;
+        case SEWALD_ROTLET:
+            realspace_sym_kernel<SEWALD_ROTLET, 8><<<blocks, SYM_THREADS, 0, st>>>(cg, a, packed, cell_off, N, c0, c1,
+                                                                                    u, pair_count, err);
+            break;
+        default:
+            realspace_sym_kernel<SEWALD_STRESSLET, 12><<<blocks, SYM_THREADS, 0, st>>>(cg, a, packed, cell_off, N, c0,
+                                                                                        c1, u, pair_count, err);
+            break;
+    }
+}
+
+}  // namespace sewald_b200

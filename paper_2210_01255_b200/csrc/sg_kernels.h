@@ -62,6 +62,13 @@ void launch_realspace(const CellGrid& cg, const RealspaceArgs& a, const double* 
                       const uint32_t* torder, int64_t Nt, double* u, int accumulate,
                       unsigned long long* pair_count, int* err, cudaStream_t st);
 
+// Symmetric real-space sum for targets == sources (realspace_sym.cu):
+// i-clusters [c0, c1) of 32 cell-ordered particles; u (original order) must
+// be zeroed beforehand and receives contributions of every particle.
+void launch_realspace_sym(const CellGrid& cg, const RealspaceArgs& a, const double* packed, int64_t N,
+                          const int64_t* cell_off, int64_t c0, int64_t c1, double* u,
+                          unsigned long long* pair_count, int* err, cudaStream_t st);
+
 // ---- k space (kspace.cu) ---------------------------------------------------
 struct KspaceTables {
     const double* k[3];      // wavenumbers per axis (DFT order)

@@ -25,8 +25,11 @@ def slice_bounds(n: int, rank: int, world: int):
 
 
 def sharded_step(session, n_sources: int, grid, u, rank: int, world: int,
-                 all_reduce: Optional[Callable] = None, precompute_0p: bool = True, parts: int = 7):
-    """One distributed full-potential step; u receives this rank's target part."""
+                 all_reduce: Optional[Callable] = None, precompute_0p: bool = True, parts: int = 7,
+                 gather_result: bool = True):
+    """One distributed full-potential step. Each rank's evaluate() output
+    holds its part's contributions (zero elsewhere); with gather_result the
+    outputs are summed so every rank ends with the full velocity field."""
     i0, i1 = slice_bounds(n_sources, rank, world)
     session.spread(i0, i1, grid)
     if world > 1:
@@ -35,3 +38,5 @@ def sharded_step(session, n_sources: int, grid, u, rank: int, world: int,
         all_reduce(grid)
     session.solve(grid, precompute_0p)
     session.evaluate(u, rank, world, parts)
+    if world > 1 and gather_result:
+        all_reduce(u)

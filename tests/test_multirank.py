@@ -40,7 +40,10 @@ class RefSession:
     def evaluate(self, u, part, nparts, parts=7):
         import torch
         from paper_2210_01255_b200.parallel import slice_bounds
-        t0, t1 = slice_bounds(self.x.shape[0], part, nparts)
+        ncl = (self.x.shape[0] + 31) // 32  # cluster-aligned parts, as the device session
+        c0, c1 = slice_bounds(ncl, part, nparts)
+        t0, t1 = min(32 * c0, self.x.shape[0]), min(32 * c1, self.x.shape[0])
+        u.zero_()
         uF = self.R.gather(self.p, self.flow, self.x[t0:t1])
         uR = self.R.realspace_potential(self.kind, self.d, self.L, self.x, self.f, self.nu, None, True,
                                         self.p.xi, self.p.rc, True)[t0:t1]
@@ -70,7 +73,6 @@ def _worker(rank, world, port, outdir):
     grid = torch.zeros(3 * p.M_ext[0] * p.M_ext[1] * p.M_ext[2], dtype=torch.float64)
     u = torch.zeros((N, 3), dtype=torch.float64)
     sharded_step(sess, N, grid, u, rank, world, all_reduce=dist.all_reduce)
-    dist.all_reduce(u)
     if rank == 0:
         np.save(os.path.join(outdir, "u.npy"), u.numpy())
         np.save(os.path.join(outdir, "uref.npy"), R.full_potential(p, x, f))
