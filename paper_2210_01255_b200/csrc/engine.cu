@@ -592,18 +592,18 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
         a.xi = s->p.xi;
         a.rc = s->p.rc;
         a.skip_self = s->same ? 1 : 0;
+        // fp32 candidate bound: coordinates (targets folded or inside the
+        // free-axis span, +-shift) are O(ext); fp32 differences carry at
+        // most a few ulp(ext) error per axis, so pad rc by 2^-18 ext.
+        double ext = a.rc;
+        for (int ax = 0; ax < 3; ++ax)
+            ext = std::max(ext, std::fabs(s->cg.origin[ax]) + s->cg.n[ax] * s->cg.w[ax] + s->cg.L[ax] + 2.0 * a.rc);
+        const double rpad = a.rc + std::ldexp(ext, -18);
+        a.thresh_f = (float)(rpad * rpad * (1.0 + std::ldexp(1.0, -16)));
         if (use_sym) {
             launch_realspace_sym(s->cg, a, s->packed.as<double>(), Nt, s->c_off.as<int64_t>(), c0, c1, u,
                                  s->pair_counter.as<unsigned long long>(), s->flags.as<int>() + FLAG_SINGULAR, st);
         } else {
-            // fp32 candidate bound: coordinates (targets folded or inside the
-            // free-axis span, +-shift) are O(ext); fp32 differences carry at
-            // most a few ulp(ext) error per axis, so pad rc by 2^-18 ext.
-            double ext = a.rc;
-            for (int ax = 0; ax < 3; ++ax)
-                ext = std::max(ext, std::fabs(s->cg.origin[ax]) + s->cg.n[ax] * s->cg.w[ax] + s->cg.L[ax] + 2.0 * a.rc);
-            const double rpad = a.rc + std::ldexp(ext, -18);
-            a.thresh_f = (float)(rpad * rpad * (1.0 + std::ldexp(1.0, -16)));
             launch_realspace(s->cg, a, s->packed.as<double>(), s->packedf.as<float4>(), s->stresslet,
                              s->c_off.as<int64_t>(), target_folded(s), torder + t0, t1 - t0, u, first ? 0 : 1,
                              s->pair_counter.as<unsigned long long>(), s->flags.as<int>() + FLAG_SINGULAR, st);

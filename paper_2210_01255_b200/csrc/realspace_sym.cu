@@ -115,6 +115,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     __shared__ double js_all[SYM_WARPS][NS][32];
     __shared__ double racc_all[SYM_WARPS][3][32];
     __shared__ long long jid_all[SYM_WARPS][32];
+    __shared__ float jf_all[SYM_WARPS][3][32];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t cl = c0 + (int64_t)blockIdx.x * SYM_WARPS + warp;
@@ -123,6 +124,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     double(*js)[32] = js_all[warp];
     double(*racc)[32] = racc_all[warp];
     long long* jid = jid_all[warp];
+    float(*jf)[32] = jf_all[warp];
 
     const int64_t istart = cl * 32;
     const int64_t ia = istart + lane;
@@ -203,6 +205,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                 if (b0 >= b1) continue;
                 const double shx = (double)sx * cg.L[0];
                 const bool pos_shift = sx > 0 || (sx == 0 && (sy > 0 || (sy == 0 && sz > 0)));
+                const float tf0 = (float)(xa0 - shx), tf1 = (float)(xa1 - shy), tf2 = (float)(xa2 - shz);
                 for (int64_t jb = b0; jb < b1; jb += 32) {
                     const int cnt = (int)min((int64_t)32, b1 - jb);
                     __syncwarp();
@@ -212,6 +215,9 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                         jx[1][lane] = q[1];
                         jx[2][lane] = q[2];
                         jid[lane] = __double_as_longlong(q[3]);
+                        jf[0][lane] = (float)q[0];
+                        jf[1][lane] = (float)q[1];
+                        jf[2][lane] = (float)q[2];
 #pragma unroll
                         for (int c = 0; c < NS; ++c) js[c][lane] = q[4 + c];
                     }
@@ -227,6 +233,11 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                             const int64_t gj = jb + j;
                             acc = acc && (gj > ia || (gj == ia && pos_shift));
                         }
+                        if (acc) {  // conservative fp32 pre-test (FP32 pipe)
+                            const float d0 = tf0 - jf[0][j], d1 = tf1 - jf[1][j], d2 = tf2 - jf[2][j];
+                            acc = fmaf(d2, d2, fmaf(d1, d1, d0 * d0)) < a.thresh_f;
+                        }
+                        if (!__any_sync(0xffffffffu, acc)) continue;
                         double r0 = 0, r1 = 0, r2 = 0, n2 = 0;
                         if (acc) {
                             r0 = (xa0 - jx[0][j]) - shx;
@@ -235,7 +246,6 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                             n2 = __dadd_rn(__dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1)), __dmul_rn(r2, r2));
                             acc = n2 < rc2;
                         }
-                        if (!__any_sync(0xffffffffu, acc)) continue;
                         if (acc) {
                             if (n2 == 0.0) {  // coincident distinct points (kernels.cpp:19-22)
                                 atomicExch(err, 1);
