@@ -11,13 +11,17 @@
 // Work unit = one warp = one i-cluster of 32 consecutive particles in cell
 // order. Its bounding box selects the cell rows within rc; each row piece is
 // streamed as j-blocks of up to 32 particles into warp-private shared
-// memory. The 32 x 32 block is swept in 32 lock-step rotations (lane l pairs
-// with j = (l + s) mod 32), so the j particles touched in one step are all
-// distinct: reactions accumulate in shared memory without atomics and are
-// flushed once per j-block with fp64 RED to global memory. Steps with no
-// accepted lane are skipped (warp vote). Half rule: a pair (a, b, shift) is
-// evaluated iff b > a, or b == a with shift > 0 lexicographically (the self
-// pair, b == a with zero shift, is the starred exclusion).
+// memory. Per 32 x 32 block: (1) each lane tests its 32 rotations
+// (lane l with j = (l + s) mod 32) with a conservative fp32 bound and the half
+// rule, (2) the accepted (l, s) pairs are compacted rotation-major into a
+// shared list with warp ballots, (3) all 32 lanes evaluate list entries
+// (exact fp64 test + kernel), so the expensive fp64 path runs with ~95 %
+// lane occupancy; i and j contributions go to shared-memory accumulators
+// (fp64 atomics; rotation-major order keeps contention rare), flushed to
+// global memory with fp64 RED once per j-block / per cluster.
+// Half rule: a pair (a, b, shift) is evaluated iff b > a, or b == a with
+// shift > 0 lexicographically (the self pair, b == a with zero shift, is the
+// starred exclusion).
 #include "device_common.cuh"
 #include "sg_kernels.h"
 #include "screened_math.cuh"
@@ -111,28 +115,35 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                      const int64_t* __restrict__ cell_off, int64_t N, int64_t c0, int64_t c1,
                      double* __restrict__ u, unsigned long long* __restrict__ pair_count, int* __restrict__ err) {
     constexpr int NS = Strength<KIND>::n;
+    __shared__ double ix_all[SYM_WARPS][3][32];
+    __shared__ double is_all[SYM_WARPS][NS][32];
+    __shared__ double iacc_all[SYM_WARPS][3][32];
     __shared__ double jx_all[SYM_WARPS][3][32];
     __shared__ double js_all[SYM_WARPS][NS][32];
     __shared__ double racc_all[SYM_WARPS][3][32];
     __shared__ long long jid_all[SYM_WARPS][32];
     __shared__ float jf_all[SYM_WARPS][3][32];
+    __shared__ uint16_t list_all[SYM_WARPS][1024];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t cl = c0 + (int64_t)blockIdx.x * SYM_WARPS + warp;
     if (cl >= c1) return;
+    double(*ix)[32] = ix_all[warp];
+    double(*is)[32] = is_all[warp];
+    double(*iacc)[32] = iacc_all[warp];
     double(*jx)[32] = jx_all[warp];
     double(*js)[32] = js_all[warp];
     double(*racc)[32] = racc_all[warp];
     long long* jid = jid_all[warp];
     float(*jf)[32] = jf_all[warp];
+    uint16_t* list = list_all[warp];
+    const unsigned lt_mask = (1u << lane) - 1u;
 
     const int64_t istart = cl * 32;
     const int64_t ia = istart + lane;
     const bool valid = ia < N;
-    double xa0 = 0, xa1 = 0, xa2 = 0, fa[NS];
+    double xa0 = 0, xa1 = 0, xa2 = 0;
     long long ida = -1;
-#pragma unroll
-    for (int c = 0; c < NS; ++c) fa[c] = 0.0;
     if (valid) {
         const double* q = packed + ia * S;
         xa0 = q[0];
@@ -140,8 +151,14 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
         xa2 = q[2];
         ida = __double_as_longlong(q[3]);
 #pragma unroll
-        for (int c = 0; c < NS; ++c) fa[c] = q[4 + c];
+        for (int c = 0; c < NS; ++c) is[c][lane] = q[4 + c];
     }
+    ix[0][lane] = xa0;
+    ix[1][lane] = xa1;
+    ix[2][lane] = xa2;
+    iacc[0][lane] = 0.0;
+    iacc[1][lane] = 0.0;
+    iacc[2][lane] = 0.0;
 
     double lo[3] = {valid ? xa0 : 1e300, valid ? xa1 : 1e300, valid ? xa2 : 1e300};
     double hi[3] = {valid ? xa0 : -1e300, valid ? xa1 : -1e300, valid ? xa2 : -1e300};
@@ -167,8 +184,6 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
             chi[ax] = min(chi[ax], cg.n[ax] - 1);
         }
     }
-
-    double ua[3] = {0.0, 0.0, 0.0};
     unsigned long long npairs = 0;
 
     for (int cz = clo[2]; cz <= chi[2]; ++cz) {
@@ -176,7 +191,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
         const int jz = cz - sz * cg.n[2];
         const double zlo = cg.origin[2] + cz * cg.w[2], zhi = zlo + cg.w[2];
         const double dz = fmax(0.0, fmax(zlo - hi[2], lo[2] - zhi));
-        const double shz = (double)sz * cg.L[2];
+        const double shz = __dmul_rn((double)sz, cg.L[2]);
         for (int cy = clo[1]; cy <= chi[1]; ++cy) {
             const int sy = 1 < cg.d ? fdiv(cy, cg.n[1]) : 0;
             const int jy = cy - sy * cg.n[1];
@@ -190,7 +205,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
             cxl = max(cxl, clo[0]);
             cxh = min(cxh, chi[0]);
             if (cxl > cxh) continue;
-            const double shy = (double)sy * cg.L[1];
+            const double shy = __dmul_rn((double)sy, cg.L[1]);
             const int64_t rowbase = ((int64_t)jz * cg.n[1] + jy) * cg.n[0];
             const int sxa = 0 < cg.d ? fdiv(cxl, cg.n[0]) : 0;
             const int sxb = 0 < cg.d ? fdiv(cxh, cg.n[0]) : 0;
@@ -203,7 +218,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                 // particle of this cluster are evaluated by their own warp
                 if (b0 < istart) b0 = istart;
                 if (b0 >= b1) continue;
-                const double shx = (double)sx * cg.L[0];
+                const double shx = __dmul_rn((double)sx, cg.L[0]);
                 const bool pos_shift = sx > 0 || (sx == 0 && (sy > 0 || (sy == 0 && sz > 0)));
                 const float tf0 = (float)(xa0 - shx), tf1 = (float)(xa1 - shy), tf2 = (float)(xa2 - shz);
                 for (int64_t jb = b0; jb < b1; jb += 32) {
@@ -225,41 +240,64 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                     racc[1][lane] = 0.0;
                     racc[2][lane] = 0.0;
                     __syncwarp();
-                    const bool overlap = jb < istart + 32;  // j-block meets this cluster
-                    for (int s = 0; s < 32; ++s) {
-                        const int j = (lane + s) & 31;
-                        bool acc = valid && j < cnt;
-                        if (overlap) {
-                            const int64_t gj = jb + j;
-                            acc = acc && (gj > ia || (gj == ia && pos_shift));
-                        }
-                        if (acc) {  // conservative fp32 pre-test (FP32 pipe)
+                    // Phase 1: this lane's candidate rotations (fp32 bound + half rule).
+                    const int dlt = (int)(istart - jb);  // pair (lane, j) is "after" iff j - lane > dlt
+                    unsigned m = 0u;
+                    if (valid) {
+#pragma unroll 8
+                        for (int s = 0; s < 32; ++s) {
+                            const int j = (lane + s) & 31;
+                            const int dj = j - lane;
+                            const bool order_ok = dj > dlt || (dj == dlt && pos_shift);
                             const float d0 = tf0 - jf[0][j], d1 = tf1 - jf[1][j], d2 = tf2 - jf[2][j];
-                            acc = fmaf(d2, d2, fmaf(d1, d1, d0 * d0)) < a.thresh_f;
+                            const bool ok = j < cnt && order_ok &&
+                                            fmaf(d2, d2, fmaf(d1, d1, d0 * d0)) < a.thresh_f;
+                            m |= (ok ? 1u : 0u) << s;
                         }
-                        if (!__any_sync(0xffffffffu, acc)) continue;
-                        double r0 = 0, r1 = 0, r2 = 0, n2 = 0;
-                        if (acc) {
-                            r0 = (xa0 - jx[0][j]) - shx;
-                            r1 = (xa1 - jx[1][j]) - shy;
-                            r2 = (xa2 - jx[2][j]) - shz;
-                            n2 = __dadd_rn(__dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1)), __dmul_rn(r2, r2));
-                            acc = n2 < rc2;
-                        }
-                        if (acc) {
-                            if (n2 == 0.0) {  // coincident distinct points (kernels.cpp:19-22)
-                                atomicExch(err, 1);
-                            } else {
-                                double sj[NS];
+                    }
+                    // Phase 2: rotation-major compaction of (lane, s) pairs.
+                    int T = 0;
+#pragma unroll 4
+                    for (int s = 0; s < 32; ++s) {
+                        const bool bit = (m >> s) & 1u;
+                        const unsigned bal = __ballot_sync(0xffffffffu, bit);
+                        if (bit) list[T + __popc(bal & lt_mask)] = (uint16_t)(lane | (s << 5));
+                        T += __popc(bal);
+                    }
+                    __syncwarp();
+                    // Phase 3: all lanes evaluate compacted pairs.
+                    for (int e0 = 0; e0 < T; e0 += 32) {
+                        const int e = e0 + lane;
+                        if (e < T) {
+                            const int code = list[e];
+                            const int il = code & 31;
+                            const int j = (il + (code >> 5)) & 31;
+                            const double r0 = (ix[0][il] - jx[0][j]) - shx;
+                            const double r1 = (ix[1][il] - jx[1][j]) - shy;
+                            const double r2 = (ix[2][il] - jx[2][j]) - shz;
+                            const double n2 =
+                                __dadd_rn(__dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1)), __dmul_rn(r2, r2));
+                            if (n2 < rc2) {
+                                if (n2 == 0.0) {  // coincident distinct points (kernels.cpp:19-22)
+                                    atomicExch(err, 1);
+                                } else {
+                                    double si[NS], sj[NS];
 #pragma unroll
-                                for (int c = 0; c < NS; ++c) sj[c] = js[c][j];
-                                const Screened sc = screened(n2, a.xi, xi2);
-                                double ub[3];
-                                pair_both<KIND>(sc, xi2, n2, r0, r1, r2, sj, fa, ua, ub);
-                                racc[0][j] += ub[0];
-                                racc[1][j] += ub[1];
-                                racc[2][j] += ub[2];
-                                npairs += 2;
+                                    for (int c = 0; c < NS; ++c) {
+                                        si[c] = is[c][il];
+                                        sj[c] = js[c][j];
+                                    }
+                                    const Screened sc = screened(n2, a.xi, xi2);
+                                    double ua[3] = {0.0, 0.0, 0.0}, ub[3];
+                                    pair_both<KIND>(sc, xi2, n2, r0, r1, r2, sj, si, ua, ub);
+                                    atomicAdd(&iacc[0][il], ua[0]);
+                                    atomicAdd(&iacc[1][il], ua[1]);
+                                    atomicAdd(&iacc[2][il], ua[2]);
+                                    atomicAdd(&racc[0][j], ub[0]);
+                                    atomicAdd(&racc[1][j], ub[1]);
+                                    atomicAdd(&racc[2][j], ub[2]);
+                                    npairs += 2;
+                                }
                             }
                         }
                     }
@@ -274,11 +312,12 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
             }
         }
     }
+    __syncwarp();
     if (valid) {
         double* dst = u + 3 * ida;
-        atomicAdd(dst, ua[0]);
-        atomicAdd(dst + 1, ua[1]);
-        atomicAdd(dst + 2, ua[2]);
+        atomicAdd(dst, iacc[0][lane]);
+        atomicAdd(dst + 1, iacc[1][lane]);
+        atomicAdd(dst + 2, iacc[2][lane]);
     }
     if (pair_count) {
 #pragma unroll
