@@ -13,12 +13,13 @@
 // streamed as j-blocks of up to 32 particles into warp-private shared
 // memory. Per 32 x 32 block: (1) each lane tests its 32 rotations
 // (lane l with j = (l + s) mod 32) with a conservative fp32 bound and the half
-// rule, (2) the accepted (l, s) pairs are compacted rotation-major into a
-// shared list with warp ballots, (3) all 32 lanes evaluate list entries
-// (exact fp64 test + kernel), so the expensive fp64 path runs with ~95 %
-// lane occupancy; i and j contributions go to shared-memory accumulators
-// (fp64 atomics; rotation-major order keeps contention rare), flushed to
-// global memory with fp64 RED once per j-block / per cluster.
+// rule, (2) the rotations are packed greedily into rounds whose lane sets and
+// j sets are disjoint (warp ballots + bit masks), (3) each round evaluates at
+// most one pair per lane (exact fp64 test + kernel) with its own i in
+// registers and each j touched once, so reactions accumulate in shared memory
+// without atomics; packing sparse rotations together keeps the fp64 path
+// occupied. Reactions are flushed to global memory with fp64 RED once per
+// j-block, the i sums once per cluster.
 // Half rule: a pair (a, b, shift) is evaluated iff b > a, or b == a with
 // shift > 0 lexicographically (the self pair, b == a with zero shift, is the
 // starred exclusion).
@@ -115,35 +116,28 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                      const int64_t* __restrict__ cell_off, int64_t N, int64_t c0, int64_t c1,
                      double* __restrict__ u, unsigned long long* __restrict__ pair_count, int* __restrict__ err) {
     constexpr int NS = Strength<KIND>::n;
-    __shared__ double ix_all[SYM_WARPS][3][32];
-    __shared__ double is_all[SYM_WARPS][NS][32];
-    __shared__ double iacc_all[SYM_WARPS][3][32];
     __shared__ double jx_all[SYM_WARPS][3][32];
     __shared__ double js_all[SYM_WARPS][NS][32];
     __shared__ double racc_all[SYM_WARPS][3][32];
     __shared__ long long jid_all[SYM_WARPS][32];
     __shared__ float jf_all[SYM_WARPS][3][32];
-    __shared__ uint16_t list_all[SYM_WARPS][1024];
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t cl = c0 + (int64_t)blockIdx.x * SYM_WARPS + warp;
     if (cl >= c1) return;
-    double(*ix)[32] = ix_all[warp];
-    double(*is)[32] = is_all[warp];
-    double(*iacc)[32] = iacc_all[warp];
     double(*jx)[32] = jx_all[warp];
     double(*js)[32] = js_all[warp];
     double(*racc)[32] = racc_all[warp];
     long long* jid = jid_all[warp];
     float(*jf)[32] = jf_all[warp];
-    uint16_t* list = list_all[warp];
-    const unsigned lt_mask = (1u << lane) - 1u;
 
     const int64_t istart = cl * 32;
     const int64_t ia = istart + lane;
     const bool valid = ia < N;
-    double xa0 = 0, xa1 = 0, xa2 = 0;
+    double xa0 = 0, xa1 = 0, xa2 = 0, fa[NS];
     long long ida = -1;
+#pragma unroll
+    for (int c = 0; c < NS; ++c) fa[c] = 0.0;
     if (valid) {
         const double* q = packed + ia * S;
         xa0 = q[0];
@@ -151,14 +145,9 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
         xa2 = q[2];
         ida = __double_as_longlong(q[3]);
 #pragma unroll
-        for (int c = 0; c < NS; ++c) is[c][lane] = q[4 + c];
+        for (int c = 0; c < NS; ++c) fa[c] = q[4 + c];
     }
-    ix[0][lane] = xa0;
-    ix[1][lane] = xa1;
-    ix[2][lane] = xa2;
-    iacc[0][lane] = 0.0;
-    iacc[1][lane] = 0.0;
-    iacc[2][lane] = 0.0;
+    double ua[3] = {0.0, 0.0, 0.0};
 
     double lo[3] = {valid ? xa0 : 1e300, valid ? xa1 : 1e300, valid ? xa2 : 1e300};
     double hi[3] = {valid ? xa0 : -1e300, valid ? xa1 : -1e300, valid ? xa2 : -1e300};
@@ -255,51 +244,53 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                             m |= (ok ? 1u : 0u) << s;
                         }
                     }
-                    // Phase 2: rotation-major compaction of (lane, s) pairs.
-                    int T = 0;
-#pragma unroll 4
-                    for (int s = 0; s < 32; ++s) {
-                        const bool bit = (m >> s) & 1u;
-                        const unsigned bal = __ballot_sync(0xffffffffu, bit);
-                        if (bit) list[T + __popc(bal & lt_mask)] = (uint16_t)(lane | (s << 5));
-                        T += __popc(bal);
-                    }
-                    __syncwarp();
-                    // Phase 3: all lanes evaluate compacted pairs.
-                    for (int e0 = 0; e0 < T; e0 += 32) {
-                        const int e = e0 + lane;
-                        if (e < T) {
-                            const int code = list[e];
-                            const int il = code & 31;
-                            const int j = (il + (code >> 5)) & 31;
-                            const double r0 = (ix[0][il] - jx[0][j]) - shx;
-                            const double r1 = (ix[1][il] - jx[1][j]) - shy;
-                            const double r2 = (ix[2][il] - jx[2][j]) - shz;
+                    // Phase 2: pack rotations into conflict-free rounds. A rotation s
+                    // pairs lane l with j = (l + s) mod 32; rotations whose lane
+                    // sets and j sets are disjoint from the current round join it,
+                    // so every lane evaluates at most one pair per round (its own
+                    // i, kept in registers) and every j is touched at most once
+                    // (plain shared-memory accumulation, no atomics).
+                    int s = 0;
+                    for (;;) {
+                        unsigned Lr = 0u, Jr = 0u;
+                        int my_s = -1;
+                        for (; s < 32; ++s) {
+                            const bool bit = (m >> s) & 1u;
+                            const unsigned Ls = __ballot_sync(0xffffffffu, bit);
+                            if (Ls == 0u) continue;
+                            const unsigned Js = __funnelshift_l(Ls, Ls, s);
+                            if ((Ls & Lr) | (Js & Jr)) break;
+                            Lr |= Ls;
+                            Jr |= Js;
+                            if (bit) my_s = s;
+                        }
+                        if (Lr == 0u) break;
+                        // Phase 3: exact fp64 test and kernel for this round.
+                        if (my_s >= 0) {
+                            const int j = (lane + my_s) & 31;
+                            const double r0 = (xa0 - jx[0][j]) - shx;
+                            const double r1 = (xa1 - jx[1][j]) - shy;
+                            const double r2 = (xa2 - jx[2][j]) - shz;
                             const double n2 =
                                 __dadd_rn(__dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1)), __dmul_rn(r2, r2));
                             if (n2 < rc2) {
                                 if (n2 == 0.0) {  // coincident distinct points (kernels.cpp:19-22)
                                     atomicExch(err, 1);
                                 } else {
-                                    double si[NS], sj[NS];
+                                    double sj[NS];
 #pragma unroll
-                                    for (int c = 0; c < NS; ++c) {
-                                        si[c] = is[c][il];
-                                        sj[c] = js[c][j];
-                                    }
+                                    for (int c = 0; c < NS; ++c) sj[c] = js[c][j];
                                     const Screened sc = screened(n2, a.xi, xi2);
-                                    double ua[3] = {0.0, 0.0, 0.0}, ub[3];
-                                    pair_both<KIND>(sc, xi2, n2, r0, r1, r2, sj, si, ua, ub);
-                                    atomicAdd(&iacc[0][il], ua[0]);
-                                    atomicAdd(&iacc[1][il], ua[1]);
-                                    atomicAdd(&iacc[2][il], ua[2]);
-                                    atomicAdd(&racc[0][j], ub[0]);
-                                    atomicAdd(&racc[1][j], ub[1]);
-                                    atomicAdd(&racc[2][j], ub[2]);
+                                    double ub[3];
+                                    pair_both<KIND>(sc, xi2, n2, r0, r1, r2, sj, fa, ua, ub);
+                                    racc[0][j] += ub[0];
+                                    racc[1][j] += ub[1];
+                                    racc[2][j] += ub[2];
                                     npairs += 2;
                                 }
                             }
                         }
+                        __syncwarp();
                     }
                     __syncwarp();
                     if (lane < cnt) {
@@ -312,12 +303,11 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
             }
         }
     }
-    __syncwarp();
     if (valid) {
         double* dst = u + 3 * ida;
-        atomicAdd(dst, iacc[0][lane]);
-        atomicAdd(dst + 1, iacc[1][lane]);
-        atomicAdd(dst + 2, iacc[2][lane]);
+        atomicAdd(dst, ua[0]);
+        atomicAdd(dst + 1, ua[1]);
+        atomicAdd(dst + 2, ua[2]);
     }
     if (pair_count) {
 #pragma unroll
