@@ -11,18 +11,13 @@
 // Work unit = one warp = one i-cluster of 32 consecutive particles in cell
 // order. Its bounding box selects the cell rows within rc; each row piece is
 // streamed as j-blocks of up to 32 particles into warp-private shared
-// memory. Per 32 x 32 block: (1) each lane tests its 32 rotations
-// (lane l with j = (l + s) mod 32) with a conservative fp32 bound and the half
-// rule, (2) the rotations are packed greedily into rounds whose lane sets and
-// j sets are disjoint (warp ballots + bit masks), (3) each round evaluates at
-// most one pair per lane (exact fp64 test + kernel) with its own i in
-// registers and each j touched once, so reactions accumulate in shared memory
-// without atomics; packing sparse rotations together keeps the fp64 path
-// occupied. Reactions are flushed to global memory with fp64 RED once per
-// j-block, the i sums once per cluster.
-// Half rule: a pair (a, b, shift) is evaluated iff b > a, or b == a with
-// shift > 0 lexicographically (the self pair, b == a with zero shift, is the
-// starred exclusion).
+// memory. The 32 x 32 block is swept in 32 lock-step rotations (lane l pairs
+// with j = (l + s) mod 32), so the j particles touched in one step are all
+// distinct: reactions accumulate in shared memory without atomics and are
+// flushed once per j-block with fp64 RED to global memory. Steps with no
+// accepted lane are skipped (warp vote). Half rule: a pair (a, b, shift) is
+// evaluated iff b > a, or b == a with shift > 0 lexicographically (the self
+// pair, b == a with zero shift, is the starred exclusion).
 #include "device_common.cuh"
 #include "sg_kernels.h"
 #include "screened_math.cuh"
@@ -147,7 +142,6 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
 #pragma unroll
         for (int c = 0; c < NS; ++c) fa[c] = q[4 + c];
     }
-    double ua[3] = {0.0, 0.0, 0.0};
 
     double lo[3] = {valid ? xa0 : 1e300, valid ? xa1 : 1e300, valid ? xa2 : 1e300};
     double hi[3] = {valid ? xa0 : -1e300, valid ? xa1 : -1e300, valid ? xa2 : -1e300};
@@ -173,6 +167,8 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
             chi[ax] = min(chi[ax], cg.n[ax] - 1);
         }
     }
+
+    double ua[3] = {0.0, 0.0, 0.0};
     unsigned long long npairs = 0;
 
     for (int cz = clo[2]; cz <= chi[2]; ++cz) {
@@ -229,68 +225,41 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                     racc[1][lane] = 0.0;
                     racc[2][lane] = 0.0;
                     __syncwarp();
-                    // Phase 1: this lane's candidate rotations (fp32 bound + half rule).
-                    const int dlt = (int)(istart - jb);  // pair (lane, j) is "after" iff j - lane > dlt
-                    unsigned m = 0u;
-                    if (valid) {
-#pragma unroll 8
-                        for (int s = 0; s < 32; ++s) {
-                            const int j = (lane + s) & 31;
-                            const int dj = j - lane;
-                            const bool order_ok = dj > dlt || (dj == dlt && pos_shift);
+                    // pair (lane, j) is "after" in sorted order iff j - lane > dlt
+                    const int dlt = (int)max((int64_t)-64, istart - jb);
+                    for (int s = 0; s < 32; ++s) {
+                        const int j = (lane + s) & 31;
+                        const int dj = j - lane;
+                        bool acc = valid && j < cnt && (dj > dlt || (dj == dlt && pos_shift));
+                        if (acc) {  // conservative fp32 pre-test (FP32 pipe)
                             const float d0 = tf0 - jf[0][j], d1 = tf1 - jf[1][j], d2 = tf2 - jf[2][j];
-                            const bool ok = j < cnt && order_ok &&
-                                            fmaf(d2, d2, fmaf(d1, d1, d0 * d0)) < a.thresh_f;
-                            m |= (ok ? 1u : 0u) << s;
+                            acc = fmaf(d2, d2, fmaf(d1, d1, d0 * d0)) < a.thresh_f;
                         }
-                    }
-                    // Phase 2: pack rotations into conflict-free rounds. A rotation s
-                    // pairs lane l with j = (l + s) mod 32; rotations whose lane
-                    // sets and j sets are disjoint from the current round join it,
-                    // so every lane evaluates at most one pair per round (its own
-                    // i, kept in registers) and every j is touched at most once
-                    // (plain shared-memory accumulation, no atomics).
-                    int s = 0;
-                    for (;;) {
-                        unsigned Lr = 0u, Jr = 0u;
-                        int my_s = -1;
-                        for (; s < 32; ++s) {
-                            const bool bit = (m >> s) & 1u;
-                            const unsigned Ls = __ballot_sync(0xffffffffu, bit);
-                            if (Ls == 0u) continue;
-                            const unsigned Js = __funnelshift_l(Ls, Ls, s);
-                            if ((Ls & Lr) | (Js & Jr)) break;
-                            Lr |= Ls;
-                            Jr |= Js;
-                            if (bit) my_s = s;
+                        if (!__any_sync(0xffffffffu, acc)) continue;
+                        double r0 = 0, r1 = 0, r2 = 0, n2 = 0;
+                        if (acc) {
+                            r0 = (xa0 - jx[0][j]) - shx;
+                            r1 = (xa1 - jx[1][j]) - shy;
+                            r2 = (xa2 - jx[2][j]) - shz;
+                            n2 = __dadd_rn(__dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1)), __dmul_rn(r2, r2));
+                            acc = n2 < rc2;
                         }
-                        if (Lr == 0u) break;
-                        // Phase 3: exact fp64 test and kernel for this round.
-                        if (my_s >= 0) {
-                            const int j = (lane + my_s) & 31;
-                            const double r0 = (xa0 - jx[0][j]) - shx;
-                            const double r1 = (xa1 - jx[1][j]) - shy;
-                            const double r2 = (xa2 - jx[2][j]) - shz;
-                            const double n2 =
-                                __dadd_rn(__dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1)), __dmul_rn(r2, r2));
-                            if (n2 < rc2) {
-                                if (n2 == 0.0) {  // coincident distinct points (kernels.cpp:19-22)
-                                    atomicExch(err, 1);
-                                } else {
-                                    double sj[NS];
+                        if (acc) {
+                            if (n2 == 0.0) {  // coincident distinct points (kernels.cpp:19-22)
+                                atomicExch(err, 1);
+                            } else {
+                                double sj[NS];
 #pragma unroll
-                                    for (int c = 0; c < NS; ++c) sj[c] = js[c][j];
-                                    const Screened sc = screened(n2, a.xi, xi2);
-                                    double ub[3];
-                                    pair_both<KIND>(sc, xi2, n2, r0, r1, r2, sj, fa, ua, ub);
-                                    racc[0][j] += ub[0];
-                                    racc[1][j] += ub[1];
-                                    racc[2][j] += ub[2];
-                                    npairs += 2;
-                                }
+                                for (int c = 0; c < NS; ++c) sj[c] = js[c][j];
+                                const Screened sc = screened(n2, a.xi, xi2);
+                                double ub[3];
+                                pair_both<KIND>(sc, xi2, n2, r0, r1, r2, sj, fa, ua, ub);
+                                racc[0][j] += ub[0];
+                                racc[1][j] += ub[1];
+                                racc[2][j] += ub[2];
+                                npairs += 2;
                             }
                         }
-                        __syncwarp();
                     }
                     __syncwarp();
                     if (lane < cnt) {
