@@ -274,15 +274,26 @@ void ensure_spread_order(sewald_gpu_session* s, int64_t i0, int64_t i1) {
     const int64_t n = i1 - i0;
     cudaStream_t st = s->ctx->stream;
     s->shape = spread_plan_shape(s->g, s->p.P);
-    const int nb = s->shape.nb[0] * s->shape.nb[1] * s->shape.nb[2];
+    s->sweep = sweep_shape(s->g, s->p.P);
+    static const bool sweep_enabled = [] {
+        const char* e = getenv("SEWALD_SPREAD_SWEEP");
+        return !(e && e[0] == '0');
+    }();
+    if (!sweep_enabled) s->sweep.ok = false;
+    const int64_t nb = s->sweep.ok ? s->sweep.nkeys
+                                   : (int64_t)s->shape.nb[0] * s->shape.nb[1] * s->shape.nb[2];
     s->sp_keys.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1));
     s->sp_keys2.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1));
     s->sp_vals.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1));
     s->sp_order.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1));
     s->sp_off.ensure(sizeof(int64_t) * (nb + 1));
     int* bad = s->flags.as<int>() + FLAG_SPREAD_BOX;
-    launch_spread_bucket(s->g, s->p.P, s->x.as<double>() + 3 * i0, n, s->shape,
-                         s->sp_keys.as<uint32_t>(), s->sp_vals.as<uint32_t>(), bad, st);
+    if (s->sweep.ok)
+        launch_sweep_bucket(s->g, s->p.P, s->x.as<double>() + 3 * i0, n, s->sweep, s->sp_keys.as<uint32_t>(),
+                            s->sp_vals.as<uint32_t>(), bad, st);
+    else
+        launch_spread_bucket(s->g, s->p.P, s->x.as<double>() + 3 * i0, n, s->shape,
+                             s->sp_keys.as<uint32_t>(), s->sp_vals.as<uint32_t>(), bad, st);
     ++s->ctx->launches;
     check_flag(s, FLAG_SPREAD_BOX, SEWALD_EINVAL,
                "point too close to the extended box boundary; free-direction padding is too small");
@@ -290,7 +301,7 @@ void ensure_spread_order(sewald_gpu_session* s, int64_t i0, int64_t i1) {
         sort_pairs(s, s->sp_keys.as<uint32_t>(), s->sp_keys2.as<uint32_t>(), s->sp_vals.as<uint32_t>(),
                    s->sp_order.as<uint32_t>(), n, bits_for((uint64_t)nb + 1));
     }
-    launch_bucket_offsets(s->sp_keys2.as<uint32_t>(), n, nb, s->sp_off.as<int64_t>(), st);
+    launch_bucket_offsets(s->sp_keys2.as<uint32_t>(), n, (int)nb, s->sp_off.as<int64_t>(), st);
     ++s->ctx->launches;
     s->sp_i0 = i0;
     s->sp_i1 = i1;
@@ -523,6 +534,14 @@ void session_spread(sewald_gpu_session* s, int64_t i0, int64_t i1, double* grid)
     ensure_spread_order(s, i0, i1);
     cudaStream_t st = s->ctx->stream;
     const int64_t vol = (int64_t)s->g.n[0] * s->g.n[1] * s->g.n[2];
+    if (s->sweep.ok) {
+        s->ctx->launches += launch_spread_sweep(s->g, s->w, s->x.as<double>() + 3 * i0, s->f.as<double>() + 3 * i0,
+                                                s->stresslet ? s->nu.as<double>() + 3 * i0 : nullptr, s->stresslet,
+                                                s->sp_order.as<uint32_t>(), s->sp_off.as<int64_t>(), s->sweep, grid,
+                                                st);
+        cuda_check(cudaGetLastError(), "spread sweep launch");
+        return;
+    }
     if (!s->shape.tiled) {
         cuda_check(cudaMemsetAsync(grid, 0, sizeof(double) * s->C * vol, st), "grid zero");
         launch_spread_atomic(s->g, s->w, s->x.as<double>() + 3 * i0, s->f.as<double>() + 3 * i0,

@@ -33,6 +33,20 @@ void launch_gather(const DevGrid& g, const DevWindow& w, const double* grid, con
 void launch_stencil_bounds(const DevGrid& g, int P, const double* x, int64_t N, int* bad,
                            cudaStream_t st);
 
+// z-sweep spread (spread_sweep.cu): buckets = 4x8 (x,y) patches x z start.
+struct SweepShape {
+    int nbx, nby, nseg;
+    int64_t nkeys;
+    bool ok;
+};
+SweepShape sweep_shape(const DevGrid& g, int P);
+void launch_sweep_bucket(const DevGrid& g, int P, const double* x, int64_t N, const SweepShape& s, uint32_t* keys,
+                         uint32_t* vals, int* bad, cudaStream_t st);
+// Returns the number of kernel launches issued.
+int launch_spread_sweep(const DevGrid& g, const DevWindow& w, const double* x, const double* f, const double* nu,
+                        int stresslet, const uint32_t* order, const int64_t* off, const SweepShape& s, double* out,
+                        cudaStream_t st);
+
 // ---- real space (realspace.cu) -------------------------------------------
 struct CellGrid {
     int d;

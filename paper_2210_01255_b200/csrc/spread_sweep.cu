@@ -1,0 +1,351 @@
+// Spread by z-sweep: output-stationary in (x, y), register ring in z.
+//
+// Reference: spread /root/reference/proj/src/fourier.cpp:237-274 (stencil
+// :168-188). Same window values, stencil origins and periodic wrap; only the
+// summation order differs.
+//
+// One CTA = one warp = one 4 x 8 (x, y) patch of grid columns and one z
+// segment. Each lane owns one column and keeps a ring of WIN = PMAX + ZSTEP - 1
+// z-planes x NC components in registers. Points are bucketed by the (x, y)
+// patch of their stencil start and sorted by their z start. The warp sweeps z
+// in windows of ZSTEP planes: for every window it streams the points whose z
+// start falls inside the window from the relevant buckets through shared
+// memory (lanes evaluate the window taps in parallel from a shared copy of
+// the PKB table), adds each point's P x P x P block with a compile-time
+// register offset (switch over the point's offset inside the window: exactly
+// P z-taps per point, no padding waste), then stores the ZSTEP planes that no
+// later point can reach and rotates the ring. Every grid value is written
+// exactly once; no atomics.
+#include "device_common.cuh"
+#include "sg_kernels.h"
+
+#include <algorithm>
+
+namespace sewald_b200 {
+
+namespace {
+
+constexpr int SX = 4, SY = 8;  // (x, y) patch per warp
+
+__device__ __forceinline__ int wrapi(int j, int n) {
+    j %= n;
+    return j < 0 ? j + n : j;
+}
+
+// Window value with the PKB table read from shared memory (per-lane rows).
+__device__ __forceinline__ double window_eval_s(const DevWindow& w, const double* coef, double r) {
+    if (fabs(r) > w.half_width) return 0.0;
+    if (w.kind == 1) {
+        int l = (int)floor(r / w.h);
+        l = l < -w.P / 2 ? -w.P / 2 : (l > w.P / 2 - 1 ? w.P / 2 - 1 : l);
+        const double u = 2.0 * (r - l * w.h) / w.h - 1.0;
+        const double* c = coef + (l + w.P / 2) * (w.nu + 1);
+        double acc = 0.0;
+        for (int i = w.nu; i >= 0; --i) acc = c[i] + acc * u;
+        return acc;
+    }
+    const double t = r / w.half_width;
+    if (w.kind == 2) return exp(-w.alpha * t * t);
+    const double arg = fmax(1.0 - t * t, 0.0);
+    return cyl_bessel_i0(w.beta * sqrt(arg)) / w.i0_beta;
+}
+
+// Bucket key: (bx, by) patch of the wrapped stencil start, then z start.
+__global__ void sweep_bucket_kernel(DevGrid g, int P, const double* __restrict__ x, int64_t N, int nby,
+                                    uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, int* __restrict__ bad) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    int s[3];
+    for (int ax = 0; ax < 3; ++ax) {
+        int j0;
+        double rel;
+        stencil_origin(g, P, ax, x[3 * i + ax], j0, rel);
+        if (ax < g.d) {
+            j0 = wrapi(j0, g.n[ax]);
+        } else if (j0 < 0 || j0 + P > g.n[ax]) {
+            atomicExch(bad, 1);
+            j0 = 0;
+        }
+        s[ax] = j0;
+    }
+    keys[i] = (uint32_t)(((int64_t)(s[0] / SX) * nby + s[1] / SY) * g.n[2] + s[2]);
+    vals[i] = (uint32_t)i;
+}
+
+struct Pieces {
+    int lo[2], hi[2], n;
+};
+
+// Bucket index ranges along x or y whose stencil starts reach [T0, T0+T).
+__device__ __forceinline__ Pieces reach(int T0, int T, int n, int P, bool periodic, int nb) {
+    Pieces p;
+    int s_lo = T0 - P + 1, s_hi = min(T0 + T - 1, n - 1);
+    if (!periodic) {
+        s_lo = max(s_lo, 0);
+        p.n = 1;
+        p.lo[0] = s_lo / T;
+        p.hi[0] = s_hi / T;
+        return p;
+    }
+    if (s_lo >= 0) {
+        p.n = 1;
+        p.lo[0] = s_lo / T;
+        p.hi[0] = s_hi / T;
+        return p;
+    }
+    p.n = 2;
+    p.lo[0] = 0;
+    p.hi[0] = s_hi / T;
+    p.lo[1] = (s_lo + n) / T;
+    p.hi[1] = nb - 1;
+    if (p.lo[1] <= p.hi[0]) {
+        p.n = 1;
+        p.lo[0] = 0;
+        p.hi[0] = nb - 1;
+    }
+    return p;
+}
+
+__device__ __forceinline__ int delta_to(int T0, int s, int n, bool periodic, int P) {
+    int d = T0 - s;
+    if (periodic) {
+        d %= n;
+        if (d < 0) d += n;
+        if (d > P - 1) d -= n;
+    }
+    return d;
+}
+
+template <int PMAX, int NC, int ZSTEP>
+struct Ring {
+    static constexpr int WIN = PMAX + ZSTEP - 1;
+    double a[WIN][NC];
+};
+
+template <int PMAX, int NC, int ZSTEP, int O>
+__device__ __forceinline__ void add_block(double (&acc)[PMAX + ZSTEP - 1][NC], const double* s, const double* wz) {
+#pragma unroll
+    for (int k = 0; k < PMAX; ++k) {
+        const double w = wz[k];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[O + k][c] = fma(s[c], w, acc[O + k][c]);
+    }
+}
+
+template <int PMAX, int NC, int ZSTEP>
+__global__ void __launch_bounds__(32)
+spread_sweep_kernel(DevGrid g, DevWindow win, const double* __restrict__ x, const double* __restrict__ f,
+                    const double* __restrict__ nu, int stresslet, int comp0, const uint32_t* __restrict__ order,
+                    const int64_t* __restrict__ off, int nbx, int nby, int nseg, double* __restrict__ out) {
+    constexpr int WIN = PMAX + ZSTEP - 1;
+    __shared__ double coef[kMaxP * (kMaxNu + 1)];
+    __shared__ double pwx[32][SX];
+    __shared__ double pwy[32][SY];
+    __shared__ double pwz[32][PMAX];
+    __shared__ double ps[32][NC];
+    __shared__ int pdx[32], pdy[32], po[32];
+    __shared__ uint32_t cidx[32];
+
+    const int lane = threadIdx.x;
+    const int tx = lane % SX, ty = lane / SX;
+    const int bxt = blockIdx.x % nbx, byt = blockIdx.x / nbx;
+    const int X0 = bxt * SX, Y0 = byt * SY;
+    const int n2 = g.n[2];
+    const int seg = blockIdx.y;
+    const int z0 = (int)((int64_t)n2 * seg / nseg), z1 = (int)((int64_t)n2 * (seg + 1) / nseg);
+    const int P = win.P;
+    const bool perx = g.d > 0, pery = g.d > 1, perz = g.d > 2;
+
+    if (win.kind == 1)
+        for (int e = lane; e < P * (win.nu + 1); e += 32) coef[e] = win.coef[e];
+    __syncwarp();
+
+    const Pieces px = reach(X0, SX, g.n[0], P, perx, nbx);
+    const Pieces py = reach(Y0, SY, g.n[1], P, pery, nby);
+
+    double acc[WIN][NC];
+#pragma unroll
+    for (int w = 0; w < WIN; ++w)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[w][c] = 0.0;
+
+    const int zpre = ((P - 1 + ZSTEP - 1) / ZSTEP) * ZSTEP;
+    const int gx = X0 + tx, gy = Y0 + ty;
+    const bool own = gx < g.n[0] && gy < g.n[1];
+    const int64_t cs = (int64_t)g.n[0] * g.n[1] * n2;
+    double* col = out + ((int64_t)gx * g.n[1] + gy) * n2;
+
+    for (int zb = z0 - zpre; zb < z1; zb += ZSTEP) {
+        // z-start range [zb, zb + ZSTEP) as at most two wrapped key runs
+        int zr_lo[2], zr_hi[2], nzr = 0;
+        if (perz) {
+            int a = zb, b = zb + ZSTEP - 1;
+            if (b - a + 1 >= n2) {
+                zr_lo[0] = 0; zr_hi[0] = n2 - 1; nzr = 1;
+            } else {
+                int aw = wrapi(a, n2), bw = wrapi(b, n2);
+                if (aw <= bw) { zr_lo[0] = aw; zr_hi[0] = bw; nzr = 1; }
+                else { zr_lo[0] = aw; zr_hi[0] = n2 - 1; zr_lo[1] = 0; zr_hi[1] = bw; nzr = 2; }
+            }
+        } else {
+            const int a = max(zb, 0), b = min(zb + ZSTEP - 1, n2 - 1);
+            if (a <= b) { zr_lo[0] = a; zr_hi[0] = b; nzr = 1; }
+        }
+        int filled = 0;
+        // iterate the relevant buckets and their key runs; process full chunks
+        for (int ip = 0; ip < px.n; ++ip)
+        for (int bx = px.lo[ip]; bx <= px.hi[ip]; ++bx)
+        for (int jp = 0; jp < py.n; ++jp)
+        for (int by = py.lo[jp]; by <= py.hi[jp]; ++by)
+        for (int r = 0; r < nzr; ++r) {
+            const int64_t kb = ((int64_t)bx * nby + by) * n2;
+            int64_t p0 = off[kb + zr_lo[r]];
+            const int64_t p1 = off[kb + zr_hi[r] + 1];
+            while (p0 < p1) {
+                const int take = (int)min((int64_t)(32 - filled), p1 - p0);
+                if (lane < take) cidx[filled + lane] = order[p0 + lane];
+                filled += take;
+                p0 += take;
+                if (filled < 32) break;
+                // ---- stage + accumulate a full chunk (executed by the macro below)
+#define SEWALD_SWEEP_CHUNK(CNT)                                                                       \
+                {                                                                                     \
+                    __syncwarp();                                                                     \
+                    if (lane < (CNT)) {                                                               \
+                        const int64_t i = cidx[lane];                                                 \
+                        int j0[3];                                                                    \
+                        double rel[3];                                                                \
+                        for (int a = 0; a < 3; ++a) stencil_origin(g, P, a, x[3 * i + a], j0[a], rel[a]); \
+                        const int swx = perx ? wrapi(j0[0], g.n[0]) : j0[0];                          \
+                        const int swy = pery ? wrapi(j0[1], g.n[1]) : j0[1];                          \
+                        const int swz = perz ? wrapi(j0[2], n2) : j0[2];                              \
+                        const int dx = delta_to(X0, swx, g.n[0], perx, P);                            \
+                        const int dy = delta_to(Y0, swy, g.n[1], pery, P);                            \
+                        pdx[lane] = dx;                                                               \
+                        pdy[lane] = dy;                                                               \
+                        po[lane] = perz ? wrapi(swz - zb, n2) : swz - zb;                             \
+                        for (int t = 0; t < SX; ++t) {                                                \
+                            const int p = dx + t;                                                     \
+                            pwx[lane][t] = (p >= 0 && p < P)                                          \
+                                ? window_eval_s(win, coef, ((double)(j0[0] + p) - rel[0]) * g.h) : 0.0; \
+                        }                                                                             \
+                        for (int t = 0; t < SY; ++t) {                                                \
+                            const int p = dy + t;                                                     \
+                            pwy[lane][t] = (p >= 0 && p < P)                                          \
+                                ? window_eval_s(win, coef, ((double)(j0[1] + p) - rel[1]) * g.h) : 0.0; \
+                        }                                                                             \
+                        for (int k = 0; k < PMAX; ++k)                                                \
+                            pwz[lane][k] = k < P                                                      \
+                                ? window_eval_s(win, coef, ((double)(j0[2] + k) - rel[2]) * g.h) : 0.0; \
+                        if (!stresslet) {                                                             \
+                            for (int c = 0; c < NC; ++c) ps[lane][c] = f[3 * i + comp0 + c];          \
+                        } else {                                                                      \
+                            for (int c = 0; c < NC; ++c) {                                            \
+                                const int cc = comp0 + c;                                             \
+                                ps[lane][c] = f[3 * i + cc / 3] * nu[3 * i + cc % 3];                 \
+                            }                                                                         \
+                        }                                                                             \
+                    }                                                                                 \
+                    __syncwarp();                                                                     \
+                    for (int k = 0; k < (CNT); ++k) {                                                 \
+                        const int ox = pdx[k] + tx, oy = pdy[k] + ty;                                 \
+                        if (ox < 0 || ox >= P || oy < 0 || oy >= P) continue;                         \
+                        const double wxy = pwx[k][tx] * pwy[k][ty];                                   \
+                        double sv[NC];                                                                \
+                        for (int c = 0; c < NC; ++c) sv[c] = wxy * ps[k][c];                          \
+                        const double* wz = pwz[k];                                                    \
+                        switch (po[k]) {                                                              \
+                            case 0: add_block<PMAX, NC, ZSTEP, 0>(acc, sv, wz); break;                \
+                            case 1: if (ZSTEP > 1) add_block<PMAX, NC, ZSTEP, (ZSTEP > 1 ? 1 : 0)>(acc, sv, wz); break; \
+                            case 2: if (ZSTEP > 2) add_block<PMAX, NC, ZSTEP, (ZSTEP > 2 ? 2 : 0)>(acc, sv, wz); break; \
+                            default: if (ZSTEP > 3) add_block<PMAX, NC, ZSTEP, (ZSTEP > 3 ? 3 : 0)>(acc, sv, wz); break; \
+                        }                                                                             \
+                    }                                                                                 \
+                    __syncwarp();                                                                     \
+                }
+                SEWALD_SWEEP_CHUNK(32)
+                filled = 0;
+            }
+        }
+        if (filled > 0) {
+            SEWALD_SWEEP_CHUNK(filled)
+            filled = 0;
+        }
+#undef SEWALD_SWEEP_CHUNK
+        // planes [zb, zb + ZSTEP) are final: store the owned ones, rotate
+        if (own) {
+#pragma unroll
+            for (int q = 0; q < ZSTEP; ++q) {
+                const int z = zb + q;
+                if (z >= z0 && z < z1)
+#pragma unroll
+                    for (int c = 0; c < NC; ++c) col[(int64_t)(comp0 + c) * cs + z] = acc[q][c];
+            }
+        }
+#pragma unroll
+        for (int w = 0; w < WIN - ZSTEP; ++w)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) acc[w][c] = acc[w + ZSTEP][c];
+#pragma unroll
+        for (int w = WIN - ZSTEP; w < WIN; ++w)
+#pragma unroll
+            for (int c = 0; c < NC; ++c) acc[w][c] = 0.0;
+    }
+}
+
+template <int PMAX, int NC, int ZSTEP>
+void launch_sweep(const DevGrid& g, const DevWindow& w, const double* x, const double* f, const double* nu,
+                  int stresslet, const uint32_t* order, const int64_t* off, int nbx, int nby, int nseg,
+                  double* out, cudaStream_t st) {
+    const int C = stresslet ? 9 : 3;
+    dim3 grid(nbx * nby, nseg);
+    for (int c0 = 0; c0 < C; c0 += NC)
+        spread_sweep_kernel<PMAX, NC, ZSTEP><<<grid, 32, 0, st>>>(g, w, x, f, nu, stresslet, c0, order, off, nbx,
+                                                                  nby, nseg, out);
+}
+
+}  // namespace
+
+SweepShape sweep_shape(const DevGrid& g, int P) {
+    SweepShape s{};
+    s.nbx = (g.n[0] + SX - 1) / SX;
+    s.nby = (g.n[1] + SY - 1) / SY;
+    s.nkeys = (int64_t)s.nbx * s.nby * g.n[2];
+    s.ok = P <= 32 && s.nkeys < (int64_t(1) << 31);
+    if (g.d > 0 && P + SX - 1 > g.n[0]) s.ok = false;
+    if (g.d > 1 && P + SY - 1 > g.n[1]) s.ok = false;
+    if (g.d > 2 && P > g.n[2]) s.ok = false;
+    const int tiles = s.nbx * s.nby;
+    int nseg = (6 * 148 + tiles - 1) / tiles;
+    const int maxseg = std::max(1, g.n[2] / (2 * std::max(P, 4)));
+    s.nseg = std::max(1, std::min(nseg, maxseg));
+    return s;
+}
+
+void launch_sweep_bucket(const DevGrid& g, int P, const double* x, int64_t N, const SweepShape& s, uint32_t* keys,
+                         uint32_t* vals, int* bad, cudaStream_t st) {
+    if (N == 0) return;
+    sweep_bucket_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(g, P, x, N, s.nby, keys, vals, bad);
+}
+
+int launch_spread_sweep(const DevGrid& g, const DevWindow& w, const double* x, const double* f, const double* nu,
+                        int stresslet, const uint32_t* order, const int64_t* off, const SweepShape& s, double* out,
+                        cudaStream_t st) {
+    const int P = w.P;
+    if (P <= 8) {
+        launch_sweep<8, 3, 4>(g, w, x, f, nu, stresslet, order, off, s.nbx, s.nby, s.nseg, out, st);
+        return stresslet ? 3 : 1;
+    }
+    if (P <= 16) {
+        launch_sweep<16, 3, 4>(g, w, x, f, nu, stresslet, order, off, s.nbx, s.nby, s.nseg, out, st);
+        return stresslet ? 3 : 1;
+    }
+    if (P <= 24) {
+        launch_sweep<24, 3, 2>(g, w, x, f, nu, stresslet, order, off, s.nbx, s.nby, s.nseg, out, st);
+        return stresslet ? 3 : 1;
+    }
+    launch_sweep<32, 1, 4>(g, w, x, f, nu, stresslet, order, off, s.nbx, s.nby, s.nseg, out, st);
+    return stresslet ? 9 : 3;
+}
+
+}  // namespace sewald_b200
