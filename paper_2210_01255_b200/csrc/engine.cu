@@ -535,10 +535,16 @@ void session_spread(sewald_gpu_session* s, int64_t i0, int64_t i1, double* grid)
     cudaStream_t st = s->ctx->stream;
     const int64_t vol = (int64_t)s->g.n[0] * s->g.n[1] * s->g.n[2];
     if (s->sweep.ok) {
-        s->ctx->launches += launch_spread_sweep(s->g, s->w, s->x.as<double>() + 3 * i0, s->f.as<double>() + 3 * i0,
-                                                s->stresslet ? s->nu.as<double>() + 3 * i0 : nullptr, s->stresslet,
-                                                s->sp_order.as<uint32_t>(), s->sp_off.as<int64_t>(), s->sweep, grid,
-                                                st);
+        const int64_t n = i1 - i0;
+        const int P = s->p.P;
+        double* W = static_cast<double*>(s->sp_w.ensure(sizeof(double) * 3 * P * std::max<int64_t>(n, 1)));
+        int4* SW = static_cast<int4*>(s->sp_sw.ensure(sizeof(int4) * std::max<int64_t>(n, 1)));
+        double* STR = static_cast<double*>(s->sp_str.ensure(sizeof(double) * s->C * std::max<int64_t>(n, 1)));
+        launch_sweep_weights(s->g, s->w, s->x.as<double>() + 3 * i0, s->f.as<double>() + 3 * i0,
+                             s->stresslet ? s->nu.as<double>() + 3 * i0 : nullptr, s->stresslet,
+                             s->sp_order.as<uint32_t>(), n, W, SW, STR, st);
+        s->ctx->launches += 1 + launch_spread_sweep(s->g, P, W, SW, STR, s->C, s->sp_off.as<int64_t>(), s->sweep,
+                                                    grid, st);
         cuda_check(cudaGetLastError(), "spread sweep launch");
         return;
     }

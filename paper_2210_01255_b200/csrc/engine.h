@@ -71,7 +71,7 @@ struct sewald_gpu_session {
     int64_t sp_i0 = -1, sp_i1 = -1;
     sewald_b200::SpreadPlanShape shape{};
     sewald_b200::SweepShape sweep{};
-    sewald_b200::DevBuf sp_keys, sp_keys2, sp_vals, sp_order, sp_off, cub_tmp;
+    sewald_b200::DevBuf sp_keys, sp_keys2, sp_vals, sp_order, sp_off, cub_tmp, sp_w, sp_sw, sp_str;
     // real-space cell list
     sewald_b200::CellGrid cg{};
     bool cells_ready = false;

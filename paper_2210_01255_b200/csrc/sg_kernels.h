@@ -42,10 +42,14 @@ struct SweepShape {
 SweepShape sweep_shape(const DevGrid& g, int P);
 void launch_sweep_bucket(const DevGrid& g, int P, const double* x, int64_t N, const SweepShape& s, uint32_t* keys,
                          uint32_t* vals, int* bad, cudaStream_t st);
+// Per-point taps / starts / strengths in bucket-sorted order (W: N*3*P,
+// SW: N int4, STR: N*C).
+void launch_sweep_weights(const DevGrid& g, const DevWindow& w, const double* x, const double* f, const double* nu,
+                          int stresslet, const uint32_t* order, int64_t N, double* W, int4* SW, double* STR,
+                          cudaStream_t st);
 // Returns the number of kernel launches issued.
-int launch_spread_sweep(const DevGrid& g, const DevWindow& w, const double* x, const double* f, const double* nu,
-                        int stresslet, const uint32_t* order, const int64_t* off, const SweepShape& s, double* out,
-                        cudaStream_t st);
+int launch_spread_sweep(const DevGrid& g, int P, const double* W, const int4* SW, const double* STR, int C,
+                        const int64_t* off, const SweepShape& s, double* out, cudaStream_t st);
 
 // ---- real space (realspace.cu) -------------------------------------------
 struct CellGrid {

@@ -32,24 +32,6 @@ __device__ __forceinline__ int wrapi(int j, int n) {
     return j < 0 ? j + n : j;
 }
 
-// Window value with the PKB table read from shared memory (per-lane rows).
-__device__ __forceinline__ double window_eval_s(const DevWindow& w, const double* coef, double r) {
-    if (fabs(r) > w.half_width) return 0.0;
-    if (w.kind == 1) {
-        int l = (int)floor(r / w.h);
-        l = l < -w.P / 2 ? -w.P / 2 : (l > w.P / 2 - 1 ? w.P / 2 - 1 : l);
-        const double u = 2.0 * (r - l * w.h) / w.h - 1.0;
-        const double* c = coef + (l + w.P / 2) * (w.nu + 1);
-        double acc = 0.0;
-        for (int i = w.nu; i >= 0; --i) acc = c[i] + acc * u;
-        return acc;
-    }
-    const double t = r / w.half_width;
-    if (w.kind == 2) return exp(-w.alpha * t * t);
-    const double arg = fmax(1.0 - t * t, 0.0);
-    return cyl_bessel_i0(w.beta * sqrt(arg)) / w.i0_beta;
-}
-
 // Bucket key: (bx, by) patch of the wrapped stencil start, then z start.
 __global__ void sweep_bucket_kernel(DevGrid g, int P, const double* __restrict__ x, int64_t N, int nby,
                                     uint32_t* __restrict__ keys, uint32_t* __restrict__ vals, int* __restrict__ bad) {
@@ -70,6 +52,36 @@ __global__ void sweep_bucket_kernel(DevGrid g, int P, const double* __restrict__
     }
     keys[i] = (uint32_t)(((int64_t)(s[0] / SX) * nby + s[1] / SY) * g.n[2] + s[2]);
     vals[i] = (uint32_t)i;
+}
+
+// Per-point stencil data in bucket-sorted order (computed once per spread,
+// not once per tile): the P window taps of each axis with the reference's
+// per-tap formula (fourier.cpp:181-186), the wrapped stencil starts, and the
+// strength components (stresslet: q_l nu_m, fourier.cpp:253-258).
+__global__ void sweep_weights_kernel(DevGrid g, DevWindow win, const double* __restrict__ x,
+                                     const double* __restrict__ f, const double* __restrict__ nu, int stresslet,
+                                     const uint32_t* __restrict__ order, int64_t N, double* __restrict__ W,
+                                     int4* __restrict__ SW, double* __restrict__ STR) {
+    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (k >= N) return;
+    const int64_t i = order[k];
+    const int P = win.P;
+    int sw[3];
+    for (int ax = 0; ax < 3; ++ax) {
+        int j0;
+        double rel;
+        stencil_origin(g, P, ax, x[3 * i + ax], j0, rel);
+        double* w = W + (k * 3 + ax) * P;
+        for (int p = 0; p < P; ++p) w[p] = window_eval(win, ((double)(j0 + p) - rel) * g.h);
+        sw[ax] = ax < g.d ? wrapi(j0, g.n[ax]) : j0;
+    }
+    SW[k] = make_int4(sw[0], sw[1], sw[2], 0);
+    if (!stresslet) {
+        for (int c = 0; c < 3; ++c) STR[k * 3 + c] = f[3 * i + c];
+    } else {
+        for (int l = 0; l < 3; ++l)
+            for (int m = 0; m < 3; ++m) STR[k * 9 + 3 * l + m] = f[3 * i + l] * nu[3 * i + m];
+    }
 }
 
 struct Pieces {
@@ -134,11 +146,10 @@ __device__ __forceinline__ void add_block(double (&acc)[PMAX + ZSTEP - 1][NC], c
 
 template <int PMAX, int NC, int ZSTEP>
 __global__ void __launch_bounds__(32)
-spread_sweep_kernel(DevGrid g, DevWindow win, const double* __restrict__ x, const double* __restrict__ f,
-                    const double* __restrict__ nu, int stresslet, int comp0, const uint32_t* __restrict__ order,
-                    const int64_t* __restrict__ off, int nbx, int nby, int nseg, double* __restrict__ out) {
+spread_sweep_kernel(DevGrid g, int P, const double* __restrict__ W, const int4* __restrict__ SW,
+                    const double* __restrict__ STR, int C, int comp0, const int64_t* __restrict__ off, int nbx,
+                    int nby, int nseg, double* __restrict__ out) {
     constexpr int WIN = PMAX + ZSTEP - 1;
-    __shared__ double coef[kMaxP * (kMaxNu + 1)];
     __shared__ double pwx[32][SX];
     __shared__ double pwy[32][SY];
     __shared__ double pwz[32][PMAX];
@@ -153,12 +164,7 @@ spread_sweep_kernel(DevGrid g, DevWindow win, const double* __restrict__ x, cons
     const int n2 = g.n[2];
     const int seg = blockIdx.y;
     const int z0 = (int)((int64_t)n2 * seg / nseg), z1 = (int)((int64_t)n2 * (seg + 1) / nseg);
-    const int P = win.P;
     const bool perx = g.d > 0, pery = g.d > 1, perz = g.d > 2;
-
-    if (win.kind == 1)
-        for (int e = lane; e < P * (win.nu + 1); e += 32) coef[e] = win.coef[e];
-    __syncwarp();
 
     const Pieces px = reach(X0, SX, g.n[0], P, perx, nbx);
     const Pieces py = reach(Y0, SY, g.n[1], P, pery, nby);
@@ -203,7 +209,7 @@ spread_sweep_kernel(DevGrid g, DevWindow win, const double* __restrict__ x, cons
             const int64_t p1 = off[kb + zr_hi[r] + 1];
             while (p0 < p1) {
                 const int take = (int)min((int64_t)(32 - filled), p1 - p0);
-                if (lane < take) cidx[filled + lane] = order[p0 + lane];
+                if (lane < take) cidx[filled + lane] = (uint32_t)(p0 + lane);
                 filled += take;
                 p0 += take;
                 if (filled < 32) break;
@@ -212,39 +218,24 @@ spread_sweep_kernel(DevGrid g, DevWindow win, const double* __restrict__ x, cons
                 {                                                                                     \
                     __syncwarp();                                                                     \
                     if (lane < (CNT)) {                                                               \
-                        const int64_t i = cidx[lane];                                                 \
-                        int j0[3];                                                                    \
-                        double rel[3];                                                                \
-                        for (int a = 0; a < 3; ++a) stencil_origin(g, P, a, x[3 * i + a], j0[a], rel[a]); \
-                        const int swx = perx ? wrapi(j0[0], g.n[0]) : j0[0];                          \
-                        const int swy = pery ? wrapi(j0[1], g.n[1]) : j0[1];                          \
-                        const int swz = perz ? wrapi(j0[2], n2) : j0[2];                              \
-                        const int dx = delta_to(X0, swx, g.n[0], perx, P);                            \
-                        const int dy = delta_to(Y0, swy, g.n[1], pery, P);                            \
+                        const int64_t kk = cidx[lane];                                                \
+                        const int4 sw = SW[kk];                                                       \
+                        const double* wrow = W + kk * 3 * P;                                          \
+                        const int dx = delta_to(X0, sw.x, g.n[0], perx, P);                           \
+                        const int dy = delta_to(Y0, sw.y, g.n[1], pery, P);                           \
                         pdx[lane] = dx;                                                               \
                         pdy[lane] = dy;                                                               \
-                        po[lane] = perz ? wrapi(swz - zb, n2) : swz - zb;                             \
+                        po[lane] = perz ? wrapi(sw.z - zb, n2) : sw.z - zb;                           \
                         for (int t = 0; t < SX; ++t) {                                                \
                             const int p = dx + t;                                                     \
-                            pwx[lane][t] = (p >= 0 && p < P)                                          \
-                                ? window_eval_s(win, coef, ((double)(j0[0] + p) - rel[0]) * g.h) : 0.0; \
+                            pwx[lane][t] = (p >= 0 && p < P) ? __ldg(wrow + p) : 0.0;                 \
                         }                                                                             \
                         for (int t = 0; t < SY; ++t) {                                                \
                             const int p = dy + t;                                                     \
-                            pwy[lane][t] = (p >= 0 && p < P)                                          \
-                                ? window_eval_s(win, coef, ((double)(j0[1] + p) - rel[1]) * g.h) : 0.0; \
+                            pwy[lane][t] = (p >= 0 && p < P) ? __ldg(wrow + P + p) : 0.0;             \
                         }                                                                             \
-                        for (int k = 0; k < PMAX; ++k)                                                \
-                            pwz[lane][k] = k < P                                                      \
-                                ? window_eval_s(win, coef, ((double)(j0[2] + k) - rel[2]) * g.h) : 0.0; \
-                        if (!stresslet) {                                                             \
-                            for (int c = 0; c < NC; ++c) ps[lane][c] = f[3 * i + comp0 + c];          \
-                        } else {                                                                      \
-                            for (int c = 0; c < NC; ++c) {                                            \
-                                const int cc = comp0 + c;                                             \
-                                ps[lane][c] = f[3 * i + cc / 3] * nu[3 * i + cc % 3];                 \
-                            }                                                                         \
-                        }                                                                             \
+                        for (int k = 0; k < PMAX; ++k) pwz[lane][k] = k < P ? __ldg(wrow + 2 * P + k) : 0.0; \
+                        for (int c = 0; c < NC; ++c) ps[lane][c] = __ldg(STR + kk * C + comp0 + c);   \
                     }                                                                                 \
                     __syncwarp();                                                                     \
                     for (int k = 0; k < (CNT); ++k) {                                                 \
@@ -294,14 +285,13 @@ spread_sweep_kernel(DevGrid g, DevWindow win, const double* __restrict__ x, cons
 }
 
 template <int PMAX, int NC, int ZSTEP>
-void launch_sweep(const DevGrid& g, const DevWindow& w, const double* x, const double* f, const double* nu,
-                  int stresslet, const uint32_t* order, const int64_t* off, int nbx, int nby, int nseg,
-                  double* out, cudaStream_t st) {
-    const int C = stresslet ? 9 : 3;
+int launch_sweep(const DevGrid& g, int P, const double* W, const int4* SW, const double* STR, int C,
+                 const int64_t* off, int nbx, int nby, int nseg, double* out, cudaStream_t st) {
     dim3 grid(nbx * nby, nseg);
-    for (int c0 = 0; c0 < C; c0 += NC)
-        spread_sweep_kernel<PMAX, NC, ZSTEP><<<grid, 32, 0, st>>>(g, w, x, f, nu, stresslet, c0, order, off, nbx,
-                                                                  nby, nseg, out);
+    int n = 0;
+    for (int c0 = 0; c0 < C; c0 += NC, ++n)
+        spread_sweep_kernel<PMAX, NC, ZSTEP><<<grid, 32, 0, st>>>(g, P, W, SW, STR, C, c0, off, nbx, nby, nseg, out);
+    return n;
 }
 
 }  // namespace
@@ -328,24 +318,20 @@ void launch_sweep_bucket(const DevGrid& g, int P, const double* x, int64_t N, co
     sweep_bucket_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(g, P, x, N, s.nby, keys, vals, bad);
 }
 
-int launch_spread_sweep(const DevGrid& g, const DevWindow& w, const double* x, const double* f, const double* nu,
-                        int stresslet, const uint32_t* order, const int64_t* off, const SweepShape& s, double* out,
-                        cudaStream_t st) {
-    const int P = w.P;
-    if (P <= 8) {
-        launch_sweep<8, 3, 4>(g, w, x, f, nu, stresslet, order, off, s.nbx, s.nby, s.nseg, out, st);
-        return stresslet ? 3 : 1;
-    }
-    if (P <= 16) {
-        launch_sweep<16, 3, 4>(g, w, x, f, nu, stresslet, order, off, s.nbx, s.nby, s.nseg, out, st);
-        return stresslet ? 3 : 1;
-    }
-    if (P <= 24) {
-        launch_sweep<24, 3, 2>(g, w, x, f, nu, stresslet, order, off, s.nbx, s.nby, s.nseg, out, st);
-        return stresslet ? 3 : 1;
-    }
-    launch_sweep<32, 1, 4>(g, w, x, f, nu, stresslet, order, off, s.nbx, s.nby, s.nseg, out, st);
-    return stresslet ? 9 : 3;
+void launch_sweep_weights(const DevGrid& g, const DevWindow& w, const double* x, const double* f, const double* nu,
+                          int stresslet, const uint32_t* order, int64_t N, double* W, int4* SW, double* STR,
+                          cudaStream_t st) {
+    if (N == 0) return;
+    sweep_weights_kernel<<<(unsigned)((N + 127) / 128), 128, 0, st>>>(g, w, x, f, nu, stresslet, order, N, W, SW,
+                                                                       STR);
+}
+
+int launch_spread_sweep(const DevGrid& g, int P, const double* W, const int4* SW, const double* STR, int C,
+                        const int64_t* off, const SweepShape& s, double* out, cudaStream_t st) {
+    if (P <= 8) return launch_sweep<8, 3, 4>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
+    if (P <= 16) return launch_sweep<16, 3, 4>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
+    if (P <= 24) return launch_sweep<24, 3, 2>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
+    return launch_sweep<32, 1, 4>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
 }
 
 }  // namespace sewald_b200
