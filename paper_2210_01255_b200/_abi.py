@@ -12,7 +12,7 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libsewald_gpu.so")
+LIB_PATH = os.environ.get("SEWALD_LIB") or os.path.join(_HERE, "lib", "libsewald_gpu.so")
 
 OK, EINVAL, EDOMAIN, ERUNTIME, ECUDA, ECUFFT, ENOMEM = range(7)
 STOKESLET, STRESSLET, ROTLET = 0, 1, 2

@@ -29,6 +29,9 @@ namespace {
 
 constexpr int SYM_WARPS = 4;
 constexpr int SYM_THREADS = 32 * SYM_WARPS;
+#ifndef SEWALD_SYM_MINB
+#define SEWALD_SYM_MINB 4
+#endif
 
 __device__ __forceinline__ int fdiv(int a, int b) {
     int q = a / b;
@@ -106,7 +109,7 @@ __device__ __forceinline__ void pair_both(const Screened& sc, double xi2, double
 }
 
 template <int KIND, int S>
-__global__ void __launch_bounds__(SYM_THREADS, 4)
+__global__ void __launch_bounds__(SYM_THREADS, SEWALD_SYM_MINB)
 realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed,
                      const int64_t* __restrict__ cell_off, int64_t N, int64_t c0, int64_t c1,
                      double* __restrict__ u, unsigned long long* __restrict__ pair_count, int* __restrict__ err) {
