@@ -108,7 +108,7 @@ __device__ __forceinline__ void pair_both(const Screened& sc, double xi2, double
     }
 }
 
-template <int KIND, int S>
+template <int KIND, int S, bool SHORT>
 __global__ void __launch_bounds__(SYM_THREADS, SEWALD_SYM_MINB)
 realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed,
                      const int64_t* __restrict__ cell_off, int64_t N, int64_t c0, int64_t c1,
@@ -119,6 +119,9 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     __shared__ double racc_all[SYM_WARPS][3][32];
     __shared__ long long jid_all[SYM_WARPS][32];
     __shared__ float jf_all[SYM_WARPS][3][32];
+    __shared__ double exp_tab[32];
+    if (threadIdx.x < 32) exp_tab[threadIdx.x] = c_exp2_tab32[threadIdx.x];
+    __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t cl = c0 + (int64_t)blockIdx.x * SYM_WARPS + warp;
@@ -254,7 +257,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                                 double sj[NS];
 #pragma unroll
                                 for (int c = 0; c < NS; ++c) sj[c] = js[c][j];
-                                const Screened sc = screened(n2, a.xi, xi2);
+                                const Screened sc = screened<SHORT>(n2, a.xi, xi2, exp_tab);
                                 double ub[3];
                                 pair_both<KIND>(sc, xi2, n2, r0, r1, r2, sj, fa, ua, ub);
                                 racc[0][j] += ub[0];
@@ -295,20 +298,20 @@ void launch_realspace_sym(const CellGrid& cg, const RealspaceArgs& a, const doub
                           unsigned long long* pair_count, int* err, cudaStream_t st) {
     if (c1 <= c0) return;
     const unsigned blocks = (unsigned)((c1 - c0 + SYM_WARPS - 1) / SYM_WARPS);
+    const bool shrt = a.xi * a.rc <= SEWALD_ERFCX8_XMAX;
+#define SEWALD_SYM_LAUNCH(K, S)                                                                            \
+    if (shrt)                                                                                              \
+        realspace_sym_kernel<K, S, true><<<blocks, SYM_THREADS, 0, st>>>(cg, a, packed, cell_off, N, c0, c1, u, \
+                                                                          pair_count, err);                \
+    else                                                                                                   \
+        realspace_sym_kernel<K, S, false><<<blocks, SYM_THREADS, 0, st>>>(cg, a, packed, cell_off, N, c0, c1, u, \
+                                                                           pair_count, err);
     switch (a.kind) {
-        case SEWALD_STOKESLET:
-            realspace_sym_kernel<SEWALD_STOKESLET, 8><<<blocks, SYM_THREADS, 0, st>>>(cg, a, packed, cell_off, N, c0,
-                                                                                       c1, u, pair_count, err);
-            break;
-        case SEWALD_ROTLET:
-            realspace_sym_kernel<SEWALD_ROTLET, 8><<<blocks, SYM_THREADS, 0, st>>>(cg, a, packed, cell_off, N, c0, c1,
-                                                                                    u, pair_count, err);
-            break;
-        default:
-            realspace_sym_kernel<SEWALD_STRESSLET, 12><<<blocks, SYM_THREADS, 0, st>>>(cg, a, packed, cell_off, N, c0,
-                                                                                        c1, u, pair_count, err);
-            break;
+        case SEWALD_STOKESLET: SEWALD_SYM_LAUNCH(SEWALD_STOKESLET, 8) break;
+        case SEWALD_ROTLET: SEWALD_SYM_LAUNCH(SEWALD_ROTLET, 8) break;
+        default: SEWALD_SYM_LAUNCH(SEWALD_STRESSLET, 12) break;
     }
+#undef SEWALD_SYM_LAUNCH
 }
 
 }  // namespace sewald_b200

@@ -15,6 +15,7 @@
 #pragma once
 
 #include "erfcx_coeffs.h"
+#include "exp2_table.h"
 
 namespace sewald_b200 {
 
@@ -22,6 +23,14 @@ namespace sewald_b200 {
 // c[][] operands (as literals they are rebuilt with UMOVs on every use).
 __constant__ double c_erfcx_p[10] = SEWALD_ERFCX_P;
 __constant__ double c_erfcx_q[10] = SEWALD_ERFCX_Q;
+__constant__ double c_erfcx8_p[9] = SEWALD_ERFCX8_P;
+__constant__ double c_erfcx8_q[9] = SEWALD_ERFCX8_Q;
+// 2^(j/32), j < 32 (copied to shared memory by the kernels: per-lane index)
+__constant__ double c_exp2_tab32[32] = SEWALD_EXP2_TAB32;
+// e^f on |f| <= ln2/64: Taylor degree 6 (truncation < 4e-18)
+__constant__ double c_exp6[7] = {1.0, 1.0, 0.5, 1.6666666666666666667e-01, 4.1666666666666666667e-02,
+                                 8.3333333333333333333e-03, 1.3888888888888888889e-03};
+__constant__ double c_exp_tab_k[3] = {SEWALD_INV_LN2_32, -SEWALD_LN2_32_HI, -SEWALD_LN2_32_LO};
 __constant__ double c_exp_poly[14] = {
     1.0, 1.0, 0.5, 1.6666666666666666667e-01, 4.1666666666666666667e-02, 8.3333333333333333333e-03,
     1.3888888888888888889e-03, 1.9841269841269841270e-04, 2.4801587301587301587e-05,
@@ -68,13 +77,44 @@ __device__ __forceinline__ double exp_neg(double y) {
     return p * __hiloint2double((n + 1023) << 20, 0);
 }
 
-// erfcx(x) = e^{x^2} erfc(x) for x >= 0 (rational P9/Q9).
-__device__ __forceinline__ double erfcx_rat(double x) {
-    double p = c_erfcx_p[9], q = c_erfcx_q[9];
+// e^{-y} for y >= 0 via 2^(j/32) table (tab: shared-memory copy of
+// c_exp2_tab32) and a degree-6 polynomial: 9 fp64 FMAs instead of 16.
+__device__ __forceinline__ double exp_neg_tab(double y, const double* tab) {
+    y = fmin(y, 708.0);
+    const double shifter = c_misc[0];
+    const double t = fma(-y, c_exp_tab_k[0], shifter);
+    const int n = __double2loint(t);
+    const double dn = t - shifter;
+    double f = fma(dn, c_exp_tab_k[1], -y);
+    f = fma(dn, c_exp_tab_k[2], f);
+    double p = c_exp6[6];
 #pragma unroll
-    for (int i = 8; i >= 0; --i) {
-        p = fma(p, x, c_erfcx_p[i]);
-        q = fma(q, x, c_erfcx_q[i]);
+    for (int i = 5; i >= 0; --i) p = fma(p, f, c_exp6[i]);
+    const int m = n >> 5;  // n = 32 m + j, n <= 0
+    return (p * tab[n & 31]) * __hiloint2double((m + 1023) << 20, 0);
+}
+
+// erfcx(x) = e^{x^2} erfc(x) for x >= 0: rational P9/Q9 on [0,10], or the
+// shorter P8/Q8 valid on [0,7] (SHORT, when xi * rc <= 7).
+template <bool SHORT = false>
+__device__ __forceinline__ double erfcx_rat(double x) {
+    double p, q;
+    if (SHORT) {
+        p = c_erfcx8_p[8];
+        q = c_erfcx8_q[8];
+#pragma unroll
+        for (int i = 7; i >= 0; --i) {
+            p = fma(p, x, c_erfcx8_p[i]);
+            q = fma(q, x, c_erfcx8_q[i]);
+        }
+    } else {
+        p = c_erfcx_p[9];
+        q = c_erfcx_q[9];
+#pragma unroll
+        for (int i = 8; i >= 0; --i) {
+            p = fma(p, x, c_erfcx_p[i]);
+            q = fma(q, x, c_erfcx_q[i]);
+        }
     }
     double y = rcp_approx(q);
     y = fma(y, fma(-q, y, 1.0), y);
@@ -91,14 +131,15 @@ struct Screened {
     double iy, Ey, R, cx, E;
 };
 
-__device__ __forceinline__ Screened screened(double n2, double xi, double xi2) {
+template <bool SHORT = false>
+__device__ __forceinline__ Screened screened(double n2, double xi, double xi2, const double* exp_tab = nullptr) {
     Screened s;
     s.iy = rsqrt_nr(n2);
     const double r = n2 * s.iy;
     const double x = xi * r;
-    s.E = exp_neg(xi2 * n2);
+    s.E = exp_tab ? exp_neg_tab(xi2 * n2, exp_tab) : exp_neg(xi2 * n2);
     s.Ey = s.E * s.iy;
-    s.R = erfcx_rat(x);
+    s.R = erfcx_rat<SHORT>(x);
     s.cx = c_misc[4] * x;
     return s;
 }
