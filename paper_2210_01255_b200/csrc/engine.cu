@@ -627,7 +627,9 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
         a.thresh_f = (float)(rpad * rpad * (1.0 + std::ldexp(1.0, -16)));
         if (use_sym) {
             launch_realspace_sym(s->cg, a, s->packed.as<double>(), Nt, s->c_off.as<int64_t>(), c0, c1, u,
-                                 s->pair_counter.as<unsigned long long>(), s->flags.as<int>() + FLAG_SINGULAR, st);
+                                 s->pair_counter.as<unsigned long long>(), s->flags.as<int>() + FLAG_SINGULAR,
+                                 static_cast<unsigned long long*>(s->work_counter.ensure(sizeof(unsigned long long))),
+                                 st);
         } else {
             launch_realspace(s->cg, a, s->packed.as<double>(), s->packedf.as<float4>(), s->stresslet,
                              s->c_off.as<int64_t>(), target_folded(s), torder + t0, t1 - t0, u, first ? 0 : 1,

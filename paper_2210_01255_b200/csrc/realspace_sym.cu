@@ -23,6 +23,8 @@
 #include "screened_math.cuh"
 #include "../../include/sewald_gpu.h"
 
+#include <algorithm>
+
 namespace sewald_b200 {
 
 namespace {
@@ -112,7 +114,8 @@ template <int KIND, int S, bool SHORT>
 __global__ void __launch_bounds__(SYM_THREADS, SEWALD_SYM_MINB)
 realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed,
                      const int64_t* __restrict__ cell_off, int64_t N, int64_t c0, int64_t c1,
-                     double* __restrict__ u, unsigned long long* __restrict__ pair_count, int* __restrict__ err) {
+                     double* __restrict__ u, unsigned long long* __restrict__ pair_count, int* __restrict__ err,
+                     unsigned long long* __restrict__ work) {
     constexpr int NS = Strength<KIND>::n;
     __shared__ double jx_all[SYM_WARPS][3][32];
     __shared__ double js_all[SYM_WARPS][NS][32];
@@ -124,13 +127,20 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int64_t cl = c0 + (int64_t)blockIdx.x * SYM_WARPS + warp;
-    if (cl >= c1) return;
     double(*jx)[32] = jx_all[warp];
     double(*js)[32] = js_all[warp];
     double(*racc)[32] = racc_all[warp];
     long long* jid = jid_all[warp];
     float(*jf)[32] = jf_all[warp];
+    unsigned long long npairs = 0;
+    // Persistent warps: clusters are taken from a global counter, so the
+    // uneven per-cluster work (row geometry, half rule) does not leave SMs
+    // idle in the tail.
+    for (;;) {
+    long long next = 0;
+    if (lane == 0) next = (long long)atomicAdd(work, 1ull);
+    const int64_t cl = c0 + __shfl_sync(0xffffffffu, next, 0);
+    if (cl >= c1) break;
 
     const int64_t istart = cl * 32;
     const int64_t ia = istart + lane;
@@ -175,7 +185,6 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     }
 
     double ua[3] = {0.0, 0.0, 0.0};
-    unsigned long long npairs = 0;
 
     for (int cz = clo[2]; cz <= chi[2]; ++cz) {
         const int sz = 2 < cg.d ? fdiv(cz, cg.n[2]) : 0;
@@ -257,7 +266,11 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                                 double sj[NS];
 #pragma unroll
                                 for (int c = 0; c < NS; ++c) sj[c] = js[c][j];
+                                #ifdef SEWALD_NO_EXPTAB
+                                const Screened sc = screened<SHORT>(n2, a.xi, xi2, nullptr);
+#else
                                 const Screened sc = screened<SHORT>(n2, a.xi, xi2, exp_tab);
+#endif
                                 double ub[3];
                                 pair_both<KIND>(sc, xi2, n2, r0, r1, r2, sj, fa, ua, ub);
                                 racc[0][j] += ub[0];
@@ -284,6 +297,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
         atomicAdd(dst + 1, ua[1]);
         atomicAdd(dst + 2, ua[2]);
     }
+    }  // persistent loop
     if (pair_count) {
 #pragma unroll
         for (int s = 16; s > 0; s >>= 1) npairs += __shfl_xor_sync(0xffffffffu, npairs, s);
@@ -295,17 +309,38 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
 
 void launch_realspace_sym(const CellGrid& cg, const RealspaceArgs& a, const double* packed, int64_t N,
                           const int64_t* cell_off, int64_t c0, int64_t c1, double* u,
-                          unsigned long long* pair_count, int* err, cudaStream_t st) {
+                          unsigned long long* pair_count, int* err, unsigned long long* work, cudaStream_t st) {
     if (c1 <= c0) return;
-    const unsigned blocks = (unsigned)((c1 - c0 + SYM_WARPS - 1) / SYM_WARPS);
+    cudaMemsetAsync(work, 0, sizeof(unsigned long long), st);
+    int dev = 0, sms = 148, per_sm = 4;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+#ifdef SEWALD_NO_SHORT
+    const bool shrt = false;
+#else
     const bool shrt = a.xi * a.rc <= SEWALD_ERFCX8_XMAX;
+#endif
+    if (a.kind == SEWALD_STRESSLET)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, shrt ? realspace_sym_kernel<SEWALD_STRESSLET, 12, true> : realspace_sym_kernel<SEWALD_STRESSLET, 12, false>,
+            SYM_THREADS, 0);
+    else if (a.kind == SEWALD_ROTLET)
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, shrt ? realspace_sym_kernel<SEWALD_ROTLET, 8, true> : realspace_sym_kernel<SEWALD_ROTLET, 8, false>,
+            SYM_THREADS, 0);
+    else
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+            &per_sm, shrt ? realspace_sym_kernel<SEWALD_STOKESLET, 8, true> : realspace_sym_kernel<SEWALD_STOKESLET, 8, false>,
+            SYM_THREADS, 0);
+    const int64_t need = (c1 - c0 + SYM_WARPS - 1) / SYM_WARPS;
+    const unsigned blocks = (unsigned)std::min<int64_t>(need, (int64_t)sms * std::max(per_sm, 1));
 #define SEWALD_SYM_LAUNCH(K, S)                                                                            \
     if (shrt)                                                                                              \
         realspace_sym_kernel<K, S, true><<<blocks, SYM_THREADS, 0, st>>>(cg, a, packed, cell_off, N, c0, c1, u, \
-                                                                          pair_count, err);                \
+                                                                          pair_count, err, work);          \
     else                                                                                                   \
         realspace_sym_kernel<K, S, false><<<blocks, SYM_THREADS, 0, st>>>(cg, a, packed, cell_off, N, c0, c1, u, \
-                                                                           pair_count, err);
+                                                                           pair_count, err, work);
     switch (a.kind) {
         case SEWALD_STOKESLET: SEWALD_SYM_LAUNCH(SEWALD_STOKESLET, 8) break;
         case SEWALD_ROTLET: SEWALD_SYM_LAUNCH(SEWALD_ROTLET, 8) break;

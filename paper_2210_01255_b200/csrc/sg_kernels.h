@@ -85,7 +85,7 @@ void launch_realspace(const CellGrid& cg, const RealspaceArgs& a, const double* 
 // be zeroed beforehand and receives contributions of every particle.
 void launch_realspace_sym(const CellGrid& cg, const RealspaceArgs& a, const double* packed, int64_t N,
                           const int64_t* cell_off, int64_t c0, int64_t c1, double* u,
-                          unsigned long long* pair_count, int* err, cudaStream_t st);
+                          unsigned long long* pair_count, int* err, unsigned long long* work, cudaStream_t st);
 
 // ---- k space (kspace.cu) ---------------------------------------------------
 struct KspaceTables {
