@@ -242,15 +242,27 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                     __syncwarp();
                     // pair (lane, j) is "after" in sorted order iff j - lane > dlt
                     const int dlt = (int)max((int64_t)-64, istart - jb);
-                    for (int s = 0; s < 32; ++s) {
-                        const int j = (lane + s) & 31;
-                        const int dj = j - lane;
-                        bool acc = valid && j < cnt && (dj > dlt || (dj == dlt && pos_shift));
-                        if (acc) {  // conservative fp32 pre-test (FP32 pipe)
+                    // (1) candidate rotations of this lane, fp32 bound (independent
+                    // iterations, FP32 pipe); (2) steps with any candidate (one
+                    // warp OR-reduction); (3) fp64 work only on those steps.
+                    unsigned m = 0u;
+                    if (valid) {
+#pragma unroll 8
+                        for (int s = 0; s < 32; ++s) {
+                            const int j = (lane + s) & 31;
+                            const int dj = j - lane;
                             const float d0 = tf0 - jf[0][j], d1 = tf1 - jf[1][j], d2 = tf2 - jf[2][j];
-                            acc = fmaf(d2, d2, fmaf(d1, d1, d0 * d0)) < a.thresh_f;
+                            const bool ok = j < cnt && (dj > dlt || (dj == dlt && pos_shift)) &&
+                                            fmaf(d2, d2, fmaf(d1, d1, d0 * d0)) < a.thresh_f;
+                            m |= (ok ? 1u : 0u) << s;
                         }
-                        if (!__any_sync(0xffffffffu, acc)) continue;
+                    }
+                    unsigned steps = __reduce_or_sync(0xffffffffu, m);
+                    while (steps) {
+                        const int s = __ffs(steps) - 1;
+                        steps &= steps - 1;
+                        const int j = (lane + s) & 31;
+                        bool acc = (m >> s) & 1u;
                         double r0 = 0, r1 = 0, r2 = 0, n2 = 0;
                         if (acc) {
                             r0 = (xa0 - jx[0][j]) - shx;
