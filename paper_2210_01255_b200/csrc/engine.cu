@@ -365,6 +365,41 @@ const uint32_t* target_order(sewald_gpu_session* s) {
     return s->same ? s->c_order.as<uint32_t>() : s->t_order.as<uint32_t>();
 }
 
+// Targets bucketed / sorted for the z-sweep gather, with their window taps.
+bool ensure_gather_sweep(sewald_gpu_session* s) {
+    static const bool enabled = [] {
+        const char* e = getenv("SEWALD_GATHER_SWEEP");
+        return !(e && e[0] == '0');
+    }();
+    const SweepShape sh = sweep_shape(s->g, s->p.P);
+    if (!enabled || !sh.ok) return false;
+    if (s->tg_ready) return true;
+    cudaStream_t st = s->ctx->stream;
+    const int64_t Nt = s->Nt;
+    const double* xt = s->same ? s->x.as<double>() : s->xt.as<double>();
+    const int64_t n = std::max<int64_t>(Nt, 1);
+    s->tg_keys.ensure(sizeof(uint32_t) * n);
+    s->tg_keys2.ensure(sizeof(uint32_t) * n);
+    s->tg_vals.ensure(sizeof(uint32_t) * n);
+    s->tg_order.ensure(sizeof(uint32_t) * n);
+    s->tg_off.ensure(sizeof(int64_t) * (sh.nkeys + 1));
+    s->tg_w.ensure(sizeof(double) * 3 * s->p.P * n);
+    s->tg_sw.ensure(sizeof(int4) * n);
+    int* bad = s->flags.as<int>() + FLAG_GATHER_BOX;
+    launch_sweep_bucket(s->g, s->p.P, xt, Nt, sh, s->tg_keys.as<uint32_t>(), s->tg_vals.as<uint32_t>(), bad, st);
+    check_flag(s, FLAG_GATHER_BOX, SEWALD_EINVAL,
+               "point too close to the extended box boundary; free-direction padding is too small");
+    if (Nt > 0)
+        sort_pairs(s, s->tg_keys.as<uint32_t>(), s->tg_keys2.as<uint32_t>(), s->tg_vals.as<uint32_t>(),
+                   s->tg_order.as<uint32_t>(), Nt, bits_for((uint64_t)sh.nkeys + 1));
+    launch_bucket_offsets(s->tg_keys2.as<uint32_t>(), Nt, (int)sh.nkeys, s->tg_off.as<int64_t>(), st);
+    launch_sweep_weights(s->g, s->w, xt, nullptr, nullptr, 0, s->tg_order.as<uint32_t>(), Nt, s->tg_w.as<double>(),
+                         s->tg_sw.as<int4>(), nullptr, st);
+    s->ctx->launches += 3;
+    s->tg_ready = true;
+    return true;
+}
+
 void d3_prepare(sewald_gpu_session* s) {
     if (s->d3) return;
     auto P = std::make_unique<FourierPlanD3>();
@@ -508,11 +543,13 @@ void session_set_sources(sewald_gpu_session* s, const double* x, const double* f
     s->sp_i0 = s->sp_i1 = -1;
     s->cells_ready = false;
     s->sums_ready = false;
+    s->tg_ready = false;
     if (s->same) s->Nt = N;
 }
 
 void session_set_targets(sewald_gpu_session* s, const double* xt, int64_t Nt, bool same) {
     s->same = same;
+    s->tg_ready = false;
     if (same) {
         s->Nt = s->N;
         return;
@@ -640,8 +677,14 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
     }
     if (parts & 1) {
         const double h3 = s->p.h * s->p.h * s->p.h;
-        launch_gather(s->g, s->w, s->flow.as<double>(), target_positions(s), torder + t0, t1 - t0, h3,
-                      first ? 0 : 1, u, st);
+        if (ensure_gather_sweep(s)) {
+            if (first) cuda_check(cudaMemsetAsync(u, 0, sizeof(double) * 3 * Nt, st), "u zero");
+            launch_gather_sweep(s->g, s->p.P, s->tg_w.as<double>(), s->tg_sw.as<int4>(), s->tg_off.as<int64_t>(),
+                                sweep_shape(s->g, s->p.P), part, nparts, s->flow.as<double>(), h3, u, st);
+        } else {
+            launch_gather(s->g, s->w, s->flow.as<double>(), target_positions(s), torder + t0, t1 - t0, h3,
+                          first ? 0 : 1, u, st);
+        }
         ++s->ctx->launches;
         first = false;
     }

@@ -80,6 +80,9 @@ struct sewald_gpu_session {
     int64_t Nt = 0;
     bool same = false;
     sewald_b200::DevBuf xt, t_folded, t_keys, t_keys2, t_vals, t_order;
+    // gather sweep ordering of the targets
+    bool tg_ready = false;
+    sewald_b200::DevBuf tg_keys, tg_keys2, tg_vals, tg_order, tg_off, tg_w, tg_sw;
     // grids
     sewald_b200::DevBuf grid, flow;
     // global sums: f (3), q.nu (1), x (q.nu) (3); partials

@@ -51,6 +51,12 @@ void launch_sweep_weights(const DevGrid& g, const DevWindow& w, const double* x,
 int launch_spread_sweep(const DevGrid& g, int P, const double* W, const int4* SW, const double* STR, int C,
                         const int64_t* off, const SweepShape& s, double* out, cudaStream_t st);
 
+// z-sweep gather (spread_sweep.cu): tiles [part/nparts] of the (x,y) patches;
+// u must be initialised (contributions are added with fp64 RED).
+void launch_gather_sweep(const DevGrid& g, int P, const double* W, const int4* SW, const int64_t* off,
+                         const SweepShape& s, int part, int nparts, const double* grid, double h3, double* u,
+                         cudaStream_t st);
+
 // ---- real space (realspace.cu) -------------------------------------------
 struct CellGrid {
     int d;

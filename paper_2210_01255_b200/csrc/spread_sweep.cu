@@ -75,7 +75,8 @@ __global__ void sweep_weights_kernel(DevGrid g, DevWindow win, const double* __r
         for (int p = 0; p < P; ++p) w[p] = window_eval(win, ((double)(j0 + p) - rel) * g.h);
         sw[ax] = ax < g.d ? wrapi(j0, g.n[ax]) : j0;
     }
-    SW[k] = make_int4(sw[0], sw[1], sw[2], 0);
+    SW[k] = make_int4(sw[0], sw[1], sw[2], (int)i);
+    if (!f) return;
     if (!stresslet) {
         for (int c = 0; c < 3; ++c) STR[k * 3 + c] = f[3 * i + c];
     } else {
@@ -284,6 +285,180 @@ spread_sweep_kernel(DevGrid g, int P, const double* __restrict__ W, const int4* 
     }
 }
 
+
+// Gather by z-sweep (the adjoint of spread_sweep_kernel): the warp keeps a
+// ring of WIN grid planes x 3 components of its 4 x 8 columns in registers;
+// for each target whose stencil z start lies in the current window, every
+// lane reduces its column (16 z-taps) and scales by the (x, y) weights; the
+// 32 column partials of each target are summed through shared memory and
+// added to u with one fp64 RED per component and tile. Reference:
+// gather /root/reference/proj/src/fourier.cpp:276-309.
+template <int PMAX, int ZSTEP, int O>
+__device__ __forceinline__ void col_dot(const double (&ring)[PMAX + ZSTEP - 1][3], const double* wz, double& a0,
+                                        double& a1, double& a2) {
+#pragma unroll
+    for (int k = 0; k < PMAX; ++k) {
+        const double w = wz[k];
+        a0 = fma(w, ring[O + k][0], a0);
+        a1 = fma(w, ring[O + k][1], a1);
+        a2 = fma(w, ring[O + k][2], a2);
+    }
+}
+
+template <int PMAX, int ZSTEP>
+__global__ void __launch_bounds__(32)
+gather_sweep_kernel(DevGrid g, int P, const double* __restrict__ W, const int4* __restrict__ SW,
+                    const int64_t* __restrict__ off, int nbx, int nby, int nseg, int tile0,
+                    const double* __restrict__ grid, double h3, double* __restrict__ u) {
+    constexpr int WIN = PMAX + ZSTEP - 1;
+    __shared__ double pwx[32][SX];
+    __shared__ double pwy[32][SY];
+    __shared__ double pwz[32][PMAX];
+    __shared__ int pdx[32], pdy[32], po[32], pid[32];
+    __shared__ uint32_t cidx[32];
+    __shared__ double red[3][32][33];
+
+    const int lane = threadIdx.x;
+    const int tx = lane % SX, ty = lane / SX;
+    const int tile = tile0 + blockIdx.x;
+    const int bxt = tile % nbx, byt = tile / nbx;
+    const int X0 = bxt * SX, Y0 = byt * SY;
+    const int n2 = g.n[2];
+    const int seg = blockIdx.y;
+    const int z0 = (int)((int64_t)n2 * seg / nseg), z1 = (int)((int64_t)n2 * (seg + 1) / nseg);
+    const bool perx = g.d > 0, pery = g.d > 1, perz = g.d > 2;
+    const Pieces px = reach(X0, SX, g.n[0], P, perx, nbx);
+    const Pieces py = reach(Y0, SY, g.n[1], P, pery, nby);
+
+    const int gx = X0 + tx, gy = Y0 + ty;
+    const bool own = gx < g.n[0] && gy < g.n[1];
+    const int64_t cs = (int64_t)g.n[0] * g.n[1] * n2;
+    const double* col = grid + ((int64_t)(own ? gx : 0) * g.n[1] + (own ? gy : 0)) * n2;
+    auto plane = [&](int z, int c) -> double {
+        if (!own) return 0.0;
+        if (perz) z = wrapi(z, n2);
+        else if (z < 0 || z >= n2) return 0.0;
+        return __ldg(col + c * cs + z);
+    };
+    double ring[WIN][3];
+#pragma unroll
+    for (int w = 0; w < WIN; ++w)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) ring[w][c] = plane(z0 + w, c);
+
+    for (int zb = z0; zb < z1; zb += ZSTEP) {
+        int zr_lo[2], zr_hi[2], nzr = 0;
+        {
+            const int a = zb, b = min(zb + ZSTEP, z1) - 1;
+            if (perz) {
+                zr_lo[0] = a; zr_hi[0] = b; nzr = 1;  // a, b already in [0, n2)
+            } else if (a <= b) {
+                zr_lo[0] = a; zr_hi[0] = b; nzr = 1;
+            }
+        }
+        int filled = 0;
+        for (int ip = 0; ip < px.n; ++ip)
+        for (int bx = px.lo[ip]; bx <= px.hi[ip]; ++bx)
+        for (int jp = 0; jp < py.n; ++jp)
+        for (int by = py.lo[jp]; by <= py.hi[jp]; ++by)
+        for (int r = 0; r < nzr; ++r) {
+            const int64_t kb = ((int64_t)bx * nby + by) * n2;
+            int64_t p0 = off[kb + zr_lo[r]];
+            const int64_t p1 = off[kb + zr_hi[r] + 1];
+            while (p0 < p1) {
+                const int take = (int)min((int64_t)(32 - filled), p1 - p0);
+                if (lane < take) cidx[filled + lane] = (uint32_t)(p0 + lane);
+                filled += take;
+                p0 += take;
+                if (filled < 32) break;
+#define SEWALD_GSWEEP_CHUNK(CNT)                                                                         \
+                {                                                                                        \
+                    __syncwarp();                                                                        \
+                    if (lane < (CNT)) {                                                                  \
+                        const int64_t kk = cidx[lane];                                                   \
+                        const int4 sw = SW[kk];                                                          \
+                        const double* wrow = W + kk * 3 * P;                                             \
+                        const int dx = delta_to(X0, sw.x, g.n[0], perx, P);                              \
+                        const int dy = delta_to(Y0, sw.y, g.n[1], pery, P);                              \
+                        pdx[lane] = dx;                                                                  \
+                        pdy[lane] = dy;                                                                  \
+                        po[lane] = sw.z - zb;                                                            \
+                        pid[lane] = sw.w;                                                                \
+                        for (int t = 0; t < SX; ++t) {                                                   \
+                            const int p = dx + t;                                                        \
+                            pwx[lane][t] = (p >= 0 && p < P) ? __ldg(wrow + p) : 0.0;                    \
+                        }                                                                                \
+                        for (int t = 0; t < SY; ++t) {                                                   \
+                            const int p = dy + t;                                                        \
+                            pwy[lane][t] = (p >= 0 && p < P) ? __ldg(wrow + P + p) : 0.0;                \
+                        }                                                                                \
+                        for (int k = 0; k < PMAX; ++k) pwz[lane][k] = k < P ? __ldg(wrow + 2 * P + k) : 0.0; \
+                    }                                                                                    \
+                    __syncwarp();                                                                        \
+                    for (int k = 0; k < (CNT); ++k) {                                                    \
+                        const int ox = pdx[k] + tx, oy = pdy[k] + ty;                                    \
+                        double a0 = 0.0, a1 = 0.0, a2 = 0.0;                                             \
+                        if (ox >= 0 && ox < P && oy >= 0 && oy < P) {                                    \
+                            const double* wz = pwz[k];                                                   \
+                            switch (po[k]) {                                                             \
+                                case 0: col_dot<PMAX, ZSTEP, 0>(ring, wz, a0, a1, a2); break;            \
+                                case 1: if (ZSTEP > 1) col_dot<PMAX, ZSTEP, (ZSTEP > 1 ? 1 : 0)>(ring, wz, a0, a1, a2); break; \
+                                case 2: if (ZSTEP > 2) col_dot<PMAX, ZSTEP, (ZSTEP > 2 ? 2 : 0)>(ring, wz, a0, a1, a2); break; \
+                                default: if (ZSTEP > 3) col_dot<PMAX, ZSTEP, (ZSTEP > 3 ? 3 : 0)>(ring, wz, a0, a1, a2); break; \
+                            }                                                                            \
+                            const double wxy = pwx[k][tx] * pwy[k][ty];                                  \
+                            a0 *= wxy;                                                                   \
+                            a1 *= wxy;                                                                   \
+                            a2 *= wxy;                                                                   \
+                        }                                                                                \
+                        red[0][k][lane] = a0;                                                            \
+                        red[1][k][lane] = a1;                                                            \
+                        red[2][k][lane] = a2;                                                            \
+                    }                                                                                    \
+                    __syncwarp();                                                                        \
+                    if (lane < (CNT)) {                                                                  \
+                        double s0 = 0.0, s1 = 0.0, s2 = 0.0;                                             \
+                        for (int l = 0; l < 32; ++l) {                                                   \
+                            s0 += red[0][lane][l];                                                       \
+                            s1 += red[1][lane][l];                                                       \
+                            s2 += red[2][lane][l];                                                       \
+                        }                                                                                \
+                        double* dst = u + 3 * (int64_t)pid[lane];                                        \
+                        atomicAdd(dst, h3 * s0);                                                         \
+                        atomicAdd(dst + 1, h3 * s1);                                                     \
+                        atomicAdd(dst + 2, h3 * s2);                                                     \
+                    }                                                                                    \
+                    __syncwarp();                                                                        \
+                }
+                SEWALD_GSWEEP_CHUNK(32)
+                filled = 0;
+            }
+        }
+        if (filled > 0) {
+            SEWALD_GSWEEP_CHUNK(filled)
+            filled = 0;
+        }
+#undef SEWALD_GSWEEP_CHUNK
+        // rotate the ring by ZSTEP planes and load the next ones
+#pragma unroll
+        for (int w = 0; w < WIN - ZSTEP; ++w)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ring[w][c] = ring[w + ZSTEP][c];
+#pragma unroll
+        for (int w = WIN - ZSTEP; w < WIN; ++w)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) ring[w][c] = plane(zb + ZSTEP + w, c);
+    }
+}
+
+template <int PMAX, int ZSTEP>
+void launch_gsweep(const DevGrid& g, int P, const double* W, const int4* SW, const int64_t* off, int nbx, int nby,
+                   int nseg, int tile0, int tile1, const double* grid, double h3, double* u, cudaStream_t st) {
+    if (tile1 <= tile0) return;
+    dim3 gr(tile1 - tile0, nseg);
+    gather_sweep_kernel<PMAX, ZSTEP><<<gr, 32, 0, st>>>(g, P, W, SW, off, nbx, nby, nseg, tile0, grid, h3, u);
+}
+
 template <int PMAX, int NC, int ZSTEP>
 int launch_sweep(const DevGrid& g, int P, const double* W, const int4* SW, const double* STR, int C,
                  const int64_t* off, int nbx, int nby, int nseg, double* out, cudaStream_t st) {
@@ -332,6 +507,17 @@ int launch_spread_sweep(const DevGrid& g, int P, const double* W, const int4* SW
     if (P <= 16) return launch_sweep<16, 3, 4>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
     if (P <= 24) return launch_sweep<24, 3, 2>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
     return launch_sweep<32, 1, 4>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
+}
+
+void launch_gather_sweep(const DevGrid& g, int P, const double* W, const int4* SW, const int64_t* off,
+                         const SweepShape& s, int part, int nparts, const double* grid, double h3, double* u,
+                         cudaStream_t st) {
+    const int tiles = s.nbx * s.nby;
+    const int t0 = (int)((int64_t)tiles * part / nparts), t1 = (int)((int64_t)tiles * (part + 1) / nparts);
+    if (P <= 8) launch_gsweep<8, 4>(g, P, W, SW, off, s.nbx, s.nby, s.nseg, t0, t1, grid, h3, u, st);
+    else if (P <= 16) launch_gsweep<16, 4>(g, P, W, SW, off, s.nbx, s.nby, s.nseg, t0, t1, grid, h3, u, st);
+    else if (P <= 24) launch_gsweep<24, 2>(g, P, W, SW, off, s.nbx, s.nby, s.nseg, t0, t1, grid, h3, u, st);
+    else launch_gsweep<32, 2>(g, P, W, SW, off, s.nbx, s.nby, s.nseg, t0, t1, grid, h3, u, st);
 }
 
 }  // namespace sewald_b200
