@@ -367,12 +367,15 @@ const uint32_t* target_order(sewald_gpu_session* s) {
 
 // Targets bucketed / sorted for the z-sweep gather, with their window taps.
 bool ensure_gather_sweep(sewald_gpu_session* s) {
-    static const bool enabled = [] {
+    // The sweep wins for wide windows (P > 16: c3, c4); the warp-per-target
+    // gather is faster for P <= 16. SEWALD_GATHER_SWEEP=1/0 forces either.
+    static const int mode = [] {
         const char* e = getenv("SEWALD_GATHER_SWEEP");
-        return !(e && e[0] == '0');
+        return e ? (e[0] == '0' ? 0 : 1) : -1;
     }();
     const SweepShape sh = sweep_shape(s->g, s->p.P);
-    if (!enabled || !sh.ok) return false;
+    const bool use = mode == 1 || (mode == -1 && s->p.P > 16);
+    if (!use || !sh.ok) return false;
     if (s->tg_ready) return true;
     cudaStream_t st = s->ctx->stream;
     const int64_t Nt = s->Nt;
