@@ -283,3 +283,49 @@ def test_live_free_axes_selected(S, ref, d, kind):
         u = S.full_potential(sysm, tg, sel.params)
         ur = ref.full_potential(rp, x, f, nu, None if same else xt, same)
         assert rel_rms(u, ur) < TOL, (d, kind, same)
+
+
+# ---------------------------------------------------------------------------
+# device session: multi-part evaluation (the multi-GPU decomposition run on
+# one GPU as sequential parts) must sum to the single-part result
+# ---------------------------------------------------------------------------
+
+@pytest.mark.parametrize("kind,d,same", [(0, 3, True), (1, 2, True), (2, 1, False), (0, 0, True)])
+def test_session_parts_sum_to_whole(S, kind, d, same):
+    import torch
+    from paper_2210_01255_b200.parallel import slice_bounds
+    rng = np.random.default_rng(300 + kind + d)
+    N = 2500
+    L = (1.0, 1.0, 1.0) if d else (2.0, 1.0, 1.0)
+    x = rng.random((N, 3)) * np.asarray(L)
+    f = rng.standard_normal((N, 3))
+    nu = rng.standard_normal((N, 3)) if kind == 1 else None
+    xt = None if same else rng.random((1700, 3)) * np.asarray(L)
+    sysm = S.SourceSystem(S.Kernel(kind), S.Cell(L), d, x, f, nu)
+    sel = S.select_parameters(sysm.kind, d, sysm.cell, S.source_quantity(sysm), 9.0, S.ToleranceSpec(1e-8))
+    tg = S.TargetSet.from_sources(sysm) if same else S.TargetSet(xt, False)
+    u_ref = S.full_potential(sysm, tg, sel.params)
+    dev = torch.device("cuda", 0)
+    T = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    sess = S.Session(sel.params, sysm.cell)
+    sess.set_sources(T(x), T(f), T(nu))
+    sess.set_targets(T(xt), same)
+    nt = N if same else xt.shape[0]
+    for world in (1, 2, 3):
+        grid = torch.zeros(sess.grid_size(), dtype=torch.float64, device=dev)
+        total = torch.zeros((nt, 3), dtype=torch.float64, device=dev)
+        grids = []
+        for r in range(world):  # per-rank source slices, summed like the all-reduce
+            g = torch.zeros_like(grid)
+            i0, i1 = slice_bounds(N, r, world)
+            sess.spread(i0, i1, g)
+            grids.append(g)
+        grid = sum(grids)
+        sess.solve(grid)
+        for r in range(world):
+            u = torch.zeros((nt, 3), dtype=torch.float64, device=dev)
+            sess.evaluate(u, r, world, 7)
+            total += u
+        torch.cuda.synchronize()
+        assert rel_rms(total.cpu().numpy(), u_ref) < TOL, world
+    sess.close()
