@@ -122,7 +122,8 @@ const char* sewald_last_error(void);
 int sewald_gpu_create(int device, sewald_gpu_ctx** out);
 void sewald_gpu_destroy(sewald_gpu_ctx* ctx);
 const char* sewald_gpu_last_error(const sewald_gpu_ctx* ctx);
-/* Run all work on this cudaStream_t (NULL = the context's own stream). */
+/* Run all work on this cudaStream_t (NULL = the legacy default stream). A new
+ * context uses its own non-blocking stream until this is called. */
 int sewald_gpu_set_stream(sewald_gpu_ctx* ctx, void* stream);
 int sewald_gpu_get_timings(const sewald_gpu_ctx* ctx, sewald_timings_c* out);
 /* 1 = record per-stage CUDA events (adds event overhead), 0 = off. */

@@ -473,11 +473,14 @@ def gather(field: np.ndarray, params: EwaldParams, targets: TargetSet,
 
 class Session:
     """Device-resident session (sewald_gpu_session_*): inputs and outputs are
-    torch CUDA tensors; torch is used only for memory and streams."""
+    torch CUDA tensors; torch is used only for memory and streams. Every call
+    runs on torch's current CUDA stream, so it is ordered with the caller's
+    torch work (allocation, collectives) without extra synchronisation."""
 
     def __init__(self, params: EwaldParams, cell: Optional[Cell] = None, engine: Optional[Engine] = None):
         self.engine = engine or default_engine()
         self._lib = self.engine._lib
+        self._sync_stream()
         c = params.to_c()
         if cell is not None:
             for i in range(3):
@@ -498,6 +501,10 @@ class Session:
         except Exception:
             pass
 
+    def _sync_stream(self):
+        import torch
+        self.engine.set_stream(torch.cuda.current_stream().cuda_stream)
+
     @staticmethod
     def _ptr(t):
         if t is None:
@@ -506,11 +513,13 @@ class Session:
         return C.c_void_p(t.data_ptr())
 
     def set_sources(self, x, f, nu=None):
+        self._sync_stream()
         self._keep = [x, f, nu]
         self.engine.check(self._lib.sewald_gpu_session_set_sources(
             self.s, self._ptr(x), self._ptr(f), self._ptr(nu), int(x.shape[0])))
 
     def set_targets(self, xt=None, same_as_sources: bool = True):
+        self._sync_stream()
         n = 0 if xt is None else int(xt.shape[0])
         self.engine.check(self._lib.sewald_gpu_session_set_targets(self.s, self._ptr(xt), n, int(same_as_sources)))
 
@@ -518,12 +527,15 @@ class Session:
         return int(self._lib.sewald_gpu_session_grid_size(self.s))
 
     def spread(self, i0: int, i1: int, grid=None):
+        self._sync_stream()
         self.engine.check(self._lib.sewald_gpu_session_spread(self.s, int(i0), int(i1), self._ptr(grid)))
 
     def solve(self, grid=None, precompute_0p: bool = True):
+        self._sync_stream()
         self.engine.check(self._lib.sewald_gpu_session_solve(self.s, self._ptr(grid), int(precompute_0p)))
 
     def evaluate(self, u, part: int = 0, nparts: int = 1, parts: int = 7):
+        self._sync_stream()
         self.engine.check(self._lib.sewald_gpu_session_evaluate(self.s, int(part), int(nparts), int(parts),
                                                                 self._ptr(u)))
 
@@ -531,4 +543,5 @@ class Session:
         return int(self._lib.sewald_gpu_session_pair_count(self.s, int(reset)))
 
     def run(self, u, precompute_0p: bool = True):
+        self._sync_stream()
         self.engine.check(self._lib.sewald_gpu_session_run(self.s, int(precompute_0p), self._ptr(u)))

@@ -860,7 +860,9 @@ const char* sewald_gpu_last_error(const sewald_gpu_ctx* ctx) { return ctx ? ctx-
 
 int sewald_gpu_set_stream(sewald_gpu_ctx* ctx, void* stream) {
     if (!ctx) return SEWALD_EINVAL;
-    ctx->stream = stream ? static_cast<cudaStream_t>(stream) : ctx->own_stream;
+    // The value is used as is: NULL is the legacy default stream (what
+    // torch.cuda.current_stream().cuda_stream returns for the default).
+    ctx->stream = static_cast<cudaStream_t>(stream);
     return SEWALD_OK;
 }
 
