@@ -1,0 +1,328 @@
+// Drop-in C++ host API (include/sewald/sewald_b200.hpp) on top of the C-ABI.
+// Each function keeps the reference signature and semantics
+// (/root/reference/proj/include/sewald/*.h) and forwards the numeric work to
+// the device engine through sewald_gpu.h; status codes are rethrown as the
+// reference's exception types.
+#include "../../include/sewald/sewald_b200.hpp"
+
+#include "../../include/sewald_gpu.h"
+#include "host_params.h"
+
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+namespace sewald {
+
+namespace {
+
+std::mutex g_mu;
+
+sewald_gpu_ctx* context() {
+    static sewald_gpu_ctx* ctx = [] {
+        sewald_gpu_ctx* c = nullptr;
+        if (sewald_gpu_create(0, &c) != SEWALD_OK)
+            throw std::runtime_error("sewald: no usable CUDA device for the B200 engine");
+        return c;
+    }();
+    return ctx;
+}
+
+void rethrow(int rc, const char* msg) {
+    switch (rc) {
+        case SEWALD_OK: return;
+        case SEWALD_EINVAL: throw std::invalid_argument(msg);
+        case SEWALD_EDOMAIN: throw std::domain_error(msg);
+        default: throw std::runtime_error(msg);
+    }
+}
+
+void check_ctx(int rc) { rethrow(rc, sewald_gpu_last_error(context())); }
+void check_host(int rc) { rethrow(rc, sewald_last_error()); }
+
+int kernel_id(Kernel k) {
+    return k == Kernel::stokeslet ? SEWALD_STOKESLET : (k == Kernel::stresslet ? SEWALD_STRESSLET : SEWALD_ROTLET);
+}
+Kernel kernel_of(int k) {
+    return k == SEWALD_STOKESLET ? Kernel::stokeslet : (k == SEWALD_STRESSLET ? Kernel::stresslet : Kernel::rotlet);
+}
+int window_id(WindowKind w) { return w == WindowKind::kb ? SEWALD_WIN_KB : (w == WindowKind::pkb ? SEWALD_WIN_PKB : SEWALD_WIN_TG); }
+WindowKind window_of(int w) {
+    return w == SEWALD_WIN_KB ? WindowKind::kb : (w == SEWALD_WIN_PKB ? WindowKind::pkb : WindowKind::tg);
+}
+
+void put_window(const WindowSpec& w, sewald_params_c& p) {
+    p.win_kind = window_id(w.kind);
+    p.P = w.P;
+    p.win_h = w.h;
+    p.beta = w.beta;
+    p.nu = w.nu;
+    p.alpha = w.alpha;
+}
+
+void put_grid(const GridSpec& g, sewald_params_c& p) {
+    p.h = g.h;
+    p.f_m = g.f_m;
+    for (int i = 0; i < 3; ++i) {
+        p.M[i] = g.M[i];
+        p.M_ext[i] = g.M_ext[i];
+        p.L[i] = g.L[i];
+        p.L_ext[i] = g.L_ext[i];
+        p.pad[i] = g.pad[i];
+    }
+}
+
+sewald_params_c to_c(const EwaldParams& e) {
+    sewald_params_c p{};
+    p.kind = kernel_id(e.kind);
+    p.d = e.d;
+    p.xi = e.xi;
+    p.rc = e.rc;
+    p.R = e.R;
+    put_grid(e.grid, p);
+    put_window(e.window, p);
+    p.s0 = e.upsampling.s0;
+    p.s_star = e.upsampling.s_star;
+    p.s0_raw = e.upsampling.s0_raw;
+    p.s_star_raw = e.upsampling.s_star_raw;
+    for (int i = 0; i < 3; ++i) p.k_star[i] = e.upsampling.k_star[i];
+    return p;
+}
+
+EwaldParams from_c(const sewald_params_c& p) {
+    EwaldParams e;
+    e.kind = kernel_of(p.kind);
+    e.d = p.d;
+    e.xi = p.xi;
+    e.rc = p.rc;
+    e.R = p.R;
+    e.grid.d = p.d;
+    e.grid.h = p.h;
+    e.grid.f_m = p.f_m;
+    for (int i = 0; i < 3; ++i) {
+        e.grid.M[i] = p.M[i];
+        e.grid.M_ext[i] = p.M_ext[i];
+        e.grid.L[i] = p.L[i];
+        e.grid.L_ext[i] = p.L_ext[i];
+        e.grid.pad[i] = p.pad[i];
+        e.upsampling.k_star[i] = p.k_star[i];
+    }
+    e.window.kind = window_of(p.win_kind);
+    e.window.P = p.P;
+    e.window.h = p.win_h;
+    e.window.beta = p.beta;
+    e.window.nu = p.nu;
+    e.window.alpha = p.alpha;
+    e.upsampling.s0 = p.s0;
+    e.upsampling.s_star = p.s_star;
+    e.upsampling.s0_raw = p.s0_raw;
+    e.upsampling.s_star_raw = p.s_star_raw;
+    return e;
+}
+
+const double* D(const std::vector<Vec3>& v) { return v.empty() ? nullptr : reinterpret_cast<const double*>(v.data()); }
+
+}  // namespace
+
+// ---- domain ---------------------------------------------------------------------
+Screening screening_of(Kernel kind) { return kind == Kernel::rotlet ? Screening::ewald : Screening::hasimoto; }
+
+const char* kernel_name(Kernel kind) {
+    return kind == Kernel::stokeslet ? "stokeslet" : (kind == Kernel::stresslet ? "stresslet" : "rotlet");
+}
+
+int strength_components(Kernel kind) { return kind == Kernel::stresslet ? 9 : 3; }
+
+void validate_system(const SourceSystem& s) {
+    if (s.d < 0 || s.d > 3) throw std::invalid_argument("periodicity d must be in 0..3");
+    for (double Li : s.cell.L)
+        if (!(Li > 0.0)) throw std::invalid_argument("cell lengths must be positive");
+    if (s.f.size() != s.x.size()) throw std::invalid_argument("strength count does not match position count");
+    if (s.kind == Kernel::stresslet) {
+        if (s.nu.size() != s.x.size()) throw std::invalid_argument("stresslet needs one orientation per source");
+    } else if (!s.nu.empty()) {
+        throw std::invalid_argument("orientations only apply to the stresslet");
+    }
+    for (const Vec3& p : s.x)
+        for (double c : p)
+            if (!std::isfinite(c)) throw std::invalid_argument("non-finite source position");
+}
+
+double source_quantity(const SourceSystem& s) {
+    return sewald_source_quantity(kernel_id(s.kind), D(s.f), s.kind == Kernel::stresslet ? D(s.nu) : nullptr,
+                                  static_cast<int64_t>(s.f.size()));
+}
+
+Vec3 wrap_position(const Vec3& x, const Cell& cell, int d) {
+    Vec3 y = x;
+    for (int i = 0; i < d; ++i) {
+        y[i] = std::fmod(y[i], cell.L[i]);
+        if (y[i] < 0.0) y[i] += cell.L[i];
+    }
+    return y;
+}
+
+// ---- window / grid ------------------------------------------------------------------
+WindowSpec WindowSpec::make(WindowKind kind, int P, double h) {
+    sewald_params_c p{};
+    check_host(sewald_window_make(window_id(kind), P, h, &p));
+    return from_c(p).window;
+}
+
+Window::Window(const WindowSpec& spec) : spec_(spec) {
+    sewald_params_c p{};
+    put_window(spec, p);
+    sewald_b200::validate_window(p);
+    if (spec.kind == WindowKind::pkb) coef_ = sewald_b200::pkb_coefficients(p);
+}
+
+double Window::eval1d(double r) const {
+    sewald_params_c p{};
+    put_window(spec_, p);
+    return sewald_b200::window_value(p, coef_, r);
+}
+
+double Window::hat1d(double k) const {
+    sewald_params_c p{};
+    put_window(spec_, p);
+    return sewald_b200::window_transform(p, k);
+}
+
+double GridSpec::kinf() const { return sewald_b200::kPi / h; }
+
+GridSpec build_grid(const Cell& cell, int d, double h_target, int P, Kernel kind, int f_m) {
+    sewald_params_c p{};
+    check_host(sewald_build_grid(cell.L.data(), d, h_target, P, kernel_id(kind), f_m, &p));
+    return from_c(p).grid;
+}
+
+ParameterSelection select_parameters(Kernel kind, int d, const Cell& cell, double Q, double xi,
+                                     const ToleranceSpec& tol, const SelectionOptions& opt) {
+    sewald_params_c p{};
+    sewald_report_c r{};
+    check_host(sewald_select_parameters(kernel_id(kind), d, cell.L.data(), Q, xi, tol.value, tol.relative ? 1 : 0,
+                                        opt.f_m, window_id(opt.window), opt.pollution_fix ? 1 : 0, &p, &r));
+    ParameterSelection out;
+    out.params = from_c(p);
+    EstimateReport& e = out.report;
+    e.tau_abs = r.tau_abs;
+    e.U = r.U;
+    e.kinf = r.kinf;
+    e.fourier_trunc = r.fourier_trunc;
+    e.realspace_trunc = r.realspace_trunc;
+    e.window_err = r.window_err;
+    e.h_estimate = r.h_estimate;
+    e.P_estimate = r.P_estimate;
+    e.h_target = r.h_target;
+    e.P_target = r.P_target;
+    e.rc_clamped = r.rc_clamped != 0;
+    e.kinf_clamped = r.kinf_clamped != 0;
+    e.window_saturated = r.window_saturated != 0;
+    e.tg_support_from_pkb = r.tg_support_from_pkb != 0;
+    return out;
+}
+
+// ---- Fourier / real space / full ---------------------------------------------------------
+RealField RealField::zeros(const std::array<int, 3>& n, int comps) {
+    RealField f;
+    f.n = n;
+    f.comps = comps;
+    f.v.assign(static_cast<std::size_t>(comps) * n[0] * n[1] * n[2], 0.0);
+    return f;
+}
+
+RealField spread(const SourceSystem& system, const GridSpec& grid, const Window& window) {
+    validate_system(system);
+    if (std::fabs(window.spec().h - grid.h) > 1e-12 * grid.h)
+        throw std::invalid_argument("window was built for a different grid spacing");
+    if (system.d != grid.d) throw std::invalid_argument("system and grid periodicity differ");
+    EwaldParams e;
+    e.kind = system.kind;
+    e.d = system.d;
+    e.grid = grid;
+    e.window = window.spec();
+    sewald_params_c p = to_c(e);
+    RealField out = RealField::zeros(grid.M_ext, strength_components(system.kind));
+    std::lock_guard<std::mutex> lk(g_mu);
+    check_ctx(sewald_gpu_spread(context(), &p, D(system.x), D(system.f),
+                                system.kind == Kernel::stresslet ? D(system.nu) : nullptr,
+                                static_cast<int64_t>(system.size()), out.v.data()));
+    return out;
+}
+
+std::vector<Vec3> gather(const RealField& field, const GridSpec& grid, const Window& window,
+                         const TargetSet& targets) {
+    if (field.n != grid.M_ext) throw std::invalid_argument("field shape does not match the extended grid");
+    if (field.comps != 3) throw std::invalid_argument("gather expects a 3-component field");
+    if (std::fabs(window.spec().h - grid.h) > 1e-12 * grid.h)
+        throw std::invalid_argument("window was built for a different grid spacing");
+    EwaldParams e;
+    e.d = grid.d;
+    e.grid = grid;
+    e.window = window.spec();
+    sewald_params_c p = to_c(e);
+    std::vector<Vec3> u(targets.x.size());
+    std::lock_guard<std::mutex> lk(g_mu);
+    check_ctx(sewald_gpu_gather(context(), &p, field.v.data(), D(targets.x), static_cast<int64_t>(targets.x.size()),
+                                reinterpret_cast<double*>(u.data())));
+    return u;
+}
+
+namespace {
+
+std::vector<Vec3> pipeline(bool full, const SourceSystem& s, const TargetSet& t, const EwaldParams& e,
+                           const SePipelineOptions& opt) {
+    validate_system(s);
+    if (s.kind != e.kind || s.d != e.d) throw std::invalid_argument("parameter set was built for a different system");
+    if (!(e.xi > 0.0)) throw std::invalid_argument("xi must be positive");
+    if (opt.table && opt.table->kind != e.kind)
+        throw std::invalid_argument("kernel table was built for a different kernel");
+    sewald_params_c p = to_c(e);
+    for (int i = 0; i < 3; ++i) p.L[i] = s.cell.L[i];
+    const std::size_t nt = t.same_as_sources ? s.size() : t.x.size();
+    std::vector<Vec3> u(nt);
+    const double* nu = s.kind == Kernel::stresslet ? D(s.nu) : nullptr;
+    std::lock_guard<std::mutex> lk(g_mu);
+    auto fn = full ? sewald_gpu_full_potential : sewald_gpu_fourier_potential;
+    check_ctx(fn(context(), &p, D(s.x), D(s.f), nu, static_cast<int64_t>(s.size()),
+                 t.same_as_sources ? nullptr : D(t.x), static_cast<int64_t>(nt), t.same_as_sources ? 1 : 0,
+                 opt.precompute_0p ? 1 : 0, reinterpret_cast<double*>(u.data())));
+    return u;
+}
+
+}  // namespace
+
+std::vector<Vec3> se_fourier_potential(const SourceSystem& system, const TargetSet& targets,
+                                       const EwaldParams& params, const SePipelineOptions& opt) {
+    return pipeline(false, system, targets, params, opt);
+}
+
+std::vector<Vec3> full_potential(const SourceSystem& system, const TargetSet& targets, const EwaldParams& params,
+                                 const SePipelineOptions& opt) {
+    return pipeline(true, system, targets, params, opt);
+}
+
+std::vector<Vec3> realspace_potential(const SourceSystem& system, const TargetSet& targets, double xi, double rc,
+                                      bool starred, int n_threads) {
+    (void)n_threads;  // accepted for compatibility; the sum runs on the GPU
+    if (!(xi > 0.0)) throw std::invalid_argument("split parameter must be positive");
+    const bool skip_self = starred && targets.same_as_sources;
+    if (skip_self && targets.x.size() != system.size())
+        throw std::invalid_argument("starred evaluation needs one target per source");
+    validate_system(system);
+    for (const Vec3& p : targets.x)
+        for (double c : p)
+            if (!std::isfinite(c)) throw std::invalid_argument("target coordinates must be finite");
+    std::vector<Vec3> u(targets.x.size());
+    std::lock_guard<std::mutex> lk(g_mu);
+    check_ctx(sewald_gpu_realspace_potential(
+        context(), kernel_id(system.kind), system.d, system.cell.L.data(), D(system.x), D(system.f),
+        system.kind == Kernel::stresslet ? D(system.nu) : nullptr, static_cast<int64_t>(system.size()),
+        D(targets.x), static_cast<int64_t>(targets.x.size()), targets.same_as_sources ? 1 : 0, xi, rc,
+        starred ? 1 : 0, reinterpret_cast<double*>(u.data())));
+    return u;
+}
+
+}  // namespace sewald

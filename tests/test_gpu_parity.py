@@ -329,3 +329,16 @@ def test_session_parts_sum_to_whole(S, kind, d, same):
         torch.cuda.synchronize()
         assert rel_rms(total.cpu().numpy(), u_ref) < TOL, world
     sess.close()
+
+
+def test_cpp_dropin_binary():
+    """C++ user code against the reference header names (tests/cpp/test_dropin.cpp)."""
+    import os
+    import subprocess
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "paper_2210_01255_b200", "lib", "test_dropin")
+    assert os.path.exists(exe), "build() did not produce the drop-in test binary"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=600)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "dropin: OK" in r.stdout
