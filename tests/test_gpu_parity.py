@@ -342,3 +342,43 @@ def test_cpp_dropin_binary():
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "dropin: OK" in r.stdout
+
+
+# ---------------------------------------------------------------------------
+# BASELINE config 2 at full size (N = 1e6): size-independent properties
+# ---------------------------------------------------------------------------
+
+def test_full_size_c2_xi_invariance(S):
+    """The full velocity does not depend on the split parameter beyond the
+    tolerance (test_realspace.cpp:516-540 at the BASELINE size): xi = 37
+    (pinned, M = 128) vs xi = 45."""
+    from paper_2210_01255_b200.workloads import CONFIGS, generate
+    cfg = CONFIGS[2]
+    x, f, nu, xt = generate(cfg)
+    sysm = S.SourceSystem(cfg.kind, S.Cell(cfg.L), cfg.d, x, f, nu)
+    tg = S.TargetSet.from_sources(sysm)
+    Q = S.source_quantity(sysm)
+    pa = S.select_parameters(cfg.kind, cfg.d, sysm.cell, Q, 37.0, S.ToleranceSpec(cfg.tol)).params
+    pb = S.select_parameters(cfg.kind, cfg.d, sysm.cell, Q, 45.0, S.ToleranceSpec(cfg.tol)).params
+    ua = S.full_potential(sysm, tg, pa)
+    ub = S.full_potential(sysm, tg, pb)
+    rms = float(np.sqrt(np.mean(np.sum((ua - ub) ** 2, 1))))
+    rms_u = float(np.sqrt(np.mean(np.sum(ua ** 2, 1))))
+    print(f"c2 full size: rms(u)={rms_u:.6g} rms(u37-u45)={rms:.3e} (tau={cfg.tol})")
+    assert rms <= 10.0 * (cfg.tol + cfg.tol)
+
+
+@pytest.mark.oracle
+def test_full_size_c2_realspace_subset(S, ref):
+    """Real-space sum at N = 1e6 for a subset of targets against the reference
+    (all sources; targets nudged off the source points, unstarred sum)."""
+    from paper_2210_01255_b200.workloads import CONFIGS, generate
+    cfg = CONFIGS[2]
+    x, f, nu, _ = generate(cfg)
+    rng = np.random.default_rng(5)
+    xt = x[rng.choice(x.shape[0], 400, replace=False)] + 3.3e-7
+    sysm = S.SourceSystem(cfg.kind, S.Cell(cfg.L), cfg.d, x, f, nu)
+    p = S.select_parameters(cfg.kind, cfg.d, sysm.cell, S.source_quantity(sysm), cfg.xi, S.ToleranceSpec(cfg.tol)).params
+    u = S.realspace_potential(sysm, S.TargetSet(xt, False), p.xi, p.rc, False)
+    ur = ref.realspace_potential(0, 3, cfg.L, x, f, None, xt, False, p.xi, p.rc, False, 16)
+    assert rel_rms(u, ur) < TOL
