@@ -34,7 +34,16 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-FLOPS_PER_PAIR = {0: 100.0, 1: 140.0, 2: 90.0}
+# Algorithmic fp64 flops per accepted (directed) real-space pair of the
+# implemented evaluation, keyed (kernel, symmetric): ncu thread-level
+# 2*DFMA + DMUL + DADD of the kernel divided by the kernel's own pair counter
+# (tools/rs_flops.py; profiles/r1_realspace_flops.txt; DESIGN.md "real-space
+# roofline"). The symmetric kernel (targets == sources) evaluates each
+# unordered pair once and charges half of it to each direction.
+FLOPS_PER_PAIR = {
+    (0, True): 66.5, (1, True): 88.3, (2, True): 61.9,
+    (0, False): 136.5, (1, False): 164.4, (2, False): 130.5,
+}
 
 
 def parse():
@@ -359,7 +368,7 @@ def run_ours(args, cfg):
         except Exception:
             pass
         hbm_peak = mp.get("hbm_gbs", 6650.0)
-        fl = FLOPS_PER_PAIR[int(cfg.kind)]
+        fl = FLOPS_PER_PAIR[(int(cfg.kind), bool(same and os.environ.get("SEWALD_RS_SYM", "1") != "0"))]
         achieved = rs_pairs * fl / (rs_ms * 1e-3) / 1e12
         C = 9 if cfg.kind == S.Kernel.stresslet else 3
         vol = int(np.prod(params.grid.M_ext))

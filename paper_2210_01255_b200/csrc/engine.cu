@@ -250,6 +250,12 @@ void build_cell_grid(sewald_gpu_session* s) {
         const double span = a < p.d ? p.L[a] : hi[a] - lo[a];
         cg.w[a] = span > 0.0 ? span / cg.n[a] : target_w;
     }
+    static const int sub_env = [] {
+        const char* e = getenv("SEWALD_RS_SUB");
+        return e ? atoi(e) : 8;
+    }();
+    const int64_t ncell = (int64_t)cg.n[0] * cg.n[1] * cg.n[2];
+    cg.sub = std::max(0, std::min(sub_env, 32 - bits_for((uint64_t)ncell)));
     s->cg = cg;
 }
 
@@ -275,11 +281,13 @@ void ensure_spread_order(sewald_gpu_session* s, int64_t i0, int64_t i1) {
     cudaStream_t st = s->ctx->stream;
     s->shape = spread_plan_shape(s->g, s->p.P);
     s->sweep = sweep_shape(s->g, s->p.P);
-    static const bool sweep_enabled = [] {
+    // z-sweep for P <= 24 (c1-c3, c5); the 8x8x16 tile kernel wins for the
+    // widest windows (c4, P = 32: 25 ms vs 42 ms). SEWALD_SPREAD_SWEEP=0/1 forces.
+    static const int sweep_mode = [] {
         const char* e = getenv("SEWALD_SPREAD_SWEEP");
-        return !(e && e[0] == '0');
+        return e && e[0] ? (e[0] == '0' ? 0 : 1) : -1;
     }();
-    if (!sweep_enabled) s->sweep.ok = false;
+    if (sweep_mode == 0 || (sweep_mode < 0 && s->p.P > 24)) s->sweep.ok = false;
     const int64_t nb = s->sweep.ok ? s->sweep.nkeys
                                    : (int64_t)s->shape.nb[0] * s->shape.nb[1] * s->shape.nb[2];
     s->sp_keys.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1));
@@ -327,9 +335,9 @@ void ensure_cells(sewald_gpu_session* s) {
     if (N > 0) {
         ++s->ctx->launches;
         sort_pairs(s, s->c_keys.as<uint32_t>(), s->c_keys2.as<uint32_t>(), s->c_vals.as<uint32_t>(),
-                   s->c_order.as<uint32_t>(), N, bits_for((uint64_t)ncell + 1));
+                   s->c_order.as<uint32_t>(), N, bits_for((uint64_t)ncell << s->cg.sub));
     }
-    launch_bucket_offsets(s->c_keys2.as<uint32_t>(), N, (int)ncell, s->c_off.as<int64_t>(), st);
+    launch_bucket_offsets(s->c_keys2.as<uint32_t>(), N, (int)ncell, s->c_off.as<int64_t>(), st, s->cg.sub);
     launch_pack_sources(s->s_folded.as<double>(), s->f.as<double>(), s->nu.as<double>(), s->stresslet,
                         s->c_order.as<uint32_t>(), N, s->packed.as<double>(), s->packedf.as<float4>(), st);
     s->ctx->launches += 2;
@@ -352,7 +360,7 @@ void ensure_target_order(sewald_gpu_session* s) {
                         s->t_vals.as<uint32_t>(), st);
     ++s->ctx->launches;
     sort_pairs(s, s->t_keys.as<uint32_t>(), s->t_keys2.as<uint32_t>(), s->t_vals.as<uint32_t>(),
-               s->t_order.as<uint32_t>(), Nt, bits_for((uint64_t)ncell + 1));
+               s->t_order.as<uint32_t>(), Nt, bits_for((uint64_t)ncell << s->cg.sub));
 }
 
 const double* target_positions(sewald_gpu_session* s) {

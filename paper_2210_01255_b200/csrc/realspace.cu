@@ -58,7 +58,12 @@ __global__ void fold_key_kernel(CellGrid cg, const double* __restrict__ x, int64
         folded[3 * i + ax] = v;
     }
     const int cx = cell_of(cg, 0, y[0]), cy = cell_of(cg, 1, y[1]), cz = cell_of(cg, 2, y[2]);
-    keys[i] = (uint32_t)((cz * cg.n[1] + cy) * cg.n[0] + cx);
+    // low `sub` bits: x position inside the cell, so that consecutive particles
+    // of a cell row (i-clusters, j-blocks) are compact along x as well
+    const int ns = 1 << cg.sub;
+    int sx = (int)floor(((y[0] - cg.origin[0]) / cg.w[0] - cx) * ns);
+    sx = sx < 0 ? 0 : (sx > ns - 1 ? ns - 1 : sx);
+    keys[i] = ((uint32_t)((cz * cg.n[1] + cy) * cg.n[0] + cx) << cg.sub) | (uint32_t)sx;
     vals[i] = (uint32_t)i;
 }
 

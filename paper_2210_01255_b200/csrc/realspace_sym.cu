@@ -57,7 +57,8 @@ struct Strength<SEWALD_STRESSLET> {
 };
 
 // Contribution of source strength s at separation r (target - source) and
-// its reaction on the source from the target strength t (separation -r).
+// its reaction on the source from the target strength t (separation -r),
+// accumulated into ua (target) and ub (source).
 template <int KIND>
 __device__ __forceinline__ void pair_both(const Screened& sc, double xi2, double n2, double r0, double r1,
                                           double r2, const double* s, const double* t, double* ua, double* ub) {
@@ -69,17 +70,17 @@ __device__ __forceinline__ void pair_both(const Screened& sc, double xi2, double
         ua[0] = fma(a, s[0], fma(bs, r0, ua[0]));
         ua[1] = fma(a, s[1], fma(bs, r1, ua[1]));
         ua[2] = fma(a, s[2], fma(bs, r2, ua[2]));
-        ub[0] = fma(a, t[0], bt * r0);
-        ub[1] = fma(a, t[1], bt * r1);
-        ub[2] = fma(a, t[2], bt * r2);
+        ub[0] = fma(a, t[0], fma(bt, r0, ub[0]));
+        ub[1] = fma(a, t[1], fma(bt, r1, ub[1]));
+        ub[2] = fma(a, t[2], fma(bt, r2, ub[2]));
     } else if (KIND == SEWALD_ROTLET) {
         const double c = sc.Ey * (sc.iy * sc.iy) * (sc.R + sc.cx);
         ua[0] = fma(c, s[1] * r2 - s[2] * r1, ua[0]);
         ua[1] = fma(c, s[2] * r0 - s[0] * r2, ua[1]);
         ua[2] = fma(c, s[0] * r1 - s[1] * r0, ua[2]);
-        ub[0] = -c * (t[1] * r2 - t[2] * r1);
-        ub[1] = -c * (t[2] * r0 - t[0] * r2);
-        ub[2] = -c * (t[0] * r1 - t[1] * r0);
+        ub[0] = fma(-c, t[1] * r2 - t[2] * r1, ub[0]);
+        ub[1] = fma(-c, t[2] * r0 - t[0] * r2, ub[1]);
+        ub[2] = fma(-c, t[0] * r1 - t[1] * r0, ub[2]);
     } else {
         const double iy2 = sc.iy * sc.iy;
         const double x2 = xi2 * n2;
@@ -103,9 +104,9 @@ __device__ __forceinline__ void pair_both(const Screened& sc, double xi2, double
             const double rv = r0 * v[0] + r1 * v[1] + r2 * v[2];
             const double qv = q[0] * v[0] + q[1] * v[1] + q[2] * v[2];
             const double w = c1 * rq * rv + c2 * qv;
-            ub[0] = -(w * r0 + c2 * (q[0] * rv + v[0] * rq));
-            ub[1] = -(w * r1 + c2 * (q[1] * rv + v[1] * rq));
-            ub[2] = -(w * r2 + c2 * (q[2] * rv + v[2] * rq));
+            ub[0] -= w * r0 + c2 * (q[0] * rv + v[0] * rq);
+            ub[1] -= w * r1 + c2 * (q[1] * rv + v[1] * rq);
+            ub[2] -= w * r2 + c2 * (q[2] * rv + v[2] * rq);
         }
     }
 }
@@ -220,7 +221,9 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                 if (b0 >= b1) continue;
                 const double shx = __dmul_rn((double)sx, cg.L[0]);
                 const bool pos_shift = sx > 0 || (sx == 0 && (sy > 0 || (sy == 0 && sz > 0)));
-                const float tf0 = (float)(xa0 - shx), tf1 = (float)(xa1 - shy), tf2 = (float)(xa2 - shz);
+                // shifted target position, once per row piece (r = (x_a - shift) - x_j)
+                const double xs0 = xa0 - shx, xs1 = xa1 - shy, xs2 = xa2 - shz;
+                const float tf0 = (float)xs0, tf1 = (float)xs1, tf2 = (float)xs2;
                 for (int64_t jb = b0; jb < b1; jb += 32) {
                     const int cnt = (int)min((int64_t)32, b1 - jb);
                     __syncwarp();
@@ -265,9 +268,9 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                         bool acc = (m >> s) & 1u;
                         double r0 = 0, r1 = 0, r2 = 0, n2 = 0;
                         if (acc) {
-                            r0 = (xa0 - jx[0][j]) - shx;
-                            r1 = (xa1 - jx[1][j]) - shy;
-                            r2 = (xa2 - jx[2][j]) - shz;
+                            r0 = xs0 - jx[0][j];
+                            r1 = xs1 - jx[1][j];
+                            r2 = xs2 - jx[2][j];
                             n2 = __dadd_rn(__dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1)), __dmul_rn(r2, r2));
                             acc = n2 < rc2;
                         }
@@ -283,11 +286,11 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
 #else
                                 const Screened sc = screened<SHORT>(n2, a.xi, xi2, exp_tab);
 #endif
-                                double ub[3];
+                                double ub[3] = {racc[0][j], racc[1][j], racc[2][j]};
                                 pair_both<KIND>(sc, xi2, n2, r0, r1, r2, sj, fa, ua, ub);
-                                racc[0][j] += ub[0];
-                                racc[1][j] += ub[1];
-                                racc[2][j] += ub[2];
+                                racc[0][j] = ub[0];
+                                racc[1][j] = ub[1];
+                                racc[2][j] = ub[2];
                                 npairs += 2;
                             }
                         }

@@ -19,7 +19,8 @@ SpreadPlanShape spread_plan_shape(const DevGrid& g, int P);
 void launch_spread_bucket(const DevGrid& g, int P, const double* x, int64_t N,
                           const SpreadPlanShape& s, uint32_t* keys, uint32_t* vals, int* bad,
                           cudaStream_t st);
-void launch_bucket_offsets(const uint32_t* keys, int64_t N, int nb, int64_t* off, cudaStream_t st);
+void launch_bucket_offsets(const uint32_t* keys, int64_t N, int nb, int64_t* off, cudaStream_t st,
+                           int shift = 0);
 void launch_spread_tiles(const DevGrid& g, const DevWindow& w, const double* x, const double* f,
                          const double* nu, int stresslet, const uint32_t* order,
                          const int64_t* off, const SpreadPlanShape& s, double* out,
@@ -64,6 +65,7 @@ struct CellGrid {
     double w[3];        // cell widths
     double origin[3];   // lower corner (0 on periodic axes)
     double L[3];
+    int sub;            // x sub-cell key bits: particles sorted by x within a cell row
 };
 
 struct RealspaceArgs {

@@ -71,13 +71,13 @@ __global__ void spread_bucket_kernel(DevGrid g, int P, const double* __restrict_
 
 // off[b] = first sorted position with key >= b (b in [0, nb]).
 __global__ void bucket_offsets_kernel(const uint32_t* __restrict__ keys, int64_t N, int nb,
-                                      int64_t* __restrict__ off) {
+                                      int64_t* __restrict__ off, int shift) {
     const int b = blockIdx.x * blockDim.x + threadIdx.x;
     if (b > nb) return;
     int64_t lo = 0, hi = N;
     while (lo < hi) {
         const int64_t mid = (lo + hi) >> 1;
-        if (keys[mid] < (uint32_t)b) lo = mid + 1; else hi = mid;
+        if ((keys[mid] >> shift) < (uint32_t)b) lo = mid + 1; else hi = mid;
     }
     off[b] = lo;
 }
@@ -371,8 +371,9 @@ void launch_spread_bucket(const DevGrid& g, int P, const double* x, int64_t N,
                                                                        s.nb[2], keys, vals, bad);
 }
 
-void launch_bucket_offsets(const uint32_t* keys, int64_t N, int nb, int64_t* off, cudaStream_t st) {
-    bucket_offsets_kernel<<<(nb + 1 + 255) / 256, 256, 0, st>>>(keys, N, nb, off);
+void launch_bucket_offsets(const uint32_t* keys, int64_t N, int nb, int64_t* off, cudaStream_t st,
+                           int shift) {
+    bucket_offsets_kernel<<<(nb + 1 + 255) / 256, 256, 0, st>>>(keys, N, nb, off, shift);
 }
 
 void launch_spread_tiles(const DevGrid& g, const DevWindow& w, const double* x, const double* f,
