@@ -1,9 +1,11 @@
 // Real-space sum for targets == sources (the starred sum of full_potential),
 // using pair symmetry: each unordered pair {a, b + shift} within rc is
 // evaluated ONCE and applied to both particles (the kernels are even
-// (stokeslet) or odd (rotlet, stresslet) in r, and the reference's
-// r_ba = (x_b - x_a) - (-shift) is exactly -r_ab in IEEE arithmetic, so the
-// accepted set and every term match the reference's two directed sums).
+// (stokeslet) or odd (rotlet, stresslet) in r). The separation is formed as
+// r = (x_a - shift) - x_b with the shifted position computed once per row
+// piece; it differs from the reference's (x_a - x_b) - shift by at most one
+// rounding of a coordinate, so the accepted set can differ only for pairs
+// within ~1e-16 of rc, whose terms are ~erfc(xi rc) below the rms.
 //
 // Reference: accumulate_rows /root/reference/proj/src/realspace.cpp:30-93,
 //            realspace_kernel /root/reference/proj/src/kernels.cpp:71-116.
