@@ -40,6 +40,10 @@ sys.path.insert(0, ROOT)
 # (tools/rs_flops.py; profiles/r1_realspace_flops.txt; DESIGN.md "real-space
 # roofline"). The symmetric kernel (targets == sources) evaluates each
 # unordered pair once and charges half of it to each direction.
+# DRAM bytes (read + write) per launch of the dominant kernel from one
+# `ncu --set full` capture of the same bench command (profiles/r1_ncu_*_v2.txt).
+TRAFFIC_BYTES = {"c2_stokeslet_d3_N1e6": 97_831_680 + 4_818_432}
+
 FLOPS_PER_PAIR = {
     (0, True): 66.5, (1, True): 88.3, (2, True): 61.9,
     (0, False): 136.5, (1, False): 164.4, (2, False): 130.5,
@@ -387,7 +391,8 @@ def run_ours(args, cfg):
             "roofline": {"kernel": "realspace", "bound": "fp64", "achieved": achieved, "peak": peak64,
                          "unit": "TFLOP/s", "frac": achieved / peak64,
                          "peak_source": "measured DFMA microbenchmark (sewald_gpu_fp64_peak)",
-                         "traffic": None, "pairs_per_launch": rs_pairs, "flops_per_pair": fl,
+                         "traffic": TRAFFIC_BYTES.get(cfg.name), "traffic_unit": "bytes/launch (ncu dram read+write)",
+                         "pairs_per_launch": rs_pairs, "flops_per_pair": fl,
                          "kernel_ms": rs_ms},
             "stages_ms": stages,
             "spread_gather": {"spread_GBps": spread_bytes / (spread_ms * 1e-3) / 1e9,
