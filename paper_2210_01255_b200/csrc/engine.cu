@@ -373,42 +373,54 @@ const uint32_t* target_order(sewald_gpu_session* s) {
     return s->same ? s->c_order.as<uint32_t>() : s->t_order.as<uint32_t>();
 }
 
-// Targets bucketed / sorted for the z-sweep gather, with their window taps.
-bool ensure_gather_sweep(sewald_gpu_session* s) {
-    // The sweep wins for wide windows (P > 16: c3, c4); the warp-per-target
-    // gather is faster for P <= 16. SEWALD_GATHER_SWEEP=1/0 forces either.
-    static const int mode = [] {
-        const char* e = getenv("SEWALD_GATHER_SWEEP");
-        return e ? (e[0] == '0' ? 0 : 1) : -1;
+// Targets bucketed / sorted for the tiled gather (P <= 16) or the z-sweep
+// gather (P > 16), with their window taps. Returns 0 (warp-per-target
+// gather), 1 (sweep) or 2 (tiles). SEWALD_GATHER=warp|sweep|tile forces one.
+int ensure_gather_order(sewald_gpu_session* s) {
+    static const int forced = [] {
+        const char* e = getenv("SEWALD_GATHER");
+        if (!e) return -1;
+        if (!strcmp(e, "warp")) return 0;
+        if (!strcmp(e, "sweep")) return 1;
+        if (!strcmp(e, "tile")) return 2;
+        return -1;
     }();
     const SweepShape sh = sweep_shape(s->g, s->p.P);
-    const bool use = mode == 1 || (mode == -1 && s->p.P > 16);
-    if (!use || !sh.ok) return false;
-    if (s->tg_ready) return true;
+    const TileShape ts = tile_shape(s->g, s->p.P);
+    int mode = forced >= 0 ? forced : (s->p.P > 16 ? 1 : 2);
+    if (mode == 2 && !ts.ok) mode = sh.ok ? 1 : 0;
+    if (mode == 1 && !sh.ok) mode = 0;
+    if (mode == 0) return 0;
+    if (s->tg_ready && s->tg_mode == mode) return mode;
     cudaStream_t st = s->ctx->stream;
     const int64_t Nt = s->Nt;
     const double* xt = s->same ? s->x.as<double>() : s->xt.as<double>();
     const int64_t n = std::max<int64_t>(Nt, 1);
+    const int64_t nkeys = mode == 1 ? sh.nkeys : ts.ntiles;
     s->tg_keys.ensure(sizeof(uint32_t) * n);
     s->tg_keys2.ensure(sizeof(uint32_t) * n);
     s->tg_vals.ensure(sizeof(uint32_t) * n);
     s->tg_order.ensure(sizeof(uint32_t) * n);
-    s->tg_off.ensure(sizeof(int64_t) * (sh.nkeys + 1));
+    s->tg_off.ensure(sizeof(int64_t) * (nkeys + 1));
     s->tg_w.ensure(sizeof(double) * 3 * s->p.P * n);
     s->tg_sw.ensure(sizeof(int4) * n);
     int* bad = s->flags.as<int>() + FLAG_GATHER_BOX;
-    launch_sweep_bucket(s->g, s->p.P, xt, Nt, sh, s->tg_keys.as<uint32_t>(), s->tg_vals.as<uint32_t>(), bad, st);
+    if (mode == 1)
+        launch_sweep_bucket(s->g, s->p.P, xt, Nt, sh, s->tg_keys.as<uint32_t>(), s->tg_vals.as<uint32_t>(), bad, st);
+    else
+        launch_tile_bucket(s->g, s->p.P, ts, xt, Nt, s->tg_keys.as<uint32_t>(), s->tg_vals.as<uint32_t>(), bad, st);
     check_flag(s, FLAG_GATHER_BOX, SEWALD_EINVAL,
                "point too close to the extended box boundary; free-direction padding is too small");
     if (Nt > 0)
         sort_pairs(s, s->tg_keys.as<uint32_t>(), s->tg_keys2.as<uint32_t>(), s->tg_vals.as<uint32_t>(),
-                   s->tg_order.as<uint32_t>(), Nt, bits_for((uint64_t)sh.nkeys + 1));
-    launch_bucket_offsets(s->tg_keys2.as<uint32_t>(), Nt, (int)sh.nkeys, s->tg_off.as<int64_t>(), st);
+                   s->tg_order.as<uint32_t>(), Nt, bits_for((uint64_t)nkeys + 1));
+    launch_bucket_offsets(s->tg_keys2.as<uint32_t>(), Nt, (int)nkeys, s->tg_off.as<int64_t>(), st);
     launch_sweep_weights(s->g, s->w, xt, nullptr, nullptr, 0, s->tg_order.as<uint32_t>(), Nt, s->tg_w.as<double>(),
                          s->tg_sw.as<int4>(), nullptr, st);
     s->ctx->launches += 3;
     s->tg_ready = true;
-    return true;
+    s->tg_mode = mode;
+    return mode;
 }
 
 void d3_prepare(sewald_gpu_session* s) {
@@ -688,10 +700,15 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
     }
     if (parts & 1) {
         const double h3 = s->p.h * s->p.h * s->p.h;
-        if (ensure_gather_sweep(s)) {
+        const int gmode = ensure_gather_order(s);
+        if (gmode == 1) {
             if (first) cuda_check(cudaMemsetAsync(u, 0, sizeof(double) * 3 * Nt, st), "u zero");
             launch_gather_sweep(s->g, s->p.P, s->tg_w.as<double>(), s->tg_sw.as<int4>(), s->tg_off.as<int64_t>(),
                                 sweep_shape(s->g, s->p.P), part, nparts, s->flow.as<double>(), h3, u, st);
+        } else if (gmode == 2) {
+            launch_gather_tile(s->g, s->p.P, tile_shape(s->g, s->p.P), s->tg_w.as<double>(), s->tg_sw.as<int4>(),
+                               s->tg_off.as<int64_t>(), part, nparts, s->flow.as<double>(), h3, first ? 0 : 1, u,
+                               st);
         } else {
             launch_gather(s->g, s->w, s->flow.as<double>(), target_positions(s), torder + t0, t1 - t0, h3,
                           first ? 0 : 1, u, st);

@@ -82,6 +82,7 @@ struct sewald_gpu_session {
     sewald_b200::DevBuf xt, t_folded, t_keys, t_keys2, t_vals, t_order;
     // gather sweep ordering of the targets
     bool tg_ready = false;
+    int tg_mode = 0;  // 1: z-sweep gather, 2: tiled gather
     sewald_b200::DevBuf tg_keys, tg_keys2, tg_vals, tg_order, tg_off, tg_w, tg_sw;
     // grids
     sewald_b200::DevBuf grid, flow;

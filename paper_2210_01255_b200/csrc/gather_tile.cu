@@ -1,0 +1,184 @@
+// Gather through shared-memory grid tiles (P <= 16).
+//
+// Reference: gather /root/reference/proj/src/fourier.cpp:276-309 (stencil
+// :168-188). Same taps, stencil origins and wrap; only the summation order
+// differs.
+//
+// Targets are bucketed by the B x B x B block of their (wrapped) stencil
+// start. One CTA owns one block: it stages the L^3 region (L = B + P - 1)
+// that every stencil of the block lies in, one flow component at a time,
+// into shared memory, then each warp evaluates whole targets from it (lanes
+// = 16 z taps x 2 y rows, warp reduction). The L2 stream per target drops
+// from P^3 x 3 values (warp-per-target gather) to the region share, and the
+// tap loop reads shared memory only. Every target is owned by one block, so
+// results are written without atomics.
+#include "device_common.cuh"
+#include "sg_kernels.h"
+
+#include <algorithm>
+
+namespace sewald_b200 {
+
+namespace {
+
+constexpr int GT_WARPS = 8;
+constexpr int GT_THREADS = 32 * GT_WARPS;
+constexpr int GT_PMAX = 16;
+
+__global__ void tile_bucket_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, const double* __restrict__ x,
+                                   int64_t N, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
+                                   int* __restrict__ bad) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    int t[3];
+    const int nt[3] = {ntx, nty, ntz};
+    for (int ax = 0; ax < 3; ++ax) {
+        int j0;
+        double rel;
+        stencil_origin(g, P, ax, x[3 * i + ax], j0, rel);
+        if (ax < g.d) {
+            j0 = wrap_index(j0, g.n[ax]);
+        } else if (j0 < 0 || j0 + P > g.n[ax]) {
+            atomicExch(bad, 1);
+            j0 = 0;
+        }
+        t[ax] = min(j0 / B, nt[ax] - 1);
+    }
+    keys[i] = (uint32_t)(((int64_t)t[0] * nty + t[1]) * ntz + t[2]);
+    vals[i] = (uint32_t)i;
+}
+
+__global__ void __launch_bounds__(GT_THREADS)
+gather_tile_kernel(DevGrid g, int P, int B, int L, int ntx, int nty, int ntz, int64_t tile0,
+                   const double* __restrict__ W, const int4* __restrict__ SW, const int64_t* __restrict__ off,
+                   const double* __restrict__ grid, double h3, int accumulate, double* __restrict__ u) {
+    extern __shared__ double sm[];
+    const int64_t tile = tile0 + blockIdx.x;
+    const int64_t p0 = off[tile], p1 = off[tile + 1];
+    if (p0 >= p1) return;
+    const int tz = (int)(tile % ntz);
+    const int ty = (int)((tile / ntz) % nty);
+    const int tx = (int)(tile / ((int64_t)ntz * nty));
+    const int X0 = tx * B, Y0 = ty * B, Z0 = tz * B;
+    const int L2 = L * L, L3 = L2 * L;
+    // region + zero pad (lanes past the stencil read it with zero weight)
+    const int pad = 2 * GT_PMAX * L + 2 * GT_PMAX;
+    double* region = sm;
+    double* wsm = sm + L3 + pad;  // per warp: 3 * P taps
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* wt_s = wsm + warp * 3 * GT_PMAX;
+    int* rowoff = reinterpret_cast<int*>(wsm + GT_WARPS * 3 * GT_PMAX);  // L^2 row offsets (-1: outside)
+    int* zoff = rowoff + L2;                                            // L z offsets (-1: outside)
+    for (int e = threadIdx.x; e < pad; e += GT_THREADS) region[L3 + e] = 0.0;
+    for (int row = threadIdx.x; row < L2; row += GT_THREADS) {
+        const int i = row / L, j = row - i * L;
+        int gx = X0 + i, gy = Y0 + j;
+        bool ok = true;
+        if (g.d > 0) gx %= g.n[0]; else ok = gx < g.n[0];
+        if (g.d > 1) gy %= g.n[1]; else ok = ok && gy < g.n[1];
+        rowoff[row] = ok ? (gx * g.n[1] + gy) * g.n[2] : -1;
+    }
+    if (threadIdx.x < L) {
+        int gz = Z0 + threadIdx.x;
+        bool ok = true;
+        if (g.d > 2) gz %= g.n[2]; else ok = gz < g.n[2];
+        zoff[threadIdx.x] = ok ? gz : -1;
+    }
+
+    const int64_t cs = (int64_t)g.n[0] * g.n[1] * g.n[2];
+    const int z = lane & 15, half = lane >> 4;
+    for (int c = 0; c < 3; ++c) {
+        __syncthreads();
+        const double* gc = grid + c * cs;
+        // cp.async row copies: L z-values per (x, y) row, offsets precomputed
+        for (int row = warp; row < L2; row += GT_WARPS) {
+            const int ro = rowoff[row];
+            if (lane < L) {
+                double* dst = region + row * L + lane;
+                const int zo = zoff[lane];
+                if (ro >= 0 && zo >= 0) {
+                    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gc + ro + zo));
+                } else {
+                    *dst = 0.0;
+                }
+            }
+        }
+        asm volatile("cp.async.wait_all;\n" ::);
+        __syncthreads();
+        for (int64_t t = p0 + warp; t < p1; t += GT_WARPS) {
+            __syncwarp();
+            const double* wt = W + t * 3 * P;
+            for (int q = lane; q < 3 * P; q += 32) wt_s[(q / P) * GT_PMAX + q % P] = __ldg(wt + q);
+            const int4 sw = SW[t];
+            __syncwarp();
+            const double wz = z < P ? wt_s[2 * GT_PMAX + z] : 0.0;
+            double cy[GT_PMAX / 2];
+#pragma unroll
+            for (int m = 0; m < GT_PMAX / 2; ++m) {
+                const int b = half + 2 * m;
+                cy[m] = b < P ? wt_s[GT_PMAX + b] * wz : 0.0;
+            }
+            const int ox = sw.x - X0, oy = sw.y - Y0, oz = sw.z - Z0;
+            const double* rp = region + (ox * L + oy + half) * L + oz + z;
+            double acc = 0.0, acc2 = 0.0;
+            for (int a = 0; a < P; ++a) {
+                const double wx = wt_s[a];
+#pragma unroll
+                for (int m = 0; m < GT_PMAX / 2; m += 2) {
+                    acc = fma(wx * cy[m], rp[2 * m * L], acc);
+                    acc2 = fma(wx * cy[m + 1], rp[2 * (m + 1) * L], acc2);
+                }
+                rp += L2;
+            }
+            acc += acc2;
+#pragma unroll
+            for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
+            if (lane == 0) {
+                double* dst = u + 3 * (int64_t)sw.w + c;
+                *dst = accumulate ? *dst + h3 * acc : h3 * acc;
+            }
+        }
+    }
+}
+
+}  // namespace
+
+TileShape tile_shape(const DevGrid& g, int P) {
+    TileShape s{};
+    s.ok = P <= GT_PMAX;
+    s.B = std::max(1, 20 - P);
+    s.L = s.B + P - 1;
+    for (int ax = 0; ax < 3; ++ax) s.nt[ax] = (g.n[ax] + s.B - 1) / s.B;
+    s.ntiles = (int64_t)s.nt[0] * s.nt[1] * s.nt[2];
+    if (s.ntiles >= (int64_t(1) << 31)) s.ok = false;
+    const int pad = 2 * GT_PMAX * s.L + 2 * GT_PMAX;
+    s.smem = sizeof(double) * ((size_t)s.L * s.L * s.L + pad + GT_WARPS * 3 * GT_PMAX) +
+             sizeof(int) * ((size_t)s.L * s.L + s.L);
+    if ((int64_t)g.n[0] * g.n[1] * g.n[2] >= (int64_t(1) << 31)) s.ok = false;  // int offsets
+    if (s.smem > 200 * 1024 || s.L > 32) s.ok = false;
+    return s;
+}
+
+void launch_tile_bucket(const DevGrid& g, int P, const TileShape& s, const double* x, int64_t N, uint32_t* keys,
+                        uint32_t* vals, int* bad, cudaStream_t st) {
+    if (N == 0) return;
+    tile_bucket_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], x, N,
+                                                                     keys, vals, bad);
+}
+
+void launch_gather_tile(const DevGrid& g, int P, const TileShape& s, const double* W, const int4* SW,
+                        const int64_t* off, int part, int nparts, const double* grid, double h3, int accumulate,
+                        double* u, cudaStream_t st) {
+    const int64_t t0 = s.ntiles * part / nparts, t1 = s.ntiles * (part + 1) / nparts;
+    if (t1 <= t0) return;
+    cudaFuncSetAttribute(gather_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s.smem);
+    // grid.x limit is 2^31 - 1: launch in chunks
+    for (int64_t a = t0; a < t1; a += (int64_t)1 << 30) {
+        const int64_t n = std::min<int64_t>(t1 - a, (int64_t)1 << 30);
+        gather_tile_kernel<<<(unsigned)n, GT_THREADS, s.smem, st>>>(g, P, s.B, s.L, s.nt[0], s.nt[1], s.nt[2], a, W,
+                                                                     SW, off, grid, h3, accumulate, u);
+    }
+}
+
+}  // namespace sewald_b200

@@ -35,6 +35,22 @@ void launch_stencil_bounds(const DevGrid& g, int P, const double* x, int64_t N, 
                            cudaStream_t st);
 
 // z-sweep spread (spread_sweep.cu): buckets = 4x8 (x,y) patches x z start.
+// Tiled gather (gather_tile.cu): targets bucketed by the B^3 block of their
+// stencil start; one CTA stages the L^3 region (L = B + P - 1) in shared memory.
+struct TileShape {
+    int B, L;
+    int nt[3];
+    int64_t ntiles;
+    size_t smem;
+    bool ok;
+};
+TileShape tile_shape(const DevGrid& g, int P);
+void launch_tile_bucket(const DevGrid& g, int P, const TileShape& s, const double* x, int64_t N, uint32_t* keys,
+                        uint32_t* vals, int* bad, cudaStream_t st);
+void launch_gather_tile(const DevGrid& g, int P, const TileShape& s, const double* W, const int4* SW,
+                        const int64_t* off, int part, int nparts, const double* grid, double h3, int accumulate,
+                        double* u, cudaStream_t st);
+
 struct SweepShape {
     int nbx, nby, nseg;
     int64_t nkeys;
