@@ -26,6 +26,9 @@ namespace sewald_b200 {
 namespace {
 
 constexpr int SX = 4, SY = 8;  // (x, y) patch per warp
+#ifndef SEWALD_SWEEP_NC16
+#define SEWALD_SWEEP_NC16 3
+#endif
 
 __device__ __forceinline__ int wrapi(int j, int n) {
     j %= n;
@@ -151,6 +154,7 @@ spread_sweep_kernel(DevGrid g, int P, const double* __restrict__ W, const int4* 
                     const double* __restrict__ STR, int C, int comp0, const int64_t* __restrict__ off, int nbx,
                     int nby, int nseg, double* __restrict__ out) {
     constexpr int WIN = PMAX + ZSTEP - 1;
+    comp0 += blockIdx.z * NC;  // component groups run as independent CTAs
     __shared__ double pwx[32][SX];
     __shared__ double pwy[32][SY];
     __shared__ double pwz[32][PMAX];
@@ -462,11 +466,10 @@ void launch_gsweep(const DevGrid& g, int P, const double* W, const int4* SW, con
 template <int PMAX, int NC, int ZSTEP>
 int launch_sweep(const DevGrid& g, int P, const double* W, const int4* SW, const double* STR, int C,
                  const int64_t* off, int nbx, int nby, int nseg, double* out, cudaStream_t st) {
-    dim3 grid(nbx * nby, nseg);
-    int n = 0;
-    for (int c0 = 0; c0 < C; c0 += NC, ++n)
-        spread_sweep_kernel<PMAX, NC, ZSTEP><<<grid, 32, 0, st>>>(g, P, W, SW, STR, C, c0, off, nbx, nby, nseg, out);
-    return n;
+    // C is a multiple of NC (3 or 9 components)
+    dim3 grid(nbx * nby, nseg, C / NC);
+    spread_sweep_kernel<PMAX, NC, ZSTEP><<<grid, 32, 0, st>>>(g, P, W, SW, STR, C, 0, off, nbx, nby, nseg, out);
+    return 1;
 }
 
 }  // namespace
@@ -504,7 +507,7 @@ void launch_sweep_weights(const DevGrid& g, const DevWindow& w, const double* x,
 int launch_spread_sweep(const DevGrid& g, int P, const double* W, const int4* SW, const double* STR, int C,
                         const int64_t* off, const SweepShape& s, double* out, cudaStream_t st) {
     if (P <= 8) return launch_sweep<8, 3, 4>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
-    if (P <= 16) return launch_sweep<16, 3, 4>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
+    if (P <= 16) return launch_sweep<16, SEWALD_SWEEP_NC16, 4>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
     if (P <= 24) return launch_sweep<24, 3, 2>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
     return launch_sweep<32, 1, 4>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
 }
