@@ -18,6 +18,7 @@
 #include "engine.h"
 #include "host_params.h"
 #include "modified_kernels.cuh"
+#include "aft_d0.h"
 
 #include <cufft.h>
 
@@ -284,6 +285,8 @@ struct FourierPlanAFT {
     DevBuf far, zero, near, rows_near, rows_zero, tables, mask, table0p;
     ClassBlock cb_far{}, cb_zero{}, cb_near{};
     ModSpec spec{};
+    std::unique_ptr<D0Real> d0r;  // d = 0: real pruned transforms (aft_d0.cu)
+    D0ScaleArgs d0sa{};
     ~FourierPlanAFT() {
         for (auto p : plans) cufftDestroy(p);
     }
@@ -399,9 +402,19 @@ void prepare(sewald_gpu_session* s, bool use_table) {
         const double s0 = A.table_path ? 2.0 : p.s0;
         for (int ax = 0; ax < 3; ++ax) A.nz[ax] = padded_length(s0, p.M_ext[ax]);
         const int64_t zvol = (int64_t)A.nz[0] * A.nz[1] * A.nz[2];
-        A.zero.ensure(sizeof(cuDoubleComplex) * zvol * A.C);
-        int nn3[3] = {A.nz[0], A.nz[1], A.nz[2]};
-        A.p_box = A.make(3, nn3, nn3, 1, (int)zvol, A.C, st);
+        // SEWALD_D0_C2C=1: the reference's full complex box transform (A/B checks)
+        static const bool c2c = [] {
+            const char* e = getenv("SEWALD_D0_C2C");
+            return e && e[0] == '1';
+        }();
+        if (c2c) {
+            A.zero.ensure(sizeof(cuDoubleComplex) * zvol * A.C);
+            int nn3[3] = {A.nz[0], A.nz[1], A.nz[2]};
+            A.p_box = A.make(3, nn3, nn3, 1, (int)zvol, A.C, st);
+        } else {
+            A.d0r.reset(new D0Real());
+            A.d0r->setup(A.n, A.nz, A.C, st);
+        }
         // rows = axis 0 of the padded box (free), free block = axes 1, 2
         std::vector<double> k0 = wavenumbers(A.nz[0], h), k1 = wavenumbers(A.nz[1], h), k2 = wavenumbers(A.nz[2], h);
         std::vector<double> w0 = window_hat_table(p, k0), w1 = window_hat_table(p, k1), w2 = window_hat_table(p, k2);
@@ -417,7 +430,9 @@ void prepare(sewald_gpu_session* s, bool use_table) {
         const double* dw2 = t + o;
         A.cb_zero = ClassBlock{A.nz[0], A.nz[1], A.nz[2], 0, dk0, nullptr, dw0, nullptr, dk1, dw1, dk2, dw2,
                                1.0 / static_cast<double>(zvol), zvol};
+        A.d0sa = D0ScaleArgs{0, 0, 0, 0, 0, dk0, dk1, dk2, dw0, dw1, dw2, 1.0 / static_cast<double>(zvol)};
         if (A.table_path) build_table_0p(s, A);
+        if (A.table_path && A.d0r) A.d0r->build_herm_table(A.table0p.as<cuDoubleComplex>(), st);
         cuda_check(cudaStreamSynchronize(st), "aft prepare");
         return;
     }
@@ -579,6 +594,10 @@ void aft_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p) {
     const int C = A.C;
     double* flow = s->flow.as<double>();
 
+    if (p.d == 0 && A.d0r) {
+        s->ctx->launches += A.d0r->solve(grid, A.spec, p.kind, p.xi, A.d0sa, A.table_path, flow, st);
+        return;
+    }
     if (p.d == 0) {
         const int64_t zvol = (int64_t)A.nz[0] * A.nz[1] * A.nz[2];
         cuDoubleComplex* z = A.zero.as<cuDoubleComplex>();
