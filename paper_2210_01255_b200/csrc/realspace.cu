@@ -88,7 +88,7 @@ __global__ void pack_kernel(const double* __restrict__ folded, const double* __r
         o[7] = nu[3 * i];
         o[8] = nu[3 * i + 1];
         o[9] = nu[3 * i + 2];
-        o[10] = 0.0;
+        o[10] = fma(f[3 * i + 2], nu[3 * i + 2], fma(f[3 * i + 1], nu[3 * i + 1], f[3 * i] * nu[3 * i]));  // q.nu
         o[11] = 0.0;
     } else {
         o[7] = 0.0;

@@ -55,7 +55,7 @@ struct Strength<SEWALD_ROTLET> {
 };
 template <>
 struct Strength<SEWALD_STRESSLET> {
-    static constexpr int n = 6;
+    static constexpr int n = 7;  // q, nu, q.nu (packed record slot 10)
 };
 
 // Contribution of source strength s at separation r (target - source) and
@@ -84,31 +84,28 @@ __device__ __forceinline__ void pair_both(const Screened& sc, double xi2, double
         ub[1] = fma(-c, t[2] * r0 - t[0] * r2, ub[1]);
         ub[2] = fma(-c, t[0] * r1 - t[1] * r0, ub[2]);
     } else {
+        // stresslet: s, t = (q, nu, q.nu) with q.nu precomputed per particle
         const double iy2 = sc.iy * sc.iy;
         const double x2 = xi2 * n2;
         const double c1 = -2.0 * sc.Ey * (iy2 * iy2) * (3.0 * sc.R + (3.0 + 2.0 * x2) * sc.cx);
         const double c2 = 2.0 * xi2 * sc.Ey * sc.cx;
         {
-            const double* q = s;
-            const double* v = s + 3;
-            const double rq = r0 * q[0] + r1 * q[1] + r2 * q[2];
-            const double rv = r0 * v[0] + r1 * v[1] + r2 * v[2];
-            const double qv = q[0] * v[0] + q[1] * v[1] + q[2] * v[2];
-            const double w = c1 * rq * rv + c2 * qv;
-            ua[0] += w * r0 + c2 * (q[0] * rv + v[0] * rq);
-            ua[1] += w * r1 + c2 * (q[1] * rv + v[1] * rq);
-            ua[2] += w * r2 + c2 * (q[2] * rv + v[2] * rq);
+            const double rq = r0 * s[0] + r1 * s[1] + r2 * s[2];
+            const double rv = r0 * s[3] + r1 * s[4] + r2 * s[5];
+            const double w = fma(c1 * rq, rv, c2 * s[6]);
+            const double cv = c2 * rv, cq = c2 * rq;
+            ua[0] = fma(cq, s[3], fma(cv, s[0], fma(w, r0, ua[0])));
+            ua[1] = fma(cq, s[4], fma(cv, s[1], fma(w, r1, ua[1])));
+            ua[2] = fma(cq, s[5], fma(cv, s[2], fma(w, r2, ua[2])));
         }
         {
-            const double* q = t;
-            const double* v = t + 3;
-            const double rq = r0 * q[0] + r1 * q[1] + r2 * q[2];
-            const double rv = r0 * v[0] + r1 * v[1] + r2 * v[2];
-            const double qv = q[0] * v[0] + q[1] * v[1] + q[2] * v[2];
-            const double w = c1 * rq * rv + c2 * qv;
-            ub[0] -= w * r0 + c2 * (q[0] * rv + v[0] * rq);
-            ub[1] -= w * r1 + c2 * (q[1] * rv + v[1] * rq);
-            ub[2] -= w * r2 + c2 * (q[2] * rv + v[2] * rq);
+            const double rq = r0 * t[0] + r1 * t[1] + r2 * t[2];
+            const double rv = r0 * t[3] + r1 * t[4] + r2 * t[5];
+            const double w = fma(c1 * rq, rv, c2 * t[6]);
+            const double cv = c2 * rv, cq = c2 * rq;
+            ub[0] = fma(-cq, t[3], fma(-cv, t[0], fma(-w, r0, ub[0])));
+            ub[1] = fma(-cq, t[4], fma(-cv, t[1], fma(-w, r1, ub[1])));
+            ub[2] = fma(-cq, t[5], fma(-cv, t[2], fma(-w, r2, ub[2])));
         }
     }
 }
