@@ -6,10 +6,11 @@
 // both share E = e^{-x^2}: erfc(x) = E * erfcx(x), and erfcx is smooth on
 // [0, inf) so one branch-free rational P9/Q9 (tools/fit_erfcx.py, max rel.
 // error 7e-16 on [0,10]) covers every pair; beyond x = 10 the product with
-// E (< 4e-44) is negligible. exp uses a Cody-Waite reduction and a degree-13
-// polynomial; 1/r and 1/Q start from the MUFU approximations and take Newton
-// steps. Together ~60 fp64 instructions per pair instead of ~600 for
-// erfc() + exp() + sqrt() + two divisions from libdevice.
+// E (< 4e-44) is negligible. exp uses a Cody-Waite reduction, a 2^(j/32)
+// table and a degree-6 polynomial; 1/r and 1/Q start from the MUFU
+// approximations and take one third-order correction step. Together ~45
+// fp64 instructions per pair instead of ~600 for erfc() + exp() + sqrt() +
+// two divisions from libdevice.
 //
 // Reference formulas: /root/reference/proj/src/kernels.cpp:71-116.
 #pragma once
@@ -53,13 +54,13 @@ __device__ __forceinline__ double rsqrt_approx(double a) {
     return r;
 }
 
-// 1/sqrt(a), a > 0 normal: MUFU seed + two Newton steps (~1 ulp).
+// 1/sqrt(a), a > 0 normal: MUFU seed y0 = (1 + d)/sqrt(a), |d| < 2^-22, and
+// one third-order step y0 (1 + e/2 + 3e^2/8), e = 1 - a y0^2 (truncation
+// 2.5 d^3 < 2^-64): 5 fp64 ops instead of 8 for two Newton steps.
 __device__ __forceinline__ double rsqrt_nr(double a) {
-    double y = rsqrt_approx(a);
-    double e = fma(-a * y, y, 1.0);
-    y = fma(0.5 * y, e, y);
-    e = fma(-a * y, y, 1.0);
-    return fma(0.5 * y, e, y);
+    const double y = rsqrt_approx(a);
+    const double e = fma(-a * y, y, 1.0);
+    return fma(y * e, fma(0.375, e, 0.5), y);
 }
 
 // e^{-y} for y >= 0 (clamped at 708 where the result is < 1e-307).
@@ -80,7 +81,7 @@ __device__ __forceinline__ double exp_neg(double y) {
 // e^{-y} for y >= 0 via 2^(j/32) table (tab: shared-memory copy of
 // c_exp2_tab32) and a degree-6 polynomial: 9 fp64 FMAs instead of 16.
 __device__ __forceinline__ double exp_neg_tab(double y, const double* tab) {
-    y = fmin(y, 708.0);
+    y = fmin(y, 700.0);
     const double shifter = c_misc[0];
     const double t = fma(-y, c_exp_tab_k[0], shifter);
     const int n = __double2loint(t);
@@ -91,7 +92,9 @@ __device__ __forceinline__ double exp_neg_tab(double y, const double* tab) {
 #pragma unroll
     for (int i = 5; i >= 0; --i) p = fma(p, f, c_exp6[i]);
     const int m = n >> 5;  // n = 32 m + j, n <= 0
-    return (p * tab[n & 31]) * __hiloint2double((m + 1023) << 20, 0);
+    // scale by 2^m in the exponent field (y <= 700 keeps the result normal)
+    const double v = p * tab[n & 31];
+    return __hiloint2double(__double2hiint(v) + (m << 20), __double2loint(v));
 }
 
 // erfcx(x) = e^{x^2} erfc(x) for x >= 0: rational P9/Q9 on [0,10], or the
@@ -116,10 +119,11 @@ __device__ __forceinline__ double erfcx_rat(double x) {
             q = fma(q, x, c_erfcx_q[i]);
         }
     }
-    double y = rcp_approx(q);
-    y = fma(y, fma(-q, y, 1.0), y);
+    // p/q = p y0 (1 + e + e^2), e = 1 - q y0, y0 = MUFU 1/q (|e| < 2^-22)
+    const double y = rcp_approx(q);
+    const double e = fma(-q, y, 1.0);
     const double r = p * y;
-    return fma(y, fma(-q, r, p), r);
+    return fma(r, fma(e, e, e), r);
 }
 
 // Shared screened factors for one pair at squared distance n2:
