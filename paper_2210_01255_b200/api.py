@@ -370,8 +370,8 @@ def _system_arrays(system: SourceSystem, params: Optional[EwaldParams] = None):
         raise InvalidArgument("periodicity d must be in 0..3")
     if any(not (float(v) > 0.0) for v in system.cell.L):
         raise InvalidArgument("cell lengths must be positive")
-    if x.size and not np.all(np.isfinite(x)):
-        raise InvalidArgument("non-finite source position")
+    # non-finite positions are rejected on the device (finite_check_kernel,
+    # InvalidArgument "non-finite source position"), not by a host pass
     return x, f, nu
 
 
@@ -382,17 +382,24 @@ def _params_for(system: SourceSystem, params: EwaldParams) -> sewald_params_c:
     return c
 
 
+def _out_array(out, nt: int) -> np.ndarray:
+    if out is None:
+        return np.empty((nt, 3))
+    if not (isinstance(out, np.ndarray) and out.dtype == np.float64 and out.shape == (nt, 3)
+            and out.flags.c_contiguous and out.flags.writeable):
+        raise InvalidArgument("out must be a writeable C-contiguous float64 array of shape (n_targets, 3)")
+    return out
+
+
 def _pipeline(entry: str, system: SourceSystem, targets: TargetSet, params: EwaldParams,
-              opt: SePipelineOptions, engine: Optional[Engine]) -> np.ndarray:
+              opt: SePipelineOptions, engine: Optional[Engine], out=None) -> np.ndarray:
     x, f, nu = _system_arrays(system, params)
     if not (float(params.xi) > 0.0):
         raise InvalidArgument("xi must be positive")
     same = bool(targets.same_as_sources)
     xt = x if same else _vec3(targets.x, "targets")
-    if not same and xt.size and not np.all(np.isfinite(xt)):
-        raise InvalidArgument("target coordinates must be finite")
     nt = xt.shape[0]
-    u = np.zeros((nt, 3))
+    u = _out_array(out, nt)
     eng = engine or default_engine()
     c = _params_for(system, params)
     with eng._lock:
@@ -403,16 +410,18 @@ def _pipeline(entry: str, system: SourceSystem, targets: TargetSet, params: Ewal
 
 
 def full_potential(system: SourceSystem, targets: TargetSet, params: EwaldParams,
-                   opt: SePipelineOptions = SePipelineOptions(), engine: Optional[Engine] = None) -> np.ndarray:
-    """full_potential (realspace.h:46-47): u_R + u_F + self + zero-mode terms, (Nt, 3)."""
-    return _pipeline("sewald_gpu_full_potential", system, targets, params, opt, engine)
+                   opt: SePipelineOptions = SePipelineOptions(), engine: Optional[Engine] = None,
+                   out: Optional[np.ndarray] = None) -> np.ndarray:
+    """full_potential (realspace.h:46-47): u_R + u_F + self + zero-mode terms, (Nt, 3).
+    `out` (optional, e.g. pinned host memory) receives the result and is returned."""
+    return _pipeline("sewald_gpu_full_potential", system, targets, params, opt, engine, out)
 
 
 def se_fourier_potential(system: SourceSystem, targets: TargetSet, params: EwaldParams,
                          opt: SePipelineOptions = SePipelineOptions(),
-                         engine: Optional[Engine] = None) -> np.ndarray:
+                         engine: Optional[Engine] = None, out: Optional[np.ndarray] = None) -> np.ndarray:
     """se_fourier_potential (fourier.h:81-82)."""
-    return _pipeline("sewald_gpu_fourier_potential", system, targets, params, opt, engine)
+    return _pipeline("sewald_gpu_fourier_potential", system, targets, params, opt, engine, out)
 
 
 def realspace_potential(system: SourceSystem, targets: TargetSet, xi: float, rc: float,
