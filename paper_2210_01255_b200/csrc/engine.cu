@@ -676,6 +676,8 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
         a.kind = s->p.kind;
         a.xi = s->p.xi;
         a.rc = s->p.rc;
+        a.xi2 = a.xi * a.xi;
+        a.rc2 = a.rc * a.rc;
         a.skip_self = s->same ? 1 : 0;
         // fp32 candidate bound: coordinates (targets folded or inside the
         // free-axis span, +-shift) are O(ext); fp32 differences carry at

@@ -117,9 +117,12 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                      double* __restrict__ u, unsigned long long* __restrict__ pair_count, int* __restrict__ err,
                      unsigned long long* __restrict__ work) {
     constexpr int NS = Strength<KIND>::n;
-    __shared__ double jx_all[SYM_WARPS][3][32];
-    __shared__ double js_all[SYM_WARPS][NS][32];
-    __shared__ double racc_all[SYM_WARPS][3][32];
+    // j record: [x y | z s0 | s1 s2 | ... | r0 r1 | r2 pad], a multiple of 16 B
+    // so positions, strengths and reactions move with 128-bit shared accesses
+    // (stride 80 B / 112 B: conflict-free per quarter warp).
+    constexpr int RS = (3 + NS + 3 + 1) & ~1;
+    constexpr int RO = RS - 4;  // reaction offset
+    __shared__ __align__(16) double jrec_all[SYM_WARPS][32][RS];
     __shared__ long long jid_all[SYM_WARPS][32];
     __shared__ float jf_all[SYM_WARPS][3][32];
     __shared__ double exp_tab[32];
@@ -127,9 +130,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    double(*jx)[32] = jx_all[warp];
-    double(*js)[32] = js_all[warp];
-    double(*racc)[32] = racc_all[warp];
+    double(*jrec)[RS] = jrec_all[warp];
     long long* jid = jid_all[warp];
     float(*jf)[32] = jf_all[warp];
     unsigned long long npairs = 0;
@@ -169,8 +170,8 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
             hi[ax] = fmax(hi[ax], __shfl_xor_sync(0xffffffffu, hi[ax], s));
         }
 
-    const double rc2 = a.rc * a.rc;
-    const double xi2 = a.xi * a.xi;
+    const double rc2 = a.rc2;  // kernel-parameter operands: no registers
+    const double xi2 = a.xi2;
     const double rcm = a.rc * (1.0 + 1e-10) + 1e-12 * fmax(fmax(cg.L[0], cg.L[1]), cg.L[2]);
     const double rcm2 = rcm * rcm;
     int clo[3], chi[3];
@@ -228,19 +229,19 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                     __syncwarp();
                     if (lane < cnt) {
                         const double* q = packed + (jb + lane) * S;
-                        jx[0][lane] = q[0];
-                        jx[1][lane] = q[1];
-                        jx[2][lane] = q[2];
+                        double* rec = jrec[lane];
+                        rec[0] = q[0];
+                        rec[1] = q[1];
+                        rec[2] = q[2];
                         jid[lane] = __double_as_longlong(q[3]);
                         jf[0][lane] = (float)q[0];
                         jf[1][lane] = (float)q[1];
                         jf[2][lane] = (float)q[2];
 #pragma unroll
-                        for (int c = 0; c < NS; ++c) js[c][lane] = q[4 + c];
+                        for (int c = 0; c < NS; ++c) rec[3 + c] = q[4 + c];
                     }
-                    racc[0][lane] = 0.0;
-                    racc[1][lane] = 0.0;
-                    racc[2][lane] = 0.0;
+                    *reinterpret_cast<double2*>(&jrec[lane][RO]) = make_double2(0.0, 0.0);
+                    jrec[lane][RO + 2] = 0.0;
                     __syncwarp();
                     // pair (lane, j) is "after" in sorted order iff j - lane > dlt
                     const int dlt = (int)max((int64_t)-64, istart - jb);
@@ -266,10 +267,14 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                         const int j = (lane + s) & 31;
                         bool acc = (m >> s) & 1u;
                         double r0 = 0, r1 = 0, r2 = 0, n2 = 0;
+                        double* rec = jrec[j];
+                        double2 zs0;
                         if (acc) {
-                            r0 = xs0 - jx[0][j];
-                            r1 = xs1 - jx[1][j];
-                            r2 = xs2 - jx[2][j];
+                            const double2 xy = *reinterpret_cast<const double2*>(rec);
+                            zs0 = *reinterpret_cast<const double2*>(rec + 2);
+                            r0 = xs0 - xy.x;
+                            r1 = xs1 - xy.y;
+                            r2 = xs2 - zs0.x;
                             n2 = __dadd_rn(__dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1)), __dmul_rn(r2, r2));
                             acc = n2 < rc2;
                         }
@@ -278,18 +283,19 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                                 atomicExch(err, 1);
                             } else {
                                 double sj[NS];
+                                sj[0] = zs0.y;
 #pragma unroll
-                                for (int c = 0; c < NS; ++c) sj[c] = js[c][j];
-                                #ifdef SEWALD_NO_EXPTAB
-                                const Screened sc = screened<SHORT>(n2, a.xi, xi2, nullptr);
-#else
+                                for (int c = 1; c < NS; c += 2) {
+                                    const double2 v = *reinterpret_cast<const double2*>(rec + 3 + c);
+                                    sj[c] = v.x;
+                                    if (c + 1 < NS) sj[c + 1] = v.y;
+                                }
                                 const Screened sc = screened<SHORT>(n2, a.xi, xi2, exp_tab);
-#endif
-                                double ub[3] = {racc[0][j], racc[1][j], racc[2][j]};
+                                const double2 r01 = *reinterpret_cast<const double2*>(rec + RO);
+                                double ub[3] = {r01.x, r01.y, rec[RO + 2]};
                                 pair_both<KIND>(sc, xi2, n2, r0, r1, r2, sj, fa, ua, ub);
-                                racc[0][j] = ub[0];
-                                racc[1][j] = ub[1];
-                                racc[2][j] = ub[2];
+                                *reinterpret_cast<double2*>(rec + RO) = make_double2(ub[0], ub[1]);
+                                rec[RO + 2] = ub[2];
                                 npairs += 2;
                             }
                         }
@@ -297,9 +303,9 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                     __syncwarp();
                     if (lane < cnt) {
                         double* dst = u + 3 * jid[lane];
-                        atomicAdd(dst, racc[0][lane]);
-                        atomicAdd(dst + 1, racc[1][lane]);
-                        atomicAdd(dst + 2, racc[2][lane]);
+                        atomicAdd(dst, jrec[lane][RO]);
+                        atomicAdd(dst + 1, jrec[lane][RO + 1]);
+                        atomicAdd(dst + 2, jrec[lane][RO + 2]);
                     }
                 }
             }

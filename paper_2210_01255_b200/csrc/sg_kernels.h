@@ -88,6 +88,7 @@ struct RealspaceArgs {
     int kind;           // SEWALD_STOKESLET / STRESSLET / ROTLET
     double xi;
     double rc;
+    double xi2, rc2;    // xi^2, rc^2 (host-computed; kernels read them as parameters)
     int skip_self;      // starred && targets are the sources
     float thresh_f;     // conservative fp32 bound on rc^2 for the candidate pass
 };
