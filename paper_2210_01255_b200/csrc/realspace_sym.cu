@@ -133,7 +133,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     double(*jrec)[RS] = jrec_all[warp];
     long long* jid = jid_all[warp];
     float(*jf)[32] = jf_all[warp];
-    unsigned long long npairs = 0;
+    unsigned long long npairs = 0;  // flushed per cluster from the 32-bit step counter
     // Persistent warps: clusters are taken from a global counter, so the
     // uneven per-cluster work (row geometry, half rule) does not leave SMs
     // idle in the tail.
@@ -145,6 +145,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
 
     const int64_t istart = cl * 32;
     const int64_t ia = istart + lane;
+    unsigned npairs32 = 0;
     const bool valid = ia < N;
     double xa0 = 0, xa1 = 0, xa2 = 0, fa[NS];
     long long ida = -1;
@@ -262,8 +263,8 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                     }
                     unsigned steps = __reduce_or_sync(0xffffffffu, m);
                     while (steps) {
-                        const int s = __ffs(steps) - 1;
-                        steps &= steps - 1;
+                        const int s = 31 - __clz(steps);  // highest step first: one FLO
+                        steps ^= 1u << s;
                         const int j = (lane + s) & 31;
                         bool acc = (m >> s) & 1u;
                         double r0 = 0, r1 = 0, r2 = 0, n2 = 0;
@@ -296,7 +297,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                                 pair_both<KIND>(sc, xi2, n2, r0, r1, r2, sj, fa, ua, ub);
                                 *reinterpret_cast<double2*>(rec + RO) = make_double2(ub[0], ub[1]);
                                 rec[RO + 2] = ub[2];
-                                npairs += 2;
+                                npairs32 += 2;
                             }
                         }
                     }
@@ -311,6 +312,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
             }
         }
     }
+    npairs += npairs32;
     if (valid) {
         double* dst = u + 3 * ida;
         atomicAdd(dst, ua[0]);
