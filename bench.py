@@ -283,7 +283,8 @@ def run_ours(args, cfg):
     def step():
         sess.set_sources(dx, df, dnu)
         sess.set_targets(dxt, same)
-        sharded_step(sess, N, grid, u, rank, ws, all_reduce=dist.all_reduce if ws > 1 else None)
+        sharded_step(sess, N, grid, u, rank, ws, all_reduce=dist.all_reduce if ws > 1 else None,
+                     slab_dist=dist if (ws > 1 and cfg.d == 0) else None)
 
     def barrier():
         if ws > 1:
@@ -386,7 +387,8 @@ def run_ours(args, cfg):
             "config": {"workload": cfg.name, "N": N, "Nt": Nt, "kernel": cfg.kind.name, "d": cfg.d,
                        "xi": cfg.xi, "tol": cfg.tol, "M_ext": list(params.grid.M_ext),
                        "P": params.window.P, "window": params.window.kind.name, "rc": params.rc,
-                       "parallelism": f"targets+source-slices x{ws} (NCCL all-reduce of the grid)",
+                       "parallelism": (f"targets+source-slices x{ws} (NCCL all-reduce of the grid)" if cfg.d != 0 or ws == 1 else
+                                       f"targets+source-slices x{ws}, slab FFT (NCCL reduce-scatter, 2 all-to-all, all-gather)"),
                        "l2": "flushed between steps (256 MB write inside the timed loop)"},
             "roofline": {"kernel": "realspace", "bound": "fp64", "achieved": achieved, "peak": peak64,
                          "unit": "TFLOP/s", "frac": achieved / peak64,

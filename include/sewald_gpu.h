@@ -203,6 +203,26 @@ int sewald_gpu_session_solve(sewald_gpu_session* s, const double* grid_dev, int 
  * zero-mode / gauge terms. */
 int sewald_gpu_session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts,
                                 double* u_dev);
+/* ---- slab-distributed D = 0 solve (one rank of `world`) -------
+ * Replaces se_fourier_potential's single-box transform (fourier.cpp:311-520,
+ * :668-720) by x-slabs of the M_ext box for the z transforms and kz-slabs of
+ * the half spectrum for the (x, y) transforms and the scale, with two
+ * all-to-all exchanges done by the caller (NCCL). Bounds arrays hold world+1
+ * split points (x over m[0], kz over h2). Buffer layouts (complex doubles):
+ *   forward send chunk q: [C][xb-xa][m1][kz in q]     (sum over q = C*(xb-xa)*m1*h2)
+ *   middle  recv chunk p: [C][x in p][m1][kb-ka]     -> send chunk q: [3][kb-ka][x in q][m1]
+ *   inverse recv chunk p: [3][kz in p][xb-xa][m1]    -> flow slab [3][xb-xa][m1][m2] (real)
+ * The grid slab passed to forward is [C][xb-xa][m1][m2] (real). */
+int sewald_gpu_session_d0_geometry(sewald_gpu_session* s, int precompute_0p, int m[3], int n[3], int* h2,
+                                   int* C);
+int sewald_gpu_session_d0_forward(sewald_gpu_session* s, int precompute_0p, const double* grid_slab, int xa,
+                                  int xb, int world, const int* kz_bounds, void* send_dev);
+int sewald_gpu_session_d0_middle(sewald_gpu_session* s, int precompute_0p, const void* recv_dev, int world,
+                                 const int* x_bounds, int ka, int kb, void* send_dev);
+int sewald_gpu_session_d0_inverse(sewald_gpu_session* s, int precompute_0p, const void* recv_dev, int xa, int xb,
+                                  int world, const int* kz_bounds, double* flow_slab_dev);
+/* Install a full flow field (3 comps, M_ext, device) for evaluate()'s gather. */
+int sewald_gpu_session_set_flow(sewald_gpu_session* s, const double* flow_dev);
 /* Accepted real-space pairs counted since the last reset (synchronises). */
 int64_t sewald_gpu_session_pair_count(sewald_gpu_session* s, int reset);
 /* Whole pipeline on one GPU: spread all, solve, evaluate all (parts = 7). */

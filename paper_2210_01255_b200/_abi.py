@@ -54,6 +54,7 @@ class sewald_timings_c(C.Structure):
 DP = C.POINTER(C.c_double)
 VP = C.c_void_p
 I64 = C.c_int64
+IP = C.POINTER(C.c_int)
 
 # (name, restype, argtypes)
 _SIGS = [
@@ -94,6 +95,11 @@ _SIGS = [
     ("sewald_gpu_session_solve", C.c_int, [VP, VP, C.c_int]),
     ("sewald_gpu_session_evaluate", C.c_int, [VP, C.c_int, C.c_int, C.c_int, VP]),
     ("sewald_gpu_session_run", C.c_int, [VP, C.c_int, VP]),
+    ("sewald_gpu_session_d0_geometry", C.c_int, [VP, C.c_int, IP, IP, IP, IP]),
+    ("sewald_gpu_session_d0_forward", C.c_int, [VP, C.c_int, VP, C.c_int, C.c_int, C.c_int, IP, VP]),
+    ("sewald_gpu_session_d0_middle", C.c_int, [VP, C.c_int, VP, C.c_int, IP, C.c_int, C.c_int, VP]),
+    ("sewald_gpu_session_d0_inverse", C.c_int, [VP, C.c_int, VP, C.c_int, C.c_int, C.c_int, IP, VP]),
+    ("sewald_gpu_session_set_flow", C.c_int, [VP, VP]),
 ]
 
 EXPORTED = [s[0] for s in _SIGS]

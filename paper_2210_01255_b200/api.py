@@ -548,6 +548,46 @@ class Session:
         self.engine.check(self._lib.sewald_gpu_session_evaluate(self.s, int(part), int(nparts), int(parts),
                                                                 self._ptr(u)))
 
+    # ---- slab-distributed D = 0 solve (parallel.d0_sharded_solve) ----------
+    def d0_geometry(self, precompute_0p: bool = True) -> dict:
+        """Padded-box geometry of the D = 0 real-transform solve: m (M_ext),
+        n (transform box), h2 = n[2]//2 + 1, C (grid components)."""
+        self._sync_stream()
+        m, n = (C.c_int * 3)(), (C.c_int * 3)()
+        h2, c = C.c_int(), C.c_int()
+        self.engine.check(self._lib.sewald_gpu_session_d0_geometry(self.s, int(precompute_0p), m, n,
+                                                                   C.byref(h2), C.byref(c)))
+        return {"m": tuple(m), "n": tuple(n), "h2": h2.value, "C": c.value}
+
+    @staticmethod
+    def _bounds(b):
+        arr = (C.c_int * len(b))(*[int(v) for v in b])
+        return len(b) - 1, arr
+
+    def d0_forward(self, grid_slab, xa: int, xb: int, kz_bounds, send, precompute_0p: bool = True):
+        self._sync_stream()
+        w, arr = self._bounds(kz_bounds)
+        self.engine.check(self._lib.sewald_gpu_session_d0_forward(
+            self.s, int(precompute_0p), self._ptr(grid_slab), int(xa), int(xb), w, arr, C.c_void_p(send.data_ptr())))
+
+    def d0_middle(self, recv, x_bounds, ka: int, kb: int, send, precompute_0p: bool = True):
+        self._sync_stream()
+        w, arr = self._bounds(x_bounds)
+        self.engine.check(self._lib.sewald_gpu_session_d0_middle(
+            self.s, int(precompute_0p), C.c_void_p(recv.data_ptr()), w, arr, int(ka), int(kb),
+            C.c_void_p(send.data_ptr())))
+
+    def d0_inverse(self, recv, xa: int, xb: int, kz_bounds, flow_slab, precompute_0p: bool = True):
+        self._sync_stream()
+        w, arr = self._bounds(kz_bounds)
+        self.engine.check(self._lib.sewald_gpu_session_d0_inverse(
+            self.s, int(precompute_0p), C.c_void_p(recv.data_ptr()), int(xa), int(xb), w, arr,
+            self._ptr(flow_slab)))
+
+    def set_flow(self, flow):
+        self._sync_stream()
+        self.engine.check(self._lib.sewald_gpu_session_set_flow(self.s, self._ptr(flow)))
+
     def pair_count(self, reset: bool = False) -> int:
         return int(self._lib.sewald_gpu_session_pair_count(self.s, int(reset)))
 

@@ -660,4 +660,46 @@ void aft_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p) {
     cuda_check(cudaGetLastError(), "aft d12");
 }
 
+// ---- slab-distributed D = 0 solve: stage wrappers ------------------
+
+static D0Real& d0_plan(sewald_gpu_session* s, bool use_table) {
+    if (s->p.d != 0) throw EngineError(SEWALD_EINVAL, "slab-distributed solve is the D=0 path");
+    prepare(s, use_table);
+    FourierPlanAFT& A = *s->aft;
+    if (!A.d0r) throw EngineError(SEWALD_EINVAL, "slab-distributed solve needs the real-transform D=0 path");
+    return *A.d0r;
+}
+
+void aft_d0_geometry(sewald_gpu_session* s, bool use_table, int m[3], int n[3], int* h2, int* C) {
+    D0Real& D = d0_plan(s, use_table);
+    for (int a = 0; a < 3; ++a) {
+        m[a] = D.m[a];
+        n[a] = D.n[a];
+    }
+    *h2 = D.h2;
+    *C = D.C;
+}
+
+void aft_d0_slab_forward(sewald_gpu_session* s, bool use_table, const double* grid_slab, int xa, int xb,
+                         const SlabBounds& kzb, void* send) {
+    D0Real& D = d0_plan(s, use_table);
+    s->ctx->launches += D.slab_forward(grid_slab, xa, xb, kzb, static_cast<cuDoubleComplex*>(send), s->ctx->stream);
+}
+
+void aft_d0_slab_middle(sewald_gpu_session* s, bool use_table, const void* recv, const SlabBounds& xbd, int ka,
+                        int kb, void* send) {
+    D0Real& D = d0_plan(s, use_table);
+    FourierPlanAFT& A = *s->aft;
+    s->ctx->launches += D.slab_middle(static_cast<const cuDoubleComplex*>(recv), xbd, ka, kb, A.spec, s->p.kind,
+                                      s->p.xi, A.d0sa, A.table_path, static_cast<cuDoubleComplex*>(send),
+                                      s->ctx->stream);
+}
+
+void aft_d0_slab_inverse(sewald_gpu_session* s, bool use_table, const void* recv, int xa, int xb,
+                         const SlabBounds& kzb, double* flow_slab) {
+    D0Real& D = d0_plan(s, use_table);
+    s->ctx->launches += D.slab_inverse(static_cast<const cuDoubleComplex*>(recv), xa, xb, kzb, flow_slab,
+                                       s->ctx->stream);
+}
+
 }  // namespace sewald_b200

@@ -126,7 +126,7 @@ __global__ void d0_scale_kernel(ModSpec spec, D0ScaleArgs a, double xi, cuDouble
     const int ky = (int)(idx % a.n1);
     const int64_t t = idx / a.n1;
     const int kx = (int)(t % a.n0);
-    const int kz = (int)(t / a.n0);
+    const int kz = a.kz0 + (int)(t / a.n0);  // a.h2 = kz count of this launch
     const double k0 = a.k0[kx], k1 = a.k1[ky], k2 = a.k2[kz];
     const double wp = a.w0[kx] * a.w1[ky] * a.w2[kz];
     const double kk = k0 * k0 + k1 * k1 + k2 * k2;
@@ -151,7 +151,7 @@ __global__ void d0_scale_kernel(ModSpec spec, D0ScaleArgs a, double xi, cuDouble
         }
     }
     if (table) {
-        const cuDoubleComplex tv = Th[idx];
+        const cuDoubleComplex tv = Th[idx + (int64_t)a.kz0 * a.n0 * a.n1];
 #pragma unroll
         for (int e = 0; e < NG; ++e) {
             const double x = re[e], y = im[e];
@@ -254,6 +254,7 @@ int D0Real::solve(const double* grid, const ModSpec& spec, int kind, double xi, 
     sa.n1 = n[1];
     sa.n2 = n[2];
     sa.h2 = h2;
+    sa.kz0 = 0;
     sa.cstride = slab;
     const cuDoubleComplex* th = table ? Th.as<cuDoubleComplex>() : nullptr;
     const unsigned sb = (unsigned)((slab + 127) / 128);
@@ -273,6 +274,198 @@ int D0Real::solve(const double* grid, const ModSpec& spec, int kind, double xi, 
     ++launches;
     cuda_check(cudaGetLastError(), "d0 solve");
     return launches;
+}
+
+
+// ---------------------------------------------------------------------------
+// slab-distributed stages
+// ---------------------------------------------------------------------------
+
+namespace {
+
+__device__ __forceinline__ int owner_of(const SlabBounds& b, int i) {
+    int r = 0;
+    while (r + 1 < b.world && b.b[r + 1] <= i) ++r;
+    return r;
+}
+
+// Z slab [C][nxs][m1][h2] -> send chunks q: [C][nxs][m1][kz - ka_q]
+__global__ void d0_pack_fwd_kernel(const cuDoubleComplex* __restrict__ Z, int C, int nxs, int m1, int h2,
+                                   SlabBounds kzb, cuDoubleComplex* __restrict__ send) {
+    const int64_t tot = (int64_t)C * nxs * m1 * h2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        const int kz = (int)(i % h2);
+        const int64_t line = i / h2;  // (c, xs, y)
+        const int q = owner_of(kzb, kz);
+        const int ka = kzb.b[q], nk = kzb.b[q + 1] - ka;
+        send[(int64_t)C * nxs * m1 * ka + line * nk + (kz - ka)] = Z[i];
+    }
+}
+
+// recv chunks p: [C][nxs_p][m1][nk] -> Tin [C][nk][n0][n1] (x < m0, y < m1)
+__global__ void d0_unpack_mid_kernel(const cuDoubleComplex* __restrict__ recv, int C, int m0, int m1, int n0,
+                                     int n1, int nk, SlabBounds xbd, cuDoubleComplex* __restrict__ Tin) {
+    const int64_t tot = (int64_t)C * nk * m0 * m1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        const int y = (int)(i % m1);
+        int64_t t = i / m1;
+        const int x = (int)(t % m0);
+        t /= m0;
+        const int kl = (int)(t % nk);
+        const int c = (int)(t / nk);
+        const int p = owner_of(xbd, x);
+        const int xa = xbd.b[p], nxs = xbd.b[p + 1] - xa;
+        const int64_t src = (int64_t)C * m1 * nk * xa + (((int64_t)c * nxs + (x - xa)) * m1 + y) * nk + kl;
+        Tin[(((int64_t)c * nk + kl) * n0 + x) * n1 + y] = recv[src];
+    }
+}
+
+// Tout [3][nk][n0][n1] (x < m0, y < m1) -> send chunks q: [3][nk][nxs_q][m1]
+__global__ void d0_pack_mid_kernel(const cuDoubleComplex* __restrict__ Tout, int m0, int m1, int n0, int n1,
+                                   int nk, SlabBounds xbd, cuDoubleComplex* __restrict__ send) {
+    const int64_t tot = (int64_t)3 * nk * m0 * m1;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        const int y = (int)(i % m1);
+        int64_t t = i / m1;
+        const int x = (int)(t % m0);
+        const int64_t ck = t / m0;  // c * nk + kl
+        const int q = owner_of(xbd, x);
+        const int xa = xbd.b[q], nxs = xbd.b[q + 1] - xa;
+        send[(int64_t)3 * nk * m1 * xa + (ck * nxs + (x - xa)) * m1 + y] = Tout[(ck * n0 + x) * n1 + y];
+    }
+}
+
+// recv chunks p: [3][nk_p][nxs][m1] -> Z slab [3][nxs][m1][h2]
+__global__ void d0_unpack_inv_kernel(const cuDoubleComplex* __restrict__ recv, int nxs, int m1, int h2,
+                                     SlabBounds kzb, cuDoubleComplex* __restrict__ Z) {
+    const int64_t tot = (int64_t)3 * nxs * m1 * h2;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
+        const int kz = (int)(i % h2);
+        int64_t t = i / h2;
+        const int y = (int)(t % m1);
+        t /= m1;
+        const int xs = (int)(t % nxs);
+        const int c = (int)(t / nxs);
+        const int p = owner_of(kzb, kz);
+        const int ka = kzb.b[p], nk = kzb.b[p + 1] - ka;
+        Z[i] = recv[(int64_t)3 * nxs * m1 * ka + (((int64_t)c * nk + (kz - ka)) * nxs + xs) * m1 + y];
+    }
+}
+
+}  // namespace
+
+D0SlabPlan::~D0SlabPlan() {
+    for (auto h : plans) cufftDestroy(h);
+}
+
+void D0Real::slab_plans(int nxs, int nk, cudaStream_t st) {
+    D0SlabPlan& S = slab;
+    if (S.nxs == nxs && S.nk == nk) return;
+    for (auto h : S.plans) cufftDestroy(h);
+    S.plans.clear();
+    S.nxs = nxs;
+    S.nk = nk;
+    const int64_t lin = (int64_t)C * nxs * m[1], lout = (int64_t)3 * nxs * m[1];
+    S.R.ensure(sizeof(double) * std::max<int64_t>(lin, 1) * n[2]);
+    S.Z.ensure(sizeof(cuDoubleComplex) * std::max<int64_t>(lin, 1) * h2);
+    const int64_t plane = (int64_t)n[0] * n[1];
+    S.Tin.ensure(sizeof(cuDoubleComplex) * C * std::max(nk, 1) * plane);
+    S.Tout.ensure(sizeof(cuDoubleComplex) * C * std::max(nk, 1) * plane);
+    // the x >= m0 / y >= m1 parts of Tin are a resident zero block
+    cuda_check(cudaMemsetAsync(S.Tin.ptr, 0, sizeof(cuDoubleComplex) * C * std::max(nk, 1) * plane, st),
+               "slab Tin zero");
+    size_t ws = 0, w = 0;
+    auto mk = [&](cufftHandle& h, int rank, const int* nl, long long is, long long id, long long os, long long od,
+                  cufftType ty, long long batch, const int* inem, const int* onem) {
+        fft_check(cufftCreate(&h), "create");
+        S.plans.push_back(h);
+        fft_check(cufftSetAutoAllocation(h, 0), "auto alloc");
+        long long nn[2], ie[2], oe[2];
+        for (int r = 0; r < rank; ++r) {
+            nn[r] = nl[r];
+            ie[r] = inem[r];
+            oe[r] = onem[r];
+        }
+        fft_check(cufftMakePlanMany64(h, rank, nn, ie, is, id, oe, os, od, ty, batch, &w), "slab plan");
+        fft_check(cufftSetStream(h, st), "stream");
+        ws = std::max(ws, w);
+    };
+    int e_n2[1] = {n[2]}, e_h2[1] = {h2};
+    if (lin > 0) {
+        mk(S.pz_f, 1, n + 2, 1, n[2], 1, h2, CUFFT_D2Z, lin, e_n2, e_h2);
+        mk(S.pz_i, 1, n + 2, 1, h2, 1, n[2], CUFFT_Z2D, lout, e_h2, e_n2);
+    }
+    if (nk > 0) {
+        mk(S.pxy_f, 2, n, 1, plane, 1, plane, CUFFT_Z2Z, (long long)C * nk, n, n);
+        mk(S.pxy_i, 2, n, 1, plane, 1, plane, CUFFT_Z2Z, (long long)3 * nk, n, n);
+    }
+    S.work.ensure(std::max<size_t>(ws, 16));
+    for (auto h : S.plans) fft_check(cufftSetWorkArea(h, S.work.ptr), "work area");
+}
+
+int D0Real::slab_forward(const double* grid_slab, int xa, int xb, const SlabBounds& kzb, cuDoubleComplex* send,
+                         cudaStream_t st) {
+    const int nxs = xb - xa;
+    const int nk = slab.nk < 0 ? 0 : slab.nk;
+    slab_plans(nxs, std::max(slab.nk, 0), st);
+    (void)nk;
+    const int64_t lines = (int64_t)C * nxs * m[1];
+    if (lines == 0) return 0;
+    double* r = slab.R.as<double>();
+    cuDoubleComplex* z = slab.Z.as<cuDoubleComplex>();
+    d0_pad_z_kernel<<<blocks_for(lines * n[2]), 256, 0, st>>>(grid_slab, lines, m[2], n[2], r);
+    fft_check(cufftExecD2Z(slab.pz_f, r, z), "slab z forward");
+    d0_pack_fwd_kernel<<<blocks_for(lines * h2), 256, 0, st>>>(z, C, nxs, m[1], h2, kzb, send);
+    cuda_check(cudaGetLastError(), "slab forward");
+    return 2;
+}
+
+int D0Real::slab_middle(const cuDoubleComplex* recv, const SlabBounds& xbd, int ka, int kb, const ModSpec& spec,
+                        int kind, double xi, const D0ScaleArgs& sa_in, bool table, cuDoubleComplex* send,
+                        cudaStream_t st) {
+    const int nk = kb - ka;
+    slab_plans(std::max(slab.nxs, 0), nk, st);
+    if (nk == 0) return 0;
+    const int64_t plane = (int64_t)n[0] * n[1];
+    cuDoubleComplex* ti = slab.Tin.as<cuDoubleComplex>();
+    cuDoubleComplex* to = slab.Tout.as<cuDoubleComplex>();
+    const int64_t nin = (int64_t)C * nk * m[0] * m[1];
+    d0_unpack_mid_kernel<<<blocks_for(nin), 256, 0, st>>>(recv, C, m[0], m[1], n[0], n[1], nk, xbd, ti);
+    fft_check(cufftExecZ2Z(slab.pxy_f, ti, to, CUFFT_FORWARD), "slab xy forward");
+    D0ScaleArgs sa = sa_in;
+    sa.n0 = n[0];
+    sa.n1 = n[1];
+    sa.n2 = n[2];
+    sa.h2 = nk;
+    sa.kz0 = ka;
+    sa.cstride = (int64_t)nk * plane;
+    const cuDoubleComplex* th = table ? Th.as<cuDoubleComplex>() : nullptr;
+    const unsigned sb = (unsigned)((sa.cstride + 127) / 128);
+    switch (kind) {
+        case SEWALD_STOKESLET: d0_scale_kernel<SEWALD_STOKESLET><<<sb, 128, 0, st>>>(spec, sa, xi, to, th); break;
+        case SEWALD_ROTLET: d0_scale_kernel<SEWALD_ROTLET><<<sb, 128, 0, st>>>(spec, sa, xi, to, th); break;
+        default: d0_scale_kernel<SEWALD_STRESSLET><<<sb, 128, 0, st>>>(spec, sa, xi, to, th); break;
+    }
+    fft_check(cufftExecZ2Z(slab.pxy_i, to, to, CUFFT_INVERSE), "slab xy inverse");
+    const int64_t nout = (int64_t)3 * nk * m[0] * m[1];
+    d0_pack_mid_kernel<<<blocks_for(nout), 256, 0, st>>>(to, m[0], m[1], n[0], n[1], nk, xbd, send);
+    cuda_check(cudaGetLastError(), "slab middle");
+    return 3;
+}
+
+int D0Real::slab_inverse(const cuDoubleComplex* recv, int xa, int xb, const SlabBounds& kzb, double* flow_slab,
+                         cudaStream_t st) {
+    const int nxs = xb - xa;
+    slab_plans(nxs, std::max(slab.nk, 0), st);
+    const int64_t lines = (int64_t)3 * nxs * m[1];
+    if (lines == 0) return 0;
+    cuDoubleComplex* z = slab.Z.as<cuDoubleComplex>();
+    double* r = slab.R.as<double>();
+    d0_unpack_inv_kernel<<<blocks_for(lines * h2), 256, 0, st>>>(recv, nxs, m[1], h2, kzb, z);
+    fft_check(cufftExecZ2D(slab.pz_i, z, r), "slab z inverse");
+    d0_extract_kernel<<<blocks_for(lines * m[2]), 256, 0, st>>>(r, lines, m[2], n[2], flow_slab);
+    cuda_check(cudaGetLastError(), "slab inverse");
+    return 2;
 }
 
 }  // namespace sewald_b200

@@ -10,6 +10,7 @@
 // wrap a cached session with one H2D and one D2H copy.
 #include "engine.h"
 #include "host_params.h"
+#include "aft_d0.h"
 
 #include <cub/cub.cuh>
 
@@ -1044,6 +1045,58 @@ int sewald_gpu_session_solve(sewald_gpu_session* s, const double* grid, int prec
 int sewald_gpu_session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, double* u) {
     if (!s) return SEWALD_EINVAL;
     return ctx_guard(s->ctx, [&] { session_evaluate(s, part, nparts, parts, u); });
+}
+
+static sewald_b200::SlabBounds slab_bounds_from(int world, const int* b) {
+    if (world < 1 || world > sewald_b200::kMaxWorld || !b)
+        throw sewald_b200::EngineError(SEWALD_EINVAL, "bad slab bounds");
+    sewald_b200::SlabBounds sb{};
+    sb.world = world;
+    for (int r = 0; r <= world; ++r) {
+        sb.b[r] = b[r];
+        if (r > 0 && b[r] < b[r - 1]) throw sewald_b200::EngineError(SEWALD_EINVAL, "slab bounds must be sorted");
+    }
+    return sb;
+}
+
+int sewald_gpu_session_d0_geometry(sewald_gpu_session* s, int precompute_0p, int m[3], int n[3], int* h2,
+                                   int* C) {
+    if (!s || !m || !n || !h2 || !C) return SEWALD_EINVAL;
+    return ctx_guard(s->ctx, [&] { aft_d0_geometry(s, precompute_0p != 0, m, n, h2, C); });
+}
+
+int sewald_gpu_session_d0_forward(sewald_gpu_session* s, int precompute_0p, const double* grid_slab, int xa,
+                                  int xb, int world, const int* kz_bounds, void* send) {
+    if (!s) return SEWALD_EINVAL;
+    return ctx_guard(s->ctx, [&] {
+        aft_d0_slab_forward(s, precompute_0p != 0, grid_slab, xa, xb, slab_bounds_from(world, kz_bounds), send);
+    });
+}
+
+int sewald_gpu_session_d0_middle(sewald_gpu_session* s, int precompute_0p, const void* recv, int world,
+                                 const int* x_bounds, int ka, int kb, void* send) {
+    if (!s) return SEWALD_EINVAL;
+    return ctx_guard(s->ctx, [&] {
+        aft_d0_slab_middle(s, precompute_0p != 0, recv, slab_bounds_from(world, x_bounds), ka, kb, send);
+    });
+}
+
+int sewald_gpu_session_d0_inverse(sewald_gpu_session* s, int precompute_0p, const void* recv, int xa, int xb,
+                                  int world, const int* kz_bounds, double* flow_slab) {
+    if (!s) return SEWALD_EINVAL;
+    return ctx_guard(s->ctx, [&] {
+        aft_d0_slab_inverse(s, precompute_0p != 0, recv, xa, xb, slab_bounds_from(world, kz_bounds), flow_slab);
+    });
+}
+
+int sewald_gpu_session_set_flow(sewald_gpu_session* s, const double* flow_dev) {
+    if (!s || !flow_dev) return SEWALD_EINVAL;
+    return ctx_guard(s->ctx, [&] {
+        const int64_t vol = (int64_t)s->g.n[0] * s->g.n[1] * s->g.n[2];
+        double* f = static_cast<double*>(s->flow.ensure(sizeof(double) * 3 * vol));
+        cuda_check(cudaMemcpyAsync(f, flow_dev, sizeof(double) * 3 * vol, cudaMemcpyDeviceToDevice, s->ctx->stream),
+                   "set flow");
+    });
 }
 
 int64_t sewald_gpu_launch_count(const sewald_gpu_ctx* ctx) { return ctx ? ctx->launches : -1; }

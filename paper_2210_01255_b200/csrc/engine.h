@@ -108,5 +108,14 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
 
 // Fourier solve for d < 3 (aft.cu): grid (C comps, real) -> s->flow (3 comps).
 void aft_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p);
+// Slab-distributed D = 0 solve stages (aft.cu / aft_d0.cu).
+struct SlabBounds;
+void aft_d0_geometry(sewald_gpu_session* s, bool use_table, int m[3], int n[3], int* h2, int* C);
+void aft_d0_slab_forward(sewald_gpu_session* s, bool use_table, const double* grid_slab, int xa, int xb,
+                         const SlabBounds& kzb, void* send);
+void aft_d0_slab_middle(sewald_gpu_session* s, bool use_table, const void* recv, const SlabBounds& xbd, int ka,
+                        int kb, void* send);
+void aft_d0_slab_inverse(sewald_gpu_session* s, bool use_table, const void* recv, int xa, int xb,
+                         const SlabBounds& kzb, double* flow_slab);
 
 }  // namespace sewald_b200
