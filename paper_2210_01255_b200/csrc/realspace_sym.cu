@@ -129,7 +129,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     constexpr bool BF = SEWALD_SYM_BRANCHFREE && KIND != SEWALD_STRESSLET;
     __shared__ __align__(16) double jrec_all[SYM_WARPS][32][RS];
     __shared__ long long jid_all[SYM_WARPS][32];
-    __shared__ float jf_all[SYM_WARPS][3][32];
+    __shared__ float4 jf_all[SYM_WARPS][32];  // fp32 positions for the candidate pass
     __shared__ double exp_tab[32];
     if (threadIdx.x < 32) exp_tab[threadIdx.x] = c_exp2_tab32[threadIdx.x];
     __syncthreads();
@@ -137,7 +137,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double(*jrec)[RS] = jrec_all[warp];
     long long* jid = jid_all[warp];
-    float(*jf)[32] = jf_all[warp];
+    float4* jf = jf_all[warp];
     unsigned long long npairs = 0;  // flushed per cluster from the 32-bit step counter
     // Persistent warps: clusters are taken from a global counter, so the
     // uneven per-cluster work (row geometry, half rule) does not leave SMs
@@ -240,9 +240,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                         rec[1] = q[1];
                         rec[2] = q[2];
                         jid[lane] = __double_as_longlong(q[3]);
-                        jf[0][lane] = (float)q[0];
-                        jf[1][lane] = (float)q[1];
-                        jf[2][lane] = (float)q[2];
+                        jf[lane] = make_float4((float)q[0], (float)q[1], (float)q[2], 0.0f);
 #pragma unroll
                         for (int c = 0; c < NS; ++c) rec[3 + c] = q[4 + c];
                     } else {
@@ -262,14 +260,26 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                     // warp OR-reduction); (3) fp64 work only on those steps.
                     unsigned m = 0u;
                     if (valid) {
+                        if (cnt == 32 && dlt <= -32) {
+                            // full block entirely after the cluster: no slot or
+                            // half-rule tests
 #pragma unroll 8
-                        for (int s = 0; s < 32; ++s) {
-                            const int j = (lane + s) & 31;
-                            const int dj = j - lane;
-                            const float d0 = tf0 - jf[0][j], d1 = tf1 - jf[1][j], d2 = tf2 - jf[2][j];
-                            const bool ok = j < cnt && (dj > dlt || (dj == dlt && pos_shift)) &&
-                                            fmaf(d2, d2, fmaf(d1, d1, d0 * d0)) < a.thresh_f;
-                            m |= (ok ? 1u : 0u) << s;
+                            for (int s = 0; s < 32; ++s) {
+                                const float4 p = jf[(lane + s) & 31];
+                                const float d0 = tf0 - p.x, d1 = tf1 - p.y, d2 = tf2 - p.z;
+                                m |= (fmaf(d2, d2, fmaf(d1, d1, d0 * d0)) < a.thresh_f ? 1u : 0u) << s;
+                            }
+                        } else {
+#pragma unroll 8
+                            for (int s = 0; s < 32; ++s) {
+                                const int j = (lane + s) & 31;
+                                const int dj = j - lane;
+                                const float4 p = jf[j];
+                                const float d0 = tf0 - p.x, d1 = tf1 - p.y, d2 = tf2 - p.z;
+                                const bool ok = j < cnt && (dj > dlt || (dj == dlt && pos_shift)) &&
+                                                fmaf(d2, d2, fmaf(d1, d1, d0 * d0)) < a.thresh_f;
+                                m |= (ok ? 1u : 0u) << s;
+                            }
                         }
                     }
                     unsigned steps = __reduce_or_sync(0xffffffffu, m);
