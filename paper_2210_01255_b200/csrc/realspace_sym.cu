@@ -244,7 +244,9 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
 #pragma unroll
                         for (int c = 0; c < NS; ++c) rec[3 + c] = q[4 + c];
                     } else {
-                        // unused slots stay finite (branch-free steps read them)
+                        // unused slots: far away in fp32 (never candidates) and
+                        // finite in fp64 (branch-free steps read them)
+                        jf[lane] = make_float4(1e30f, 1e30f, 1e30f, 0.0f);
                         double* rec = jrec[lane];
                         rec[0] = rec[1] = rec[2] = 1e100;
 #pragma unroll
@@ -260,9 +262,9 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                     // warp OR-reduction); (3) fp64 work only on those steps.
                     unsigned m = 0u;
                     if (valid) {
-                        if (cnt == 32 && dlt <= -32) {
-                            // full block entirely after the cluster: no slot or
-                            // half-rule tests
+                        if (dlt <= -32) {
+                            // block entirely after the cluster: no half-rule test
+                            // (unused slots are far away and fail the distance test)
 #pragma unroll 8
                             for (int s = 0; s < 32; ++s) {
                                 const float4 p = jf[(lane + s) & 31];
