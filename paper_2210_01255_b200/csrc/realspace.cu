@@ -139,7 +139,7 @@ __device__ __forceinline__ void pair_accumulate(const Screened& sc, double xi2, 
 // One WARP = one independent work unit: 32 consecutive targets in cell
 // order (spatially compact), their bounding box, the cell rows within rc of
 // it, and a private shared-memory staging area. No block-wide barriers.
-template <int KIND, int S>
+template <int KIND, int S, bool SHORT>
 __global__ void __launch_bounds__(RS_THREADS, 4)
 realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed,
                  const float4* __restrict__ packedf, const int64_t* __restrict__ cell_off,
@@ -149,6 +149,9 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
     __shared__ __align__(16) double src_all[RS_WARPS][WCHUNK * S];
     __shared__ float4 srcf_all[RS_WARPS][WCHUNK];
     __shared__ uint8_t queue_all[RS_WARPS][WCHUNK][32];
+    __shared__ double exp_tab[32];
+    if (threadIdx.x < 32) exp_tab[threadIdx.x] = c_exp2_tab32[threadIdx.x];
+    __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* src = src_all[warp];
@@ -179,8 +182,8 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
         }
     }
 
-    const double rc2 = a.rc * a.rc;
-    const double xi2 = a.xi * a.xi;
+    const double rc2 = a.rc2;  // kernel-parameter operands
+    const double xi2 = a.xi2;
     const double rcm = a.rc * (1.0 + 1e-10) + 1e-12 * fmax(fmax(cg.L[0], cg.L[1]), cg.L[2]);
     const double rcm2 = rcm * rcm;
 
@@ -264,7 +267,7 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
                                 atomicExch(err, 1);
                             continue;
                         }
-                        const Screened sc = screened(n2, a.xi, xi2);
+                        const Screened sc = screened<SHORT>(n2, a.xi, xi2, exp_tab);
                         pair_accumulate<KIND>(sc, xi2, n2, r0, r1, r2, q + 4, acc0, acc1, acc2);
                         ++npairs;
                     }
@@ -313,20 +316,20 @@ void launch_realspace(const CellGrid& cg, const RealspaceArgs& a, const double* 
                       unsigned long long* pair_count, int* err, cudaStream_t st) {
     if (Nt == 0) return;
     const unsigned blocks = (unsigned)((Nt + RS_THREADS - 1) / RS_THREADS);
+    const bool shrt = a.xi * a.rc <= SEWALD_ERFCX8_XMAX;  // shorter erfcx rational suffices
+#define SEWALD_RS_LAUNCH(K, SZ)                                                                              \
+    if (shrt)                                                                                                \
+        realspace_kernel<K, SZ, true><<<blocks, RS_THREADS, 0, st>>>(cg, a, packed, packedf, cell_off, tfolded, \
+                                                                     torder, Nt, u, accumulate, pair_count, err); \
+    else                                                                                                     \
+        realspace_kernel<K, SZ, false><<<blocks, RS_THREADS, 0, st>>>(cg, a, packed, packedf, cell_off, tfolded, \
+                                                                      torder, Nt, u, accumulate, pair_count, err);
     switch (a.kind) {
-        case SEWALD_STOKESLET:
-            realspace_kernel<SEWALD_STOKESLET, 8><<<blocks, RS_THREADS, 0, st>>>(
-                cg, a, packed, packedf, cell_off, tfolded, torder, Nt, u, accumulate, pair_count, err);
-            break;
-        case SEWALD_ROTLET:
-            realspace_kernel<SEWALD_ROTLET, 8><<<blocks, RS_THREADS, 0, st>>>(
-                cg, a, packed, packedf, cell_off, tfolded, torder, Nt, u, accumulate, pair_count, err);
-            break;
-        default:
-            realspace_kernel<SEWALD_STRESSLET, 12><<<blocks, RS_THREADS, 0, st>>>(
-                cg, a, packed, packedf, cell_off, tfolded, torder, Nt, u, accumulate, pair_count, err);
-            break;
+        case SEWALD_STOKESLET: SEWALD_RS_LAUNCH(SEWALD_STOKESLET, 8) break;
+        case SEWALD_ROTLET: SEWALD_RS_LAUNCH(SEWALD_ROTLET, 8) break;
+        default: SEWALD_RS_LAUNCH(SEWALD_STRESSLET, 12) break;
     }
+#undef SEWALD_RS_LAUNCH
 }
 
 }  // namespace sewald_b200
