@@ -34,19 +34,20 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# DRAM bytes (read + write) per launch of the dominant kernel from one
+# `ncu --set full` capture of the same bench command (profiles/r1_ncu_realspace_sym_v3.txt).
+TRAFFIC_BYTES = {"c2_stokeslet_d3_N1e6": 97_382_400 + 4_394_240}
+
 # Algorithmic fp64 flops per accepted (directed) real-space pair of the
 # implemented evaluation, keyed (kernel, symmetric): ncu thread-level
 # 2*DFMA + DMUL + DADD of the kernel divided by the kernel's own pair counter
-# (tools/rs_flops.py; profiles/r1_realspace_flops.txt; DESIGN.md "real-space
+# (tools/gpu_probe3.sh: branchy kernel variant so idle lanes execute nothing;
+# profiles/r1_realspace_flops_v2.txt; DESIGN.md "real-space
 # roofline"). The symmetric kernel (targets == sources) evaluates each
 # unordered pair once and charges half of it to each direction.
-# DRAM bytes (read + write) per launch of the dominant kernel from one
-# `ncu --set full` capture of the same bench command (profiles/r1_ncu_*_v2.txt).
-TRAFFIC_BYTES = {"c2_stokeslet_d3_N1e6": 97_831_680 + 4_818_432}
-
 FLOPS_PER_PAIR = {
-    (0, True): 66.5, (1, True): 88.3, (2, True): 61.9,
-    (0, False): 136.5, (1, False): 164.4, (2, False): 130.5,
+    (0, True): 62.0, (1, True): 80.8, (2, True): 57.4,
+    (0, False): 111.5, (1, False): 139.4, (2, False): 105.4,
 }
 
 
