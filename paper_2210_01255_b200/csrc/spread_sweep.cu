@@ -507,7 +507,10 @@ void launch_sweep_weights(const DevGrid& g, const DevWindow& w, const double* x,
 int launch_spread_sweep(const DevGrid& g, int P, const double* W, const int4* SW, const double* STR, int C,
                         const int64_t* off, const SweepShape& s, double* out, cudaStream_t st) {
     if (P <= 8) return launch_sweep<8, 3, 4>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
+    if (P <= 12) return launch_sweep<12, 3, 4>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
+    if (P <= 14) return launch_sweep<14, 3, 4>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
     if (P <= 16) return launch_sweep<16, SEWALD_SWEEP_NC16, 4>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
+    if (P <= 20) return launch_sweep<20, 3, 2>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
     if (P <= 24) return launch_sweep<24, 3, 2>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
     return launch_sweep<32, 1, 4>(g, P, W, SW, STR, C, off, s.nbx, s.nby, s.nseg, out, st);
 }
@@ -519,6 +522,7 @@ void launch_gather_sweep(const DevGrid& g, int P, const double* W, const int4* S
     const int t0 = (int)((int64_t)tiles * part / nparts), t1 = (int)((int64_t)tiles * (part + 1) / nparts);
     if (P <= 8) launch_gsweep<8, 4>(g, P, W, SW, off, s.nbx, s.nby, s.nseg, t0, t1, grid, h3, u, st);
     else if (P <= 16) launch_gsweep<16, 4>(g, P, W, SW, off, s.nbx, s.nby, s.nseg, t0, t1, grid, h3, u, st);
+    else if (P <= 20) launch_gsweep<20, 2>(g, P, W, SW, off, s.nbx, s.nby, s.nseg, t0, t1, grid, h3, u, st);
     else if (P <= 24) launch_gsweep<24, 2>(g, P, W, SW, off, s.nbx, s.nby, s.nseg, t0, t1, grid, h3, u, st);
     else launch_gsweep<32, 2>(g, P, W, SW, off, s.nbx, s.nby, s.nseg, t0, t1, grid, h3, u, st);
 }
