@@ -285,6 +285,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                         }
                     }
                     unsigned steps = __reduce_or_sync(0xffffffffu, m);
+                    bool coincident = false;
                     while (steps) {
                         const int s = 31 - __clz(steps);  // highest step first: one FLO
                         steps ^= 1u << s;
@@ -301,7 +302,8 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                             const double r0 = xs0 - xy.x, r1 = xs1 - xy.y, r2 = xs2 - zs0.x;
                             const double n2 = __dadd_rn(__dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1)), __dmul_rn(r2, r2));
                             bool acc = in && n2 < rc2;
-                            if (acc && n2 == 0.0) atomicExch(err, 1);  // coincident distinct points (kernels.cpp:19-22)
+                            // coincident distinct points (kernels.cpp:19-22): flagged per block
+                            coincident |= acc && n2 == 0.0;
                             acc = acc && n2 != 0.0;
                             const double n2e = acc ? n2 : 0.25 * rc2;
                             double sj[NS];
@@ -357,6 +359,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                             }
                         }
                     }
+                    if (coincident) atomicExch(err, 1);
                     __syncwarp();
                     if (lane < cnt) {
                         double* dst = u + 3 * jid[lane];

@@ -80,8 +80,10 @@ __device__ __forceinline__ double exp_neg(double y) {
 
 // e^{-y} for y >= 0 via 2^(j/32) table (tab: shared-memory copy of
 // c_exp2_tab32) and a degree-6 polynomial: 9 fp64 FMAs instead of 16.
+template <bool CLAMP = true>
 __device__ __forceinline__ double exp_neg_tab(double y, const double* tab) {
-    y = fmin(y, 700.0);
+    // callers that guarantee y <= 49 (x <= 7, the SHORT real-space kernels) skip the clamp
+    if (CLAMP) y = fmin(y, 700.0);
     const double shifter = c_misc[0];
     const double t = fma(-y, c_exp_tab_k[0], shifter);
     const int n = __double2loint(t);
@@ -141,7 +143,7 @@ __device__ __forceinline__ Screened screened(double n2, double xi, double xi2, c
     s.iy = rsqrt_nr(n2);
     const double r = n2 * s.iy;
     const double x = xi * r;
-    s.E = exp_tab ? exp_neg_tab(xi2 * n2, exp_tab) : exp_neg(xi2 * n2);
+    s.E = exp_tab ? exp_neg_tab<!SHORT>(xi2 * n2, exp_tab) : exp_neg(xi2 * n2);
     s.Ey = s.E * s.iy;
     s.R = erfcx_rat<SHORT>(x);
     s.cx = c_misc[4] * x;
