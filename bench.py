@@ -251,8 +251,15 @@ def run_ours(args, cfg):
     from paper_2210_01255_b200.workloads import generate
 
     ws, rank, local = dist_env()
+    # SEWALD_DIST_BACKEND=gloo: functional multi-rank check on a box with fewer GPUs
+    # than ranks (ranks share devices; not a timing configuration)
+    backend = os.environ.get("SEWALD_DIST_BACKEND", "nccl")
+    local = local % max(torch.cuda.device_count(), 1) if backend != "nccl" else local
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
 
