@@ -16,6 +16,7 @@
 #include "sg_kernels.h"
 
 #include <algorithm>
+#include <cstdlib>
 
 namespace sewald_b200 {
 
@@ -142,6 +143,179 @@ gather_tile_kernel(DevGrid g, int P, int B, int L, int ntx, int nty, int ntz, in
     }
 }
 
+// ---------------------------------------------------------------------------
+// FP64 tensor-core variant (DMMA m8n8k4). With L = B + P - 1 = 19 for every
+// P <= 19, the tile contraction is
+//   H[(a,b), t] = sum_c G[a][b][c] Wz'[c][t]     (GEMM: 361 x 20 x T, zero-padded)
+//   u_t         = sum_(a,b) H[(a,b), t] Wx'[a][t] Wy'[b][t]
+// where Wx', Wy', Wz' are each target's taps placed at its offset in the
+// region (zero elsewhere). The GEMM runs on the fp64 tensor cores (one DMMA
+// = 256 FMAs per warp instruction), the second contraction in the fragment
+// epilogue. Shared-memory traffic per tile drops ~15x against the per-target
+// tap loop.
+constexpr int MM_L = 19;             // region edge
+constexpr int MM_LS = 20;            // padded row (K = 20 = 5 k-steps of 4)
+constexpr int MM_ROWS = MM_L * MM_L; // 361 GEMM rows (a, b)
+constexpr int MM_RB = (MM_ROWS + 7) / 8;  // 46 row blocks
+constexpr int MM_TG = 32;            // targets per group (4 n-blocks of 8)
+constexpr int MM_WARPS = 8;
+constexpr int MM_THREADS = 32 * MM_WARPS;
+
+__device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(MM_THREADS)
+gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64_t tile0,
+                       const double* __restrict__ W, const int4* __restrict__ SW, const int64_t* __restrict__ off,
+                       const double* __restrict__ grid, double h3, int accumulate, double* __restrict__ u) {
+    extern __shared__ __align__(16) double sm[];
+    const int64_t tile = tile0 + blockIdx.x;
+    const int64_t p0 = off[tile], p1 = off[tile + 1];
+    if (p0 >= p1) return;
+    const int tz = (int)(tile % ntz);
+    const int ty = (int)((tile / ntz) % nty);
+    const int tx = (int)(tile / ((int64_t)ntz * nty));
+    const int X0 = tx * B, Y0 = ty * B, Z0 = tz * B;
+
+    double* region = sm;                                   // [MM_RB*8][MM_LS] (rows >= 361 zero)
+    double* wz = region + MM_RB * 8 * MM_LS;               // [MM_TG][MM_LS]   Wz'[t][c]
+    double* wx = wz + MM_TG * MM_LS;                       // [MM_LS][MM_TG]   Wx'[a][t] (a = 19 zero)
+    double* wy = wx + MM_LS * MM_TG;                       // [MM_LS][MM_TG]   Wy'[b][t]
+    double* part = wy + MM_LS * MM_TG;                     // [MM_WARPS][MM_TG]
+    int* rowoff = reinterpret_cast<int*>(part + MM_WARPS * MM_TG);  // [361]
+    int* zoff = rowoff + MM_ROWS;                                  // [19]
+    int* tid = zoff + MM_L;                                        // [MM_TG] target ids
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // zero padding only: column c = 19 of every row and the rows >= 361 (never loaded)
+    for (int e = threadIdx.x; e < MM_ROWS; e += MM_THREADS) region[e * MM_LS + MM_L] = 0.0;
+    for (int e = threadIdx.x; e < (MM_RB * 8 - MM_ROWS) * MM_LS; e += MM_THREADS) region[MM_ROWS * MM_LS + e] = 0.0;
+    for (int row = threadIdx.x; row < MM_ROWS; row += MM_THREADS) {
+        const int i = row / MM_L, j = row - i * MM_L;
+        int gx = X0 + i, gy = Y0 + j;
+        bool ok = true;
+        if (g.d > 0) gx %= g.n[0]; else ok = gx < g.n[0];
+        if (g.d > 1) gy %= g.n[1]; else ok = ok && gy < g.n[1];
+        rowoff[row] = ok ? (gx * g.n[1] + gy) * g.n[2] : -1;
+    }
+    if (threadIdx.x < MM_L) {
+        int gz = Z0 + threadIdx.x;
+        bool ok = true;
+        if (g.d > 2) gz %= g.n[2]; else ok = gz < g.n[2];
+        zoff[threadIdx.x] = ok ? gz : -1;
+    }
+    const int64_t cs = (int64_t)g.n[0] * g.n[1] * g.n[2];
+    const int ngroups = (int)((p1 - p0 + MM_TG - 1) / MM_TG);
+
+    for (int grp = 0; grp < ngroups; ++grp) {
+        const int64_t q0 = p0 + (int64_t)grp * MM_TG;
+        const int T = (int)min((int64_t)MM_TG, p1 - q0);
+        __syncthreads();
+        // per-target taps placed at the target's offset in the region (warp per
+        // target, lane = region index k)
+        for (int t = warp; t < MM_TG; t += MM_WARPS) {
+            int4 sw = make_int4(0, 0, 0, -1);
+            if (t < T) sw = SW[q0 + t];
+            if (lane < MM_LS) {
+                const int k = lane;
+                double vz = 0.0, vx = 0.0, vy = 0.0;
+                if (t < T && k < MM_L) {
+                    const double* wt = W + (q0 + t) * 3 * P;
+                    const int kx = k - (sw.x - X0), ky = k - (sw.y - Y0), kz = k - (sw.z - Z0);
+                    if (kx >= 0 && kx < P) vx = __ldg(wt + kx);
+                    if (ky >= 0 && ky < P) vy = __ldg(wt + P + ky);
+                    if (kz >= 0 && kz < P) vz = __ldg(wt + 2 * P + kz);
+                }
+                wz[t * MM_LS + k] = vz;
+                wx[k * MM_TG + t] = vx;
+                wy[k * MM_TG + t] = vy;
+            }
+            if (lane == 0) tid[t] = sw.w;
+        }
+        const int nblk = (T + 7) / 8;
+        for (int c = 0; c < 3; ++c) {
+            __syncthreads();
+            const double* gc = grid + c * cs;
+            {
+                const int zo = lane < MM_L ? zoff[lane] : -1;
+                const unsigned sbase = (unsigned)__cvta_generic_to_shared(region + lane);
+#pragma unroll 4
+                for (int row = warp; row < MM_ROWS; row += MM_WARPS) {
+                    const int ro = rowoff[row];
+                    if (lane < MM_L) {
+                        if (ro >= 0 && zo >= 0)
+                            asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sbase + row * MM_LS * 8),
+                                         "l"(gc + ro + zo));
+                        else
+                            region[row * MM_LS + lane] = 0.0;
+                    }
+                }
+            }
+            asm volatile("cp.async.wait_all;\n" ::);
+            __syncthreads();
+            // B fragments (k-steps x n-blocks): lane holds Wz'[k0 + lane%4][n0 + lane/4]
+            double bf[5][4];
+#pragma unroll
+            for (int ks = 0; ks < 5; ++ks)
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb)
+                    bf[ks][nb] = wz[(nb * 8 + (lane >> 2)) * MM_LS + ks * 4 + (lane & 3)];
+            double acc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+            const int tc = 2 * (lane & 3);  // this lane's two target columns within an n-block
+            for (int rb = warp; rb < MM_RB; rb += MM_WARPS) {
+                const int row_a = rb * 8 + (lane >> 2);  // A-fragment row of this lane
+                double af[5];
+#pragma unroll
+                for (int ks = 0; ks < 5; ++ks) af[ks] = region[row_a * MM_LS + ks * 4 + (lane & 3)];
+                const int a = row_a / MM_L, b = row_a - a * MM_L;  // C rows = A rows (groupID)
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb) {
+                    if (nb < nblk) {
+                        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                        for (int ks = 0; ks < 5; ++ks) dmma_8x8x4(d0, d1, af[ks], bf[ks][nb]);
+                        const int t = nb * 8 + tc;
+                        const double2 vx = *reinterpret_cast<const double2*>(wx + a * MM_TG + t);
+                        const double2 vy = *reinterpret_cast<const double2*>(wy + b * MM_TG + t);
+                        acc[nb][0] = fma(d0, vx.x * vy.x, acc[nb][0]);
+                        acc[nb][1] = fma(d1, vx.y * vy.y, acc[nb][1]);
+                    }
+                }
+            }
+            // reduce over the 8 lanes sharing a column pair (lane % 4)
+#pragma unroll
+            for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int s = 4; s < 32; s <<= 1) acc[nb][h] += __shfl_xor_sync(0xffffffffu, acc[nb][h], s);
+            if (lane < 4) {
+#pragma unroll
+                for (int nb = 0; nb < 4; ++nb) {
+                    part[warp * MM_TG + nb * 8 + 2 * lane] = acc[nb][0];
+                    part[warp * MM_TG + nb * 8 + 2 * lane + 1] = acc[nb][1];
+                }
+            }
+            __syncthreads();
+            if (threadIdx.x < T) {
+                double v = 0.0;
+#pragma unroll
+                for (int w = 0; w < MM_WARPS; ++w) v += part[w * MM_TG + threadIdx.x];
+                double* dst = u + 3 * (int64_t)tid[threadIdx.x] + c;
+                *dst = accumulate ? *dst + h3 * v : h3 * v;
+            }
+        }
+    }
+}
+
+size_t mma_smem_bytes() {
+    return sizeof(double) * (MM_RB * 8 * MM_LS + MM_TG * MM_LS + 2 * MM_LS * MM_TG + MM_WARPS * MM_TG) +
+           sizeof(int) * (MM_ROWS + MM_L + MM_TG);
+}
+
 }  // namespace
 
 TileShape tile_shape(const DevGrid& g, int P) {
@@ -172,6 +346,20 @@ void launch_gather_tile(const DevGrid& g, int P, const TileShape& s, const doubl
                         double* u, cudaStream_t st) {
     const int64_t t0 = s.ntiles * part / nparts, t1 = s.ntiles * (part + 1) / nparts;
     if (t1 <= t0) return;
+    static const bool use_mma = [] {
+        const char* e = getenv("SEWALD_GATHER_MMA");
+        return !(e && e[0] == '0');
+    }();
+    if (use_mma && s.L == MM_L) {
+        const size_t sm = mma_smem_bytes();
+        cudaFuncSetAttribute(gather_tile_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        for (int64_t a = t0; a < t1; a += (int64_t)1 << 30) {
+            const int64_t n = std::min<int64_t>(t1 - a, (int64_t)1 << 30);
+            gather_tile_mma_kernel<<<(unsigned)n, MM_THREADS, sm, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W,
+                                                                         SW, off, grid, h3, accumulate, u);
+        }
+        return;
+    }
     cudaFuncSetAttribute(gather_tile_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s.smem);
     // grid.x limit is 2^31 - 1: launch in chunks
     for (int64_t a = t0; a < t1; a += (int64_t)1 << 30) {
