@@ -289,15 +289,26 @@ void ensure_spread_order(sewald_gpu_session* s, int64_t i0, int64_t i1) {
         return e && e[0] ? (e[0] == '0' ? 0 : 1) : -1;
     }();
     if (sweep_mode == 0 || (sweep_mode < 0 && s->p.P > 24)) s->sweep.ok = false;
-    const int64_t nb = s->sweep.ok ? s->sweep.nkeys
-                                   : (int64_t)s->shape.nb[0] * s->shape.nb[1] * s->shape.nb[2];
+    // tensor-core tiles for P <= 16 (SEWALD_SPREAD_MMA=0 disables)
+    static const bool mma_enabled = [] {
+        const char* e = getenv("SEWALD_SPREAD_MMA");
+        return !(e && e[0] == '0');
+    }();
+    s->sm_shape = spread_mma_shape(s->g, s->p.P);
+    s->sp_mode = (mma_enabled && s->sm_shape.ok) ? 2 : (s->sweep.ok ? 1 : 0);
+    const int64_t nb = s->sp_mode == 2 ? s->sm_shape.ntiles
+                       : s->sweep.ok   ? s->sweep.nkeys
+                                       : (int64_t)s->shape.nb[0] * s->shape.nb[1] * s->shape.nb[2];
     s->sp_keys.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1));
     s->sp_keys2.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1));
     s->sp_vals.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1));
     s->sp_order.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1));
     s->sp_off.ensure(sizeof(int64_t) * (nb + 1));
     int* bad = s->flags.as<int>() + FLAG_SPREAD_BOX;
-    if (s->sweep.ok)
+    if (s->sp_mode == 2)
+        launch_spread_mma_bucket(s->g, s->p.P, s->sm_shape, s->x.as<double>() + 3 * i0, n, s->sp_keys.as<uint32_t>(),
+                                 s->sp_vals.as<uint32_t>(), bad, st);
+    else if (s->sweep.ok)
         launch_sweep_bucket(s->g, s->p.P, s->x.as<double>() + 3 * i0, n, s->sweep, s->sp_keys.as<uint32_t>(),
                             s->sp_vals.as<uint32_t>(), bad, st);
     else
@@ -595,7 +606,7 @@ void session_spread(sewald_gpu_session* s, int64_t i0, int64_t i1, double* grid)
     ensure_spread_order(s, i0, i1);
     cudaStream_t st = s->ctx->stream;
     const int64_t vol = (int64_t)s->g.n[0] * s->g.n[1] * s->g.n[2];
-    if (s->sweep.ok) {
+    if (s->sp_mode == 2 || s->sweep.ok) {
         const int64_t n = i1 - i0;
         const int P = s->p.P;
         double* W = static_cast<double*>(s->sp_w.ensure(sizeof(double) * 3 * P * std::max<int64_t>(n, 1)));
@@ -604,8 +615,12 @@ void session_spread(sewald_gpu_session* s, int64_t i0, int64_t i1, double* grid)
         launch_sweep_weights(s->g, s->w, s->x.as<double>() + 3 * i0, s->f.as<double>() + 3 * i0,
                              s->stresslet ? s->nu.as<double>() + 3 * i0 : nullptr, s->stresslet,
                              s->sp_order.as<uint32_t>(), n, W, SW, STR, st);
-        s->ctx->launches += 1 + launch_spread_sweep(s->g, P, W, SW, STR, s->C, s->sp_off.as<int64_t>(), s->sweep,
-                                                    grid, st);
+        if (s->sp_mode == 2)
+            s->ctx->launches += 1 + launch_spread_mma(s->g, P, s->sm_shape, W, SW, STR, s->C,
+                                                      s->sp_off.as<int64_t>(), grid, st);
+        else
+            s->ctx->launches += 1 + launch_spread_sweep(s->g, P, W, SW, STR, s->C, s->sp_off.as<int64_t>(),
+                                                        s->sweep, grid, st);
         cuda_check(cudaGetLastError(), "spread sweep launch");
         return;
     }

@@ -81,6 +81,8 @@ struct sewald_gpu_session {
     bool same = false;
     sewald_b200::DevBuf xt, t_folded, t_keys, t_keys2, t_vals, t_order;
     // gather sweep ordering of the targets
+    int sp_mode = 0;  // spread: 0 tile kernel, 1 z-sweep, 2 tensor-core tiles
+    sewald_b200::SpreadMmaShape sm_shape{};
     bool tg_ready = false;
     int tg_mode = 0;  // 1: z-sweep gather, 2: tiled gather
     sewald_b200::DevBuf tg_keys, tg_keys2, tg_vals, tg_order, tg_off, tg_w, tg_sw;

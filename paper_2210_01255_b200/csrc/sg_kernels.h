@@ -51,6 +51,20 @@ void launch_gather_tile(const DevGrid& g, int P, const TileShape& s, const doubl
                         const int64_t* off, int part, int nparts, const double* grid, double h3, int accumulate,
                         double* u, cudaStream_t st);
 
+// Tensor-core spread (spread_mma.cu): sources bucketed by the B^3 block of
+// their stencil start, region L^3 (L = B + P - 1) per block as a DMMA GEMM.
+struct SpreadMmaShape {
+    int B, L;
+    int nt[3];
+    int64_t ntiles;
+    bool ok;
+};
+SpreadMmaShape spread_mma_shape(const DevGrid& g, int P);
+void launch_spread_mma_bucket(const DevGrid& g, int P, const SpreadMmaShape& s, const double* x, int64_t N,
+                              uint32_t* keys, uint32_t* vals, int* bad, cudaStream_t st);
+int launch_spread_mma(const DevGrid& g, int P, const SpreadMmaShape& s, const double* W, const int4* SW,
+                      const double* STR, int C, const int64_t* off, double* out, cudaStream_t st);
+
 struct SweepShape {
     int nbx, nby, nseg;
     int64_t nkeys;

@@ -1,0 +1,182 @@
+// Spread on the fp64 tensor cores (P = 15, 16): source-stationary tiles.
+//
+// Reference: spread /root/reference/proj/src/fourier.cpp:237-274 (stencil
+// :168-188). Same taps, stencil origins and wrap; only the summation order
+// differs (the north_star allows atomic spreading order).
+//
+// Sources are bucketed by the B^3 block of their (wrapped) stencil start, so
+// every stencil of a block lies in its L^3 region (L = B + P - 1). For one
+// component the region is the GEMM
+//   R[(a,b), z] = sum_t F[(a,b), t] Z[t, z],   F = f_t wx_t(a) wy_t(b),  Z = wz_t(z)
+// ((L^2 x T) . (T x L), each source's taps placed at its offset, zero
+// elsewhere), computed with mma.sync.m8n8k4.f64 (256 FMAs per warp
+// instruction) and added to the grid with fp64 RED. The grid is zeroed first.
+#include "device_common.cuh"
+#include "sg_kernels.h"
+
+#include <algorithm>
+#include <cstdlib>
+
+namespace sewald_b200 {
+
+namespace {
+
+constexpr int SM_WARPS = 8;
+constexpr int SM_THREADS = 32 * SM_WARPS;
+constexpr int SM_TG = 32;  // sources per table group (8 k-steps of 4)
+constexpr int SM_LS = 24;  // padded table width (z: 3 n-blocks of 8)
+
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+template <int L>
+__global__ void __launch_bounds__(SM_THREADS)
+spread_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64_t tile0, const double* __restrict__ W,
+                       const int4* __restrict__ SW, const double* __restrict__ STR, int C,
+                       const int64_t* __restrict__ off, double* __restrict__ out) {
+    constexpr int ROWS = L * L;
+    constexpr int RB = (ROWS + 7) / 8;
+    constexpr int RBW = (RB + SM_WARPS - 1) / SM_WARPS;  // row blocks per warp
+    __shared__ __align__(16) double wxf[SM_TG][SM_LS];    // f_t wx_t(a), zero padded
+    __shared__ __align__(16) double wy[SM_TG][SM_LS];
+    __shared__ __align__(16) double wz[SM_TG][SM_LS];
+
+    const int64_t tile = tile0 + blockIdx.x;
+    const int64_t p0 = off[tile], p1 = off[tile + 1];
+    if (p0 >= p1) return;
+    const int tz = (int)(tile % ntz);
+    const int ty = (int)((tile / ntz) % nty);
+    const int tx = (int)(tile / ((int64_t)ntz * nty));
+    const int X0 = tx * B, Y0 = ty * B, Z0 = tz * B;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t cs = (int64_t)g.n[0] * g.n[1] * g.n[2];
+    const int ngroups = (int)((p1 - p0 + SM_TG - 1) / SM_TG);
+
+    for (int c = 0; c < C; ++c) {
+        double acc[RBW][3][2];
+#pragma unroll
+        for (int j = 0; j < RBW; ++j)
+#pragma unroll
+            for (int nb = 0; nb < 3; ++nb) acc[j][nb][0] = acc[j][nb][1] = 0.0;
+        for (int grp = 0; grp < ngroups; ++grp) {
+            const int64_t q0 = p0 + (int64_t)grp * SM_TG;
+            const int T = (int)min((int64_t)SM_TG, p1 - q0);
+            __syncthreads();
+            // tables: warp per source, lane = region index
+            for (int t = warp; t < SM_TG; t += SM_WARPS) {
+                int4 sw = make_int4(0, 0, 0, 0);
+                double f = 0.0;
+                if (t < T) {
+                    sw = SW[q0 + t];
+                    f = STR[(q0 + t) * C + c];
+                }
+                if (lane < SM_LS) {
+                    const int k = lane;
+                    double vx = 0.0, vy = 0.0, vz = 0.0;
+                    if (t < T && k < L) {
+                        const double* w = W + (q0 + t) * 3 * P;
+                        const int kx = k - (sw.x - X0), ky = k - (sw.y - Y0), kz = k - (sw.z - Z0);
+                        if (kx >= 0 && kx < P) vx = __ldg(w + kx);
+                        if (ky >= 0 && ky < P) vy = __ldg(w + P + ky);
+                        if (kz >= 0 && kz < P) vz = __ldg(w + 2 * P + kz);
+                    }
+                    wxf[t][k] = f * vx;
+                    wy[t][k] = vy;
+                    wz[t][k] = vz;
+                }
+            }
+            __syncthreads();
+#pragma unroll
+            for (int j = 0; j < RBW; ++j) {
+                const int rb = warp + j * SM_WARPS;
+                if (rb < RB) {
+                    const int row = rb * 8 + (lane >> 2);  // A / C row of this lane
+                    const int a = row / L, b = row - a * L;
+#pragma unroll
+                    for (int ks = 0; ks < SM_TG / 4; ++ks) {
+                        const int t = ks * 4 + (lane & 3);
+                        const double af = wxf[t][a] * wy[t][b];
+                        const int tb = ks * 4 + (lane & 3);
+#pragma unroll
+                        for (int nb = 0; nb < 3; ++nb) dmma(acc[j][nb][0], acc[j][nb][1], af, wz[tb][nb * 8 + (lane >> 2)]);
+                    }
+                }
+            }
+        }
+        // add the region to the grid
+        double* oc = out + (int64_t)c * cs;
+#pragma unroll
+        for (int j = 0; j < RBW; ++j) {
+            const int rb = warp + j * SM_WARPS;
+            if (rb >= RB) continue;
+            const int row = rb * 8 + (lane >> 2);
+            if (row >= ROWS) continue;
+            const int a = row / L, b = row - a * L;
+            int gx = X0 + a, gy = Y0 + b;
+            if (g.d > 0) gx %= g.n[0]; else if (gx >= g.n[0]) continue;
+            if (g.d > 1) gy %= g.n[1]; else if (gy >= g.n[1]) continue;
+            double* col = oc + ((int64_t)gx * g.n[1] + gy) * g.n[2];
+#pragma unroll
+            for (int nb = 0; nb < 3; ++nb)
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int z = nb * 8 + 2 * (lane & 3) + h;
+                    if (z >= L) continue;
+                    int gz = Z0 + z;
+                    if (g.d > 2) gz %= g.n[2]; else if (gz >= g.n[2]) continue;
+                    const double v = acc[j][nb][h];
+                    if (v != 0.0) atomicAdd(col + gz, v);
+                }
+        }
+    }
+}
+
+}  // namespace
+
+SpreadMmaShape spread_mma_shape(const DevGrid& g, int P) {
+    SpreadMmaShape s{};
+    static const int Lenv = [] {
+        const char* e = getenv("SEWALD_SPREAD_MMA_L");
+        return e ? atoi(e) : 23;
+    }();
+    s.L = Lenv == 19 ? 19 : 23;
+    // The region work is fixed by L (L^2 x 24 per 32 sources) while the sweep's
+    // shrinks as P^3: measured, the tensor-core form wins at P = 16 (c2: 5.9
+    // vs 7.1 ms) and loses at P = 14 (c5: 22.5 vs 14.0 ms).
+    s.ok = P >= 15 && P <= 16;
+    s.B = std::max(1, s.L + 1 - P);
+    for (int ax = 0; ax < 3; ++ax) s.nt[ax] = (g.n[ax] + s.B - 1) / s.B;
+    s.ntiles = (int64_t)s.nt[0] * s.nt[1] * s.nt[2];
+    if (s.ntiles >= (int64_t(1) << 31) || (int64_t)g.n[0] * g.n[1] * g.n[2] >= (int64_t(1) << 31)) s.ok = false;
+    return s;
+}
+
+void launch_spread_mma_bucket(const DevGrid& g, int P, const SpreadMmaShape& s, const double* x, int64_t N,
+                              uint32_t* keys, uint32_t* vals, int* bad, cudaStream_t st) {
+    TileShape ts{};
+    ts.B = s.B;
+    ts.L = s.L;
+    for (int ax = 0; ax < 3; ++ax) ts.nt[ax] = s.nt[ax];
+    ts.ntiles = s.ntiles;
+    launch_tile_bucket(g, P, ts, x, N, keys, vals, bad, st);
+}
+
+int launch_spread_mma(const DevGrid& g, int P, const SpreadMmaShape& s, const double* W, const int4* SW,
+                      const double* STR, int C, const int64_t* off, double* out, cudaStream_t st) {
+    cudaMemsetAsync(out, 0, sizeof(double) * C * (size_t)g.n[0] * g.n[1] * g.n[2], st);
+    for (int64_t a = 0; a < s.ntiles; a += (int64_t)1 << 30) {
+        const int64_t n = std::min<int64_t>(s.ntiles - a, (int64_t)1 << 30);
+        if (s.L == 23)
+            spread_tile_mma_kernel<23><<<(unsigned)n, SM_THREADS, 0, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W,
+                                                                           SW, STR, C, off, out);
+        else
+            spread_tile_mma_kernel<19><<<(unsigned)n, SM_THREADS, 0, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W,
+                                                                           SW, STR, C, off, out);
+    }
+    return 1;
+}
+
+}  // namespace sewald_b200
