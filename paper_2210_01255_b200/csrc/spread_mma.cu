@@ -21,7 +21,10 @@ namespace sewald_b200 {
 
 namespace {
 
-constexpr int SM_WARPS = 8;
+#ifndef SEWALD_SPREAD_MMA_WARPS
+#define SEWALD_SPREAD_MMA_WARPS 16
+#endif
+constexpr int SM_WARPS = SEWALD_SPREAD_MMA_WARPS;
 constexpr int SM_THREADS = 32 * SM_WARPS;
 constexpr int SM_TG = 32;  // sources per table group (8 k-steps of 4)
 constexpr int SM_LS = 24;  // padded table width (z: 3 n-blocks of 8)
