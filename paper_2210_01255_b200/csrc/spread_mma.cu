@@ -1,4 +1,4 @@
-// Spread on the fp64 tensor cores (P = 15, 16): source-stationary tiles.
+// Spread on the fp64 tensor cores (15 <= P <= 20): source-stationary tiles.
 //
 // Reference: spread /root/reference/proj/src/fourier.cpp:237-274 (stencil
 // :168-188). Same taps, stencil origins and wrap; only the summation order
@@ -26,6 +26,12 @@ namespace {
 #endif
 constexpr int SM_WARPS = SEWALD_SPREAD_MMA_WARPS;
 constexpr int SM_THREADS = 32 * SM_WARPS;
+#ifndef SEWALD_SPREAD_MMA_PMIN
+#define SEWALD_SPREAD_MMA_PMIN 15
+#endif
+#ifndef SEWALD_SPREAD_MMA_PMAX
+#define SEWALD_SPREAD_MMA_PMAX 20
+#endif
 constexpr int SM_TG = 32;  // sources per table group (8 k-steps of 4)
 constexpr int SM_LS = 24;  // padded table width (z: 3 n-blocks of 8)
 
@@ -147,9 +153,10 @@ SpreadMmaShape spread_mma_shape(const DevGrid& g, int P) {
     }();
     s.L = Lenv == 19 ? 19 : 23;
     // The region work is fixed by L (L^2 x 24 per 32 sources) while the sweep's
-    // shrinks as P^3: measured, the tensor-core form wins at P = 16 (c2: 5.9
-    // vs 7.1 ms) and loses at P = 14 (c5: 22.5 vs 14.0 ms).
-    s.ok = P >= 15 && P <= 16;
+    // shrinks as P^3: measured, the tensor-core form wins at P = 16 (c2: 4.9
+    // vs 7.1 ms) and P = 18 (c3: 15.1 vs 23.2 ms) and loses at P = 14 (c5:
+    // 22.5 vs 14.0 ms).
+    s.ok = P >= SEWALD_SPREAD_MMA_PMIN && P <= SEWALD_SPREAD_MMA_PMAX;
     s.B = std::max(1, s.L + 1 - P);
     for (int ax = 0; ax < 3; ++ax) s.nt[ax] = (g.n[ax] + s.B - 1) / s.B;
     s.ntiles = (int64_t)s.nt[0] * s.nt[1] * s.nt[2];
