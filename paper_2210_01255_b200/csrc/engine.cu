@@ -385,8 +385,8 @@ const uint32_t* target_order(sewald_gpu_session* s) {
     return s->same ? s->c_order.as<uint32_t>() : s->t_order.as<uint32_t>();
 }
 
-// Targets bucketed / sorted for the tiled gather (P <= 16) or the z-sweep
-// gather (P > 16), with their window taps. Returns 0 (warp-per-target
+// Targets bucketed / sorted for the tiled gather (P <= 20) or the z-sweep
+// gather (P > 20), with their window taps. Returns 0 (warp-per-target
 // gather), 1 (sweep) or 2 (tiles). SEWALD_GATHER=warp|sweep|tile forces one.
 int ensure_gather_order(sewald_gpu_session* s) {
     static const int forced = [] {
@@ -399,7 +399,7 @@ int ensure_gather_order(sewald_gpu_session* s) {
     }();
     const SweepShape sh = sweep_shape(s->g, s->p.P);
     const TileShape ts = tile_shape(s->g, s->p.P);
-    int mode = forced >= 0 ? forced : (s->p.P > 16 ? 1 : 2);
+    int mode = forced >= 0 ? forced : (s->p.P > 20 ? 1 : 2);
     if (mode == 2 && !ts.ok) mode = sh.ok ? 1 : 0;
     if (mode == 1 && !sh.ok) mode = 0;
     if (mode == 0) return 0;

@@ -153,10 +153,6 @@ gather_tile_kernel(DevGrid g, int P, int B, int L, int ntx, int nty, int ntz, in
 // = 256 FMAs per warp instruction), the second contraction in the fragment
 // epilogue. Shared-memory traffic per tile drops ~15x against the per-target
 // tap loop.
-constexpr int MM_L = 19;             // region edge
-constexpr int MM_LS = 20;            // padded row (K = 20 = 5 k-steps of 4)
-constexpr int MM_ROWS = MM_L * MM_L; // 361 GEMM rows (a, b)
-constexpr int MM_RB = (MM_ROWS + 7) / 8;  // 46 row blocks
 constexpr int MM_TG = 32;            // targets per group (4 n-blocks of 8)
 constexpr int MM_WARPS = 8;
 constexpr int MM_THREADS = 32 * MM_WARPS;
@@ -167,10 +163,15 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                  : "d"(a), "d"(b));
 }
 
+template <int MM_L>  // region edge: 19 (B = 20 - P, P <= 16) or 23 (B = 24 - P, P <= 20)
 __global__ void __launch_bounds__(MM_THREADS)
 gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64_t tile0,
                        const double* __restrict__ W, const int4* __restrict__ SW, const int64_t* __restrict__ off,
                        const double* __restrict__ grid, double h3, int accumulate, double* __restrict__ u) {
+    constexpr int MM_LS = (MM_L + 4) & ~3;         // padded row: K = MM_LS = 4 x KS
+    constexpr int KS = MM_LS / 4;
+    constexpr int MM_ROWS = MM_L * MM_L;            // GEMM rows (a, b)
+    constexpr int MM_RB = (MM_ROWS + 7) / 8;        // row blocks
     extern __shared__ __align__(16) double sm[];
     const int64_t tile = tile0 + blockIdx.x;
     const int64_t p0 = off[tile], p1 = off[tile + 1];
@@ -257,9 +258,9 @@ gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
             asm volatile("cp.async.wait_all;\n" ::);
             __syncthreads();
             // B fragments (k-steps x n-blocks): lane holds Wz'[k0 + lane%4][n0 + lane/4]
-            double bf[5][4];
+            double bf[KS][4];
 #pragma unroll
-            for (int ks = 0; ks < 5; ++ks)
+            for (int ks = 0; ks < KS; ++ks)
 #pragma unroll
                 for (int nb = 0; nb < 4; ++nb)
                     bf[ks][nb] = wz[(nb * 8 + (lane >> 2)) * MM_LS + ks * 4 + (lane & 3)];
@@ -267,16 +268,16 @@ gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
             const int tc = 2 * (lane & 3);  // this lane's two target columns within an n-block
             for (int rb = warp; rb < MM_RB; rb += MM_WARPS) {
                 const int row_a = rb * 8 + (lane >> 2);  // A-fragment row of this lane
-                double af[5];
+                double af[KS];
 #pragma unroll
-                for (int ks = 0; ks < 5; ++ks) af[ks] = region[row_a * MM_LS + ks * 4 + (lane & 3)];
+                for (int ks = 0; ks < KS; ++ks) af[ks] = region[row_a * MM_LS + ks * 4 + (lane & 3)];
                 const int a = row_a / MM_L, b = row_a - a * MM_L;  // C rows = A rows (groupID)
 #pragma unroll
                 for (int nb = 0; nb < 4; ++nb) {
                     if (nb < nblk) {
                         double d0 = 0.0, d1 = 0.0;
 #pragma unroll
-                        for (int ks = 0; ks < 5; ++ks) dmma_8x8x4(d0, d1, af[ks], bf[ks][nb]);
+                        for (int ks = 0; ks < KS; ++ks) dmma_8x8x4(d0, d1, af[ks], bf[ks][nb]);
                         const int t = nb * 8 + tc;
                         const double2 vx = *reinterpret_cast<const double2*>(wx + a * MM_TG + t);
                         const double2 vy = *reinterpret_cast<const double2*>(wy + b * MM_TG + t);
@@ -311,17 +312,20 @@ gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
     }
 }
 
-size_t mma_smem_bytes() {
-    return sizeof(double) * (MM_RB * 8 * MM_LS + MM_TG * MM_LS + 2 * MM_LS * MM_TG + MM_WARPS * MM_TG) +
-           sizeof(int) * (MM_ROWS + MM_L + MM_TG);
+size_t mma_smem_bytes(int L) {
+    const int LS = (L + 4) & ~3, rows = L * L, rb = (rows + 7) / 8;
+    return sizeof(double) * ((size_t)rb * 8 * LS + MM_TG * LS + 2 * LS * MM_TG + MM_WARPS * MM_TG) +
+           sizeof(int) * (rows + L + MM_TG);
 }
 
 }  // namespace
 
 TileShape tile_shape(const DevGrid& g, int P) {
     TileShape s{};
-    s.ok = P <= GT_PMAX;
-    s.B = std::max(1, 20 - P);
+    // P <= 16: B = 20 - P (L = 19; CUDA-core or tensor-core kernel);
+    // 16 < P <= 20: B = 24 - P (L = 23; tensor-core kernel only)
+    s.ok = P <= 20;
+    s.B = P <= GT_PMAX ? std::max(1, 20 - P) : std::max(1, 24 - P);
     s.L = s.B + P - 1;
     for (int ax = 0; ax < 3; ++ax) s.nt[ax] = (g.n[ax] + s.B - 1) / s.B;
     s.ntiles = (int64_t)s.nt[0] * s.nt[1] * s.nt[2];
@@ -350,13 +354,14 @@ void launch_gather_tile(const DevGrid& g, int P, const TileShape& s, const doubl
         const char* e = getenv("SEWALD_GATHER_MMA");
         return !(e && e[0] == '0');
     }();
-    if (use_mma && s.L == MM_L) {
-        const size_t sm = mma_smem_bytes();
-        cudaFuncSetAttribute(gather_tile_mma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if ((use_mma || P > GT_PMAX) && (s.L == 19 || s.L == 23)) {
+        const size_t sm = mma_smem_bytes(s.L);
+        auto kern = s.L == 19 ? gather_tile_mma_kernel<19> : gather_tile_mma_kernel<23>;
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         for (int64_t a = t0; a < t1; a += (int64_t)1 << 30) {
             const int64_t n = std::min<int64_t>(t1 - a, (int64_t)1 << 30);
-            gather_tile_mma_kernel<<<(unsigned)n, MM_THREADS, sm, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W,
-                                                                         SW, off, grid, h3, accumulate, u);
+            kern<<<(unsigned)n, MM_THREADS, sm, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W, SW, off, grid, h3,
+                                                      accumulate, u);
         }
         return;
     }
