@@ -59,30 +59,47 @@ __global__ void sweep_bucket_kernel(DevGrid g, int P, const double* __restrict__
 // not once per tile): the P window taps of each axis with the reference's
 // per-tap formula (fourier.cpp:181-186), the wrapped stencil starts, and the
 // strength components (stresslet: q_l nu_m, fourier.cpp:253-258).
-__global__ void sweep_weights_kernel(DevGrid g, DevWindow win, const double* __restrict__ x,
-                                     const double* __restrict__ f, const double* __restrict__ nu, int stresslet,
-                                     const uint32_t* __restrict__ order, int64_t N, double* __restrict__ W,
-                                     int4* __restrict__ SW, double* __restrict__ STR) {
-    const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (k >= N) return;
-    const int64_t i = order[k];
-    const int P = win.P;
-    int sw[3];
-    for (int ax = 0; ax < 3; ++ax) {
-        int j0;
-        double rel;
-        stencil_origin(g, P, ax, x[3 * i + ax], j0, rel);
-        double* w = W + (k * 3 + ax) * P;
-        for (int p = 0; p < P; ++p) w[p] = window_eval(win, ((double)(j0 + p) - rel) * g.h);
-        sw[ax] = ax < g.d ? wrapi(j0, g.n[ax]) : j0;
+constexpr int SWW_PTS = 64;  // points per block of the weights kernel
+
+__global__ void __launch_bounds__(SWW_PTS)
+sweep_weights_kernel(DevGrid g, DevWindow win, const double* __restrict__ x, const double* __restrict__ f,
+                     const double* __restrict__ nu, int stresslet, const uint32_t* __restrict__ order, int64_t N,
+                     double* __restrict__ W, int4* __restrict__ SW, double* __restrict__ STR) {
+    // thread per point (all lanes evaluate the same tap index: uniform
+    // window-coefficient reads), taps staged in shared memory and written
+    // back as one contiguous, coalesced block of rows
+    extern __shared__ double stage[];  // [SWW_PTS][3P + 1]
+    const int P = win.P, row = 3 * P + 1;
+    const int64_t k0 = (int64_t)blockIdx.x * SWW_PTS;
+    const int64_t k = k0 + threadIdx.x;
+    if (k < N) {
+        const int64_t i = order[k];
+        int sw[3];
+        for (int ax = 0; ax < 3; ++ax) {
+            int j0;
+            double rel;
+            stencil_origin(g, P, ax, x[3 * i + ax], j0, rel);
+            double* w = stage + threadIdx.x * row + ax * P;
+            for (int p = 0; p < P; ++p) w[p] = window_eval(win, ((double)(j0 + p) - rel) * g.h);
+            sw[ax] = ax < g.d ? wrapi(j0, g.n[ax]) : j0;
+        }
+        SW[k] = make_int4(sw[0], sw[1], sw[2], (int)i);
+        if (f) {
+            if (!stresslet) {
+                for (int c = 0; c < 3; ++c) STR[k * 3 + c] = f[3 * i + c];
+            } else {
+                for (int l = 0; l < 3; ++l)
+                    for (int m = 0; m < 3; ++m) STR[k * 9 + 3 * l + m] = f[3 * i + l] * nu[3 * i + m];
+            }
+        }
     }
-    SW[k] = make_int4(sw[0], sw[1], sw[2], (int)i);
-    if (!f) return;
-    if (!stresslet) {
-        for (int c = 0; c < 3; ++c) STR[k * 3 + c] = f[3 * i + c];
-    } else {
-        for (int l = 0; l < 3; ++l)
-            for (int m = 0; m < 3; ++m) STR[k * 9 + 3 * l + m] = f[3 * i + l] * nu[3 * i + m];
+    __syncthreads();
+    const int npts = (int)min((int64_t)SWW_PTS, N - k0);
+    const int tot = npts * 3 * P;
+    double* dst = W + k0 * 3 * P;
+    for (int e = threadIdx.x; e < tot; e += SWW_PTS) {
+        const int pt = e / (3 * P), q = e - pt * 3 * P;
+        dst[e] = stage[pt * row + q];
     }
 }
 
@@ -498,8 +515,10 @@ void launch_sweep_weights(const DevGrid& g, const DevWindow& w, const double* x,
                           int stresslet, const uint32_t* order, int64_t N, double* W, int4* SW, double* STR,
                           cudaStream_t st) {
     if (N == 0) return;
-    sweep_weights_kernel<<<(unsigned)((N + 127) / 128), 128, 0, st>>>(g, w, x, f, nu, stresslet, order, N, W, SW,
-                                                                       STR);
+    const size_t smem = sizeof(double) * SWW_PTS * (3 * w.P + 1);
+    if (smem > 48 * 1024) cudaFuncSetAttribute(sweep_weights_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    sweep_weights_kernel<<<(unsigned)((N + SWW_PTS - 1) / SWW_PTS), SWW_PTS, smem, st>>>(g, w, x, f, nu, stresslet,
+                                                                                         order, N, W, SW, STR);
 }
 
 int launch_spread_sweep(const DevGrid& g, int P, const double* W, const int4* SW, const double* STR, int C,
