@@ -412,7 +412,27 @@ const uint32_t* target_order(sewald_gpu_session* s) {
 // Targets bucketed / sorted for the tiled gather (P <= 20) or the z-sweep
 // gather (P > 20), with their window taps. Returns 0 (warp-per-target
 // gather), 1 (sweep) or 2 (tiles). SEWALD_GATHER=warp|sweep|tile forces one.
-int ensure_gather_order(sewald_gpu_session* s) {
+// Window taps of the targets in the tiles of part `part` of `nparts` (the tile
+// range evaluate() gathers); the sorted-index window is read on the device.
+void ensure_gather_weights(sewald_gpu_session* s, int mode, int part, int nparts) {
+    const int key = nparts == 1 ? 0 : part * 4096 + nparts;
+    if (s->tg_wpart == key) return;
+    const SweepShape sh = sweep_shape(s->g, s->p.P);
+    const TileShape ts = tile_shape(s->g, s->p.P);
+    const int64_t nt = mode == 1 ? (int64_t)sh.nbx * sh.nby : ts.ntiles;
+    // the sweep buckets tile (x, y) patches over all z starts; the tile path tiles
+    const int64_t per = mode == 1 ? (int64_t)s->g.n[2] : 1;
+    const int64_t t0 = nt * part / nparts, t1 = nt * (part + 1) / nparts;
+    const int64_t* off = s->tg_off.as<int64_t>();
+    const double* xt = s->same ? s->x.as<double>() : s->xt.as<double>();
+    launch_sweep_weights(s->g, s->w, xt, nullptr, nullptr, 0, s->tg_order.as<uint32_t>(), s->Nt, s->tg_w.as<double>(),
+                         s->tg_sw.as<int4>(), nullptr, s->ctx->stream, nparts == 1 ? nullptr : off + t0 * per,
+                         nparts == 1 ? nullptr : off + t1 * per);
+    ++s->ctx->launches;
+    s->tg_wpart = key;
+}
+
+int ensure_gather_order(sewald_gpu_session* s, int part, int nparts) {
     static const int forced = [] {
         const char* e = getenv("SEWALD_GATHER");
         if (!e) return -1;
@@ -427,7 +447,10 @@ int ensure_gather_order(sewald_gpu_session* s) {
     if (mode == 2 && !ts.ok) mode = sh.ok ? 1 : 0;
     if (mode == 1 && !sh.ok) mode = 0;
     if (mode == 0) return 0;
-    if (s->tg_ready && s->tg_mode == mode) return mode;
+    if (s->tg_ready && s->tg_mode == mode) {
+        ensure_gather_weights(s, mode, part, nparts);
+        return mode;
+    }
     cudaStream_t st = s->ctx->stream;
     const int64_t Nt = s->Nt;
     const double* xt = s->same ? s->x.as<double>() : s->xt.as<double>();
@@ -451,11 +474,11 @@ int ensure_gather_order(sewald_gpu_session* s) {
         sort_pairs(s, s->tg_keys.as<uint32_t>(), s->tg_keys2.as<uint32_t>(), s->tg_vals.as<uint32_t>(),
                    s->tg_order.as<uint32_t>(), Nt, bits_for((uint64_t)nkeys + 1));
     launch_bucket_offsets(s->tg_keys2.as<uint32_t>(), Nt, (int)nkeys, s->tg_off.as<int64_t>(), st);
-    launch_sweep_weights(s->g, s->w, xt, nullptr, nullptr, 0, s->tg_order.as<uint32_t>(), Nt, s->tg_w.as<double>(),
-                         s->tg_sw.as<int4>(), nullptr, st);
-    s->ctx->launches += 3;
+    s->ctx->launches += 2;
     s->tg_ready = true;
     s->tg_mode = mode;
+    s->tg_wpart = -1;
+    ensure_gather_weights(s, mode, part, nparts);
     return mode;
 }
 
@@ -743,7 +766,7 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
     }
     if (parts & 1) {
         const double h3 = s->p.h * s->p.h * s->p.h;
-        const int gmode = ensure_gather_order(s);
+        const int gmode = ensure_gather_order(s, part, nparts);
         if (gmode == 1) {
             if (first) cuda_check(cudaMemsetAsync(u, 0, sizeof(double) * 3 * Nt, st), "u zero");
             launch_gather_sweep(s->g, s->p.P, s->tg_w.as<double>(), s->tg_sw.as<int4>(), s->tg_off.as<int64_t>(),

@@ -77,7 +77,7 @@ void launch_sweep_bucket(const DevGrid& g, int P, const double* x, int64_t N, co
 // SW: N int4, STR: N*C).
 void launch_sweep_weights(const DevGrid& g, const DevWindow& w, const double* x, const double* f, const double* nu,
                           int stresslet, const uint32_t* order, int64_t N, double* W, int4* SW, double* STR,
-                          cudaStream_t st);
+                          cudaStream_t st, const int64_t* klo = nullptr, const int64_t* khi = nullptr);
 // Returns the number of kernel launches issued.
 int launch_spread_sweep(const DevGrid& g, int P, const double* W, const int4* SW, const double* STR, int C,
                         const int64_t* off, const SweepShape& s, double* out, cudaStream_t st);

@@ -64,7 +64,8 @@ constexpr int SWW_PTS = 64;  // points per block of the weights kernel
 __global__ void __launch_bounds__(SWW_PTS)
 sweep_weights_kernel(DevGrid g, DevWindow win, const double* __restrict__ x, const double* __restrict__ f,
                      const double* __restrict__ nu, int stresslet, const uint32_t* __restrict__ order, int64_t N,
-                     double* __restrict__ W, int4* __restrict__ SW, double* __restrict__ STR) {
+                     double* __restrict__ W, int4* __restrict__ SW, double* __restrict__ STR,
+                     const int64_t* __restrict__ klo, const int64_t* __restrict__ khi) {
     // thread per point (all lanes evaluate the same tap index: uniform
     // window-coefficient reads), taps staged in shared memory and written
     // back as one contiguous, coalesced block of rows
@@ -72,7 +73,10 @@ sweep_weights_kernel(DevGrid g, DevWindow win, const double* __restrict__ x, con
     const int P = win.P, row = 3 * P + 1;
     const int64_t k0 = (int64_t)blockIdx.x * SWW_PTS;
     const int64_t k = k0 + threadIdx.x;
-    if (k < N) {
+    // optional sorted-index window (one rank's part of the targets)
+    const int64_t lo = klo ? *klo : 0, hi = khi ? *khi : N;
+    if (k0 + SWW_PTS <= lo || k0 >= hi) return;
+    if (k < N && k >= lo && k < hi) {
         const int64_t i = order[k];
         int sw[3];
         for (int ax = 0; ax < 3; ++ax) {
@@ -94,12 +98,13 @@ sweep_weights_kernel(DevGrid g, DevWindow win, const double* __restrict__ x, con
         }
     }
     __syncthreads();
-    const int npts = (int)min((int64_t)SWW_PTS, N - k0);
-    const int tot = npts * 3 * P;
-    double* dst = W + k0 * 3 * P;
+    const int64_t a = max(k0, lo), b = min(min(k0 + SWW_PTS, N), hi);
+    const int tot = (int)(b - a) * 3 * P;
+    double* dst = W + a * 3 * P;
+    const int off0 = (int)(a - k0);
     for (int e = threadIdx.x; e < tot; e += SWW_PTS) {
         const int pt = e / (3 * P), q = e - pt * 3 * P;
-        dst[e] = stage[pt * row + q];
+        dst[e] = stage[(off0 + pt) * row + q];
     }
 }
 
@@ -513,12 +518,12 @@ void launch_sweep_bucket(const DevGrid& g, int P, const double* x, int64_t N, co
 
 void launch_sweep_weights(const DevGrid& g, const DevWindow& w, const double* x, const double* f, const double* nu,
                           int stresslet, const uint32_t* order, int64_t N, double* W, int4* SW, double* STR,
-                          cudaStream_t st) {
+                          cudaStream_t st, const int64_t* klo, const int64_t* khi) {
     if (N == 0) return;
     const size_t smem = sizeof(double) * SWW_PTS * (3 * w.P + 1);
     if (smem > 48 * 1024) cudaFuncSetAttribute(sweep_weights_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     sweep_weights_kernel<<<(unsigned)((N + SWW_PTS - 1) / SWW_PTS), SWW_PTS, smem, st>>>(g, w, x, f, nu, stresslet,
-                                                                                         order, N, W, SW, STR);
+                                                                                         order, N, W, SW, STR, klo, khi);
 }
 
 int launch_spread_sweep(const DevGrid& g, int P, const double* W, const int4* SW, const double* STR, int C,
