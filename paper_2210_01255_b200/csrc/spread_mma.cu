@@ -143,6 +143,103 @@ spread_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
     }
 }
 
+// Wide windows (20 < P <= 32, e.g. the Gaussian window of c4 at P = 32):
+// B = 8, region L = P + 7 <= 39, z padded to LS = 40 (5 n-blocks). The whole
+// tile's source tables stay in shared memory (up to WT_TMAX sources per pass),
+// each warp owns whole row blocks and sweeps all sources for them with every
+// n-block in flight, then flushes the row block with fp64 RED. Sources beyond
+// WT_TMAX per tile are handled in further passes (more RED, same result).
+constexpr int WT_TMAX = 128;
+constexpr int WT_LS = 40;
+constexpr int WT_WARPS = 16;
+
+template <int L>
+__global__ void __launch_bounds__(32 * WT_WARPS)
+spread_tile_mma_wide_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64_t tile0,
+                            const double* __restrict__ W, const int4* __restrict__ SW,
+                            const double* __restrict__ STR, int C, const int64_t* __restrict__ off,
+                            double* __restrict__ out) {
+    constexpr int ROWS = L * L;
+    constexpr int RB = (ROWS + 7) / 8;
+    constexpr int NB = WT_LS / 8;
+    extern __shared__ __align__(16) double wsm[];
+    double(*wxf)[WT_LS] = reinterpret_cast<double(*)[WT_LS]>(wsm);                       // f_t wx_t(a)
+    double(*wx)[WT_LS] = reinterpret_cast<double(*)[WT_LS]>(wsm + WT_TMAX * WT_LS);      // wx_t(a)
+    double(*wy)[WT_LS] = reinterpret_cast<double(*)[WT_LS]>(wsm + 2 * WT_TMAX * WT_LS);  // wy_t(b)
+    double(*wz)[WT_LS] = reinterpret_cast<double(*)[WT_LS]>(wsm + 3 * WT_TMAX * WT_LS);  // wz_t(z)
+
+    const int64_t tile = tile0 + blockIdx.x;
+    const int64_t p0 = off[tile], p1 = off[tile + 1];
+    if (p0 >= p1) return;
+    const int tz = (int)(tile % ntz);
+    const int ty = (int)((tile / ntz) % nty);
+    const int tx = (int)(tile / ((int64_t)ntz * nty));
+    const int X0 = tx * B, Y0 = ty * B, Z0 = tz * B;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t cs = (int64_t)g.n[0] * g.n[1] * g.n[2];
+
+    for (int64_t q0 = p0; q0 < p1; q0 += WT_TMAX) {
+        const int T = (int)min((int64_t)WT_TMAX, p1 - q0);
+        const int T4 = (T + 3) & ~3;
+        __syncthreads();
+        for (int t = warp; t < T4; t += WT_WARPS) {
+            int4 sw = make_int4(0, 0, 0, 0);
+            if (t < T) sw = SW[q0 + t];
+            for (int k = lane; k < WT_LS; k += 32) {
+                double vx = 0.0, vy = 0.0, vz = 0.0;
+                if (t < T && k < L) {
+                    const double* w = W + (q0 + t) * 3 * P;
+                    const int kx = k - (sw.x - X0), ky = k - (sw.y - Y0), kz = k - (sw.z - Z0);
+                    if (kx >= 0 && kx < P) vx = __ldg(w + kx);
+                    if (ky >= 0 && ky < P) vy = __ldg(w + P + ky);
+                    if (kz >= 0 && kz < P) vz = __ldg(w + 2 * P + kz);
+                }
+                wx[t][k] = vx;
+                wy[t][k] = vy;
+                wz[t][k] = vz;
+            }
+        }
+        for (int c = 0; c < C; ++c) {
+            __syncthreads();
+            for (int e = threadIdx.x; e < T4 * WT_LS; e += 32 * WT_WARPS) {
+                const int t = e / WT_LS, k = e - t * WT_LS;
+                wxf[t][k] = t < T ? STR[(q0 + t) * C + c] * wx[t][k] : 0.0;
+            }
+            __syncthreads();
+            double* oc = out + (int64_t)c * cs;
+            for (int rb = warp; rb < RB; rb += WT_WARPS) {
+                const int row = rb * 8 + (lane >> 2);
+                const int a = row / L, b = row - a * L;
+                double acc[NB][2];
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb) acc[nb][0] = acc[nb][1] = 0.0;
+                for (int ks = 0; ks < T4 / 4; ++ks) {
+                    const int t = ks * 4 + (lane & 3);
+                    const double af = wxf[t][a] * wy[t][b];
+#pragma unroll
+                    for (int nb = 0; nb < NB; ++nb) dmma(acc[nb][0], acc[nb][1], af, wz[t][nb * 8 + (lane >> 2)]);
+                }
+                if (row >= ROWS) continue;
+                int gx = X0 + a, gy = Y0 + b;
+                if (g.d > 0) gx %= g.n[0]; else if (gx >= g.n[0]) continue;
+                if (g.d > 1) gy %= g.n[1]; else if (gy >= g.n[1]) continue;
+                double* col = oc + ((int64_t)gx * g.n[1] + gy) * g.n[2];
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int z = nb * 8 + 2 * (lane & 3) + h;
+                        if (z >= L) continue;
+                        int gz = Z0 + z;
+                        if (g.d > 2) gz %= g.n[2]; else if (gz >= g.n[2]) continue;
+                        const double v = acc[nb][h];
+                        if (v != 0.0) atomicAdd(col + gz, v);
+                    }
+            }
+        }
+    }
+}
+
 }  // namespace
 
 SpreadMmaShape spread_mma_shape(const DevGrid& g, int P) {
@@ -152,6 +249,15 @@ SpreadMmaShape spread_mma_shape(const DevGrid& g, int P) {
         return e ? atoi(e) : 23;
     }();
     s.L = Lenv == 19 ? 19 : 23;
+    if (P > 20 && P <= 32) {  // wide windows: B = 8, L = P + 7 (spread_tile_mma_wide_kernel)
+        s.ok = (int64_t)g.n[0] * g.n[1] * g.n[2] < (int64_t(1) << 31);
+        s.B = 8;
+        s.L = P + 7;
+        for (int ax = 0; ax < 3; ++ax) s.nt[ax] = (g.n[ax] + s.B - 1) / s.B;
+        s.ntiles = (int64_t)s.nt[0] * s.nt[1] * s.nt[2];
+        if (s.ntiles >= (int64_t(1) << 31)) s.ok = false;
+        return s;
+    }
     // The region work is fixed by L (L^2 x 24 per 32 sources) while the sweep's
     // shrinks as P^3: measured, the tensor-core form wins at P = 16 (c2: 4.9
     // vs 7.1 ms) and P = 18 (c3: 15.1 vs 23.2 ms) and loses at P = 14 (c5:
@@ -179,7 +285,14 @@ int launch_spread_mma(const DevGrid& g, int P, const SpreadMmaShape& s, const do
     cudaMemsetAsync(out, 0, sizeof(double) * C * (size_t)g.n[0] * g.n[1] * g.n[2], st);
     for (int64_t a = 0; a < s.ntiles; a += (int64_t)1 << 30) {
         const int64_t n = std::min<int64_t>(s.ntiles - a, (int64_t)1 << 30);
-        if (s.L == 23)
+        if (s.L > 23) {
+            const size_t sm = sizeof(double) * 4 * WT_TMAX * WT_LS;
+            auto kern = s.L <= 31 ? spread_tile_mma_wide_kernel<31>
+                                  : (s.L <= 35 ? spread_tile_mma_wide_kernel<35> : spread_tile_mma_wide_kernel<39>);
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            kern<<<(unsigned)n, 32 * WT_WARPS, sm, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W, SW, STR, C, off,
+                                                        out);
+        } else if (s.L == 23)
             spread_tile_mma_kernel<23><<<(unsigned)n, SM_THREADS, 0, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W,
                                                                            SW, STR, C, off, out);
         else

@@ -426,3 +426,35 @@ def test_d0_slab_solve_emulated(S, world, kind, table):
     torch.cuda.synchronize()
     assert rel_rms(u.cpu().numpy(), u_ref.cpu().numpy()) < 1e-13
     sess.close()
+
+
+@pytest.mark.oracle
+@pytest.mark.parametrize("P", [8, 12, 14, 16, 18, 20, 24, 28, 32])
+@pytest.mark.parametrize("d,kind,window", [(3, 0, 1), (1, 1, 2), (2, 2, 1)])
+def test_live_spread_gather_widths(S, ref, P, d, kind, window):
+    """Spread and gather stages across window widths: every kernel family
+    (z-sweep, tensor-core tiles with L = 19 / 23 / 31-39, CUDA-core tiles) and
+    periodic / free axes, against the reference's spread / gather."""
+    rng = np.random.default_rng(4000 + P + 10 * d)
+    L = (1.0, 1.0, 1.0)
+    N = 700
+    x = np.empty((N, 3))
+    for ax in range(3):
+        x[:, ax] = rng.random(N) if ax < d else rng.uniform(0.05, 0.95, N)
+    f = rng.standard_normal((N, 3))
+    nu = rng.standard_normal((N, 3)) if kind == 1 else None
+    cell = S.Cell(L)
+    grid = S.build_grid(cell, d, 1.0 / 40, P, S.Kernel(kind), 4)
+    params = S.EwaldParams(S.Kernel(kind), d, 8.0, 0.2, 0.5, grid, S.WindowSpec.make(S.WindowKind(window), P, grid.h))
+    sysm = S.SourceSystem(S.Kernel(kind), cell, d, x, f, nu)
+    rp = ref.params_from(params.to_c())
+    g_gpu = S.spread(sysm, params)
+    g_ref = ref.spread(rp, x, f, nu)
+    assert np.max(np.abs(g_gpu - g_ref)) <= 1e-13 * np.max(np.abs(g_ref)), P
+    field = rng.standard_normal((3,) + tuple(grid.M_ext))
+    xt = np.empty((500, 3))
+    for ax in range(3):
+        xt[:, ax] = rng.random(500) if ax < d else rng.uniform(0.05, 0.95, 500)
+    u_gpu = S.gather(field, params, S.TargetSet(xt, False))
+    u_ref = ref.gather(rp, field, xt)
+    assert np.max(np.abs(u_gpu - u_ref)) <= 1e-13 * np.max(np.abs(u_ref)), P
