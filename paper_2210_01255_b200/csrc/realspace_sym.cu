@@ -125,8 +125,9 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     // (stride 80 B / 112 B: conflict-free per quarter warp).
     constexpr int RS = (3 + NS + 3 + 1) & ~1;
     constexpr int RO = RS - 4;  // reaction offset
-    // branch-free steps pay off for the cheaper kernels (c2 -1.5 %), not for the stresslet
-    constexpr bool BF = SEWALD_SYM_BRANCHFREE && KIND != SEWALD_STRESSLET;
+    // branch-free steps (c2 -1.5 %, stresslet neutral); the branchy form is kept for
+    // flop counting (tools/gpu_probe3.sh builds with SEWALD_SYM_BRANCHFREE=0)
+    constexpr bool BF = SEWALD_SYM_BRANCHFREE;
     __shared__ __align__(16) double jrec_all[SYM_WARPS][32][RS];
     __shared__ long long jid_all[SYM_WARPS][32];
     __shared__ float4 jf_all[SYM_WARPS][32];  // fp32 positions for the candidate pass
