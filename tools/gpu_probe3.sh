@@ -1,6 +1,8 @@
 #!/bin/bash
 # Algorithmic fp64 flops per accepted pair: ncu op counters of the branchy
 # real-space variant (idle lanes do not execute), all six kernel variants.
+# Build it first: mkdir -p build/branchy/obj && make -C paper_2210_01255_b200/csrc \
+#   OUT=$PWD/build/branchy OBJ=$PWD/build/branchy/obj NVEXTRA=-DSEWALD_SYM_BRANCHFREE=0
 set -u
 TAG=${1:-p3}
 O=gpurun_out
