@@ -458,3 +458,31 @@ def test_live_spread_gather_widths(S, ref, P, d, kind, window):
     u_gpu = S.gather(field, params, S.TargetSet(xt, False))
     u_ref = ref.gather(rp, field, xt)
     assert np.max(np.abs(u_gpu - u_ref)) <= 1e-13 * np.max(np.abs(u_ref)), P
+
+
+@pytest.mark.oracle
+@pytest.mark.parametrize("P", [16, 18, 24])
+def test_live_clustered_sources(S, ref, P):
+    """Thousands of points inside a few grid cells: one tile holds many
+    source / target groups (tensor-core spread and gather passes, dense cell
+    rows in the real-space sum)."""
+    rng = np.random.default_rng(777 + P)
+    N = 3000
+    x = 0.4 + 0.03 * rng.random((N, 3))
+    f = rng.standard_normal((N, 3))
+    cell = S.Cell((1.0, 1.0, 1.0))
+    grid = S.build_grid(cell, 3, 1.0 / 48, P, S.Kernel.stokeslet, 4)
+    params = S.EwaldParams(S.Kernel.stokeslet, 3, 10.0, 0.3, 0.5, grid,
+                           S.WindowSpec.make(S.WindowKind.pkb, P, grid.h))
+    sysm = S.SourceSystem(S.Kernel.stokeslet, cell, 3, x, f)
+    rp = ref.params_from(params.to_c())
+    g_gpu = S.spread(sysm, params)
+    g_ref = ref.spread(rp, x, f, None)
+    assert np.max(np.abs(g_gpu - g_ref)) <= 1e-13 * np.max(np.abs(g_ref))
+    field = rng.standard_normal((3,) + tuple(grid.M_ext))
+    u_gpu = S.gather(field, params, S.TargetSet(x, False))
+    u_ref = ref.gather(rp, field, x)
+    assert np.max(np.abs(u_gpu - u_ref)) <= 1e-13 * np.max(np.abs(u_ref))
+    u = S.full_potential(sysm, S.TargetSet.from_sources(sysm), params)
+    ur = ref.full_potential(rp, x, f, None, None, True)
+    assert rel_rms(u, ur) < TOL
