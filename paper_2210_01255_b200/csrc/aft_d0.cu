@@ -7,13 +7,15 @@
 // The reference transforms the whole padded box (2 M_ext per axis with the
 // table, s0 M_ext without) complex-to-complex and keeps the real part. Here:
 //   z: D2Z of the M_ext(0) x M_ext(1) input lines only (zero-padded in z),
-//   transpose to [c][kz][x][y] (x, y zero-padded: a resident zero block of
+//   transpose to [c][kz][y][x] (x, y zero-padded: a resident zero block of
 //   the out-of-place input buffer, never written),
 //   (x, y): one batched 2-D Z2Z over all (c, kz) slices, out of place,
 // scale, then the mirror passes (2-D inverse in place, transpose back of the
 // x < M_ext(0), y < M_ext(1) corner, Z2D, crop). The strided 1-D pass along x
 // that a [x][kz][y] layout needs runs at half the bandwidth of the 2-D plan
-// on B200 (tools/cpp/fft_plans.cu), hence the kz-major layout. Keeping Re of
+// on B200 (tools/cpp/fft_plans.cu), hence the kz-major layout; with x (960 at
+// c5) the contiguous axis the 2-D plan runs 1.94 ms vs 2.55 ms per component
+// (tools/fft_probe4.py). Keeping Re of
 // the C2C inverse equals applying the Hermitian part of the operator,
 // H(m) = (G(m) + conj G(-m)) / 2; with the table's Hermitian part Th and
 // k(-m) = -k~(m) (Nyquist components keep their sign) this is
@@ -22,7 +24,7 @@
 // the reference's real part.
 //
 // Layouts: input/output grid [c][x][y][z] (M_ext); R [c][x][y][n2] real;
-// Z [c][x][y][h2]; Tin/Tout [c][kz][x][y] with kz < h2, x < n0, y < n1.
+// Z [c][x][y][h2]; Tin/Tout [c][kz][y][x] with kz < h2, y < n1, x < n0 (x fastest).
 #include "engine.h"
 #include "aft_d0.h"
 #include "modified_kernels.cuh"
@@ -55,50 +57,51 @@ __global__ void d0_extract_kernel(const double* __restrict__ R, int64_t lines, i
     }
 }
 
-// Per (c, x) slab: Z[y][kz] (m1 x h2) <-> T[kz][x][y] (row stride n0 n1),
-// y < m1 only. grid (ceil(h2/32), ceil(m1/32), C*m0), block (32, 8).
+// Per (c, y) pair: Z[x][kz] (x < m0, stride m1 h2) <-> T[kz][y][x] (x fastest,
+// plane n1 n0). grid (ceil(h2/32), ceil(m0/32), C*m1), block (32, 8).
 template <bool FWD>
 __global__ void d0_transpose_kernel(cuDoubleComplex* __restrict__ Z, cuDoubleComplex* __restrict__ T, int m0, int m1,
                                     int n0, int n1, int h2) {
     __shared__ cuDoubleComplex tile[32][33];
-    const int cx = blockIdx.z;
-    const int c = cx / m0, x = cx - c * m0;
-    cuDoubleComplex* zs = Z + (int64_t)cx * m1 * h2;
+    const int cy = blockIdx.z;
+    const int c = cy / m1, y = cy - c * m1;
+    const int64_t zrow = (int64_t)m1 * h2;  // Z stride between x
+    cuDoubleComplex* zs = Z + ((int64_t)c * m0 * m1 + y) * h2;
     const int64_t plane = (int64_t)n0 * n1;
-    cuDoubleComplex* ts = T + (int64_t)c * h2 * plane + (int64_t)x * n1;
-    const int kz0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+    cuDoubleComplex* ts = T + (int64_t)c * h2 * plane + (int64_t)y * n0;
+    const int kz0 = blockIdx.x * 32, x0 = blockIdx.y * 32;
     if (FWD) {
         for (int i = threadIdx.y; i < 32; i += 8) {
-            const int y = y0 + i, kz = kz0 + threadIdx.x;
-            if (y < m1 && kz < h2) tile[i][threadIdx.x] = zs[(int64_t)y * h2 + kz];
+            const int x = x0 + i, kz = kz0 + threadIdx.x;
+            if (x < m0 && kz < h2) tile[i][threadIdx.x] = zs[x * zrow + kz];
         }
         __syncthreads();
         for (int i = threadIdx.y; i < 32; i += 8) {
-            const int kz = kz0 + i, y = y0 + threadIdx.x;
-            if (kz < h2 && y < m1) ts[kz * plane + y] = tile[threadIdx.x][i];
+            const int kz = kz0 + i, x = x0 + threadIdx.x;
+            if (kz < h2 && x < m0) ts[kz * plane + x] = tile[threadIdx.x][i];
         }
     } else {
         for (int i = threadIdx.y; i < 32; i += 8) {
-            const int kz = kz0 + i, y = y0 + threadIdx.x;
-            if (kz < h2 && y < m1) tile[threadIdx.x][i] = ts[kz * plane + y];
+            const int kz = kz0 + i, x = x0 + threadIdx.x;
+            if (kz < h2 && x < m0) tile[threadIdx.x][i] = ts[kz * plane + x];
         }
         __syncthreads();
         for (int i = threadIdx.y; i < 32; i += 8) {
-            const int y = y0 + i, kz = kz0 + threadIdx.x;
-            if (y < m1 && kz < h2) zs[(int64_t)y * h2 + kz] = tile[i][threadIdx.x];
+            const int x = x0 + i, kz = kz0 + threadIdx.x;
+            if (x < m0 && kz < h2) zs[x * zrow + kz] = tile[i][threadIdx.x];
         }
     }
 }
 
-// Th[kz][kx][ky] = (T(m) + conj T(-m)) / 2 from the full table [kx][ky][kz].
+// Th[kz][ky][kx] = (T(m) + conj T(-m)) / 2 from the full table [kx][ky][kz].
 __global__ void d0_herm_table_kernel(const cuDoubleComplex* __restrict__ T, int n0, int n1, int n2, int h2,
                                      cuDoubleComplex* __restrict__ Th) {
     const int64_t tot = (int64_t)n0 * h2 * n1;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-        const int ky = (int)(i % n1);
-        const int64_t t = i / n1;
-        const int kx = (int)(t % n0);
-        const int kz = (int)(t / n0);
+        const int kx = (int)(i % n0);
+        const int64_t t = i / n0;
+        const int ky = (int)(t % n1);
+        const int kz = (int)(t / n1);
         const int mx = kx == 0 ? 0 : n0 - kx, my = ky == 0 ? 0 : n1 - ky, mz = kz == 0 ? 0 : n2 - kz;
         const cuDoubleComplex a = T[((int64_t)kx * n1 + ky) * n2 + kz];
         const cuDoubleComplex b = T[((int64_t)mx * n1 + my) * n2 + mz];
@@ -123,10 +126,10 @@ __global__ void d0_scale_kernel(ModSpec spec, D0ScaleArgs a, double xi, cuDouble
     const int64_t n = (int64_t)a.n0 * a.h2 * a.n1;
     const int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (idx >= n) return;
-    const int ky = (int)(idx % a.n1);
-    const int64_t t = idx / a.n1;
-    const int kx = (int)(t % a.n0);
-    const int kz = a.kz0 + (int)(t / a.n0);  // a.h2 = kz count of this launch
+    const int kx = (int)(idx % a.n0);
+    const int64_t t = idx / a.n0;
+    const int ky = (int)(t % a.n1);
+    const int kz = a.kz0 + (int)(t / a.n1);  // a.h2 = kz count of this launch
     const double k0 = a.k0[kx], k1 = a.k1[ky], k2 = a.k2[kz];
     const double wp = a.w0[kx] * a.w1[ky] * a.w2[kz];
     const double kk = k0 * k0 + k1 * k1 + k2 * k2;
@@ -219,8 +222,9 @@ void D0Real::setup(const int m_[3], const int n_[3], int C_, cudaStream_t st) {
     mk(pz_f, 1, n + 2, e_n2, 1, n[2], e_h2, 1, h2, CUFFT_D2Z, lines_in);
     mk(pz_i, 1, n + 2, e_h2, 1, h2, e_n2, 1, n[2], CUFFT_Z2D, lines_out);
     const int64_t plane = (int64_t)n[0] * n[1];
-    mk(pxy_f, 2, n, n, 1, plane, n, 1, plane, CUFFT_Z2Z, (long long)C * h2);
-    mk(pxy_i, 2, n, n, 1, plane, n, 1, plane, CUFFT_Z2Z, (long long)3 * h2);
+    const int nyx[2] = {n[1], n[0]};  // [y][x] slices, x fastest
+    mk(pxy_f, 2, nyx, nyx, 1, plane, nyx, 1, plane, CUFFT_Z2Z, (long long)C * h2);
+    mk(pxy_i, 2, nyx, nyx, 1, plane, nyx, 1, plane, CUFFT_Z2Z, (long long)3 * h2);
     work.ensure(std::max<size_t>(ws, 16));
     for (auto h : plans) fft_check(cufftSetWorkArea(h, work.ptr), "work area");
 }
@@ -244,7 +248,7 @@ int D0Real::solve(const double* grid, const ModSpec& spec, int kind, double xi, 
     // forward
     d0_pad_z_kernel<<<blocks_for(lines_in * n[2]), 256, 0, st>>>(grid, lines_in, m[2], n[2], r);
     fft_check(cufftExecD2Z(pz_f, r, z), "d0 z forward");
-    const dim3 tb(32, 8), tg((h2 + 31) / 32, (m[1] + 31) / 32, C * m[0]);
+    const dim3 tb(32, 8), tg((h2 + 31) / 32, (m[0] + 31) / 32, C * m[1]);
     d0_transpose_kernel<true><<<tg, tb, 0, st>>>(z, ti, m[0], m[1], n[0], n[1], h2);
     fft_check(cufftExecZ2Z(pxy_f, ti, to, CUFFT_FORWARD), "d0 xy forward");
     launches += 2;  // own kernels only (cuFFT launches are library work)
@@ -266,7 +270,7 @@ int D0Real::solve(const double* grid, const ModSpec& spec, int kind, double xi, 
     ++launches;
     // inverse (3 flow components)
     fft_check(cufftExecZ2Z(pxy_i, to, to, CUFFT_INVERSE), "d0 xy inverse");
-    const dim3 tgi((h2 + 31) / 32, (m[1] + 31) / 32, 3 * m[0]);
+    const dim3 tgi((h2 + 31) / 32, (m[0] + 31) / 32, 3 * m[1]);
     d0_transpose_kernel<false><<<tgi, tb, 0, st>>>(z, to, m[0], m[1], n[0], n[1], h2);
     ++launches;
     fft_check(cufftExecZ2D(pz_i, z, r), "d0 z inverse");
@@ -302,25 +306,25 @@ __global__ void d0_pack_fwd_kernel(const cuDoubleComplex* __restrict__ Z, int C,
     }
 }
 
-// recv chunks p: [C][nxs_p][m1][nk] -> Tin [C][nk][n0][n1] (x < m0, y < m1)
+// recv chunks p: [C][nxs_p][m1][nk] -> Tin [C][nk][n1][n0] (x < m0, y < m1)
 __global__ void d0_unpack_mid_kernel(const cuDoubleComplex* __restrict__ recv, int C, int m0, int m1, int n0,
                                      int n1, int nk, SlabBounds xbd, cuDoubleComplex* __restrict__ Tin) {
-    const int64_t tot = (int64_t)C * nk * m0 * m1;
+    const int64_t tot = (int64_t)C * nk * m1 * m0;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < tot; i += (int64_t)gridDim.x * blockDim.x) {
-        const int y = (int)(i % m1);
-        int64_t t = i / m1;
-        const int x = (int)(t % m0);
-        t /= m0;
+        const int x = (int)(i % m0);
+        int64_t t = i / m0;
+        const int y = (int)(t % m1);
+        t /= m1;
         const int kl = (int)(t % nk);
         const int c = (int)(t / nk);
         const int p = owner_of(xbd, x);
         const int xa = xbd.b[p], nxs = xbd.b[p + 1] - xa;
         const int64_t src = (int64_t)C * m1 * nk * xa + (((int64_t)c * nxs + (x - xa)) * m1 + y) * nk + kl;
-        Tin[(((int64_t)c * nk + kl) * n0 + x) * n1 + y] = recv[src];
+        Tin[(((int64_t)c * nk + kl) * n1 + y) * n0 + x] = recv[src];
     }
 }
 
-// Tout [3][nk][n0][n1] (x < m0, y < m1) -> send chunks q: [3][nk][nxs_q][m1]
+// Tout [3][nk][n1][n0] (x < m0, y < m1) -> send chunks q: [3][nk][nxs_q][m1]
 __global__ void d0_pack_mid_kernel(const cuDoubleComplex* __restrict__ Tout, int m0, int m1, int n0, int n1,
                                    int nk, SlabBounds xbd, cuDoubleComplex* __restrict__ send) {
     const int64_t tot = (int64_t)3 * nk * m0 * m1;
@@ -331,7 +335,7 @@ __global__ void d0_pack_mid_kernel(const cuDoubleComplex* __restrict__ Tout, int
         const int64_t ck = t / m0;  // c * nk + kl
         const int q = owner_of(xbd, x);
         const int xa = xbd.b[q], nxs = xbd.b[q + 1] - xa;
-        send[(int64_t)3 * nk * m1 * xa + (ck * nxs + (x - xa)) * m1 + y] = Tout[(ck * n0 + x) * n1 + y];
+        send[(int64_t)3 * nk * m1 * xa + (ck * nxs + (x - xa)) * m1 + y] = Tout[(ck * n1 + y) * n0 + x];
     }
 }
 
@@ -396,8 +400,9 @@ void D0Real::slab_plans(int nxs, int nk, cudaStream_t st) {
         mk(S.pz_i, 1, n + 2, 1, h2, 1, n[2], CUFFT_Z2D, lout, e_h2, e_n2);
     }
     if (nk > 0) {
-        mk(S.pxy_f, 2, n, 1, plane, 1, plane, CUFFT_Z2Z, (long long)C * nk, n, n);
-        mk(S.pxy_i, 2, n, 1, plane, 1, plane, CUFFT_Z2Z, (long long)3 * nk, n, n);
+        const int nyx[2] = {n[1], n[0]};
+        mk(S.pxy_f, 2, nyx, 1, plane, 1, plane, CUFFT_Z2Z, (long long)C * nk, nyx, nyx);
+        mk(S.pxy_i, 2, nyx, 1, plane, 1, plane, CUFFT_Z2Z, (long long)3 * nk, nyx, nyx);
     }
     S.work.ensure(std::max<size_t>(ws, 16));
     for (auto h : S.plans) fft_check(cufftSetWorkArea(h, S.work.ptr), "work area");
