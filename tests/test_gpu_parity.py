@@ -486,3 +486,21 @@ def test_live_clustered_sources(S, ref, P):
     u = S.full_potential(sysm, S.TargetSet.from_sources(sysm), params)
     ur = ref.full_potential(rp, x, f, None, None, True)
     assert rel_rms(u, ur) < TOL
+
+
+@pytest.mark.oracle
+@pytest.mark.parametrize("kind", [0, 1, 2])
+def test_live_noncubic_d3(S, ref, kind):
+    """Triply periodic, non-cubic box (grid, tiles and cell rows differ per axis)."""
+    rng = np.random.default_rng(610 + kind)
+    L = (1.0, 2.0, 0.5)  # M = (40, 80, 20): a tile region (L = 23) wraps the z axis
+    N = 1500
+    x = rng.random((N, 3)) * np.asarray(L)
+    f = rng.standard_normal((N, 3))
+    nu = rng.standard_normal((N, 3)) if kind == 1 else None
+    sysm = S.SourceSystem(S.Kernel(kind), S.Cell(L), 3, x, f, nu)
+    sel = S.select_parameters(sysm.kind, 3, sysm.cell, S.source_quantity(sysm), 11.0, S.ToleranceSpec(1e-9))
+    rp = ref.params_from(sel.params.to_c())
+    u = S.full_potential(sysm, S.TargetSet.from_sources(sysm), sel.params)
+    ur = ref.full_potential(rp, x, f, nu, None, True)
+    assert rel_rms(u, ur) < TOL
