@@ -10,7 +10,7 @@
 // std::runtime_error).
 //
 // The per-file headers sewald/domain.h, estimates.h, grid.h, window.h,
-// fourier.h and realspace.h forward here.
+// modified_kernels.h, fourier.h and realspace.h forward here.
 #pragma once
 
 #include <array>
@@ -156,6 +156,21 @@ struct ParameterSelection {
 ParameterSelection select_parameters(Kernel kind, int d, const Cell& cell, double Q, double xi,
                                      const ToleranceSpec& tol, const SelectionOptions& opt = {});
 
+// ---- modified kernels (modified_kernels.h) ----------------------------------------
+struct ModifiedKernelSpec {
+    Kernel kind = Kernel::stokeslet;
+    int d = 0;
+    double R = 1.0;
+    double a_B = 0.0;
+    double b_B = 0.0;
+    double ell_H = 1.0;
+    double ell_B = 1.0;
+    double c_B = 0.0;
+    static ModifiedKernelSpec optimal(Kernel kind, int d, double R);
+};
+
+double truncation_radius(const std::array<double, 3>& L_ext, int d);
+
 // ---- Fourier part (fourier.h) ----------------------------------------------------
 struct RealField {
     std::array<int, 3> n{};
@@ -170,8 +185,23 @@ struct RealField {
     }
 };
 
-// The D = 0 kernel table is built and cached on the device per parameter set;
-// the struct is kept for source compatibility of SePipelineOptions::table.
+// Mixed-space coefficients (fourier.h:30-46): far / near / zero per mode class.
+struct FourierField {
+    int d = 3;
+    int comps = 0;
+    std::array<int, 3> n_per{1, 1, 1};
+    std::array<int, 3> n_far{1, 1, 1};
+    std::array<int, 3> n_near{1, 1, 1};
+    std::array<int, 3> n_zero{1, 1, 1};
+    std::vector<cplx> far;
+    std::vector<int> near_rows;
+    std::vector<cplx> near;
+    std::vector<cplx> zero;
+};
+
+// D = 0 kernel table (fourier.h:52-57). se_fourier_potential builds and caches
+// it on the device per parameter set; precompute_0p() returns it on the host
+// for the stage API.
 struct PrecomputedKernel0P {
     Kernel kind = Kernel::stokeslet;
     std::array<int, 3> n{};
@@ -185,6 +215,13 @@ struct SePipelineOptions {
 };
 
 RealField spread(const SourceSystem& system, const GridSpec& grid, const Window& window);
+FourierField aft_forward(const RealField& field, const GridSpec& grid, const UpsamplingPlan& plan);
+RealField aft_inverse(const FourierField& field, const GridSpec& grid, const UpsamplingPlan& plan);
+FourierField scale(const FourierField& field, const ModifiedKernelSpec& spec, double xi, const Window& window,
+                   const GridSpec& grid);
+FourierField scale(const FourierField& field, const PrecomputedKernel0P& pre, double xi, const Window& window,
+                   const GridSpec& grid);
+PrecomputedKernel0P precompute_0p(Kernel kind, const GridSpec& grid, double R);
 std::vector<Vec3> gather(const RealField& field, const GridSpec& grid, const Window& window,
                          const TargetSet& targets);
 std::vector<Vec3> se_fourier_potential(const SourceSystem& system, const TargetSet& targets,

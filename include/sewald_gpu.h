@@ -167,6 +167,71 @@ int sewald_gpu_spread(sewald_gpu_ctx* ctx, const sewald_params_c* p, const doubl
 int sewald_gpu_gather(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* grid,
                       const double* xt, int64_t Nt, double* u_out);
 
+/* ---- reference stage functions (fourier.h:59-74) -------------------- */
+/* FourierField (fourier.h:30-46) travels as this geometry plus three complex
+ * arrays of interleaved (re, im) doubles — the memory of the reference's
+ * std::vector<std::complex<double>> far / near / zero, so a C++ caller
+ * passes them zero-copy:
+ *   far  [comps][prod M_ext]                        (d = 1, 2, 3)
+ *   zero [comps][n_zero block]                      (d = 0: the whole s0-padded box)
+ *   near [comps][n_near_rows][n_near block]         (d = 1, 2)
+ * The per-row blocks are n_zero[1]*n_zero[2] (d = 1) or n_zero[2] (d = 2),
+ * likewise for near. *_len are complex element counts over all comps. */
+typedef struct sewald_fourier_geom_c {
+    int32_t d, comps;
+    int32_t n_per[3], n_far[3], n_near[3], n_zero[3];
+    int32_t n_near_rows;
+    int64_t far_len, near_len, zero_len;
+} sewald_fourier_geom_c;
+
+/* POD mirror of ModifiedKernelSpec (modified_kernels.h:10-21). */
+typedef struct sewald_modspec_c {
+    int32_t kind, d;
+    double R, a_B, b_B, ell_H, ell_B, c_B;
+} sewald_modspec_c;
+
+/* ModifiedKernelSpec::optimal (modified_kernels.cpp:52-63). */
+int sewald_modspec_optimal(int kind, int d, double R, sewald_modspec_c* out);
+
+/* Geometry aft_forward produces for a comps-component field on p's grid and
+ * upsampling plan (p->s0, p->s_star, p->k_star; the D = 0 precomputed-kernel
+ * pipeline sets p->s0 = 2, fourier.cpp:819-821). near_rows_out (may be NULL)
+ * receives n_near_rows ints: classify_rows (fourier.cpp:101-125). Host only. */
+int sewald_aft_geometry(const sewald_params_c* p, int comps, sewald_fourier_geom_c* g,
+                        int32_t* near_rows_out);
+
+/* aft_forward (fourier.h:61, fourier.cpp:311-416): field = g->comps *
+ * prod(M_ext) doubles (RealField layout); g must equal sewald_aft_geometry's.
+ * Unused arrays (e.g. near / zero for d = 3) may be NULL. */
+int sewald_gpu_aft_forward(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* field,
+                           const sewald_fourier_geom_c* g, double* far, double* near, double* zero);
+
+/* aft_inverse (fourier.h:62, fourier.cpp:418-520): field_out = g->comps *
+ * prod(M_ext) doubles. near_rows: g->n_near_rows ints (the field's own). */
+int sewald_gpu_aft_inverse(sewald_gpu_ctx* ctx, const sewald_params_c* p,
+                           const sewald_fourier_geom_c* g, const int32_t* near_rows,
+                           const double* far, const double* near, const double* zero,
+                           double* field_out);
+
+/* scale (fourier.h:66-67, fourier.cpp:522-666): the output field has the
+ * geometry g with comps = 3 (the stresslet contracts nine to three). The
+ * window is p's (its h must equal the grid's, fourier.cpp:155-158). */
+int sewald_gpu_scale(sewald_gpu_ctx* ctx, const sewald_params_c* p, const sewald_modspec_c* spec,
+                     double xi, const sewald_fourier_geom_c* g, const int32_t* near_rows,
+                     const double* far, const double* near, const double* zero, double* far_out,
+                     double* near_out, double* zero_out);
+
+/* scale with a PrecomputedKernel0P (fourier.h:68-69, fourier.cpp:668-720):
+ * table = prod(table_n) complex (interleaved); d = 0 only. */
+int sewald_gpu_scale_table(sewald_gpu_ctx* ctx, const sewald_params_c* p, int kind,
+                           const int32_t table_n[3], const double* table, double xi,
+                           const sewald_fourier_geom_c* g, const double* zero, double* zero_out);
+
+/* precompute_0p (fourier.h:74, fourier.cpp:722-803): n_out = 2 M_ext;
+ * table_out = prod(n_out) complex (interleaved), or NULL to query n_out. */
+int sewald_gpu_precompute_0p(sewald_gpu_ctx* ctx, const sewald_params_c* p, int kind, double R,
+                             int32_t n_out[3], double* table_out);
+
 /* ---- device-resident session (time stepping / multi-GPU plumbing) ---- */
 /* A session keeps sources, targets, sort permutations, grids and cuFFT plans
  * resident in HBM between calls. All pointers given to *_dev calls are

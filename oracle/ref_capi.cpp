@@ -395,6 +395,117 @@ int ref_precompute_0p(const sewald_params_c* p, double* table_out, int32_t* n_ou
     });
 }
 
+// ---- stage functions (fourier.h:61-74) on one held FourierField ----------
+// ref_aft_forward / ref_field_set load it, ref_scale / ref_scale_table
+// replace it by its scaled copy, ref_field_get / ref_aft_inverse read it.
+// Arrays cross as interleaved (re, im) doubles with the geometry of
+// sewald_fourier_geom_c (include/sewald_gpu.h).
+namespace {
+FourierField g_field;
+
+void field_geom(const FourierField& F, sewald_fourier_geom_c* g) {
+    std::memset(g, 0, sizeof(*g));
+    g->d = F.d;
+    g->comps = F.comps;
+    for (int i = 0; i < 3; ++i) {
+        g->n_per[i] = F.n_per[i];
+        g->n_far[i] = F.n_far[i];
+        g->n_near[i] = F.n_near[i];
+        g->n_zero[i] = F.n_zero[i];
+    }
+    g->n_near_rows = static_cast<int32_t>(F.near_rows.size());
+    g->far_len = static_cast<int64_t>(F.far.size());
+    g->near_len = static_cast<int64_t>(F.near.size());
+    g->zero_len = static_cast<int64_t>(F.zero.size());
+}
+
+void copy_in(std::vector<cplx>& v, const double* a, int64_t n) {
+    v.assign(static_cast<std::size_t>(n), cplx{});
+    if (n) std::memcpy(v.data(), a, sizeof(double) * 2 * n);
+}
+void copy_out(const std::vector<cplx>& v, double* a) {
+    if (a && !v.empty()) std::memcpy(a, v.data(), sizeof(double) * 2 * v.size());
+}
+}  // namespace
+
+int ref_aft_forward(const sewald_params_c* p, const double* field, int comps, sewald_fourier_geom_c* g) {
+    return guarded([&] {
+        EwaldParams e = from_c(p);
+        RealField phi = RealField::zeros(e.grid.M_ext, comps);
+        std::memcpy(phi.v.data(), field, sizeof(double) * phi.v.size());
+        g_field = aft_forward(phi, e.grid, e.upsampling);
+        field_geom(g_field, g);
+    });
+}
+
+int ref_field_get(sewald_fourier_geom_c* g, int32_t* near_rows, double* far, double* near, double* zero) {
+    return guarded([&] {
+        field_geom(g_field, g);
+        if (near_rows)
+            for (std::size_t i = 0; i < g_field.near_rows.size(); ++i) near_rows[i] = g_field.near_rows[i];
+        copy_out(g_field.far, far);
+        copy_out(g_field.near, near);
+        copy_out(g_field.zero, zero);
+    });
+}
+
+int ref_field_set(const sewald_fourier_geom_c* g, const int32_t* near_rows, const double* far, const double* near,
+                  const double* zero) {
+    return guarded([&] {
+        FourierField F;
+        F.d = g->d;
+        F.comps = g->comps;
+        for (int i = 0; i < 3; ++i) {
+            F.n_per[i] = g->n_per[i];
+            F.n_far[i] = g->n_far[i];
+            F.n_near[i] = g->n_near[i];
+            F.n_zero[i] = g->n_zero[i];
+        }
+        F.near_rows.assign(near_rows, near_rows + g->n_near_rows);
+        copy_in(F.far, far, g->far_len);
+        copy_in(F.near, near, g->near_len);
+        copy_in(F.zero, zero, g->zero_len);
+        g_field = std::move(F);
+    });
+}
+
+int ref_scale(const sewald_params_c* p, const sewald_modspec_c* m, double xi, sewald_fourier_geom_c* g) {
+    return guarded([&] {
+        EwaldParams e = from_c(p);
+        ModifiedKernelSpec spec;
+        spec.kind = to_kernel(m->kind);
+        spec.d = m->d;
+        spec.R = m->R;
+        spec.a_B = m->a_B;
+        spec.b_B = m->b_B;
+        spec.ell_H = m->ell_H;
+        spec.ell_B = m->ell_B;
+        spec.c_B = m->c_B;
+        const Window window(e.window);
+        g_field = scale(g_field, spec, xi, window, e.grid);
+        field_geom(g_field, g);
+    });
+}
+
+// scale with precompute_0p(kind, grid, R) (fourier.cpp:668-720, :722-803).
+int ref_scale_table(const sewald_params_c* p, int kind, double R, double xi, sewald_fourier_geom_c* g) {
+    return guarded([&] {
+        EwaldParams e = from_c(p);
+        const Window window(e.window);
+        PrecomputedKernel0P t = precompute_0p(to_kernel(kind), e.grid, R);
+        g_field = scale(g_field, t, xi, window, e.grid);
+        field_geom(g_field, g);
+    });
+}
+
+int ref_aft_inverse(const sewald_params_c* p, double* field_out) {
+    return guarded([&] {
+        EwaldParams e = from_c(p);
+        RealField out = aft_inverse(g_field, e.grid, e.upsampling);
+        std::memcpy(field_out, out.v.data(), sizeof(double) * out.v.size());
+    });
+}
+
 // Scalar kernel probes for restatement pinning.
 int ref_realspace_kernel(int kind, const double r[3], double xi, double* out27) {
     return guarded([&] {

@@ -50,6 +50,23 @@ DP = C.POINTER(C.c_double)
 I64 = C.c_int64
 PP = C.POINTER(RefParams)
 
+
+class RefGeom(C.Structure):
+    """sewald_fourier_geom_c (include/sewald_gpu.h) for the stage wrappers."""
+    _fields_ = [("d", C.c_int32), ("comps", C.c_int32),
+                ("n_per", C.c_int32 * 3), ("n_far", C.c_int32 * 3), ("n_near", C.c_int32 * 3),
+                ("n_zero", C.c_int32 * 3), ("n_near_rows", C.c_int32),
+                ("far_len", C.c_int64), ("near_len", C.c_int64), ("zero_len", C.c_int64)]
+
+
+class RefModSpec(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("d", C.c_int32), ("R", C.c_double), ("a_B", C.c_double),
+                ("b_B", C.c_double), ("ell_H", C.c_double), ("ell_B", C.c_double), ("c_B", C.c_double)]
+
+
+GP = C.POINTER(RefGeom)
+IP32 = C.POINTER(C.c_int32)
+
 _SIGS = {
     "ref_last_error": (C.c_char_p, []),
     "ref_last_seconds": (None, [DP]),
@@ -69,6 +86,12 @@ _SIGS = {
     "ref_full_potential": (C.c_int, [PP, DP, DP, DP, I64, DP, I64, C.c_int, C.c_int, DP]),
     "ref_full_split": (C.c_int, [PP, DP, DP, DP, I64, DP, I64, C.c_int, C.c_int, C.c_int, DP]),
     "ref_precompute_0p": (C.c_int, [PP, DP, C.POINTER(C.c_int32)]),
+    "ref_aft_forward": (C.c_int, [PP, DP, C.c_int, GP]),
+    "ref_field_get": (C.c_int, [GP, IP32, DP, DP, DP]),
+    "ref_field_set": (C.c_int, [GP, IP32, DP, DP, DP]),
+    "ref_scale": (C.c_int, [PP, C.POINTER(RefModSpec), C.c_double, GP]),
+    "ref_scale_table": (C.c_int, [PP, C.c_int, C.c_double, C.c_double, GP]),
+    "ref_aft_inverse": (C.c_int, [PP, DP]),
     "ref_realspace_kernel": (C.c_int, [C.c_int, DP, C.c_double, DP]),
     "ref_modified_kernel_hat": (C.c_int, [C.c_int, C.c_int, C.c_double, DP, DP]),
 }
@@ -272,3 +295,68 @@ def modified_kernel_hat(kind, d, R, k) -> np.ndarray:
     _chk(lib().ref_modified_kernel_hat(int(kind), int(d), float(R), _dp(k), _dp(out)))
     z = out[0::2] + 1j * out[1::2]
     return z[:9].reshape(3, 3) if kind != 1 else z.reshape(3, 3, 3)
+
+
+# ---- stage functions (fourier.h:61-74), FourierField as a dict ----------------
+# {"d", "comps", "n_per", "n_far", "n_near", "n_zero", "near_rows" (int32),
+#  "far", "near", "zero" (complex128, flat as the reference's vectors)}
+
+def _field_from_lib() -> dict:
+    g = RefGeom()
+    _chk(lib().ref_field_get(C.byref(g), None, None, None, None))
+    rows = np.zeros(max(g.n_near_rows, 1), dtype=np.int32)
+    arr = {k: np.zeros(2 * max(getattr(g, k + "_len"), 1)) for k in ("far", "near", "zero")}
+    _chk(lib().ref_field_get(C.byref(g), rows.ctypes.data_as(IP32), _dp(arr["far"]), _dp(arr["near"]),
+                             _dp(arr["zero"])))
+    out = {"d": g.d, "comps": g.comps, "n_per": tuple(g.n_per), "n_far": tuple(g.n_far),
+           "n_near": tuple(g.n_near), "n_zero": tuple(g.n_zero), "near_rows": rows[:g.n_near_rows].copy()}
+    for k in ("far", "near", "zero"):
+        n = getattr(g, k + "_len")
+        out[k] = arr[k][0:2 * n:2] + 1j * arr[k][1:2 * n:2]
+    return out
+
+
+def _field_to_lib(F: dict):
+    g = RefGeom()
+    g.d, g.comps = F["d"], F["comps"]
+    for i in range(3):
+        g.n_per[i], g.n_far[i], g.n_near[i], g.n_zero[i] = F["n_per"][i], F["n_far"][i], F["n_near"][i], F["n_zero"][i]
+    rows = np.ascontiguousarray(F["near_rows"], dtype=np.int32)
+    g.n_near_rows = rows.size
+    arrs = {}
+    for k in ("far", "near", "zero"):
+        a = np.ascontiguousarray(F[k], dtype=np.complex128)
+        setattr(g, k + "_len", a.size)
+        arrs[k] = a.view(np.float64) if a.size else np.zeros(1)
+    _chk(lib().ref_field_set(C.byref(g), rows.ctypes.data_as(IP32) if rows.size else None, _dp(arrs["far"]),
+                             _dp(arrs["near"]), _dp(arrs["zero"])))
+
+
+def aft_forward(p: RefParams, field) -> dict:
+    field = np.ascontiguousarray(field, dtype=np.float64)
+    g = RefGeom()
+    _chk(lib().ref_aft_forward(C.byref(p), _dp(field), int(field.shape[0]), C.byref(g)))
+    return _field_from_lib()
+
+
+def scale(p: RefParams, F: dict, spec: tuple, xi: float) -> dict:
+    """spec = (kind, d, R, a_B, b_B, ell_H, ell_B, c_B)."""
+    _field_to_lib(F)
+    m = RefModSpec(*spec)
+    g = RefGeom()
+    _chk(lib().ref_scale(C.byref(p), C.byref(m), float(xi), C.byref(g)))
+    return _field_from_lib()
+
+
+def scale_table(p: RefParams, F: dict, kind: int, R: float, xi: float) -> dict:
+    _field_to_lib(F)
+    g = RefGeom()
+    _chk(lib().ref_scale_table(C.byref(p), int(kind), float(R), float(xi), C.byref(g)))
+    return _field_from_lib()
+
+
+def aft_inverse(p: RefParams, F: dict) -> np.ndarray:
+    _field_to_lib(F)
+    out = np.zeros((F["comps"], p.M_ext[0], p.M_ext[1], p.M_ext[2]))
+    _chk(lib().ref_aft_inverse(C.byref(p), _dp(out)))
+    return out

@@ -51,6 +51,18 @@ class sewald_timings_c(C.Structure):
         ("kernel_launches", C.c_int64), ("realspace_pairs", C.c_int64)]
 
 
+class sewald_fourier_geom_c(C.Structure):
+    _fields_ = [("d", C.c_int32), ("comps", C.c_int32),
+                ("n_per", C.c_int32 * 3), ("n_far", C.c_int32 * 3), ("n_near", C.c_int32 * 3),
+                ("n_zero", C.c_int32 * 3), ("n_near_rows", C.c_int32),
+                ("far_len", C.c_int64), ("near_len", C.c_int64), ("zero_len", C.c_int64)]
+
+
+class sewald_modspec_c(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("d", C.c_int32), ("R", C.c_double), ("a_B", C.c_double),
+                ("b_B", C.c_double), ("ell_H", C.c_double), ("ell_B", C.c_double), ("c_B", C.c_double)]
+
+
 DP = C.POINTER(C.c_double)
 VP = C.c_void_p
 I64 = C.c_int64
@@ -86,6 +98,19 @@ _SIGS = [
                                                  C.c_int, C.c_double, C.c_double, C.c_int, DP]),
     ("sewald_gpu_spread", C.c_int, [VP, C.POINTER(sewald_params_c), DP, DP, DP, I64, DP]),
     ("sewald_gpu_gather", C.c_int, [VP, C.POINTER(sewald_params_c), DP, DP, I64, DP]),
+    ("sewald_modspec_optimal", C.c_int, [C.c_int, C.c_int, C.c_double, C.POINTER(sewald_modspec_c)]),
+    ("sewald_aft_geometry", C.c_int, [C.POINTER(sewald_params_c), C.c_int, C.POINTER(sewald_fourier_geom_c),
+                                      C.POINTER(C.c_int32)]),
+    ("sewald_gpu_aft_forward", C.c_int, [VP, C.POINTER(sewald_params_c), DP, C.POINTER(sewald_fourier_geom_c),
+                                         DP, DP, DP]),
+    ("sewald_gpu_aft_inverse", C.c_int, [VP, C.POINTER(sewald_params_c), C.POINTER(sewald_fourier_geom_c),
+                                         C.POINTER(C.c_int32), DP, DP, DP, DP]),
+    ("sewald_gpu_scale", C.c_int, [VP, C.POINTER(sewald_params_c), C.POINTER(sewald_modspec_c), C.c_double,
+                                   C.POINTER(sewald_fourier_geom_c), C.POINTER(C.c_int32), DP, DP, DP, DP, DP, DP]),
+    ("sewald_gpu_scale_table", C.c_int, [VP, C.POINTER(sewald_params_c), C.c_int, C.POINTER(C.c_int32), DP,
+                                         C.c_double, C.POINTER(sewald_fourier_geom_c), DP, DP]),
+    ("sewald_gpu_precompute_0p", C.c_int, [VP, C.POINTER(sewald_params_c), C.c_int, C.c_double,
+                                           C.POINTER(C.c_int32), DP]),
     ("sewald_gpu_session_create", C.c_int, [VP, C.POINTER(sewald_params_c), C.POINTER(VP)]),
     ("sewald_gpu_session_destroy", None, [VP]),
     ("sewald_gpu_session_set_sources", C.c_int, [VP, VP, VP, VP, I64]),

@@ -480,6 +480,173 @@ def gather(field: np.ndarray, params: EwaldParams, targets: TargetSet,
     return u
 
 
+# ---------------------------------------------------------------------------
+# reference stage functions (fourier.h:30-74)
+# ---------------------------------------------------------------------------
+
+
+@dataclass
+class ModifiedKernelSpec:
+    """struct ModifiedKernelSpec (modified_kernels.h:10-21)."""
+    kind: Kernel = Kernel.stokeslet
+    d: int = 0
+    R: float = 1.0
+    a_B: float = 0.0
+    b_B: float = 0.0
+    ell_H: float = 1.0
+    ell_B: float = 1.0
+    c_B: float = 0.0
+
+    @staticmethod
+    def optimal(kind: Kernel, d: int, R: float) -> "ModifiedKernelSpec":
+        """ModifiedKernelSpec::optimal (modified_kernels.cpp:52-63), via the C-ABI."""
+        m = _abi.sewald_modspec_c()
+        _host_call(_abi.load().sewald_modspec_optimal(int(kind), int(d), float(R), C.byref(m)))
+        return ModifiedKernelSpec(Kernel(m.kind), m.d, m.R, m.a_B, m.b_B, m.ell_H, m.ell_B, m.c_B)
+
+    def to_c(self):
+        return _abi.sewald_modspec_c(int(self.kind), int(self.d), float(self.R), float(self.a_B), float(self.b_B),
+                                     float(self.ell_H), float(self.ell_B), float(self.c_B))
+
+
+@dataclass
+class FourierField:
+    """struct FourierField (fourier.h:35-46). far / near / zero are flat
+    complex128 arrays in the reference's vector order; near_rows int32."""
+    d: int = 3
+    comps: int = 0
+    n_per: Sequence[int] = (1, 1, 1)
+    n_far: Sequence[int] = (1, 1, 1)
+    n_near: Sequence[int] = (1, 1, 1)
+    n_zero: Sequence[int] = (1, 1, 1)
+    far: np.ndarray = field(default_factory=lambda: np.zeros(0, np.complex128))
+    near_rows: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int32))
+    near: np.ndarray = field(default_factory=lambda: np.zeros(0, np.complex128))
+    zero: np.ndarray = field(default_factory=lambda: np.zeros(0, np.complex128))
+
+    def geom(self):
+        g = _abi.sewald_fourier_geom_c()
+        g.d, g.comps = int(self.d), int(self.comps)
+        for i in range(3):
+            g.n_per[i], g.n_far[i] = int(self.n_per[i]), int(self.n_far[i])
+            g.n_near[i], g.n_zero[i] = int(self.n_near[i]), int(self.n_zero[i])
+        g.n_near_rows = int(np.asarray(self.near_rows).size)
+        g.far_len, g.near_len, g.zero_len = (int(np.asarray(a).size) for a in (self.far, self.near, self.zero))
+        return g
+
+
+@dataclass
+class PrecomputedKernel0P:
+    """struct PrecomputedKernel0P (fourier.h:52-57)."""
+    kind: Kernel = Kernel.stokeslet
+    n: Sequence[int] = (0, 0, 0)
+    R: float = 0.0
+    table: np.ndarray = field(default_factory=lambda: np.zeros(0, np.complex128))
+
+
+def _stage_params(grid: GridSpec, plan: Optional[UpsamplingPlan] = None,
+                  window: Optional[WindowSpec] = None) -> sewald_params_c:
+    return EwaldParams(d=int(grid.d), grid=grid, window=window if window is not None else WindowSpec(h=grid.h),
+                       upsampling=plan if plan is not None else UpsamplingPlan()).to_c()
+
+
+def _cplx_buf(a) -> np.ndarray:
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.complex128).ravel())
+    return a
+
+
+def _cdp(a: np.ndarray):
+    return a.view(np.float64).ctypes.data_as(_abi.DP) if a.size else None
+
+
+def _rows_ptr(rows: np.ndarray):
+    return rows.ctypes.data_as(C.POINTER(C.c_int32)) if rows.size else None
+
+
+def _empty_like_geom(g, comps: int):
+    per = lambda n: np.zeros(n // max(g.comps, 1) * comps, np.complex128)  # noqa: E731
+    return per(g.far_len), per(g.near_len), per(g.zero_len)
+
+
+def aft_forward(rfield: np.ndarray, grid: GridSpec, plan: UpsamplingPlan,
+                engine: Optional[Engine] = None) -> FourierField:
+    """aft_forward (fourier.h:61, fourier.cpp:311-416): RealField values
+    (comps, *M_ext) -> FourierField, transforms on the GPU."""
+    fld = np.ascontiguousarray(np.asarray(rfield, dtype=np.float64))
+    n = tuple(int(v) for v in grid.M_ext)
+    if fld.ndim != 4 or fld.shape[1:] != n:
+        raise InvalidArgument("field shape does not match the extended grid")
+    comps = fld.shape[0]
+    c = _stage_params(grid, plan)
+    lib = _abi.load()
+    g = _abi.sewald_fourier_geom_c()
+    rows = np.zeros(max(1, int(np.prod([grid.M[i] for i in range(int(grid.d)) if i < 2] or [1]))), np.int32)
+    _host_call(lib.sewald_aft_geometry(C.byref(c), comps, C.byref(g), _rows_ptr(rows)))
+    far, near, zero = (np.zeros(k, np.complex128) for k in (g.far_len, g.near_len, g.zero_len))
+    eng = engine or default_engine()
+    with eng._lock:
+        eng.check(lib.sewald_gpu_aft_forward(eng.ctx, C.byref(c), _dp(fld), C.byref(g), _cdp(far), _cdp(near),
+                                             _cdp(zero)))
+    return FourierField(g.d, g.comps, tuple(g.n_per), tuple(g.n_far), tuple(g.n_near), tuple(g.n_zero),
+                        far, rows[:g.n_near_rows].copy(), near, zero)
+
+
+def aft_inverse(F: FourierField, grid: GridSpec, plan: Optional[UpsamplingPlan] = None,
+                engine: Optional[Engine] = None) -> np.ndarray:
+    """aft_inverse (fourier.h:62, fourier.cpp:418-520): -> (comps, *M_ext)."""
+    c = _stage_params(grid, plan)
+    g = F.geom()
+    far, near, zero = _cplx_buf(F.far), _cplx_buf(F.near), _cplx_buf(F.zero)
+    rows = np.ascontiguousarray(F.near_rows, dtype=np.int32)
+    out = np.zeros((int(F.comps),) + tuple(int(v) for v in grid.M_ext))
+    eng = engine or default_engine()
+    with eng._lock:
+        eng.check(eng._lib.sewald_gpu_aft_inverse(eng.ctx, C.byref(c), C.byref(g), _rows_ptr(rows), _cdp(far),
+                                                  _cdp(near), _cdp(zero), _dp(out)))
+    return out
+
+
+def scale(F: FourierField, spec, xi: float, window: WindowSpec, grid: GridSpec,
+          engine: Optional[Engine] = None) -> FourierField:
+    """scale (fourier.h:66-69, fourier.cpp:522-720): `spec` is a
+    ModifiedKernelSpec or a PrecomputedKernel0P. Output has 3 components."""
+    c = _stage_params(grid, None, window)
+    g = F.geom()
+    far, near, zero = _cplx_buf(F.far), _cplx_buf(F.near), _cplx_buf(F.zero)
+    rows = np.ascontiguousarray(F.near_rows, dtype=np.int32)
+    ofar, onear, ozero = _empty_like_geom(g, 3)
+    eng = engine or default_engine()
+    with eng._lock:
+        if isinstance(spec, PrecomputedKernel0P):
+            tn = (C.c_int32 * 3)(*[int(v) for v in spec.n])
+            tab = _cplx_buf(spec.table)
+            if tab.size != int(np.prod(spec.n)):
+                raise InvalidArgument("kernel table storage is inconsistent")
+            eng.check(eng._lib.sewald_gpu_scale_table(eng.ctx, C.byref(c), int(spec.kind), tn, _cdp(tab), float(xi),
+                                                      C.byref(g), _cdp(zero), _cdp(ozero)))
+        else:
+            m = spec.to_c()
+            eng.check(eng._lib.sewald_gpu_scale(eng.ctx, C.byref(c), C.byref(m), float(xi), C.byref(g),
+                                                _rows_ptr(rows), _cdp(far), _cdp(near), _cdp(zero), _cdp(ofar),
+                                                _cdp(onear), _cdp(ozero)))
+    if isinstance(spec, PrecomputedKernel0P):  # fourier.cpp:688-692: only d, comps, n_zero carried over
+        return FourierField(0, 3, n_zero=tuple(F.n_zero), zero=ozero)
+    return FourierField(F.d, 3, tuple(F.n_per), tuple(F.n_far), tuple(F.n_near), tuple(F.n_zero),
+                        ofar, rows.copy(), onear, ozero)
+
+
+def precompute_0p(kind: Kernel, grid: GridSpec, R: float, engine: Optional[Engine] = None) -> PrecomputedKernel0P:
+    """precompute_0p (fourier.h:74, fourier.cpp:722-803), built with cuFFT."""
+    c = _stage_params(grid)
+    n = (C.c_int32 * 3)()
+    eng = engine or default_engine()
+    with eng._lock:
+        eng.check(eng._lib.sewald_gpu_precompute_0p(eng.ctx, C.byref(c), int(kind), float(R), n, None))
+        tab = np.zeros(int(n[0]) * n[1] * n[2], np.complex128)
+        eng.check(eng._lib.sewald_gpu_precompute_0p(eng.ctx, C.byref(c), int(kind), float(R), n, _cdp(tab)))
+    return PrecomputedKernel0P(Kernel(kind), tuple(n), float(R), tab)
+
+
 class Session:
     """Device-resident session (sewald_gpu_session_*): inputs and outputs are
     torch CUDA tensors; torch is used only for memory and streams. Every call

@@ -52,19 +52,21 @@ Tabs make_tabs() {
     return t;
 }
 
-// ModifiedKernelSpec::optimal (modified_kernels.cpp:52-63) plus the series
-// coefficient blocks of the truncated kernels (:85-94, :104-108, :117-124).
-ModSpec make_modspec(int kind, int d, double R) {
+// ModifiedKernelSpec fields (modified_kernels.h:10-19, any gauge) plus the
+// series coefficient blocks of the truncated kernels (modified_kernels.cpp:85-94,
+// :104-108, :117-124).
+ModSpec make_modspec_full(int kind, int d, double R, double a_B, double b_B, double ell_H, double ell_B,
+                          double c_B) {
     const Tabs T = make_tabs();
     ModSpec m{};
     m.kind = kind;
     m.d = d;
     m.R = R;
-    m.a_B = -0.5 * R;
-    m.b_B = -0.5 / R;
-    m.ell_H = R;
-    m.ell_B = R * std::sqrt(M_E);
-    m.c_B = -0.5 * R * R;
+    m.a_B = a_B;
+    m.b_B = b_B;
+    m.ell_H = ell_H;
+    m.ell_B = ell_B;
+    m.c_B = c_B;
     m.bR3 = 3.0 * m.b_B * R;
     m.p0 = (m.a_B + R + m.b_B * R * R) / (2.0 * R);
     m.q0 = (m.a_B + 2.0 * R + 3.0 * m.b_B * R * R) / (2.0 * R);
@@ -78,6 +80,11 @@ ModSpec make_modspec(int kind, int d, double R) {
         m.ser_b1[n] = -T.j0[n] - (1.0 + m.g_b1) * T.xj1[n] + 0.25 * (1.0 + 2.0 * m.g_b1) * T.j0[n - 1] -
                       0.25 * m.ch_b1 * T.xj1[n - 1];
     return m;
+}
+
+// ModifiedKernelSpec::optimal gauge constants (modified_kernels.cpp:52-63).
+ModSpec make_modspec(int kind, int d, double R) {
+    return make_modspec_full(kind, d, R, -0.5 * R, -0.5 / R, R, R * std::sqrt(M_E), -0.5 * R * R);
 }
 
 double mollifier_taper(double t) {  // fourier.cpp:222-225
@@ -101,6 +108,7 @@ struct ClassBlock {
     const double* wf2;
     double norm;
     int64_t cstride;  // complex elements between components
+    int zero_masked;  // masked rows: write zeros to the 3 output comps (stage scale)
 };
 
 template <int KIND>
@@ -115,7 +123,11 @@ __global__ void scale_class_kernel(ModSpec spec, ClassBlock b, double xi, cuDoub
     const int64_t rj = idx / b.nf2;
     const int j = (int)(rj % b.nf1);
     const int r = (int)(rj / b.nf1);
-    if (b.rmask && !b.rmask[r]) return;
+    if (b.rmask && !b.rmask[r]) {
+        if (b.zero_masked)
+            for (int c = 0; c < 3; ++c) data[c * b.cstride + idx] = make_cuDoubleComplex(0.0, 0.0);
+        return;
+    }
     const double k0 = b.rk0[r];
     const double k1 = b.has_k1 ? b.rk1[r] : b.kf1[j];
     const double k2 = b.kf2[k];
@@ -154,9 +166,9 @@ __global__ void scale_class_kernel(ModSpec spec, ClassBlock b, double xi, cuDoub
     }
 }
 
-// real (C, n0, n1, n2) -> complex box (C, m0, m1, m2) corner, zero elsewhere.
+// real (C, n0, n1, n2) -> complex box (C, m0, m1, m2) corner times s, zero elsewhere.
 __global__ void real_to_padded_kernel(const double* __restrict__ src, int C, int n0, int n1, int n2, int m0,
-                                      int m1, int m2, cuDoubleComplex* __restrict__ dst) {
+                                      int m1, int m2, cuDoubleComplex* __restrict__ dst, double s = 1.0) {
     const int64_t tot = (int64_t)C * m0 * m1 * m2;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
          idx += (int64_t)gridDim.x * blockDim.x) {
@@ -167,15 +179,16 @@ __global__ void real_to_padded_kernel(const double* __restrict__ src, int C, int
         const int i = (int)(t % m0);
         const int c = (int)(t / m0);
         double v = 0.0;
-        if (i < n0 && j < n1 && k < n2) v = src[(((int64_t)c * n0 + i) * n1 + j) * n2 + k];
+        if (i < n0 && j < n1 && k < n2) v = s * src[(((int64_t)c * n0 + i) * n1 + j) * n2 + k];
         dst[idx] = make_cuDoubleComplex(v, 0.0);
     }
 }
 
-// complex box (3, m0, m1, m2) corner -> real (3, n0, n1, n2), real part.
+// complex box (C, m0, m1, m2) corner -> real (C, n0, n1, n2), real part times s.
 __global__ void padded_to_real_kernel(const cuDoubleComplex* __restrict__ src, int m0, int m1, int m2, int n0,
-                                      int n1, int n2, int64_t cstride, double* __restrict__ dst) {
-    const int64_t tot = (int64_t)3 * n0 * n1 * n2;
+                                      int n1, int n2, int64_t cstride, double* __restrict__ dst, int C = 3,
+                                      double s = 1.0) {
+    const int64_t tot = (int64_t)C * n0 * n1 * n2;
     for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < tot;
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int k = (int)(idx % n2);
@@ -184,7 +197,7 @@ __global__ void padded_to_real_kernel(const cuDoubleComplex* __restrict__ src, i
         t /= n1;
         const int i = (int)(t % n0);
         const int c = (int)(t / n0);
-        dst[idx] = src[c * cstride + ((int64_t)i * m1 + j) * m2 + k].x;
+        dst[idx] = s * src[c * cstride + ((int64_t)i * m1 + j) * m2 + k].x;
     }
 }
 
@@ -301,14 +314,10 @@ struct FourierPlanAFT {
 
 void AftDeleter::operator()(FourierPlanAFT* p) const { delete p; }
 
-namespace {
-
-// D=0 kernel table on the (2 M_ext)^3 mode grid (fourier.cpp:722-803), built
-// once per parameter set with cuFFT and kept on the device.
-void build_table_0p(sewald_gpu_session* s, FourierPlanAFT& A) {
-    const sewald_params_c& p = s->p;
-    cudaStream_t st = s->ctx->stream;
-    if (!(p.R > 0.0)) throw EngineError(SEWALD_EINVAL, "truncation radius must be positive");
+// D=0 kernel table on the (2 M_ext)^3 mode grid (fourier.cpp:722-803) with
+// cuFFT, into `out` ((2 M_ext)^3 complex, row-major). Returns kernel launches.
+int build_table_0p(const sewald_params_c& p, int kind, double R, DevBuf& out, cudaStream_t st) {
+    if (!(R > 0.0)) throw EngineError(SEWALD_EINVAL, "truncation radius must be positive");
     long g = 0;
     double Lmin = p.L_ext[0];
     for (int ax = 0; ax < 3; ++ax) {
@@ -317,13 +326,13 @@ void build_table_0p(sewald_gpu_session* s, FourierPlanAFT& A) {
         g = std::gcd(g, static_cast<long>(p.M_ext[ax] / p.f_m));
         Lmin = std::min(Lmin, p.L_ext[ax]);
     }
-    double s0 = std::ceil(10.0 * (1.0 + p.R / Lmin) - 1e-9) / 10.0;
+    double s0 = std::ceil(10.0 * (1.0 + R / Lmin) - 1e-9) / 10.0;
     s0 = std::max(std::ceil(s0 * static_cast<double>(g) - 1e-9) / static_cast<double>(g), 1.0);
     int dense[3];
     for (int ax = 0; ax < 3; ++ax) dense[ax] = padded_length(s0, p.M_ext[ax]);
     const int64_t dvol = (int64_t)dense[0] * dense[1] * dense[2];
-    const bool biharmonic = p.kind != SEWALD_ROTLET;
-    const ModSpec m = make_modspec(p.kind, 0, p.R);
+    const bool biharmonic = kind != SEWALD_ROTLET;
+    const ModSpec m = make_modspec(kind, 0, R);
 
     std::vector<double> kt;
     for (int ax = 0; ax < 3; ++ax) {
@@ -370,7 +379,7 @@ void build_table_0p(sewald_gpu_session* s, FourierPlanAFT& A) {
     int* ddst = upload(dd, dst_idx, st);
     double* dtap = upload(tap, taper, st);
     const int64_t tvol = (int64_t)M2[0] * M2[1] * M2[2];
-    cuDoubleComplex* table = static_cast<cuDoubleComplex*>(A.table0p.ensure(sizeof(cuDoubleComplex) * tvol));
+    cuDoubleComplex* table = static_cast<cuDoubleComplex*>(out.ensure(sizeof(cuDoubleComplex) * tvol));
     table_fold_kernel<<<grid_for(tvol), 256, 0, st>>>(dbox, dense[0], dense[1], dense[2], dsrc, ddst, dtap, M2[0],
                                                       M2[1], M2[2], inv, table);
     cufftHandle pt = 0;
@@ -381,90 +390,53 @@ void build_table_0p(sewald_gpu_session* s, FourierPlanAFT& A) {
     cuda_check(cudaStreamSynchronize(st), "table sync");
     cufftDestroy(pd);
     cufftDestroy(pt);
-    s->ctx->launches += 4;
+    return 4;
 }
 
-void prepare(sewald_gpu_session* s, bool use_table) {
-    const sewald_params_c& p = s->p;
-    if (s->aft && s->aft->table_path == (use_table && p.d == 0)) return;
-    s->aft.reset(new FourierPlanAFT());
-    FourierPlanAFT& A = *s->aft;
-    cudaStream_t st = s->ctx->stream;
-    A.d = p.d;
-    A.C = s->C;
-    A.table_path = use_table && p.d == 0;
-    for (int ax = 0; ax < 3; ++ax) A.n[ax] = p.M_ext[ax];
-    A.spec = make_modspec(p.kind, p.d, p.R);
-    const int d = p.d;
-    const double h = p.h;
+namespace {
 
-    if (d == 0) {
-        const double s0 = A.table_path ? 2.0 : p.s0;
-        for (int ax = 0; ax < 3; ++ax) A.nz[ax] = padded_length(s0, p.M_ext[ax]);
-        const int64_t zvol = (int64_t)A.nz[0] * A.nz[1] * A.nz[2];
-        // SEWALD_D0_C2C=1: the reference's full complex box transform (A/B checks)
-        static const bool c2c = [] {
-            const char* e = getenv("SEWALD_D0_C2C");
-            return e && e[0] == '1';
-        }();
-        if (c2c) {
-            A.zero.ensure(sizeof(cuDoubleComplex) * zvol * A.C);
-            int nn3[3] = {A.nz[0], A.nz[1], A.nz[2]};
-            A.p_box = A.make(3, nn3, nn3, 1, (int)zvol, A.C, st);
-        } else {
-            A.d0r.reset(new D0Real());
-            A.d0r->setup(A.n, A.nz, A.C, st);
-        }
-        // rows = axis 0 of the padded box (free), free block = axes 1, 2
-        std::vector<double> k0 = wavenumbers(A.nz[0], h), k1 = wavenumbers(A.nz[1], h), k2 = wavenumbers(A.nz[2], h);
-        std::vector<double> w0 = window_hat_table(p, k0), w1 = window_hat_table(p, k1), w2 = window_hat_table(p, k2);
-        std::vector<double> tab;
-        for (auto* v : {&k0, &w0, &k1, &w1, &k2, &w2}) tab.insert(tab.end(), v->begin(), v->end());
-        double* t = upload(A.tables, tab, st);
-        size_t o = 0;
-        const double* dk0 = t + o; o += k0.size();
-        const double* dw0 = t + o; o += w0.size();
-        const double* dk1 = t + o; o += k1.size();
-        const double* dw1 = t + o; o += w1.size();
-        const double* dk2 = t + o; o += k2.size();
-        const double* dw2 = t + o;
-        A.cb_zero = ClassBlock{A.nz[0], A.nz[1], A.nz[2], 0, dk0, nullptr, dw0, nullptr, dk1, dw1, dk2, dw2,
-                               1.0 / static_cast<double>(zvol), zvol};
-        A.d0sa = D0ScaleArgs{0, 0, 0, 0, 0, dk0, dk1, dk2, dw0, dw1, dw2, 1.0 / static_cast<double>(zvol)};
-        if (A.table_path) build_table_0p(s, A);
-        if (A.table_path && A.d0r) A.d0r->build_herm_table(A.table0p.as<cuDoubleComplex>(), st);
-        cuda_check(cudaStreamSynchronize(st), "aft prepare");
-        return;
-    }
+void build_table_0p(sewald_gpu_session* s, FourierPlanAFT& A) {
+    s->ctx->launches += build_table_0p(s->p, s->p.kind, s->p.R, A.table0p, s->ctx->stream);
+}
 
-    // d = 1, 2: periodic rows and the free block
-    int nper[3] = {1, 1, 1};
-    for (int ax = 0; ax < d; ++ax) nper[ax] = p.M[ax];
-    A.nrows = nper[0] * nper[1];
-    for (int ax = d; ax < 3; ++ax) {
-        A.nz[ax] = padded_length(p.s0, p.M_ext[ax]);
-        A.nn[ax] = padded_length(p.s_star, p.M_ext[ax]);
-    }
-    // classify_rows (fourier.cpp:101-125)
-    std::vector<uint8_t> cls(A.nrows, 0);
+// classify_rows (fourier.cpp:101-125): flat periodic-mode rows inside K_star
+// (excluding the zero row), in row order.
+std::vector<int> near_rows_of(const sewald_params_c& p) {
+    int nper[2] = {1, 1};
+    for (int ax = 0; ax < p.d && ax < 2; ++ax) nper[ax] = p.M[ax];
     std::vector<int> near_rows;
     for (int i = 0; i < nper[0]; ++i)
         for (int j = 0; j < nper[1]; ++j) {
             const int m[2] = {i, j};
             bool zero = true, near = true;
-            for (int ax = 0; ax < d; ++ax) {
+            for (int ax = 0; ax < p.d; ++ax) {
                 const int sm = signed_mode(m[ax], nper[ax]);
                 if (sm != 0) zero = false;
                 if (std::abs(sm) > p.k_star[ax]) near = false;
             }
-            const int row = i * nper[1] + j;
-            if (zero)
-                cls[row] = 2;
-            else if (near) {
-                cls[row] = 1;
-                near_rows.push_back(row);
-            }
+            if (!zero && near) near_rows.push_back(i * nper[1] + j);
         }
+    return near_rows;
+}
+
+// d = 1, 2: class buffers, cuFFT plans and k / window tables for the rows of
+// A.nrows periodic modes; A.nz / A.nn (padded free lengths) are set by the
+// caller. stage = true (reference stage functions): unit normalisation in
+// scale and zero output on far rows of other classes (fourier.cpp:601-615);
+// otherwise all normalisations are folded into the per-class scale.
+void setup_classes(const sewald_params_c& p, FourierPlanAFT& A, const std::vector<int>& near_rows, bool stage,
+                   cudaStream_t st) {
+    const int d = A.d;
+    const double h = p.h;
+    int nper[3] = {1, 1, 1};
+    for (int ax = 0; ax < d; ++ax) nper[ax] = p.M[ax];
+    A.nrows = nper[0] * nper[1];
+    std::vector<uint8_t> cls(A.nrows, 0);
+    cls[0] = 2;
+    for (int r : near_rows) {
+        if (r <= 0 || r >= A.nrows) throw EngineError(SEWALD_EINVAL, "near row index out of range");
+        cls[r] = 1;
+    }
     A.R = static_cast<int>(near_rows.size());
     const int b1 = d == 1 ? p.M_ext[1] : 1, b2 = p.M_ext[2];          // free block (unpadded)
     const int z1 = d == 1 ? A.nz[1] : 1, z2 = A.nz[2];                   // zero block
@@ -563,12 +535,74 @@ void prepare(sewald_gpu_session* s, bool use_table) {
         nf_near /= A.nn[ax];
     }
     const int has_k1 = d == 2 ? 1 : 0;
+    if (stage) nf_far = nf_zero = nf_near = inv_per = 1.0;
     A.cb_far = ClassBlock{A.nrows, b1, b2, has_k1, P(0), P(1), P(2), A.mask.as<uint8_t>(), P(9), P(10), P(11),
-                          P(12), nf_far * inv_per, vol};
+                          P(12), nf_far * inv_per, vol, stage ? 1 : 0};
     A.cb_zero = ClassBlock{1, z1, z2, has_k1, P(3), P(4), P(5), nullptr, P(13), P(14), P(15), P(16),
-                           nf_zero * inv_per, (int64_t)z1 * z2};
+                           nf_zero * inv_per, (int64_t)z1 * z2, 0};
     A.cb_near = ClassBlock{A.R, q1, q2, has_k1, P(6), P(7), P(8), nullptr, P(17), P(18), P(19), P(20),
-                           nf_near * inv_per, (int64_t)A.R * q1 * q2};
+                           nf_near * inv_per, (int64_t)A.R * q1 * q2, 0};
+}
+
+void prepare(sewald_gpu_session* s, bool use_table) {
+    const sewald_params_c& p = s->p;
+    if (s->aft && s->aft->table_path == (use_table && p.d == 0)) return;
+    s->aft.reset(new FourierPlanAFT());
+    FourierPlanAFT& A = *s->aft;
+    cudaStream_t st = s->ctx->stream;
+    A.d = p.d;
+    A.C = s->C;
+    A.table_path = use_table && p.d == 0;
+    for (int ax = 0; ax < 3; ++ax) A.n[ax] = p.M_ext[ax];
+    A.spec = make_modspec(p.kind, p.d, p.R);
+    const int d = p.d;
+    const double h = p.h;
+
+    if (d == 0) {
+        const double s0 = A.table_path ? 2.0 : p.s0;
+        for (int ax = 0; ax < 3; ++ax) A.nz[ax] = padded_length(s0, p.M_ext[ax]);
+        const int64_t zvol = (int64_t)A.nz[0] * A.nz[1] * A.nz[2];
+        // SEWALD_D0_C2C=1: the reference's full complex box transform (A/B checks)
+        static const bool c2c = [] {
+            const char* e = getenv("SEWALD_D0_C2C");
+            return e && e[0] == '1';
+        }();
+        if (c2c) {
+            A.zero.ensure(sizeof(cuDoubleComplex) * zvol * A.C);
+            int nn3[3] = {A.nz[0], A.nz[1], A.nz[2]};
+            A.p_box = A.make(3, nn3, nn3, 1, (int)zvol, A.C, st);
+        } else {
+            A.d0r.reset(new D0Real());
+            A.d0r->setup(A.n, A.nz, A.C, st);
+        }
+        // rows = axis 0 of the padded box (free), free block = axes 1, 2
+        std::vector<double> k0 = wavenumbers(A.nz[0], h), k1 = wavenumbers(A.nz[1], h), k2 = wavenumbers(A.nz[2], h);
+        std::vector<double> w0 = window_hat_table(p, k0), w1 = window_hat_table(p, k1), w2 = window_hat_table(p, k2);
+        std::vector<double> tab;
+        for (auto* v : {&k0, &w0, &k1, &w1, &k2, &w2}) tab.insert(tab.end(), v->begin(), v->end());
+        double* t = upload(A.tables, tab, st);
+        size_t o = 0;
+        const double* dk0 = t + o; o += k0.size();
+        const double* dw0 = t + o; o += w0.size();
+        const double* dk1 = t + o; o += k1.size();
+        const double* dw1 = t + o; o += w1.size();
+        const double* dk2 = t + o; o += k2.size();
+        const double* dw2 = t + o;
+        A.cb_zero = ClassBlock{A.nz[0], A.nz[1], A.nz[2], 0, dk0, nullptr, dw0, nullptr, dk1, dw1, dk2, dw2,
+                               1.0 / static_cast<double>(zvol), zvol};
+        A.d0sa = D0ScaleArgs{0, 0, 0, 0, 0, dk0, dk1, dk2, dw0, dw1, dw2, 1.0 / static_cast<double>(zvol)};
+        if (A.table_path) build_table_0p(s, A);
+        if (A.table_path && A.d0r) A.d0r->build_herm_table(A.table0p.as<cuDoubleComplex>(), st);
+        cuda_check(cudaStreamSynchronize(st), "aft prepare");
+        return;
+    }
+
+    // d = 1, 2: periodic rows and the free block
+    for (int ax = p.d; ax < 3; ++ax) {
+        A.nz[ax] = padded_length(p.s0, p.M_ext[ax]);
+        A.nn[ax] = padded_length(p.s_star, p.M_ext[ax]);
+    }
+    setup_classes(p, A, near_rows_of(p), false, st);
     cuda_check(cudaStreamSynchronize(st), "aft prepare");
 }
 
@@ -700,6 +734,319 @@ void aft_d0_slab_inverse(sewald_gpu_session* s, bool use_table, const void* recv
     D0Real& D = d0_plan(s, use_table);
     s->ctx->launches += D.slab_inverse(static_cast<const cuDoubleComplex*>(recv), xa, xb, kzb, flow_slab,
                                        s->ctx->stream);
+}
+
+// ---- reference stage functions on host buffers -------------------
+// aft_forward / scale / scale(table) / aft_inverse / precompute_0p with the
+// reference's FourierField layout (fourier.h:30-46): complex arrays as
+// interleaved (re, im) doubles, far [c][rows][free], zero [c][zero block],
+// near [c][r][near block]. Same transforms and kernels as the fused solve,
+// with the reference's per-stage normalisations instead of folded ones.
+
+namespace {
+
+int strength_comps(int kind) { return kind == SEWALD_STRESSLET ? 9 : 3; }
+
+void check_window_h(const sewald_params_c& p) {  // fourier.cpp:155-158
+    if (std::fabs(p.win_h - p.h) > 1e-12 * p.h)
+        throw EngineError(SEWALD_EINVAL, "window was built for a different grid spacing");
+}
+
+int64_t cells3(const int32_t* n) { return (int64_t)n[0] * n[1] * n[2]; }
+
+void fill_lengths(sewald_fourier_geom_c& g, const int32_t* M_ext) {
+    const int C = g.comps, d = g.d;
+    g.far_len = g.near_len = g.zero_len = 0;
+    if (d == 3) {
+        g.far_len = C * cells3(M_ext);
+    } else if (d == 0) {
+        g.zero_len = C * cells3(g.n_zero);
+    } else {
+        g.far_len = C * cells3(M_ext);
+        g.zero_len = (int64_t)C * (d == 1 ? g.n_zero[1] * g.n_zero[2] : g.n_zero[2]);
+        g.near_len = (int64_t)C * g.n_near_rows * (d == 1 ? g.n_near[1] * g.n_near[2] : g.n_near[2]);
+    }
+}
+
+// FourierField geometry consistent with the grid (shapes only; the reference
+// checks periodicity in aft_inverse / scale, fourier.cpp:421-422, :524-525).
+void check_geometry(const sewald_params_c& p, const sewald_fourier_geom_c& g) {
+    if (g.d != p.d) throw EngineError(SEWALD_EINVAL, "field and grid periodicity differ");
+    if (g.comps < 1) throw EngineError(SEWALD_EINVAL, "field storage is inconsistent");
+    // d = 3 reads only the grid, d = 0 only n_zero (a table-scaled field keeps
+    // the default n_per / n_far, fourier.cpp:688-692); d = 1, 2 read them all.
+    for (int ax = 0; ax < 3; ++ax) {
+        const bool per = ax < p.d;
+        const bool classes = p.d == 1 || p.d == 2;
+        if ((classes && (g.n_per[ax] != (per ? p.M[ax] : 1) || g.n_far[ax] != (per ? 1 : p.M_ext[ax]))) ||
+            g.n_near[ax] < 1 || g.n_zero[ax] < 1)
+            throw EngineError(SEWALD_EINVAL, "field shape does not match the extended grid");
+    }
+    if (g.n_near_rows < 0) throw EngineError(SEWALD_EINVAL, "field storage is inconsistent");
+    sewald_fourier_geom_c t = g;
+    fill_lengths(t, p.M_ext);
+    if (t.far_len != g.far_len || t.near_len != g.near_len || t.zero_len != g.zero_len)
+        throw EngineError(SEWALD_EINVAL, "field storage is inconsistent");
+}
+
+// Transforms / tables for the field geometry g (box path for d = 3 and 0,
+// class path for d = 1, 2 with the field's own near rows).
+void stage_plan(const sewald_params_c& p, const sewald_fourier_geom_c& g, const int32_t* near_rows,
+                bool tables, FourierPlanAFT& A, cudaStream_t st) {
+    A.d = g.d;
+    A.C = g.comps;
+    for (int ax = 0; ax < 3; ++ax) A.n[ax] = p.M_ext[ax];
+    if (g.d == 3 || g.d == 0) {
+        for (int ax = 0; ax < 3; ++ax) A.nz[ax] = g.d == 3 ? p.M_ext[ax] : g.n_zero[ax];
+        const int64_t bvol = cells3(A.nz);
+        A.zero.ensure(sizeof(cuDoubleComplex) * bvol * A.C);
+        int nn3[3] = {A.nz[0], A.nz[1], A.nz[2]};
+        A.p_box = A.make(3, nn3, nn3, 1, (int)bvol, A.C, st);
+        if (tables) {
+            std::vector<double> tab, k[3], w[3];
+            for (int ax = 0; ax < 3; ++ax) {
+                k[ax] = wavenumbers(A.nz[ax], p.h);
+                w[ax] = window_hat_table(p, k[ax]);
+            }
+            for (int ax = 0; ax < 3; ++ax) {
+                tab.insert(tab.end(), k[ax].begin(), k[ax].end());
+                tab.insert(tab.end(), w[ax].begin(), w[ax].end());
+            }
+            const double* t = upload(A.tables, tab, st);
+            const double* k0 = t;
+            const double* w0 = k0 + A.nz[0];
+            const double* k1 = w0 + A.nz[0];
+            const double* w1 = k1 + A.nz[1];
+            const double* k2 = w1 + A.nz[1];
+            const double* w2 = k2 + A.nz[2];
+            A.cb_zero = ClassBlock{A.nz[0], A.nz[1], A.nz[2], 0, k0, nullptr, w0, nullptr, k1, w1, k2, w2, 1.0, bvol, 0};
+        }
+        return;
+    }
+    for (int ax = g.d; ax < 3; ++ax) {
+        A.nz[ax] = g.n_zero[ax];
+        A.nn[ax] = g.n_near[ax];
+    }
+    std::vector<int> rows(near_rows, near_rows + g.n_near_rows);
+    setup_classes(p, A, rows, true, st);
+}
+
+void h2d(void* dst, const double* src, int64_t n, cudaStream_t st) {
+    if (n > 0) cuda_check(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDefault, st), "stage h2d");
+}
+void d2h(double* dst, const void* src, int64_t n, cudaStream_t st) {
+    if (n > 0) cuda_check(cudaMemcpyAsync(dst, src, sizeof(double) * n, cudaMemcpyDefault, st), "stage d2h");
+}
+
+}  // namespace
+
+// Host only (no device calls): errors are std::invalid_argument.
+void aft_geometry(const sewald_params_c& p, int comps, sewald_fourier_geom_c& g, std::vector<int>* near_rows) {
+    if (comps < 1) throw std::invalid_argument("field storage is inconsistent");
+    if (p.d < 0 || p.d > 3) throw std::invalid_argument("periodicity must be in 0..3");
+    g = sewald_fourier_geom_c{};
+    g.d = p.d;
+    g.comps = comps;
+    for (int ax = 0; ax < 3; ++ax) {
+        g.n_per[ax] = g.n_far[ax] = g.n_near[ax] = g.n_zero[ax] = 1;
+        if (ax < p.d) {
+            g.n_per[ax] = p.M[ax];
+        } else {
+            g.n_far[ax] = p.M_ext[ax];
+            g.n_near[ax] = padded_length(p.s_star, p.M_ext[ax]);
+            g.n_zero[ax] = padded_length(p.s0, p.M_ext[ax]);
+        }
+    }
+    std::vector<int> rows;
+    if (p.d == 1 || p.d == 2) rows = near_rows_of(p);
+    g.n_near_rows = static_cast<int32_t>(rows.size());
+    fill_lengths(g, p.M_ext);
+    if (near_rows) *near_rows = std::move(rows);
+}
+
+void stage_aft_forward(sewald_gpu_ctx* ctx, const sewald_params_c& p, const double* field,
+                       const sewald_fourier_geom_c& g, double* far, double* near, double* zero) {
+    sewald_fourier_geom_c want{};
+    std::vector<int> rows;
+    aft_geometry(p, g.comps, want, &rows);
+    if (std::memcmp(&want, &g, sizeof(g)) != 0)
+        throw EngineError(SEWALD_EINVAL, "field geometry does not match the grid and upsampling plan");
+    cudaStream_t st = ctx->stream;
+    FourierPlanAFT A;
+    stage_plan(p, g, rows.data(), false, A, st);
+    const int C = g.comps, d = g.d;
+    const double h3 = p.h * p.h * p.h;
+    const int64_t svol = cells3(p.M_ext);
+    DevBuf dfield;
+    double* df = static_cast<double*>(dfield.ensure(sizeof(double) * C * svol));
+    h2d(df, field, C * svol, st);
+    if (d == 3 || d == 0) {  // fourier.cpp:330-357
+        const int64_t bvol = cells3(A.nz);
+        cuDoubleComplex* z = A.zero.as<cuDoubleComplex>();
+        real_to_padded_kernel<<<grid_for(C * bvol), 256, 0, st>>>(df, C, A.n[0], A.n[1], A.n[2], A.nz[0], A.nz[1],
+                                                                  A.nz[2], z, h3);
+        cufft_check(cufftExecZ2Z(A.p_box, z, z, CUFFT_FORWARD), "stage box forward");
+        d2h(d == 3 ? far : zero, z, 2 * C * bvol, st);
+        ctx->launches += 2;
+    } else {  // fourier.cpp:359-415
+        const int b1 = d == 1 ? p.M_ext[1] : 1, b2 = p.M_ext[2];
+        const int z1 = d == 1 ? A.nz[1] : 1, z2 = A.nz[2];
+        const int q1 = d == 1 ? A.nn[1] : 1, q2 = A.nn[2];
+        const int64_t vol = svol;
+        cuDoubleComplex* dfar = A.far.as<cuDoubleComplex>();
+        cuDoubleComplex* dzero = A.zero.as<cuDoubleComplex>();
+        cuDoubleComplex* dnear = A.near.as<cuDoubleComplex>();
+        real_to_padded_kernel<<<grid_for(C * vol), 256, 0, st>>>(df, C, A.n[0], A.n[1], A.n[2], A.n[0], A.n[1],
+                                                                 A.n[2], dfar, h3);
+        for (int c = 0; c < C; ++c)
+            cufft_check(cufftExecZ2Z(A.p_per, dfar + c * vol, dfar + c * vol, CUFFT_FORWARD), "stage per forward");
+        class_rows_kernel<<<grid_for((int64_t)C * z1 * z2), 256, 0, st>>>(dfar, A.nrows, b1, b2, dzero, 1, z1, z2,
+                                                                           A.rows_zero.as<int>(), C, 0);
+        if (A.R > 0)
+            class_rows_kernel<<<grid_for((int64_t)C * A.R * q1 * q2), 256, 0, st>>>(
+                dfar, A.nrows, b1, b2, dnear, A.R, q1, q2, A.rows_near.as<int>(), C, 0);
+        cufft_check(cufftExecZ2Z(A.p_far, dfar, dfar, CUFFT_FORWARD), "stage far forward");
+        cufft_check(cufftExecZ2Z(A.p_zero, dzero, dzero, CUFFT_FORWARD), "stage zero forward");
+        if (A.R > 0) cufft_check(cufftExecZ2Z(A.p_near, dnear, dnear, CUFFT_FORWARD), "stage near forward");
+        d2h(far, dfar, 2 * g.far_len, st);
+        d2h(zero, dzero, 2 * g.zero_len, st);
+        d2h(near, dnear, 2 * g.near_len, st);
+        ctx->launches += 3 + C + 2 + (A.R > 0 ? 2 : 0);
+    }
+    cuda_check(cudaStreamSynchronize(st), "stage aft_forward");
+}
+
+void stage_aft_inverse(sewald_gpu_ctx* ctx, const sewald_params_c& p, const sewald_fourier_geom_c& g,
+                       const int32_t* near_rows, const double* far, const double* near, const double* zero,
+                       double* field_out) {
+    check_geometry(p, g);
+    cudaStream_t st = ctx->stream;
+    FourierPlanAFT A;
+    stage_plan(p, g, near_rows, false, A, st);
+    const int C = g.comps, d = g.d;
+    const double h3 = p.h * p.h * p.h;
+    const int64_t svol = cells3(p.M_ext);
+    DevBuf dout;
+    double* dfield = static_cast<double*>(dout.ensure(sizeof(double) * C * svol));
+    if (d == 3 || d == 0) {  // fourier.cpp:425-456
+        const int64_t bvol = cells3(A.nz);
+        cuDoubleComplex* z = A.zero.as<cuDoubleComplex>();
+        h2d(z, d == 3 ? far : zero, 2 * C * bvol, st);
+        cufft_check(cufftExecZ2Z(A.p_box, z, z, CUFFT_INVERSE), "stage box inverse");
+        padded_to_real_kernel<<<grid_for(C * svol), 256, 0, st>>>(z, A.nz[0], A.nz[1], A.nz[2], A.n[0], A.n[1],
+                                                                  A.n[2], bvol, dfield, C,
+                                                                  1.0 / (h3 * static_cast<double>(bvol)));
+        ctx->launches += 2;
+    } else {  // fourier.cpp:458-519
+        const int b1 = d == 1 ? p.M_ext[1] : 1, b2 = p.M_ext[2];
+        const int z1 = d == 1 ? A.nz[1] : 1, z2 = A.nz[2];
+        const int q1 = d == 1 ? A.nn[1] : 1, q2 = A.nn[2];
+        const int64_t vol = svol;
+        cuDoubleComplex* dfar = A.far.as<cuDoubleComplex>();
+        cuDoubleComplex* dzero = A.zero.as<cuDoubleComplex>();
+        cuDoubleComplex* dnear = A.near.as<cuDoubleComplex>();
+        h2d(dfar, far, 2 * g.far_len, st);
+        h2d(dzero, zero, 2 * g.zero_len, st);
+        h2d(dnear, near, 2 * g.near_len, st);
+        double inv_free = 1.0, inv_zero = 1.0, inv_near = 1.0, inv_per = 1.0;
+        for (int ax = d; ax < 3; ++ax) {
+            inv_free /= g.n_far[ax];
+            inv_zero /= g.n_zero[ax];
+            inv_near /= g.n_near[ax];
+        }
+        for (int ax = 0; ax < d; ++ax) inv_per /= p.M[ax];
+        cufft_check(cufftExecZ2Z(A.p_far, dfar, dfar, CUFFT_INVERSE), "stage far inverse");
+        scale_complex_kernel<<<grid_for(C * vol), 256, 0, st>>>(dfar, C * vol, inv_free);
+        cufft_check(cufftExecZ2Z(A.p_zero, dzero, dzero, CUFFT_INVERSE), "stage zero inverse");
+        scale_complex_kernel<<<grid_for(g.zero_len), 256, 0, st>>>(dzero, g.zero_len, inv_zero);
+        class_rows_kernel<<<grid_for((int64_t)C * z1 * z2), 256, 0, st>>>(dfar, A.nrows, b1, b2, dzero, 1, z1, z2,
+                                                                           A.rows_zero.as<int>(), C, 1);
+        ctx->launches += 5;
+        if (A.R > 0) {
+            cufft_check(cufftExecZ2Z(A.p_near, dnear, dnear, CUFFT_INVERSE), "stage near inverse");
+            scale_complex_kernel<<<grid_for(g.near_len), 256, 0, st>>>(dnear, g.near_len, inv_near);
+            class_rows_kernel<<<grid_for((int64_t)C * A.R * q1 * q2), 256, 0, st>>>(
+                dfar, A.nrows, b1, b2, dnear, A.R, q1, q2, A.rows_near.as<int>(), C, 1);
+            ctx->launches += 3;
+        }
+        for (int c = 0; c < C; ++c)
+            cufft_check(cufftExecZ2Z(A.p_per, dfar + c * vol, dfar + c * vol, CUFFT_INVERSE), "stage per inverse");
+        padded_to_real_kernel<<<grid_for(C * vol), 256, 0, st>>>(dfar, A.n[0], A.n[1], A.n[2], A.n[0], A.n[1], A.n[2],
+                                                                 vol, dfield, C, inv_per / h3);
+        ctx->launches += C + 1;
+    }
+    d2h(field_out, dfield, C * svol, st);
+    cuda_check(cudaStreamSynchronize(st), "stage aft_inverse");
+}
+
+// scale (fourier.cpp:522-666) with spec, or (fourier.cpp:668-720) with the
+// 0P table when table != nullptr (table_n = its mode grid).
+void stage_scale(sewald_gpu_ctx* ctx, const sewald_params_c& p, int kind, const sewald_modspec_c* spec,
+                 const int32_t* table_n, const double* table, double xi, const sewald_fourier_geom_c& g,
+                 const int32_t* near_rows, const double* far, const double* near, const double* zero,
+                 double* far_out, double* near_out, double* zero_out) {
+    if (table) {
+        if (p.d != 0 || g.d != 0) throw EngineError(SEWALD_EINVAL, "precomputed kernels apply to d = 0 only");
+        if (g.n_zero[0] != table_n[0] || g.n_zero[1] != table_n[1] || g.n_zero[2] != table_n[2])
+            throw EngineError(SEWALD_EINVAL, "kernel table was built for a different padded grid");
+    } else if (g.d != p.d || spec->d != p.d) {
+        throw EngineError(SEWALD_EINVAL, "field, kernel and grid periodicity must agree");
+    }
+    if (g.comps != strength_comps(kind))
+        throw EngineError(SEWALD_EINVAL, "field component count does not match the kernel");
+    if (!(xi > 0.0)) throw EngineError(SEWALD_EINVAL, "xi must be positive");
+    check_window_h(p);
+    check_geometry(p, g);
+    cudaStream_t st = ctx->stream;
+    FourierPlanAFT A;
+    stage_plan(p, g, near_rows, true, A, st);
+    const ModSpec m = spec ? make_modspec_full(spec->kind, spec->d, spec->R, spec->a_B, spec->b_B, spec->ell_H,
+                                               spec->ell_B, spec->c_B)
+                           : make_modspec(kind, 0, 1.0);
+    const int C = g.comps, d = g.d;
+    if (d == 3 || d == 0) {
+        const int64_t bvol = cells3(A.nz);
+        cuDoubleComplex* z = A.zero.as<cuDoubleComplex>();
+        h2d(z, d == 3 ? far : zero, 2 * C * bvol, st);
+        DevBuf dt;
+        const cuDoubleComplex* dtab = nullptr;
+        if (table) {
+            cuDoubleComplex* t = static_cast<cuDoubleComplex*>(dt.ensure(sizeof(cuDoubleComplex) * bvol));
+            h2d(t, table, 2 * bvol, st);
+            dtab = t;
+        }
+        launch_scale_class(kind, m, A.cb_zero, xi, z, dtab, st);
+        d2h(d == 3 ? far_out : zero_out, z, 2 * 3 * bvol, st);
+        ctx->launches += 1;
+    } else {
+        cuDoubleComplex* dfar = A.far.as<cuDoubleComplex>();
+        cuDoubleComplex* dzero = A.zero.as<cuDoubleComplex>();
+        cuDoubleComplex* dnear = A.near.as<cuDoubleComplex>();
+        h2d(dfar, far, 2 * g.far_len, st);
+        h2d(dzero, zero, 2 * g.zero_len, st);
+        h2d(dnear, near, 2 * g.near_len, st);
+        launch_scale_class(kind, m, A.cb_far, xi, dfar, nullptr, st);
+        launch_scale_class(kind, m, A.cb_zero, xi, dzero, nullptr, st);
+        if (A.R > 0) launch_scale_class(kind, m, A.cb_near, xi, dnear, nullptr, st);
+        d2h(far_out, dfar, 2 * 3 * (g.far_len / C), st);
+        d2h(zero_out, dzero, 2 * 3 * (g.zero_len / C), st);
+        d2h(near_out, dnear, 2 * 3 * (g.near_len / C), st);
+        ctx->launches += A.R > 0 ? 3 : 2;
+    }
+    cuda_check(cudaGetLastError(), "stage scale");
+    cuda_check(cudaStreamSynchronize(st), "stage scale");
+}
+
+void stage_precompute_0p(sewald_gpu_ctx* ctx, const sewald_params_c& p, int kind, double R, int32_t n_out[3],
+                         double* table_out) {
+    if (p.d != 0) throw EngineError(SEWALD_EINVAL, "kernel precomputation applies to d = 0 only");
+    if (!(R > 0.0)) throw EngineError(SEWALD_EINVAL, "truncation radius must be positive");
+    for (int ax = 0; ax < 3; ++ax) n_out[ax] = 2 * p.M_ext[ax];
+    if (!table_out) return;
+    DevBuf t;
+    ctx->launches += build_table_0p(p, kind, R, t, ctx->stream);
+    d2h(table_out, t.ptr, 2 * cells3(n_out), ctx->stream);
+    cuda_check(cudaStreamSynchronize(ctx->stream), "stage precompute_0p");
 }
 
 }  // namespace sewald_b200

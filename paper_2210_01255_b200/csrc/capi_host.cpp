@@ -3,6 +3,7 @@
 #include "host_params.h"
 
 #include <array>
+#include <cmath>
 #include <cstring>
 #include <stdexcept>
 #include <string>
@@ -80,6 +81,24 @@ int sewald_window_hat(const sewald_params_c* p, const double* k, int64_t n, doub
     return host_guard([&] {
         validate_window(*p);
         for (int64_t i = 0; i < n; ++i) out[i] = window_transform(*p, k[i]);
+    });
+}
+
+int sewald_modspec_optimal(int kind, int d, double R, sewald_modspec_c* out) {
+    if (!out) return SEWALD_EINVAL;
+    return host_guard([&] {
+        if (kind < 0 || kind > 2) throw std::invalid_argument("unknown kernel");
+        *out = sewald_modspec_c{kind, d, R, -0.5 * R, -0.5 / R, R, R * std::sqrt(M_E), -0.5 * R * R};
+    });
+}
+
+int sewald_aft_geometry(const sewald_params_c* p, int comps, sewald_fourier_geom_c* g, int32_t* near_rows_out) {
+    if (!p || !g) return SEWALD_EINVAL;
+    return host_guard([&] {
+        std::vector<int> rows;
+        aft_geometry(*p, comps, *g, &rows);
+        if (near_rows_out)
+            for (size_t i = 0; i < rows.size(); ++i) near_rows_out[i] = rows[i];
     });
 }
 

@@ -8,6 +8,7 @@
 #include "../../include/sewald_gpu.h"
 #include "host_params.h"
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <mutex>
@@ -268,6 +269,159 @@ std::vector<Vec3> gather(const RealField& field, const GridSpec& grid, const Win
     check_ctx(sewald_gpu_gather(context(), &p, field.v.data(), D(targets.x), static_cast<int64_t>(targets.x.size()),
                                 reinterpret_cast<double*>(u.data())));
     return u;
+}
+
+// ---- modified kernels / stage functions ---------------------------------------------
+ModifiedKernelSpec ModifiedKernelSpec::optimal(Kernel kind, int d, double R) {
+    sewald_modspec_c m{};
+    check_host(sewald_modspec_optimal(kernel_id(kind), d, R, &m));
+    ModifiedKernelSpec s;
+    s.kind = kind;
+    s.d = m.d;
+    s.R = m.R;
+    s.a_B = m.a_B;
+    s.b_B = m.b_B;
+    s.ell_H = m.ell_H;
+    s.ell_B = m.ell_B;
+    s.c_B = m.c_B;
+    return s;
+}
+
+double truncation_radius(const std::array<double, 3>& L, int d) {  // modified_kernels.cpp:65-73
+    switch (d) {
+        case 0: return std::sqrt(L[0] * L[0] + L[1] * L[1] + L[2] * L[2]);
+        case 1: return std::sqrt(L[1] * L[1] + L[2] * L[2]);
+        case 2: return L[2];
+        default: throw std::invalid_argument("truncation radius applies to d in {0,1,2}");
+    }
+}
+
+namespace {
+
+sewald_params_c stage_params(const GridSpec& grid, const UpsamplingPlan* plan, const WindowSpec* win) {
+    EwaldParams e;
+    e.d = grid.d;
+    e.grid = grid;
+    if (plan) e.upsampling = *plan;
+    if (win)
+        e.window = *win;
+    else
+        e.window.h = grid.h;
+    return to_c(e);
+}
+
+sewald_fourier_geom_c geom_of(const FourierField& F) {
+    sewald_fourier_geom_c g{};
+    g.d = F.d;
+    g.comps = F.comps;
+    for (int i = 0; i < 3; ++i) {
+        g.n_per[i] = F.n_per[i];
+        g.n_far[i] = F.n_far[i];
+        g.n_near[i] = F.n_near[i];
+        g.n_zero[i] = F.n_zero[i];
+    }
+    g.n_near_rows = static_cast<int32_t>(F.near_rows.size());
+    g.far_len = static_cast<int64_t>(F.far.size());
+    g.near_len = static_cast<int64_t>(F.near.size());
+    g.zero_len = static_cast<int64_t>(F.zero.size());
+    return g;
+}
+
+FourierField field_of(const sewald_fourier_geom_c& g, int comps) {
+    FourierField F;
+    F.d = g.d;
+    F.comps = comps;
+    for (int i = 0; i < 3; ++i) {
+        F.n_per[i] = g.n_per[i];
+        F.n_far[i] = g.n_far[i];
+        F.n_near[i] = g.n_near[i];
+        F.n_zero[i] = g.n_zero[i];
+    }
+    const int c0 = std::max(g.comps, 1);
+    F.far.resize(static_cast<std::size_t>(g.far_len / c0 * comps));
+    F.near.resize(static_cast<std::size_t>(g.near_len / c0 * comps));
+    F.zero.resize(static_cast<std::size_t>(g.zero_len / c0 * comps));
+    return F;
+}
+
+double* Z(std::vector<cplx>& v) { return v.empty() ? nullptr : reinterpret_cast<double*>(v.data()); }
+const double* Z(const std::vector<cplx>& v) { return v.empty() ? nullptr : reinterpret_cast<const double*>(v.data()); }
+const int32_t* rows_of(const std::vector<int>& r) {
+    static_assert(sizeof(int) == sizeof(int32_t), "int is 32-bit");
+    return r.empty() ? nullptr : reinterpret_cast<const int32_t*>(r.data());
+}
+
+}  // namespace
+
+FourierField aft_forward(const RealField& field, const GridSpec& grid, const UpsamplingPlan& plan) {
+    if (field.n != grid.M_ext) throw std::invalid_argument("field shape does not match the extended grid");
+    if (field.comps < 1 || field.v.size() != static_cast<std::size_t>(field.comps) * field.n[0] * field.n[1] * field.n[2])
+        throw std::invalid_argument("field storage is inconsistent");
+    sewald_params_c p = stage_params(grid, &plan, nullptr);
+    sewald_fourier_geom_c g{};
+    std::vector<int32_t> rows(static_cast<std::size_t>(std::max(1, grid.d == 1 ? grid.M[0] : grid.M[0] * grid.M[1])));
+    check_host(sewald_aft_geometry(&p, field.comps, &g, rows.data()));
+    FourierField F = field_of(g, field.comps);
+    F.near_rows.assign(rows.begin(), rows.begin() + g.n_near_rows);
+    std::lock_guard<std::mutex> lk(g_mu);
+    check_ctx(sewald_gpu_aft_forward(context(), &p, field.v.data(), &g, Z(F.far), Z(F.near), Z(F.zero)));
+    return F;
+}
+
+RealField aft_inverse(const FourierField& field, const GridSpec& grid, const UpsamplingPlan& plan) {
+    if (field.d != grid.d) throw std::invalid_argument("field and grid periodicity differ");
+    sewald_params_c p = stage_params(grid, &plan, nullptr);
+    const sewald_fourier_geom_c g = geom_of(field);
+    RealField out = RealField::zeros(grid.M_ext, field.comps);
+    std::lock_guard<std::mutex> lk(g_mu);
+    check_ctx(sewald_gpu_aft_inverse(context(), &p, &g, rows_of(field.near_rows), Z(field.far), Z(field.near),
+                                     Z(field.zero), out.v.data()));
+    return out;
+}
+
+FourierField scale(const FourierField& field, const ModifiedKernelSpec& spec, double xi, const Window& window,
+                   const GridSpec& grid) {
+    sewald_params_c p = stage_params(grid, nullptr, &window.spec());
+    const sewald_fourier_geom_c g = geom_of(field);
+    const sewald_modspec_c m{kernel_id(spec.kind), spec.d, spec.R, spec.a_B, spec.b_B, spec.ell_H, spec.ell_B, spec.c_B};
+    FourierField out = field_of(g, 3);
+    out.near_rows = field.near_rows;
+    std::lock_guard<std::mutex> lk(g_mu);
+    check_ctx(sewald_gpu_scale(context(), &p, &m, xi, &g, rows_of(field.near_rows), Z(field.far), Z(field.near),
+                               Z(field.zero), Z(out.far), Z(out.near), Z(out.zero)));
+    return out;
+}
+
+FourierField scale(const FourierField& field, const PrecomputedKernel0P& pre, double xi, const Window& window,
+                   const GridSpec& grid) {
+    sewald_params_c p = stage_params(grid, nullptr, &window.spec());
+    const sewald_fourier_geom_c g = geom_of(field);
+    if (pre.table.size() != static_cast<std::size_t>(pre.n[0]) * pre.n[1] * pre.n[2])
+        throw std::invalid_argument("kernel table storage is inconsistent");
+    const int32_t tn[3] = {pre.n[0], pre.n[1], pre.n[2]};
+    FourierField out;  // fourier.cpp:688-692: only d, comps and n_zero carried over
+    out.d = 0;
+    out.comps = 3;
+    out.n_zero = field.n_zero;
+    out.zero.resize(static_cast<std::size_t>(g.zero_len / std::max(g.comps, 1) * 3));
+    std::lock_guard<std::mutex> lk(g_mu);
+    check_ctx(sewald_gpu_scale_table(context(), &p, kernel_id(pre.kind), tn, Z(pre.table), xi, &g, Z(field.zero),
+                                     Z(out.zero)));
+    return out;
+}
+
+PrecomputedKernel0P precompute_0p(Kernel kind, const GridSpec& grid, double R) {
+    sewald_params_c p = stage_params(grid, nullptr, nullptr);
+    int32_t n[3];
+    std::lock_guard<std::mutex> lk(g_mu);
+    check_ctx(sewald_gpu_precompute_0p(context(), &p, kernel_id(kind), R, n, nullptr));
+    PrecomputedKernel0P pre;
+    pre.kind = kind;
+    pre.R = R;
+    pre.n = {n[0], n[1], n[2]};
+    pre.table.resize(static_cast<std::size_t>(n[0]) * n[1] * n[2]);
+    check_ctx(sewald_gpu_precompute_0p(context(), &p, kernel_id(kind), R, n, Z(pre.table)));
+    return pre;
 }
 
 namespace {

@@ -1058,6 +1058,51 @@ int sewald_gpu_gather(sewald_gpu_ctx* ctx, const sewald_params_c* p, const doubl
     });
 }
 
+int sewald_gpu_aft_forward(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* field,
+                           const sewald_fourier_geom_c* g, double* far, double* near, double* zero) {
+    if (!ctx || !p || !g) return SEWALD_EINVAL;
+    return ctx_guard(ctx, [&] { stage_aft_forward(ctx, *p, field, *g, far, near, zero); });
+}
+
+int sewald_gpu_aft_inverse(sewald_gpu_ctx* ctx, const sewald_params_c* p, const sewald_fourier_geom_c* g,
+                           const int32_t* near_rows, const double* far, const double* near, const double* zero,
+                           double* field_out) {
+    if (!ctx || !p || !g) return SEWALD_EINVAL;
+    return ctx_guard(ctx, [&] { stage_aft_inverse(ctx, *p, *g, near_rows, far, near, zero, field_out); });
+}
+
+int sewald_gpu_scale(sewald_gpu_ctx* ctx, const sewald_params_c* p, const sewald_modspec_c* spec, double xi,
+                     const sewald_fourier_geom_c* g, const int32_t* near_rows, const double* far,
+                     const double* near, const double* zero, double* far_out, double* near_out,
+                     double* zero_out) {
+    if (!ctx || !p || !spec || !g) return SEWALD_EINVAL;
+    return ctx_guard(ctx, [&] {
+        if (spec->kind < 0 || spec->kind > 2) throw EngineError(SEWALD_EINVAL, "unknown kernel");
+        stage_scale(ctx, *p, spec->kind, spec, nullptr, nullptr, xi, *g, near_rows, far, near, zero, far_out,
+                    near_out, zero_out);
+    });
+}
+
+int sewald_gpu_scale_table(sewald_gpu_ctx* ctx, const sewald_params_c* p, int kind, const int32_t table_n[3],
+                           const double* table, double xi, const sewald_fourier_geom_c* g, const double* zero,
+                           double* zero_out) {
+    if (!ctx || !p || !table_n || !table || !g) return SEWALD_EINVAL;
+    return ctx_guard(ctx, [&] {
+        if (kind < 0 || kind > 2) throw EngineError(SEWALD_EINVAL, "unknown kernel");
+        stage_scale(ctx, *p, kind, nullptr, table_n, table, xi, *g, nullptr, nullptr, nullptr, zero, nullptr,
+                    nullptr, zero_out);
+    });
+}
+
+int sewald_gpu_precompute_0p(sewald_gpu_ctx* ctx, const sewald_params_c* p, int kind, double R, int32_t n_out[3],
+                             double* table_out) {
+    if (!ctx || !p || !n_out) return SEWALD_EINVAL;
+    return ctx_guard(ctx, [&] {
+        if (kind < 0 || kind > 2) throw EngineError(SEWALD_EINVAL, "unknown kernel");
+        stage_precompute_0p(ctx, *p, kind, R, n_out, table_out);
+    });
+}
+
 int sewald_gpu_session_create(sewald_gpu_ctx* ctx, const sewald_params_c* p, sewald_gpu_session** out) {
     if (!ctx || !p || !out) return SEWALD_EINVAL;
     *out = nullptr;

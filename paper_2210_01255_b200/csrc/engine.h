@@ -111,6 +111,19 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
 
 // Fourier solve for d < 3 (aft.cu): grid (C comps, real) -> s->flow (3 comps).
 void aft_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p);
+// Reference stage functions on host buffers (aft.cu; fourier.cpp:311-803).
+void stage_aft_forward(sewald_gpu_ctx* ctx, const sewald_params_c& p, const double* field,
+                       const sewald_fourier_geom_c& g, double* far, double* near, double* zero);
+void stage_aft_inverse(sewald_gpu_ctx* ctx, const sewald_params_c& p, const sewald_fourier_geom_c& g,
+                       const int32_t* near_rows, const double* far, const double* near, const double* zero,
+                       double* field_out);
+void stage_scale(sewald_gpu_ctx* ctx, const sewald_params_c& p, int kind, const sewald_modspec_c* spec,
+                 const int32_t* table_n, const double* table, double xi, const sewald_fourier_geom_c& g,
+                 const int32_t* near_rows, const double* far, const double* near, const double* zero,
+                 double* far_out, double* near_out, double* zero_out);
+void stage_precompute_0p(sewald_gpu_ctx* ctx, const sewald_params_c& p, int kind, double R, int32_t n_out[3],
+                         double* table_out);
+int build_table_0p(const sewald_params_c& p, int kind, double R, DevBuf& out, cudaStream_t st);
 // Slab-distributed D = 0 solve stages (aft.cu / aft_d0.cu).
 struct SlabBounds;
 void aft_d0_geometry(sewald_gpu_session* s, bool use_table, int m[3], int n[3], int* h2, int* C);

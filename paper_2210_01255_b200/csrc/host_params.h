@@ -53,6 +53,10 @@ std::vector<double> window_hat_table(const sewald_params_c& p, const std::vector
 // Integer padded length s * m_ext (fourier.cpp:92-98).
 int padded_length(double s, int m_ext);
 
+// FourierField geometry aft_forward produces (fourier.cpp:317-328) and the
+// near rows of classify_rows (fourier.cpp:101-125); defined in aft.cu.
+void aft_geometry(const sewald_params_c& p, int comps, sewald_fourier_geom_c& g, std::vector<int>* near_rows);
+
 void validate_window(const sewald_params_c& p);
 
 }  // namespace sewald_b200

@@ -127,15 +127,15 @@ __device__ __forceinline__ void diffop_coeffs(double k0, double k1, double k2, d
     }
 }
 
-// modified_kernel_hat(spec, k) for d in {0,1,2} (d = 3 uses kspace.cu).
+// modified_kernel_hat(spec, k) for d in {0,1,2,3} (the d = 3 solve itself uses kspace.cu).
 template <int KIND>
 __device__ __forceinline__ void modified_coeffs(const ModSpec& m, double k0, double k1, double k2,
                                                 double* re, double* im) {
     constexpr int NG = KIND == SEWALD_STRESSLET ? 27 : 9;
-    const bool plain = (m.d == 2 && (k0 != 0.0 || k1 != 0.0)) || (m.d == 1 && k0 != 0.0);
+    const bool plain = (m.d == 2 && (k0 != 0.0 || k1 != 0.0)) || (m.d == 1 && k0 != 0.0) || m.d == 3;
     if (plain || m.d == 0) {
         const double kk = k0 * k0 + k1 * k1 + k2 * k2;
-        if (m.d == 0 && kk == 0.0) {
+        if ((m.d == 0 || m.d == 3) && kk == 0.0) {  // d = 3: G(0) = 0 (modified_kernels.cpp:250-252)
 #pragma unroll
             for (int q = 0; q < NG; ++q) re[q] = im[q] = 0.0;
             return;

@@ -5,7 +5,11 @@
 //   free-space potential = bare kernel sum      test_realspace.cpp:469-514
 //   full potential invariant under xi            test_realspace.cpp:516-540
 //   unstarred evaluation on a source is singular test_realspace.cpp:429-435
+// and composes the stage functions spread -> aft_forward -> scale ->
+// aft_inverse -> gather exactly as se_fourier_potential (fourier.cpp:805-852).
 #include "sewald/estimates.h"
+#include "sewald/fourier.h"
+#include "sewald/modified_kernels.h"
 #include "sewald/realspace.h"
 
 #include <cmath>
@@ -95,6 +99,43 @@ int main() {
         const double rms = std::sqrt(acc / ua.size());
         std::printf("xi invariance %-9s d=%d rms = %.3e\n", kernel_name(c.kind), c.d, rms);
         EXPECT(rms <= 10.0 * (tau + tau));
+    }
+    // stage composition == se_fourier_potential (no gauge correction for
+    // these kinds: gauge_flow_correction is stokeslet, d <= 1 only)
+    struct StageCase { Kernel kind; int d; bool table; };
+    for (const StageCase c : {StageCase{Kernel::stokeslet, 3, false}, StageCase{Kernel::stresslet, 2, false},
+                              StageCase{Kernel::rotlet, 1, false}, StageCase{Kernel::stokeslet, 2, false},
+                              StageCase{Kernel::rotlet, 0, false}, StageCase{Kernel::stresslet, 0, true}}) {
+        SourceSystem s = random_system(c.kind, c.d, 60, rng);
+        const EwaldParams p =
+            select_parameters(c.kind, c.d, s.cell, source_quantity(s), 7.0, ToleranceSpec{1e-9, false}).params;
+        const Window window(p.window);
+        RealField phi = spread(s, p.grid, window);
+        UpsamplingPlan plan = p.upsampling;
+        FourierField scaled;
+        if (c.table) {
+            plan.s0 = 2.0;
+            const PrecomputedKernel0P pre = precompute_0p(c.kind, p.grid, p.R);
+            scaled = scale(aft_forward(phi, p.grid, plan), pre, p.xi, window, p.grid);
+        } else {
+            const ModifiedKernelSpec spec = ModifiedKernelSpec::optimal(c.kind, c.d, c.d == 3 ? 1.0 : p.R);
+            scaled = scale(aft_forward(phi, p.grid, plan), spec, p.xi, window, p.grid);
+        }
+        const RealField flow = aft_inverse(scaled, p.grid, plan);
+        const TargetSet t = TargetSet::from_sources(s);
+        const auto us = gather(flow, p.grid, window, t);
+        SePipelineOptions opt;
+        opt.precompute_0p = c.table;
+        const auto ur = se_fourier_potential(s, t, p, opt);
+        double num = 0.0, den = 0.0;
+        for (std::size_t i = 0; i < ur.size(); ++i)
+            for (int k = 0; k < 3; ++k) {
+                num += (us[i][k] - ur[i][k]) * (us[i][k] - ur[i][k]);
+                den += ur[i][k] * ur[i][k];
+            }
+        const double rel = std::sqrt(num / den);
+        std::printf("stages %-9s d=%d table=%d rel = %.3e\n", kernel_name(c.kind), c.d, c.table ? 1 : 0, rel);
+        EXPECT(rel <= 1e-12);
     }
     // error behaviour
     {
