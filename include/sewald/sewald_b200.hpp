@@ -24,7 +24,22 @@ namespace sewald {
 
 // ---- value types (domain.h) ------------------------------------------------
 using Vec3 = std::array<double, 3>;
+using Mat3 = std::array<std::array<double, 3>, 3>;
+using Ten3 = std::array<Mat3, 3>;  // t[j][l][m]
 using cplx = std::complex<double>;
+using CVec3 = std::array<cplx, 3>;
+using CMat3 = std::array<CVec3, 3>;
+using CTen3 = std::array<CMat3, 3>;
+
+inline Vec3 operator+(const Vec3& a, const Vec3& b) { return {a[0] + b[0], a[1] + b[1], a[2] + b[2]}; }
+inline Vec3 operator-(const Vec3& a, const Vec3& b) { return {a[0] - b[0], a[1] - b[1], a[2] - b[2]}; }
+inline Vec3 operator*(double s, const Vec3& a) { return {s * a[0], s * a[1], s * a[2]}; }
+inline Vec3& operator+=(Vec3& a, const Vec3& b) {
+    for (int i = 0; i < 3; ++i) a[i] += b[i];
+    return a;
+}
+inline double dot(const Vec3& a, const Vec3& b) { return a[0] * b[0] + a[1] * b[1] + a[2] * b[2]; }
+inline double norm2(const Vec3& a) { return dot(a, a); }
 
 enum class Kernel { stokeslet, stresslet, rotlet };
 enum class Screening { ewald, hasimoto };
@@ -32,10 +47,16 @@ enum class Screening { ewald, hasimoto };
 Screening screening_of(Kernel kind);
 const char* kernel_name(Kernel kind);
 int strength_components(Kernel kind);
+bool kernel_from_name(const std::string& name, Kernel& out);
 
 struct Cell {
     std::array<double, 3> L{1.0, 1.0, 1.0};
     double volume() const { return L[0] * L[1] * L[2]; }
+};
+
+struct Periodicity {
+    int d = 3;
+    bool periodic(int axis) const { return axis < d; }
 };
 
 struct SourceSystem {
@@ -57,9 +78,37 @@ struct TargetSet {
 void validate_system(const SourceSystem& s);
 double source_quantity(const SourceSystem& s);
 Vec3 wrap_position(const Vec3& x, const Cell& cell, int d);
+Vec3 minimum_image(const Vec3& r, const Cell& cell, int d);
+
+// ---- kernels (kernels.h): host evaluation of the kernel tensors ---------------
+struct KernelTensor {
+    int rank = 2;
+    CMat3 m{};
+    CTen3 t{};
+};
+
+struct KernelTensorR {
+    int rank = 2;
+    Mat3 m{};
+    Ten3 t{};
+};
+
+KernelTensorR bare_kernel(Kernel kind, const Vec3& r);
+double screening_hat(Screening skind, const Vec3& k, double xi);
+KernelTensorR realspace_kernel(Kernel kind, const Vec3& r, double xi);
+KernelTensor diffop_hat(Kernel kind, const Vec3& k);
+KernelTensor fourier_kernel_hat(Kernel kind, const Vec3& k, double xi);
+Vec3 self_term(Kernel kind, double xi, const Vec3& strength);
+std::vector<Vec3> stresslet_zero_mode_3p(const TargetSet& targets, const SourceSystem& system);
+Vec3 apply(const KernelTensorR& K, const Vec3& f);
+Vec3 apply(const KernelTensorR& K, const Vec3& q, const Vec3& nu);
+CVec3 apply(const KernelTensor& K, const Vec3& f);
+CVec3 apply(const KernelTensor& K, const Vec3& q, const Vec3& nu);
 
 // ---- window (window.h) -------------------------------------------------------
 enum class WindowKind { kb, pkb, tg };
+std::string window_kind_name(WindowKind kind);
+WindowKind window_kind_from_name(const std::string& name);
 
 struct WindowSpec {
     WindowKind kind = WindowKind::pkb;
@@ -72,6 +121,20 @@ struct WindowSpec {
     static WindowSpec make(WindowKind kind, int P, double h);
 };
 
+struct PiecewisePolyWindow {
+    int P = 0;
+    int nu = 0;
+    double h = 1.0;
+    std::vector<double> coef;
+};
+
+double kb_eval(const WindowSpec& spec, double r);
+double kb_hat(const WindowSpec& spec, double k);
+PiecewisePolyWindow pkb_build(const WindowSpec& spec);
+double pkb_eval(const PiecewisePolyWindow& win, double r);
+double tg_eval(const WindowSpec& spec, double r);
+double ug_hat(const WindowSpec& spec, double k);
+
 class Window {
   public:
     explicit Window(const WindowSpec& spec);
@@ -83,6 +146,8 @@ class Window {
     WindowSpec spec_;
     std::vector<double> coef_;  // PKB table (P x (nu+1))
 };
+
+double tensor_window_eval(const Window& win, const Vec3& r);
 
 // ---- grid (grid.h) -------------------------------------------------------------
 struct GridSpec {
@@ -113,6 +178,26 @@ struct ToleranceSpec {
     bool relative = false;
     double absolute(double U) const { return relative ? value * U : value; }
 };
+
+struct CutoffResult {
+    double value = 0.0;
+    bool clamped = false;
+};
+
+struct WindowSizeResult {
+    int P = 2;
+    bool saturated = false;
+};
+
+double fourier_trunc_error(Kernel kind, double xi, double kinf, double L, double Q);
+double realspace_trunc_error(Kernel kind, double xi, double rc, double L, double Q);
+CutoffResult solve_kinf(Kernel kind, double xi, double tau, double L, double Q);
+CutoffResult solve_rc(Kernel kind, double xi, double tau, double L, double Q);
+double potential_rms(Kernel kind, double L, double Q, double xi);
+double window_error(double P, double U);
+WindowSizeResult solve_P(double tau, double U);
+std::pair<double, int> pollution_adjust(double h, int P, int d);
+UpsamplingPlan upsampling_params(const GridSpec& grid, double tau, double U);
 
 struct EwaldParams {
     Kernel kind = Kernel::stokeslet;
@@ -170,6 +255,14 @@ struct ModifiedKernelSpec {
 };
 
 double truncation_radius(const std::array<double, 3>& L_ext, int d);
+double harmonic_hat_trunc_0p(double kappa, double R);
+double biharmonic_hat_trunc_0p(double kappa, double R, double a_B, double b_B);
+double harmonic_hat_trunc_1p(double kappa, double R, double ell_H);
+double biharmonic_hat_trunc_1p(double kappa, double R, double ell_B, double c_B);
+cplx Z_hat_trunc_2p(double kappa3, double R);
+double H2p_hat_trunc(double kappa3, double R);
+KernelTensor modified_kernel_hat(const ModifiedKernelSpec& spec, const Vec3& k);
+Vec3 gauge_flow_correction(const ModifiedKernelSpec& spec, const SourceSystem& system);
 
 // ---- Fourier part (fourier.h) ----------------------------------------------------
 struct RealField {
@@ -222,12 +315,33 @@ FourierField scale(const FourierField& field, const ModifiedKernelSpec& spec, do
 FourierField scale(const FourierField& field, const PrecomputedKernel0P& pre, double xi, const Window& window,
                    const GridSpec& grid);
 PrecomputedKernel0P precompute_0p(Kernel kind, const GridSpec& grid, double R);
+
+namespace detail {
+double mollifier_taper(double t);  // fourier.cpp:222-225
+}  // namespace detail
 std::vector<Vec3> gather(const RealField& field, const GridSpec& grid, const Window& window,
                          const TargetSet& targets);
 std::vector<Vec3> se_fourier_potential(const SourceSystem& system, const TargetSet& targets,
                                        const EwaldParams& params, const SePipelineOptions& opt = {});
 
 // ---- real space and full potential (realspace.h) -----------------------------------
+// Host cell list of the reference's real-space sum (realspace.cpp:97-164); the
+// device path builds its own finer grid, this one serves callers and tests.
+struct CellList {
+    double rc = 0.0;
+    int d = 3;
+    Cell cell;
+    std::array<int, 3> n{1, 1, 1};
+    std::array<double, 3> width{};
+    std::array<double, 3> origin{};
+    std::array<int, 3> reach{1, 1, 1};
+    std::vector<std::size_t> offset;
+    std::vector<std::size_t> index;
+    std::vector<Vec3> folded;
+    std::size_t bucket_count() const { return offset.empty() ? 0 : offset.size() - 1; }
+};
+
+CellList build_cell_list(const SourceSystem& system, double rc);
 std::vector<Vec3> realspace_potential(const SourceSystem& system, const TargetSet& targets,
                                       double xi, double rc, bool starred, int n_threads = 1);
 std::vector<Vec3> full_potential(const SourceSystem& system, const TargetSet& targets,

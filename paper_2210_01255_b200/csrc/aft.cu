@@ -52,6 +52,8 @@ Tabs make_tabs() {
     return t;
 }
 
+}  // namespace
+
 // ModifiedKernelSpec fields (modified_kernels.h:10-19, any gauge) plus the
 // series coefficient blocks of the truncated kernels (modified_kernels.cpp:85-94,
 // :104-108, :117-124).
@@ -86,6 +88,8 @@ ModSpec make_modspec_full(int kind, int d, double R, double a_B, double b_B, dou
 ModSpec make_modspec(int kind, int d, double R) {
     return make_modspec_full(kind, d, R, -0.5 * R, -0.5 / R, R, R * std::sqrt(M_E), -0.5 * R * R);
 }
+
+namespace {
 
 double mollifier_taper(double t) {  // fourier.cpp:222-225
     const double a2 = 4.0 * std::log(100.0) / 49.0;

@@ -4,6 +4,7 @@
 // the device engine through sewald_gpu.h; status codes are rethrown as the
 // reference's exception types.
 #include "../../include/sewald/sewald_b200.hpp"
+#include "../../include/sewald/specfun.h"
 
 #include "../../include/sewald_gpu.h"
 #include "host_params.h"
@@ -163,6 +164,155 @@ Vec3 wrap_position(const Vec3& x, const Cell& cell, int d) {
         if (y[i] < 0.0) y[i] += cell.L[i];
     }
     return y;
+}
+
+// ---- special functions (specfun.h subset) ------------------------------------------------
+double erf(double x) { return std::erf(x); }
+double erfc(double x) { return std::erfc(x); }
+
+double bessel_J(int order, double t) {
+    if (order == 0) return ::j0(t);
+    if (order == 1) return ::j1(t);
+    throw std::invalid_argument("bessel_J supports orders 0 and 1");
+}
+
+double bessel_I0(double t) { return sewald_b200::bessel_i0(t); }
+
+double bessel_K1(double t) {
+    if (!(t > 0.0)) throw std::domain_error("bessel_K1 requires t > 0");
+    return std::cyl_bessel_k(1.0, t);
+}
+
+double bessel_Kn(int order, double t) {
+    if (!(t > 0.0)) throw std::domain_error("bessel_Kn requires t > 0");
+    return std::cyl_bessel_k(static_cast<double>(order < 0 ? -order : order), t);
+}
+
+double lambert_w0(double t) { return sewald_b200::lambert_w0(t); }
+
+bool kernel_from_name(const std::string& name, Kernel& out) {
+    for (Kernel k : {Kernel::stokeslet, Kernel::stresslet, Kernel::rotlet})
+        if (name == kernel_name(k)) {
+            out = k;
+            return true;
+        }
+    return false;
+}
+
+Vec3 minimum_image(const Vec3& r, const Cell& cell, int d) {
+    Vec3 y = r;
+    for (int i = 0; i < d; ++i) y[i] -= cell.L[i] * std::floor(y[i] / cell.L[i] + 0.5);
+    return y;
+}
+
+// ---- estimates (estimates.h:28-55) ----------------------------------------------------
+double fourier_trunc_error(Kernel kind, double xi, double kinf, double L, double Q) {
+    return sewald_b200::fourier_trunc_error(kernel_id(kind), xi, kinf, L, Q);
+}
+
+double realspace_trunc_error(Kernel kind, double xi, double rc, double L, double Q) {
+    return sewald_b200::realspace_trunc_error(kernel_id(kind), xi, rc, L, Q);
+}
+
+CutoffResult solve_kinf(Kernel kind, double xi, double tau, double L, double Q) {
+    const auto c = sewald_b200::solve_kinf(kernel_id(kind), xi, tau, L, Q);
+    return {c.value, c.clamped};
+}
+
+CutoffResult solve_rc(Kernel kind, double xi, double tau, double L, double Q) {
+    const auto c = sewald_b200::solve_rc(kernel_id(kind), xi, tau, L, Q);
+    return {c.value, c.clamped};
+}
+
+double potential_rms(Kernel kind, double L, double Q, double xi) {
+    return sewald_b200::potential_rms(kernel_id(kind), L, Q, xi);
+}
+
+double window_error(double P, double U) { return sewald_b200::window_error(P, U); }
+
+WindowSizeResult solve_P(double tau, double U) {
+    WindowSizeResult r;
+    sewald_b200::solve_P(tau, U, r.P, r.saturated);
+    return r;
+}
+
+std::pair<double, int> pollution_adjust(double h, int P, int d) {
+    std::pair<double, int> r;
+    sewald_b200::pollution_adjust(h, P, d, r.first, r.second);
+    return r;
+}
+
+UpsamplingPlan upsampling_params(const GridSpec& grid, double tau, double U) {
+    EwaldParams e;
+    e.d = grid.d;
+    e.grid = grid;
+    sewald_params_c p = to_c(e);
+    sewald_b200::upsampling_params(p, tau, U);
+    return from_c(p).upsampling;
+}
+
+// ---- window / grid ------------------------------------------------------------------
+std::string window_kind_name(WindowKind kind) {
+    return kind == WindowKind::kb ? "kb" : (kind == WindowKind::tg ? "tg" : "pkb");
+}
+
+WindowKind window_kind_from_name(const std::string& name) {
+    if (name == "kb") return WindowKind::kb;
+    if (name == "pkb") return WindowKind::pkb;
+    if (name == "tg") return WindowKind::tg;
+    throw std::invalid_argument("unknown window kind: " + name);
+}
+
+double kb_eval(const WindowSpec& spec, double r) {
+    sewald_params_c p{};
+    put_window(spec, p);
+    return sewald_b200::kb_value(p, r);
+}
+
+double kb_hat(const WindowSpec& spec, double k) {
+    sewald_params_c p{};
+    put_window(spec, p);
+    return sewald_b200::kb_transform(p, k);
+}
+
+double ug_hat(const WindowSpec& spec, double k) {
+    sewald_params_c p{};
+    put_window(spec, p);
+    return sewald_b200::ug_transform(p, k);
+}
+
+double tg_eval(const WindowSpec& spec, double r) {
+    WindowSpec t = spec;
+    t.kind = WindowKind::tg;
+    sewald_params_c p{};
+    put_window(t, p);
+    return sewald_b200::window_value(p, {}, r);
+}
+
+PiecewisePolyWindow pkb_build(const WindowSpec& spec) {
+    sewald_params_c p{};
+    put_window(spec, p);
+    sewald_b200::validate_window(p);
+    if (spec.nu < 1) throw std::invalid_argument("polynomial degree must be at least 1");
+    PiecewisePolyWindow w;
+    w.P = spec.P;
+    w.nu = spec.nu;
+    w.h = spec.h;
+    w.coef = sewald_b200::pkb_coefficients(p);
+    return w;
+}
+
+double pkb_eval(const PiecewisePolyWindow& win, double r) {
+    sewald_params_c p{};
+    p.win_kind = SEWALD_WIN_PKB;
+    p.P = win.P;
+    p.nu = win.nu;
+    p.win_h = win.h;
+    return sewald_b200::window_value(p, win.coef, r);
+}
+
+double tensor_window_eval(const Window& win, const Vec3& r) {
+    return win.eval1d(r[0]) * win.eval1d(r[1]) * win.eval1d(r[2]);
 }
 
 // ---- window / grid ------------------------------------------------------------------

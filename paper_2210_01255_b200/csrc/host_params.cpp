@@ -85,7 +85,7 @@ Cutoff invert_model(const ErrorModel& m, double tau, double floor_value) {
     return {x, false};
 }
 
-double lambert_w0(double t) {
+double lambert_w0_impl(double t) {
     // Principal branch of w e^w = t (specfun.cpp:259-284 semantics): initial
     // guess by region, then Halley iterations.
     static const double inv_e = std::exp(-1.0);
@@ -118,7 +118,7 @@ Cutoff kinf_for(int kernel, double xi, double tau, double L, double Q) {
     const ErrorModel m = kspace_model(kernel, xi, L, Q);
     if (kernel == SEWALD_ROTLET) {
         const double c2 = m.c * m.c;
-        return {xi * std::sqrt(lambert_w0(c2 * c2 / (xi * xi * std::pow(tau, 4.0)))), false};
+        return {xi * std::sqrt(lambert_w0_impl(c2 * c2 / (xi * xi * std::pow(tau, 4.0)))), false};
     }
     return invert_model(m, tau, 2.0 * kPi / L);
 }
@@ -224,6 +224,8 @@ void vandermonde_solve(int n, const long double* x, long double* rhs, double* c)
 }  // namespace
 
 double bessel_i0(double t) { return std::cyl_bessel_i(0.0, std::fabs(t)); }
+
+double lambert_w0(double t) { return lambert_w0_impl(t); }
 
 void validate_window(const sewald_params_c& p) {
     if (p.P < 2 || p.P % 2 != 0)
@@ -455,6 +457,69 @@ void select_parameters(int kernel, int d, const std::array<double, 3>& Lc, doubl
     out = p;
     if (report) *report = rep;
 }
+
+static void positive_args(double xi, double x, double L, double Q, const char* xname) {
+    must_be_positive(xi, "xi");
+    must_be_positive(x, xname);
+    must_be_positive(L, "L");
+    must_be_positive(Q, "Q");
+}
+
+double fourier_trunc_error(int kernel, double xi, double kinf, double L, double Q) {
+    positive_args(xi, kinf, L, Q, "kinf");
+    return kspace_model(kernel, xi, L, Q).at(kinf);
+}
+
+double realspace_trunc_error(int kernel, double xi, double rc, double L, double Q) {
+    positive_args(xi, rc, L, Q, "rc");
+    return rspace_model(kernel, xi, L, Q).at(rc);
+}
+
+CutoffValue solve_kinf(int kernel, double xi, double tau, double L, double Q) {
+    positive_args(xi, tau, L, Q, "tau");
+    const Cutoff c = kinf_for(kernel, xi, tau, L, Q);
+    return {c.value, c.clamped};
+}
+
+CutoffValue solve_rc(int kernel, double xi, double tau, double L, double Q) {
+    positive_args(xi, tau, L, Q, "tau");
+    const Cutoff c = invert_model(rspace_model(kernel, xi, L, Q), tau, 0.0);
+    return {c.value, c.clamped};
+}
+
+double potential_rms(int kernel, double L, double Q, double xi) {
+    must_be_positive(L, "L");
+    must_be_positive(Q, "Q");
+    must_be_positive(xi, "xi");
+    return fitted_rms(kernel, L, Q, xi);
+}
+
+double window_error(double P, double U) {
+    must_be_positive(U, "U");
+    if (P < 0.0) throw std::invalid_argument("P must be nonnegative");
+    return 10.0 * U * std::exp(-2.5 * P);
+}
+
+void solve_P(double tau, double U, int& P, bool& saturated) {
+    must_be_positive(tau, "tau");
+    must_be_positive(U, "U");
+    saturated = tau >= 10.0 * U;
+    if (saturated) {
+        P = 2;
+        return;
+    }
+    const double P_real = std::log(10.0 * U / tau) / 2.5;
+    P = std::max(2 * static_cast<int>(std::ceil(0.5 * P_real - 1e-9)), 2);
+}
+
+void pollution_adjust(double h, int P, int d, double& h_out, int& P_out) {
+    if (d < 0 || d > 3) throw std::invalid_argument("periodicity must be 0, 1, 2 or 3");
+    must_be_positive(h, "h");
+    h_out = d == 0 ? h / 1.1 : h / 1.05;
+    P_out = d == 0 ? P + 2 : P + 4;
+}
+
+void upsampling_params(sewald_params_c& g, double tau, double U) { upsampling_for(g, tau, U); }
 
 std::vector<double> wavenumbers(int n, double h) {
     std::vector<double> k(n);

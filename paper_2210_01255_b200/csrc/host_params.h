@@ -23,6 +23,7 @@ namespace sewald_b200 {
 constexpr double kPi = 3.14159265358979323846;
 
 double bessel_i0(double t);
+double lambert_w0(double t);  // principal branch (specfun.cpp:259-284)
 
 // Window shape functions on the host (tables, PKB fitting, tests).
 double kb_value(const sewald_params_c& p, double r);
@@ -58,5 +59,22 @@ int padded_length(double s, int m_ext);
 void aft_geometry(const sewald_params_c& p, int comps, sewald_fourier_geom_c& g, std::vector<int>* near_rows);
 
 void validate_window(const sewald_params_c& p);
+
+// Error-estimate layer of the reference (estimates.h:28-55), same checks and
+// arithmetic as used inside select_parameters.
+struct CutoffValue {
+    double value;
+    bool clamped;
+};
+double fourier_trunc_error(int kernel, double xi, double kinf, double L, double Q);
+double realspace_trunc_error(int kernel, double xi, double rc, double L, double Q);
+CutoffValue solve_kinf(int kernel, double xi, double tau, double L, double Q);
+CutoffValue solve_rc(int kernel, double xi, double tau, double L, double Q);
+double potential_rms(int kernel, double L, double Q, double xi);
+double window_error(double P, double U);
+void solve_P(double tau, double U, int& P, bool& saturated);
+void pollution_adjust(double h, int P, int d, double& h_out, int& P_out);
+// upsampling_params (estimates.cpp:180-209): fills g's s0 / s_star / k_star.
+void upsampling_params(sewald_params_c& g, double tau, double U);
 
 }  // namespace sewald_b200

@@ -16,6 +16,12 @@
 
 #include <cuComplex.h>
 
+#include <cmath>
+
+// Host and device: the same restatement also backs the host modified_kernel_hat
+// of the drop-in API (host_api.cu), so both sides share one implementation.
+#define SEWALD_HD __host__ __device__ __forceinline__
+
 namespace sewald_b200 {
 
 constexpr int kSeries = 13;
@@ -33,19 +39,19 @@ struct ModSpec {
 
 constexpr double kPiM = 3.14159265358979323846;
 
-__device__ __forceinline__ double series_eval(const double* c, int first, int count, double x2) {
+SEWALD_HD double series_eval(const double* c, int first, int count, double x2) {
     double acc = 0.0;
     for (int n = first + count - 1; n >= first; --n) acc = c[n] + acc * x2;
     return acc;
 }
 
-__device__ __forceinline__ double harmonic_trunc_0p(double kappa, double R) {
+SEWALD_HD double harmonic_trunc_0p(double kappa, double R) {
     if (kappa == 0.0) return 2.0 * kPiM * R * R;
     const double s = sin(0.5 * R * kappa);
     return 8.0 * kPiM * s * s / (kappa * kappa);
 }
 
-__device__ __forceinline__ double biharmonic_trunc_0p(const ModSpec& m, double kappa) {
+SEWALD_HD double biharmonic_trunc_0p(const ModSpec& m, double kappa) {
     const double x = m.R * kappa;
     if (fabs(x) < 1.0) {
         const double R2 = m.R * m.R;
@@ -56,14 +62,14 @@ __device__ __forceinline__ double biharmonic_trunc_0p(const ModSpec& m, double k
     return -8.0 * kPiM / (k2 * k2) * bracket;
 }
 
-__device__ __forceinline__ double harmonic_trunc_1p(const ModSpec& m, double kappa) {
+SEWALD_HD double harmonic_trunc_1p(const ModSpec& m, double kappa) {
     const double x = m.R * kappa;
     if (fabs(x) < 1.0) return 4.0 * kPiM * m.R * m.R * series_eval(m.ser_h1, 1, kSeries - 1, x * x);
     const double bracket = 1.0 - j0(x) - m.g_h1 * x * j1(x);
     return 4.0 * kPiM / (kappa * kappa) * bracket;
 }
 
-__device__ __forceinline__ double biharmonic_trunc_1p(const ModSpec& m, double kappa) {
+SEWALD_HD double biharmonic_trunc_1p(const ModSpec& m, double kappa) {
     const double x = m.R * kappa;
     if (fabs(x) < 1.0) {
         const double R2 = m.R * m.R;
@@ -77,13 +83,13 @@ __device__ __forceinline__ double biharmonic_trunc_1p(const ModSpec& m, double k
     return -8.0 * kPiM / (k2 * k2) * bracket;
 }
 
-__device__ __forceinline__ double Z_trunc_2p_im(double k3, double R) {
+SEWALD_HD double Z_trunc_2p_im(double k3, double R) {
     if (k3 == 0.0) return 0.0;
     const double s = sin(0.5 * R * k3);
     return -8.0 * kPiM * s * s / k3;
 }
 
-__device__ __forceinline__ double H2p_trunc(double k3, double R) {
+SEWALD_HD double H2p_trunc(double k3, double R) {
     if (k3 == 0.0) return -2.0 * kPiM * R * R;
     const double x = R * k3;
     const double s = sin(0.5 * x);
@@ -95,7 +101,7 @@ __device__ __forceinline__ double H2p_trunc(double k3, double R) {
 // (27 entries, [9j+3l+m]). diffop only (the scalar factor is applied by
 // the caller): stokeslet real, rotlet / stresslet purely imaginary.
 template <int KIND>
-__device__ __forceinline__ void diffop_coeffs(double k0, double k1, double k2, double* re, double* im) {
+SEWALD_HD void diffop_coeffs(double k0, double k1, double k2, double* re, double* im) {
     const double kk = k0 * k0 + k1 * k1 + k2 * k2;
     const double kv[3] = {k0, k1, k2};
     if (KIND == SEWALD_STOKESLET) {
@@ -129,7 +135,7 @@ __device__ __forceinline__ void diffop_coeffs(double k0, double k1, double k2, d
 
 // modified_kernel_hat(spec, k) for d in {0,1,2,3} (the d = 3 solve itself uses kspace.cu).
 template <int KIND>
-__device__ __forceinline__ void modified_coeffs(const ModSpec& m, double k0, double k1, double k2,
+SEWALD_HD void modified_coeffs(const ModSpec& m, double k0, double k1, double k2,
                                                 double* re, double* im) {
     constexpr int NG = KIND == SEWALD_STRESSLET ? 27 : 9;
     const bool plain = (m.d == 2 && (k0 != 0.0 || k1 != 0.0)) || (m.d == 1 && k0 != 0.0) || m.d == 3;
@@ -211,5 +217,11 @@ __device__ __forceinline__ void modified_coeffs(const ModSpec& m, double k0, dou
 #pragma unroll
     for (int q = 0; q < 27; ++q) im[q] = 2.0 * cth[q] * H - ctb[q] * B;
 }
+
+// ModifiedKernelSpec fields (any gauge) -> ModSpec with the series blocks
+// (aft.cu), and the optimal gauge (modified_kernels.cpp:52-63).
+ModSpec make_modspec_full(int kind, int d, double R, double a_B, double b_B, double ell_H, double ell_B,
+                          double c_B);
+ModSpec make_modspec(int kind, int d, double R);
 
 }  // namespace sewald_b200
