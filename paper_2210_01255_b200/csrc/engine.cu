@@ -418,7 +418,7 @@ void ensure_gather_weights(sewald_gpu_session* s, int mode, int part, int nparts
     const int key = nparts == 1 ? 0 : part * 4096 + nparts;
     if (s->tg_wpart == key) return;
     const SweepShape sh = sweep_shape(s->g, s->p.P);
-    const TileShape ts = tile_shape(s->g, s->p.P);
+    const TileShape ts = tile_shape(s->g, s->p.P, s->Nt);
     const int64_t nt = mode == 1 ? (int64_t)sh.nbx * sh.nby : ts.ntiles;
     // the sweep buckets tile (x, y) patches over all z starts; the tile path tiles
     const int64_t per = mode == 1 ? (int64_t)s->g.n[2] : 1;
@@ -442,7 +442,7 @@ int ensure_gather_order(sewald_gpu_session* s, int part, int nparts) {
         return -1;
     }();
     const SweepShape sh = sweep_shape(s->g, s->p.P);
-    const TileShape ts = tile_shape(s->g, s->p.P);
+    const TileShape ts = tile_shape(s->g, s->p.P, s->Nt);
     int mode = forced >= 0 ? forced : (s->p.P > 20 ? 1 : 2);
     if (mode == 2 && !ts.ok) mode = sh.ok ? 1 : 0;
     if (mode == 1 && !sh.ok) mode = 0;
@@ -772,7 +772,7 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
             launch_gather_sweep(s->g, s->p.P, s->tg_w.as<double>(), s->tg_sw.as<int4>(), s->tg_off.as<int64_t>(),
                                 sweep_shape(s->g, s->p.P), part, nparts, s->flow.as<double>(), h3, u, st);
         } else if (gmode == 2) {
-            launch_gather_tile(s->g, s->p.P, tile_shape(s->g, s->p.P), s->tg_w.as<double>(), s->tg_sw.as<int4>(),
+            launch_gather_tile(s->g, s->p.P, tile_shape(s->g, s->p.P, s->Nt), s->tg_w.as<double>(), s->tg_sw.as<int4>(),
                                s->tg_off.as<int64_t>(), part, nparts, s->flow.as<double>(), h3, first ? 0 : 1, u,
                                st);
         } else {

@@ -163,7 +163,7 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                  : "d"(a), "d"(b));
 }
 
-template <int MM_L>  // region edge: 19 (B = 20 - P, P <= 16) or 23 (B = 24 - P, P <= 20)
+template <int MM_L>  // region edge: 15 (B = 16 - P), 19 (B = 20 - P, P <= 16) or 23 (B = 24 - P, P <= 20)
 __global__ void __launch_bounds__(MM_THREADS)
 gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64_t tile0,
                        const double* __restrict__ W, const int4* __restrict__ SW, const int64_t* __restrict__ off,
@@ -320,12 +320,25 @@ size_t mma_smem_bytes(int L) {
 
 }  // namespace
 
-TileShape tile_shape(const DevGrid& g, int P) {
+TileShape tile_shape(const DevGrid& g, int P, int64_t Nt) {
     TileShape s{};
     // P <= 16: B = 20 - P (L = 19; CUDA-core or tensor-core kernel);
-    // 16 < P <= 20: B = 24 - P (L = 23; tensor-core kernel only)
+    // 16 < P <= 20: B = 24 - P (L = 23; tensor-core kernel only).
+    // Dense targets and P <= 15: L = 15 (B = 16 - P) when a tile still holds
+    // >= 12 targets on average: the GEMM does (15/19)^2 * 16/20 = 0.5x the work
+    // per target and a tile's region is loaded once per component.
     s.ok = P <= 20;
     s.B = P <= GT_PMAX ? std::max(1, 20 - P) : std::max(1, 24 - P);
+    static const int forced_l = [] {
+        const char* e = getenv("SEWALD_GATHER_L");
+        return e ? atoi(e) : 0;
+    }();
+    if (P <= 15) {
+        const double cells = (double)g.n[0] * g.n[1] * g.n[2];
+        const int b15 = 16 - P;
+        const double tpt = cells > 0 ? (double)Nt / cells * b15 * b15 * b15 : 0.0;
+        if (forced_l == 15 || (forced_l == 0 && tpt >= 12.0)) s.B = b15;
+    }
     s.L = s.B + P - 1;
     for (int ax = 0; ax < 3; ++ax) s.nt[ax] = (g.n[ax] + s.B - 1) / s.B;
     s.ntiles = (int64_t)s.nt[0] * s.nt[1] * s.nt[2];
@@ -354,9 +367,10 @@ void launch_gather_tile(const DevGrid& g, int P, const TileShape& s, const doubl
         const char* e = getenv("SEWALD_GATHER_MMA");
         return !(e && e[0] == '0');
     }();
-    if ((use_mma || P > GT_PMAX) && (s.L == 19 || s.L == 23)) {
+    if ((use_mma || P > GT_PMAX || s.L == 15) && (s.L == 15 || s.L == 19 || s.L == 23)) {
         const size_t sm = mma_smem_bytes(s.L);
-        auto kern = s.L == 19 ? gather_tile_mma_kernel<19> : gather_tile_mma_kernel<23>;
+        auto kern = s.L == 15 ? gather_tile_mma_kernel<15>
+                              : (s.L == 19 ? gather_tile_mma_kernel<19> : gather_tile_mma_kernel<23>);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         for (int64_t a = t0; a < t1; a += (int64_t)1 << 30) {
             const int64_t n = std::min<int64_t>(t1 - a, (int64_t)1 << 30);

@@ -44,7 +44,8 @@ struct TileShape {
     size_t smem;
     bool ok;
 };
-TileShape tile_shape(const DevGrid& g, int P);
+// Nt: number of targets (tile size choice for dense targets)
+TileShape tile_shape(const DevGrid& g, int P, int64_t Nt = 0);
 void launch_tile_bucket(const DevGrid& g, int P, const TileShape& s, const double* x, int64_t N, uint32_t* keys,
                         uint32_t* vals, int* bad, cudaStream_t st);
 void launch_gather_tile(const DevGrid& g, int P, const TileShape& s, const double* W, const int4* SW,
