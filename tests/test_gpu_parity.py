@@ -461,6 +461,38 @@ def test_live_spread_gather_widths(S, ref, P, d, kind, window):
 
 
 @pytest.mark.oracle
+@pytest.mark.parametrize("P,d", [(8, 3), (12, 3), (14, 0), (12, 2)])
+def test_live_gather_dense_targets(S, ref, P, d):
+    """Dense targets (>= 12 per tile): the L = 15 tensor-core gather tiles."""
+    rng = np.random.default_rng(4100 + P + d)
+    cell = S.Cell((1.0, 1.0, 1.0))
+    grid = S.build_grid(cell, d, 1.0 / 24, P, S.Kernel.stokeslet, 4)
+    params = S.EwaldParams(S.Kernel.stokeslet, d, 8.0, 0.2, 0.5, grid, S.WindowSpec.make(S.WindowKind.pkb, P, grid.h))
+    cells = int(np.prod(grid.M_ext))
+    B = 16 - P
+    nt = int(16 * cells / B ** 3) + 1000
+    xt = np.empty((nt, 3))
+    for ax in range(3):
+        xt[:, ax] = rng.random(nt) if ax < d else rng.uniform(0.1, 0.9, nt)
+    field = rng.standard_normal((3,) + tuple(grid.M_ext))
+    # the session's gather (Fourier part only, parts = 1) on an installed flow field
+    import torch
+    dev = torch.device("cuda", 0)
+    T = lambda v: torch.from_numpy(np.ascontiguousarray(v)).to(dev)
+    sess = S.Session(params, cell)
+    sess.set_sources(T(xt[:100]), T(np.zeros((100, 3))))
+    sess.set_targets(T(xt), False)
+    sess.set_flow(T(field.ravel()))
+    u = torch.zeros((nt, 3), dtype=torch.float64, device=dev)
+    sess.evaluate(u, 0, 1, 1)
+    torch.cuda.synchronize()
+    u_gpu = u.cpu().numpy()
+    sess.close()
+    u_ref = ref.gather(ref.params_from(params.to_c()), field, xt)
+    assert np.max(np.abs(u_gpu - u_ref)) <= 1e-13 * np.max(np.abs(u_ref)), (P, d, nt)
+
+
+@pytest.mark.oracle
 @pytest.mark.parametrize("P", [16, 18, 24])
 def test_live_clustered_sources(S, ref, P):
     """Thousands of points inside a few grid cells: one tile holds many
