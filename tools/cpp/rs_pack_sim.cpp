@@ -21,24 +21,28 @@ int main(int argc, char** argv) {
     const int nclusters = argc > 4 ? atoi(argv[4]) : 400;
     const int CS = argc > 5 ? atoi(argv[5]) : 32;  // i-cluster size; lanes l and l+CS.. share i
     const int W = argc > 6 ? atoi(argv[6]) : 4;    // blocks pooled by the windowed packer
+    const double AX = argc > 7 ? atof(argv[7]) : 1.0;  // cell aspect w_x / w_yz (cell volume kept)
     std::mt19937_64 rng(7);
     std::uniform_real_distribution<double> U(0.0, 1.0);
     std::vector<double> x(3 * (size_t)N);
     for (auto& v : x) v = U(rng);
-    int nc = std::max(1, (int)std::floor(std::cbrt(N / ppc)));
-    const double w = 1.0 / nc;
+    const double nc0 = std::cbrt(N / ppc);
+    const int ncx = std::max(1, (int)std::floor(nc0 / std::pow(AX, 2.0 / 3.0)));
+    const int nc = std::max(1, (int)std::floor(nc0 * std::pow(AX, 1.0 / 3.0)));  // y, z
+    const double w = 1.0 / nc, wx = 1.0 / ncx;
     std::vector<uint64_t> key(N);
     std::vector<int> idx(N);
     for (int i = 0; i < N; ++i) {
         int c[3];
-        for (int a = 0; a < 3; ++a) c[a] = std::min(nc - 1, (int)(x[3 * i + a] / w));
-        int sub = std::min(255, (int)((x[3 * i] / w - c[0]) * 256));
-        key[i] = ((((uint64_t)c[2] * nc + c[1]) * nc + c[0]) << 8) | sub;
+        c[0] = std::min(ncx - 1, (int)(x[3 * i] / wx));
+        for (int a = 1; a < 3; ++a) c[a] = std::min(nc - 1, (int)(x[3 * i + a] / w));
+        int sub = std::min(255, (int)((x[3 * i] / wx - c[0]) * 256));
+        key[i] = ((((uint64_t)c[2] * nc + c[1]) * ncx + c[0]) << 8) | sub;
         idx[i] = i;
     }
     std::sort(idx.begin(), idx.end(), [&](int a, int b) { return key[a] < key[b]; });
     std::vector<double> p(3 * (size_t)N);
-    std::vector<int64_t> off((size_t)nc * nc * nc + 1, 0);
+    std::vector<int64_t> off((size_t)nc * nc * ncx + 1, 0);
     for (int k = 0; k < N; ++k) {
         for (int a = 0; a < 3; ++a) p[3 * k + a] = x[3 * idx[k] + a];
         off[(key[idx[k]] >> 8) + 1]++;
@@ -88,8 +92,9 @@ int main(int argc, char** argv) {
         const int64_t istart = CS * (int64_t)cl;
         int clo[3], chi[3];
         for (int a = 0; a < 3; ++a) {
-            clo[a] = (int)std::floor((lo[a] - rc) / w);
-            chi[a] = (int)std::floor((hi[a] + rc) / w);
+            const double wa = a == 0 ? wx : w;
+            clo[a] = (int)std::floor((lo[a] - rc) / wa);
+            chi[a] = (int)std::floor((hi[a] + rc) / wa);
         }
         for (int cz = clo[2]; cz <= chi[2]; ++cz)
             for (int cy = clo[1]; cy <= chi[1]; ++cy) {
@@ -99,10 +104,10 @@ int main(int argc, char** argv) {
                 double lat2 = dy * dy + dz * dz;
                 if (lat2 >= rc2) continue;
                 double ext = std::sqrt(rc2 - lat2);
-                int cxl = std::max((int)std::floor((lo[0] - ext) / w), clo[0]);
-                int cxh = std::min((int)std::floor((hi[0] + ext) / w), chi[0]);
+                int cxl = std::max((int)std::floor((lo[0] - ext) / wx), clo[0]);
+                int cxh = std::min((int)std::floor((hi[0] + ext) / wx), chi[0]);
                 if (cxl > cxh) continue;
-                int64_t rb = ((int64_t)cz * nc + cy) * nc;
+                int64_t rb = ((int64_t)cz * nc + cy) * ncx;
                 int64_t b0 = off[rb + cxl], b1 = off[rb + cxh + 1];
                 if (b0 < istart) b0 = istart;
                 for (int64_t jb = b0; jb < b1; jb += 32) {
