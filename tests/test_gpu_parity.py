@@ -368,6 +368,28 @@ def test_full_size_c2_xi_invariance(S):
     assert rms <= 10.0 * (cfg.tol + cfg.tol)
 
 
+@pytest.mark.parametrize("cfg_id,xi_b", [(3, 40.0), (4, 40.0), (5, 60.0)])
+def test_full_size_xi_invariance(S, cfg_id, xi_b):
+    """BASELINE configs 3-5 at full size (D = 2 stresslet 1e6, D = 1 rotlet 5e5 + 5e5
+    separate targets with the TG window, D = 0 stokeslet 4e6): the full velocity
+    at the pinned xi and at xi_b agree to the tolerance (test_realspace.cpp:516-540)."""
+    from paper_2210_01255_b200.workloads import CONFIGS, generate
+    cfg = CONFIGS[cfg_id]
+    x, f, nu, xt = generate(cfg)
+    sysm = S.SourceSystem(cfg.kind, S.Cell(cfg.L), cfg.d, x, f, nu)
+    tg = S.TargetSet.from_sources(sysm) if xt is None else S.TargetSet(xt, False)
+    Q = S.source_quantity(sysm)
+    opt = S.SelectionOptions(4, cfg.window, True)
+    pa = S.select_parameters(cfg.kind, cfg.d, sysm.cell, Q, cfg.xi, S.ToleranceSpec(cfg.tol), opt).params
+    pb = S.select_parameters(cfg.kind, cfg.d, sysm.cell, Q, xi_b, S.ToleranceSpec(cfg.tol), opt).params
+    ua = S.full_potential(sysm, tg, pa)
+    ub = S.full_potential(sysm, tg, pb)
+    rms = float(np.sqrt(np.mean(np.sum((ua - ub) ** 2, 1))))
+    rms_u = float(np.sqrt(np.mean(np.sum(ua ** 2, 1))))
+    print(f"{cfg.name}: rms(u)={rms_u:.6g} rms(u_a-u_b)={rms:.3e} (tau={cfg.tol})")
+    assert rms <= 10.0 * (cfg.tol + cfg.tol)
+
+
 @pytest.mark.oracle
 def test_full_size_c2_realspace_subset(S, ref):
     """Real-space sum at N = 1e6 for a subset of targets against the reference
