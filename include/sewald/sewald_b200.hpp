@@ -293,8 +293,9 @@ struct FourierField {
 };
 
 // D = 0 kernel table (fourier.h:52-57). se_fourier_potential builds and caches
-// it on the device per parameter set; precompute_0p() returns it on the host
-// for the stage API.
+// it on the device per parameter set unless SePipelineOptions::table supplies
+// one (then that table is used, as in the reference); precompute_0p() returns
+// it on the host.
 struct PrecomputedKernel0P {
     Kernel kind = Kernel::stokeslet;
     std::array<int, 3> n{};

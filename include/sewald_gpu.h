@@ -232,6 +232,15 @@ int sewald_gpu_scale_table(sewald_gpu_ctx* ctx, const sewald_params_c* p, int ki
 int sewald_gpu_precompute_0p(sewald_gpu_ctx* ctx, const sewald_params_c* p, int kind, double R,
                              int32_t n_out[3], double* table_out);
 
+/* SePipelineOptions::table (fourier.h:76-79): install a caller-built D = 0
+ * kernel table (precompute_0p layout, prod(n) interleaved complex, host or
+ * device memory) for the pipelines run with parameters p on this context;
+ * table == NULL goes back to the engine's own table. n must be 2 M_ext
+ * (the table path pads with s0 = 2). Passing the same pointer again skips
+ * the upload. */
+int sewald_gpu_set_table0p(sewald_gpu_ctx* ctx, const sewald_params_c* p, const int32_t n[3],
+                           const double* table);
+
 /* ---- device-resident session (time stepping / multi-GPU plumbing) ---- */
 /* A session keeps sources, targets, sort permutations, grids and cuFFT plans
  * resident in HBM between calls. All pointers given to *_dev calls are
@@ -286,6 +295,8 @@ int sewald_gpu_session_d0_middle(sewald_gpu_session* s, int precompute_0p, const
                                  const int* x_bounds, int ka, int kb, void* send_dev);
 int sewald_gpu_session_d0_inverse(sewald_gpu_session* s, int precompute_0p, const void* recv_dev, int xa, int xb,
                                   int world, const int* kz_bounds, double* flow_slab_dev);
+/* Session form of sewald_gpu_set_table0p. */
+int sewald_gpu_session_set_table0p(sewald_gpu_session* s, const int32_t n[3], const double* table);
 /* Install a full flow field (3 comps, M_ext, device) for evaluate()'s gather. */
 int sewald_gpu_session_set_flow(sewald_gpu_session* s, const double* flow_dev);
 /* Accepted real-space pairs counted since the last reset (synchronises). */

@@ -111,6 +111,8 @@ _SIGS = [
                                          C.c_double, C.POINTER(sewald_fourier_geom_c), DP, DP]),
     ("sewald_gpu_precompute_0p", C.c_int, [VP, C.POINTER(sewald_params_c), C.c_int, C.c_double,
                                            C.POINTER(C.c_int32), DP]),
+    ("sewald_gpu_set_table0p", C.c_int, [VP, C.POINTER(sewald_params_c), C.POINTER(C.c_int32), DP]),
+    ("sewald_gpu_session_set_table0p", C.c_int, [VP, C.POINTER(C.c_int32), DP]),
     ("sewald_gpu_session_create", C.c_int, [VP, C.POINTER(sewald_params_c), C.POINTER(VP)]),
     ("sewald_gpu_session_destroy", None, [VP]),
     ("sewald_gpu_session_set_sources", C.c_int, [VP, VP, VP, VP, I64]),

@@ -108,9 +108,11 @@ class SelectionOptions:
 
 @dataclass
 class SePipelineOptions:
-    """struct SePipelineOptions (fourier.h:76-79). `table` reuse is implicit:
-    the device session caches the D=0 kernel table per parameter set."""
+    """struct SePipelineOptions (fourier.h:76-79). Without `table` the device
+    session builds the D=0 kernel table once per parameter set and keeps it;
+    a caller-built `table` (precompute_0p) is used instead."""
     precompute_0p: bool = True
+    table: Optional["PrecomputedKernel0P"] = None
 
 
 @dataclass
@@ -402,7 +404,19 @@ def _pipeline(entry: str, system: SourceSystem, targets: TargetSet, params: Ewal
     u = _out_array(out, nt)
     eng = engine or default_engine()
     c = _params_for(system, params)
+    tab = opt.table
+    if tab is not None and Kernel(tab.kind) != Kernel(params.kind):
+        raise InvalidArgument("kernel table was built for a different kernel")
     with eng._lock:
+        if int(params.d) == 0 and opt.precompute_0p:
+            if tab is None:
+                eng.check(eng._lib.sewald_gpu_set_table0p(eng.ctx, C.byref(c), None, None))
+            else:
+                tb = np.ascontiguousarray(np.asarray(tab.table, dtype=np.complex128).ravel())
+                if tb.size != int(np.prod(tab.n)):
+                    raise InvalidArgument("kernel table storage is inconsistent")
+                tn = (C.c_int32 * 3)(*[int(v) for v in tab.n])
+                eng.check(eng._lib.sewald_gpu_set_table0p(eng.ctx, C.byref(c), tn, _cdp(tb)))
         fn = getattr(eng._lib, entry)
         eng.check(fn(eng.ctx, C.byref(c), _dp(x), _dp(f), _dp(nu), x.shape[0], _dp(xt), nt,
                      int(same), int(bool(opt.precompute_0p)), _dp(u)))

@@ -400,6 +400,14 @@ int build_table_0p(const sewald_params_c& p, int kind, double R, DevBuf& out, cu
 namespace {
 
 void build_table_0p(sewald_gpu_session* s, FourierPlanAFT& A) {
+    if (s->has_user_table) {  // SePipelineOptions::table: the caller's table is used as is
+        const size_t bytes = sizeof(cuDoubleComplex) * 8 * (size_t)s->p.M_ext[0] * s->p.M_ext[1] * s->p.M_ext[2];
+        A.table0p.ensure(bytes);
+        cuda_check(cudaMemcpyAsync(A.table0p.ptr, s->user_table0p.ptr, bytes, cudaMemcpyDeviceToDevice,
+                                   s->ctx->stream),
+                   "user table");
+        return;
+    }
     s->ctx->launches += build_table_0p(s->p, s->p.kind, s->p.R, A.table0p, s->ctx->stream);
 }
 
@@ -696,6 +704,29 @@ void aft_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p) {
                                                              flow);
     s->ctx->launches += 10;
     cuda_check(cudaGetLastError(), "aft d12");
+}
+
+void session_set_table0p(sewald_gpu_session* s, const int32_t n[3], const double* table) {
+    if (!table) {
+        if (s->has_user_table) s->aft.reset();
+        s->has_user_table = false;
+        s->user_table_src = nullptr;
+        return;
+    }
+    if (s->has_user_table && s->user_table_src == table) return;  // same table object as before
+    if (s->p.d != 0) throw EngineError(SEWALD_EINVAL, "precomputed kernels apply to d = 0 only");
+    // the table path pads with s0 = 2 (fourier.cpp:819-821), so the table must
+    // live on the (2 M_ext)^3 mode grid (fourier.cpp:672-673)
+    for (int ax = 0; ax < 3; ++ax)
+        if (n[ax] != 2 * s->p.M_ext[ax])
+            throw EngineError(SEWALD_EINVAL, "kernel table was built for a different padded grid");
+    const size_t bytes = sizeof(cuDoubleComplex) * (size_t)n[0] * n[1] * n[2];
+    s->user_table0p.ensure(bytes);
+    cuda_check(cudaMemcpyAsync(s->user_table0p.ptr, table, bytes, cudaMemcpyDefault, s->ctx->stream), "table in");
+    cuda_check(cudaStreamSynchronize(s->ctx->stream), "table in");
+    s->has_user_table = true;
+    s->user_table_src = table;
+    s->aft.reset();  // the next table-path solve rebuilds its plan with this table
 }
 
 // ---- slab-distributed D = 0 solve: stage wrappers ------------------

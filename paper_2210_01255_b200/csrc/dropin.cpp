@@ -589,6 +589,15 @@ std::vector<Vec3> pipeline(bool full, const SourceSystem& s, const TargetSet& t,
     std::vector<Vec3> u(nt);
     const double* nu = s.kind == Kernel::stresslet ? D(s.nu) : nullptr;
     std::lock_guard<std::mutex> lk(g_mu);
+    // SePipelineOptions::table: the caller's table replaces the engine's own
+    // (fourier.cpp:822-829); without one the engine builds / reuses its own.
+    if (e.d == 0 && opt.precompute_0p) {
+        const int32_t tn[3] = {opt.table ? opt.table->n[0] : 0, opt.table ? opt.table->n[1] : 0,
+                               opt.table ? opt.table->n[2] : 0};
+        if (opt.table && opt.table->table.size() != static_cast<std::size_t>(tn[0]) * tn[1] * tn[2])
+            throw std::invalid_argument("kernel table storage is inconsistent");
+        check_ctx(sewald_gpu_set_table0p(context(), &p, tn, opt.table ? Z(opt.table->table) : nullptr));
+    }
     auto fn = full ? sewald_gpu_full_potential : sewald_gpu_fourier_potential;
     check_ctx(fn(context(), &p, D(s.x), D(s.f), nu, static_cast<int64_t>(s.size()),
                  t.same_as_sources ? nullptr : D(t.x), static_cast<int64_t>(nt), t.same_as_sources ? 1 : 0,

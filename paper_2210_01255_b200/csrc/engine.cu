@@ -1103,6 +1103,17 @@ int sewald_gpu_precompute_0p(sewald_gpu_ctx* ctx, const sewald_params_c* p, int 
     });
 }
 
+int sewald_gpu_set_table0p(sewald_gpu_ctx* ctx, const sewald_params_c* p, const int32_t n[3],
+                           const double* table) {
+    if (!ctx || !p || (table && !n)) return SEWALD_EINVAL;
+    return ctx_guard(ctx, [&] { session_set_table0p(cached_session(ctx, *p), n, table); });
+}
+
+int sewald_gpu_session_set_table0p(sewald_gpu_session* s, const int32_t n[3], const double* table) {
+    if (!s || (table && !n)) return SEWALD_EINVAL;
+    return ctx_guard(s->ctx, [&] { session_set_table0p(s, n, table); });
+}
+
 int sewald_gpu_session_create(sewald_gpu_ctx* ctx, const sewald_params_c* p, sewald_gpu_session** out) {
     if (!ctx || !p || !out) return SEWALD_EINVAL;
     *out = nullptr;

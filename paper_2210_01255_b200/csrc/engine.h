@@ -94,6 +94,11 @@ struct sewald_gpu_session {
     bool sums_ready = false;
     std::unique_ptr<sewald_b200::FourierPlanD3> d3;
     std::unique_ptr<sewald_b200::FourierPlanAFT, sewald_b200::AftDeleter> aft;
+    // D = 0 kernel table supplied by the caller (SePipelineOptions::table,
+    // fourier.h:76-79); used instead of building one when set
+    sewald_b200::DevBuf user_table0p;
+    bool has_user_table = false;
+    const void* user_table_src = nullptr;  // caller's pointer (re-upload skipped when unchanged)
 };
 
 namespace sewald_b200 {
@@ -124,6 +129,8 @@ void stage_scale(sewald_gpu_ctx* ctx, const sewald_params_c& p, int kind, const 
 void stage_precompute_0p(sewald_gpu_ctx* ctx, const sewald_params_c& p, int kind, double R, int32_t n_out[3],
                          double* table_out);
 int build_table_0p(const sewald_params_c& p, int kind, double R, DevBuf& out, cudaStream_t st);
+// Install (table != nullptr) or clear a caller-built D = 0 table on the session.
+void session_set_table0p(sewald_gpu_session* s, const int32_t n[3], const double* table);
 // Slab-distributed D = 0 solve stages (aft.cu / aft_d0.cu).
 struct SlabBounds;
 void aft_d0_geometry(sewald_gpu_session* s, bool use_table, int m[3], int n[3], int* h2, int* C);

@@ -228,3 +228,37 @@ def test_stage_errors(S):
     bad = S.FourierField(**{**F.__dict__, "d": 1})
     with pytest.raises(S.InvalidArgument, match="periodicity differ"):
         S.aft_inverse(bad, grid, plan)
+
+
+@pytest.mark.gpu
+@pytest.mark.oracle
+def test_pipeline_uses_caller_table(S, ref):
+    """SePipelineOptions::table (fourier.h:76-79, fourier.cpp:822-829): the
+    caller's table replaces the engine's own. With the engine's own R the
+    result is unchanged; with a table built for another R it follows that
+    table, as the reference's stage composition with the same table does."""
+    rng = np.random.default_rng(580)
+    N = 200
+    L = (0.5, 0.5, 0.5)
+    x = rng.uniform(0.15, 0.35, (N, 3))
+    f = rng.standard_normal((N, 3))
+    sysm = S.SourceSystem(S.Kernel.rotlet, S.Cell(L), 0, x, f, None)
+    tg = S.TargetSet.from_sources(sysm)
+    p = S.select_parameters(S.Kernel.rotlet, 0, sysm.cell, S.source_quantity(sysm), 12.0, S.ToleranceSpec(1e-9)).params
+    u0 = S.se_fourier_potential(sysm, tg, p)
+    own = S.precompute_0p(S.Kernel.rotlet, p.grid, p.R)
+    u1 = S.se_fourier_potential(sysm, tg, p, S.SePipelineOptions(True, own))
+    _close(u1, u0, 1e-14)
+    R2 = 0.1 * p.R  # shorter than the source spread: truncates real interactions
+    other = S.precompute_0p(S.Kernel.rotlet, p.grid, R2)
+    u2 = S.se_fourier_potential(sysm, tg, p, S.SePipelineOptions(True, other))
+    # reference stages with the same table (fourier.cpp:816-846)
+    plan2 = S.UpsamplingPlan(2.0, p.upsampling.s_star, tuple(p.upsampling.k_star))
+    rp = ref.params_from(S.EwaldParams(p.kind, 0, p.xi, p.rc, p.R, p.grid, p.window, plan2).to_c())
+    phi = ref.spread(rp, x, f, None)
+    F = ref.scale_table(rp, ref.aft_forward(rp, phi), 2, R2, p.xi)
+    ur = ref.gather(rp, ref.aft_inverse(rp, F), x)
+    _close(u2, ur, 1e-12)
+    assert np.max(np.abs(u2 - u0)) > 1e-10 * np.max(np.abs(u0))  # the table made a difference
+    # back to the engine's own table
+    _close(S.se_fourier_potential(sysm, tg, p), u0, 1e-14)
