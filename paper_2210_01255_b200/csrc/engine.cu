@@ -724,7 +724,12 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
         const char* e = getenv("SEWALD_RS_SYM");
         return !(e && e[0] == '0');
     }();
-    const bool use_sym = (parts & 2) && s->same && sym_enabled;
+    // Small target sets (fewer 32-target groups than resident warps) take the
+    // non-symmetric kernel with each group's rows split over several warps and
+    // a fixed-order combination: the whole GPU works on them and the result is
+    // independent of scheduling (no reactions, no atomics).
+    const int rs_split = realspace_split(t1 - t0);
+    const bool use_sym = (parts & 2) && s->same && sym_enabled && rs_split == 1;
     // The pair-symmetric real-space sum adds reactions to any particle, and
     // multi-part evaluation is combined by summing the per-part outputs: in
     // both cases the whole output is zeroed here and every stage accumulates.
@@ -757,9 +762,13 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
                                  static_cast<unsigned long long*>(s->work_counter.ensure(sizeof(unsigned long long))),
                                  st);
         } else {
+            double* scratch = rs_split > 1 ? static_cast<double*>(s->rs_scratch.ensure(
+                                                  sizeof(double) * 3 * (size_t)rs_split * (size_t)(t1 - t0)))
+                                            : nullptr;
             launch_realspace(s->cg, a, s->packed.as<double>(), s->packedf.as<float4>(), s->stresslet,
                              s->c_off.as<int64_t>(), target_folded(s), torder + t0, t1 - t0, u, first ? 0 : 1,
-                             s->pair_counter.as<unsigned long long>(), s->flags.as<int>() + FLAG_SINGULAR, st);
+                             s->pair_counter.as<unsigned long long>(), s->flags.as<int>() + FLAG_SINGULAR, rs_split,
+                             scratch, st);
         }
         ++s->ctx->launches;
         first = false;

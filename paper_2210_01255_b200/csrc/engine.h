@@ -90,7 +90,7 @@ struct sewald_gpu_session {
     // grids
     sewald_b200::DevBuf grid, flow;
     // global sums: f (3), q.nu (1), x (q.nu) (3); partials
-    sewald_b200::DevBuf sums, partials, flags, pair_counter, work_counter;
+    sewald_b200::DevBuf sums, partials, flags, pair_counter, work_counter, rs_scratch;
     bool sums_ready = false;
     std::unique_ptr<sewald_b200::FourierPlanD3> d3;
     std::unique_ptr<sewald_b200::FourierPlanAFT, sewald_b200::AftDeleter> aft;

@@ -19,6 +19,8 @@
 // the same order, |r|^2 formed without FMA contraction and compared with
 // rc*rc, and the self pair skipped only on the primary image.
 #include "device_common.cuh"
+
+#include <algorithm>
 #include "sg_kernels.h"
 #include "../../include/sewald_gpu.h"
 #include "screened_math.cuh"
@@ -145,7 +147,7 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
                  const float4* __restrict__ packedf, const int64_t* __restrict__ cell_off,
                  const double* __restrict__ tfolded, const uint32_t* __restrict__ torder, int64_t Nt,
                  double* __restrict__ u, int accumulate, unsigned long long* __restrict__ pair_count,
-                 int* __restrict__ err) {
+                 int* __restrict__ err, int split, double* __restrict__ scratch) {
     __shared__ __align__(16) double src_all[RS_WARPS][WCHUNK * S];
     __shared__ float4 srcf_all[RS_WARPS][WCHUNK];
     __shared__ uint8_t queue_all[RS_WARPS][WCHUNK][32];
@@ -158,8 +160,15 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
     float4* srcf = srcf_all[warp];
     uint8_t(*queue)[32] = queue_all[warp];
 
-    const int64_t t = ((int64_t)blockIdx.x * RS_WARPS + warp) * 32 + lane;
-    if (((int64_t)blockIdx.x * RS_WARPS + warp) * 32 >= Nt) return;  // whole warp idle
+    // work item = (32-target group, row part): small target sets split each
+    // group's neighbour rows over `split` warps; the parts' sums are added in
+    // a fixed order afterwards (realspace_sum_parts), so results do not
+    // depend on scheduling
+    const int64_t witem = (int64_t)blockIdx.x * RS_WARPS + warp;
+    const int64_t group = witem / split;
+    const int part = (int)(witem % split);
+    const int64_t t = group * 32 + lane;
+    if (group * 32 >= Nt) return;  // whole warp idle
     const bool valid = t < Nt;
     double xt0 = 0, xt1 = 0, xt2 = 0;
     int64_t tori = -1;
@@ -200,6 +209,7 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
 
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
     unsigned long long npairs = 0;
+    int row_id = -1;
 
     for (int cz = clo[2]; cz <= chi[2]; ++cz) {
         const int sz = 2 < cg.d ? floor_div(cz, cg.n[2]) : 0;
@@ -208,6 +218,7 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
         const double dz = fmax(0.0, fmax(zlo - hi[2], lo[2] - zhi));
         const double shz = (double)sz * cg.L[2];
         for (int cy = clo[1]; cy <= chi[1]; ++cy) {
+            if (split > 1 && (++row_id) % split != part) continue;
             const int sy = 1 < cg.d ? floor_div(cy, cg.n[1]) : 0;
             const int jy = cy - sy * cg.n[1];
             const double ylo = cg.origin[1] + cy * cg.w[1], yhi = ylo + cg.w[1];
@@ -276,7 +287,12 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
         }
     }
 
-    if (valid) {
+    if (valid && split > 1) {
+        double* o = scratch + ((int64_t)part * Nt + t) * 3;
+        o[0] = acc0;
+        o[1] = acc1;
+        o[2] = acc2;
+    } else if (valid) {
         if (accumulate) {
             u[3 * tori] += acc0;
             u[3 * tori + 1] += acc1;
@@ -294,7 +310,41 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
     }
 }
 
+// u[torder[t]] (=, +=) sum over parts p = 0, 1, ... of scratch[p][t], in order.
+__global__ void realspace_sum_parts(const double* __restrict__ scratch, int split, const uint32_t* __restrict__ torder,
+                                    int64_t Nt, double* __restrict__ u, int accumulate) {
+    const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (t >= Nt) return;
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+    for (int p = 0; p < split; ++p) {
+        const double* o = scratch + ((int64_t)p * Nt + t) * 3;
+        v0 += o[0];
+        v1 += o[1];
+        v2 += o[2];
+    }
+    double* d = u + 3 * (int64_t)torder[t];
+    if (accumulate) {
+        d[0] += v0;
+        d[1] += v1;
+        d[2] += v2;
+    } else {
+        d[0] = v0;
+        d[1] = v1;
+        d[2] = v2;
+    }
+}
+
 }  // namespace
+
+int realspace_split(int64_t Nt) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t groups = (Nt + 31) / 32;
+    const int64_t warps = (int64_t)sms * 4 * RS_WARPS;  // resident at the launch bound
+    if (groups <= 0 || groups >= warps) return 1;
+    return (int)std::min<int64_t>(16, (2 * warps + groups - 1) / groups);
+}
 
 void launch_fold_and_key(const CellGrid& cg, const double* x, int64_t N, double* folded,
                          uint32_t* keys, uint32_t* vals, cudaStream_t st) {
@@ -313,23 +363,27 @@ void launch_pack_sources(const double* folded, const double* f, const double* nu
 void launch_realspace(const CellGrid& cg, const RealspaceArgs& a, const double* packed,
                       const float4* packedf, int stresslet, const int64_t* cell_off, const double* tfolded,
                       const uint32_t* torder, int64_t Nt, double* u, int accumulate,
-                      unsigned long long* pair_count, int* err, cudaStream_t st) {
+                      unsigned long long* pair_count, int* err, int split, double* scratch, cudaStream_t st) {
     if (Nt == 0) return;
-    const unsigned blocks = (unsigned)((Nt + RS_THREADS - 1) / RS_THREADS);
+    if (!scratch) split = 1;
+    const int64_t items = ((Nt + 31) / 32) * split;
+    const unsigned blocks = (unsigned)((items + RS_WARPS - 1) / RS_WARPS);
     const bool shrt = a.xi * a.rc <= SEWALD_ERFCX8_XMAX;  // shorter erfcx rational suffices
 #define SEWALD_RS_LAUNCH(K, SZ)                                                                              \
     if (shrt)                                                                                                \
         realspace_kernel<K, SZ, true><<<blocks, RS_THREADS, 0, st>>>(cg, a, packed, packedf, cell_off, tfolded, \
-                                                                     torder, Nt, u, accumulate, pair_count, err); \
+                                                                     torder, Nt, u, accumulate, pair_count, err, split, scratch); \
     else                                                                                                     \
         realspace_kernel<K, SZ, false><<<blocks, RS_THREADS, 0, st>>>(cg, a, packed, packedf, cell_off, tfolded, \
-                                                                      torder, Nt, u, accumulate, pair_count, err);
+                                                                      torder, Nt, u, accumulate, pair_count, err, split, scratch);
     switch (a.kind) {
         case SEWALD_STOKESLET: SEWALD_RS_LAUNCH(SEWALD_STOKESLET, 8) break;
         case SEWALD_ROTLET: SEWALD_RS_LAUNCH(SEWALD_ROTLET, 8) break;
         default: SEWALD_RS_LAUNCH(SEWALD_STRESSLET, 12) break;
     }
 #undef SEWALD_RS_LAUNCH
+    if (split > 1)
+        realspace_sum_parts<<<(unsigned)((Nt + 255) / 256), 256, 0, st>>>(scratch, split, torder, Nt, u, accumulate);
 }
 
 }  // namespace sewald_b200

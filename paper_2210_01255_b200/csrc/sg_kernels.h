@@ -115,10 +115,14 @@ void launch_fold_and_key(const CellGrid& cg, const double* x, int64_t N, double*
 void launch_pack_sources(const double* folded, const double* f, const double* nu, int stresslet,
                          const uint32_t* order, int64_t N, double* packed, float4* packedf,
                          cudaStream_t st);
+// Non-symmetric real-space sum for targets torder[0..Nt). split > 1 (small
+// target sets, realspace_split) needs scratch of split * Nt * 3 doubles: the
+// row parts' sums are combined in a fixed order (deterministic results).
 void launch_realspace(const CellGrid& cg, const RealspaceArgs& a, const double* packed,
                       const float4* packedf, int stresslet, const int64_t* cell_off, const double* tfolded,
                       const uint32_t* torder, int64_t Nt, double* u, int accumulate,
-                      unsigned long long* pair_count, int* err, cudaStream_t st);
+                      unsigned long long* pair_count, int* err, int split, double* scratch, cudaStream_t st);
+int realspace_split(int64_t Nt);
 
 // Symmetric real-space sum for targets == sources (realspace_sym.cu):
 // i-clusters [c0, c1) of 32 cell-ordered particles; u (original order) must

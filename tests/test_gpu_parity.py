@@ -368,6 +368,29 @@ def test_full_size_c2_xi_invariance(S):
     assert rms <= 10.0 * (cfg.tol + cfg.tol)
 
 
+@pytest.mark.parametrize("kind,d,N", [(0, 3, 300), (1, 3, 257), (2, 1, 2000), (0, 0, 50000)])
+def test_small_systems_deterministic(S, kind, d, N):
+    """Small systems (row-split non-symmetric real space, fixed-order sums):
+    repeated real-space evaluations are bit-identical, as the reference's
+    thread-count test requires (test_realspace.cpp:449-456). The full velocity
+    also carries the spread, whose tensor-core tiles add into the grid with
+    fp64 atomics (order-dependent last bits, accepted by the north_star)."""
+    rng = np.random.default_rng(77 + kind + d)
+    L = (1.0, 1.0, 1.0)
+    x = rng.random((N, 3))
+    f = rng.standard_normal((N, 3))
+    nu = rng.standard_normal((N, 3)) if kind == 1 else None
+    sysm = S.SourceSystem(S.Kernel(kind), S.Cell(L), d, x, f, nu)
+    tg = S.TargetSet.from_sources(sysm)
+    p = S.select_parameters(sysm.kind, d, sysm.cell, S.source_quantity(sysm), 10.0, S.ToleranceSpec(1e-8)).params
+    ua = S.realspace_potential(sysm, tg, p.xi, p.rc, True)
+    ub = S.realspace_potential(sysm, tg, p.xi, p.rc, True)
+    assert np.array_equal(ua, ub)
+    fa = S.full_potential(sysm, tg, p)
+    fb = S.full_potential(sysm, tg, p)
+    assert rel_rms(fa, fb) < 1e-14
+
+
 @pytest.mark.parametrize("cfg_id,xi_b", [(3, 40.0), (4, 40.0), (5, 60.0)])
 def test_full_size_xi_invariance(S, cfg_id, xi_b):
     """BASELINE configs 3-5 at full size (D = 2 stresslet 1e6, D = 1 rotlet 5e5 + 5e5
