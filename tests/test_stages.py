@@ -68,9 +68,9 @@ def _scale_tol(d):
     return 2e-11 if d == 1 else TOL
 
 
-def _params(S, kind, grid, plan, R, xi=5.0, P=10):
-    return S.EwaldParams(S.Kernel(kind), grid.d, xi, 0.3, R, grid,
-                         S.WindowSpec.make(S.WindowKind.kb, P, grid.h), plan)
+def _params(S, kind, grid, plan, R, xi=5.0, P=10, window=None):
+    wk = S.WindowKind.kb if window is None else window
+    return S.EwaldParams(S.Kernel(kind), grid.d, xi, 0.3, R, grid, S.WindowSpec.make(wk, P, grid.h), plan)
 
 
 # ---------------------------------------------------------------------------
@@ -122,12 +122,15 @@ def test_geometry_errors(S):
 
 @pytest.mark.gpu
 @pytest.mark.oracle
+@pytest.mark.parametrize("window", [0, 1, 2])
 @pytest.mark.parametrize("kind", [0, 1, 2])
-def test_stages_against_reference(S, ref, kind):
-    rng = np.random.default_rng(500 + kind)
+def test_stages_against_reference(S, ref, kind, window):
+    """Each stage for every kernel, periodicity class and window (the scale
+    divides by the window's transform: exact KB for KB / PKB, Gaussian for TG)."""
+    rng = np.random.default_rng(500 + kind + 7 * window)
     comps = S.strength_components(S.Kernel(kind))
     for name, grid, plan, R in _cases(S):
-        p = _params(S, kind, grid, plan, R)
+        p = _params(S, kind, grid, plan, R, window=S.WindowKind(window))
         rp = ref.params_from(p.to_c())
         phi = rng.standard_normal((comps,) + tuple(grid.M_ext))
         # aft_forward
