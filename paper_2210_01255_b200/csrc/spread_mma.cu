@@ -143,6 +143,118 @@ spread_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
     }
 }
 
+// Same contraction with every source table of a tile chunk (up to CT_TMAX
+// sources) staged once in shared memory and reused by all components: the
+// per-group table rebuild (global tap loads + two block barriers per group
+// and component) of the kernel above leaves the tensor pipe waiting on memory.
+constexpr int CT_TMAX = 256;
+constexpr int CT_CMAX = 9;
+
+size_t cached_smem_bytes() { return sizeof(double) * (size_t)CT_TMAX * (3 * SM_LS + CT_CMAX); }
+
+template <int L>
+__global__ void __launch_bounds__(SM_THREADS)
+spread_tile_mma_cached_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64_t tile0,
+                              const double* __restrict__ W, const int4* __restrict__ SW,
+                              const double* __restrict__ STR, int C, const int64_t* __restrict__ off,
+                              double* __restrict__ out) {
+    constexpr int ROWS = L * L;
+    constexpr int RB = (ROWS + 7) / 8;
+    constexpr int RBW = (RB + SM_WARPS - 1) / SM_WARPS;  // row blocks per warp
+    extern __shared__ __align__(16) double csm[];
+    double(*wx)[SM_LS] = reinterpret_cast<double(*)[SM_LS]>(csm);
+    double(*wy)[SM_LS] = reinterpret_cast<double(*)[SM_LS]>(csm + CT_TMAX * SM_LS);
+    double(*wz)[SM_LS] = reinterpret_cast<double(*)[SM_LS]>(csm + 2 * CT_TMAX * SM_LS);
+    double* fs = csm + 3 * CT_TMAX * SM_LS;  // [CT_TMAX][C]
+
+    const int64_t tile = tile0 + blockIdx.x;
+    const int64_t p0 = off[tile], p1 = off[tile + 1];
+    if (p0 >= p1) return;
+    const int tz = (int)(tile % ntz);
+    const int ty = (int)((tile / ntz) % nty);
+    const int tx = (int)(tile / ((int64_t)ntz * nty));
+    const int X0 = tx * B, Y0 = ty * B, Z0 = tz * B;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t cs = (int64_t)g.n[0] * g.n[1] * g.n[2];
+
+    for (int64_t q0 = p0; q0 < p1; q0 += CT_TMAX) {
+        const int T = (int)min((int64_t)CT_TMAX, p1 - q0);
+        const int ngroups = (T + SM_TG - 1) / SM_TG;
+        __syncthreads();
+        // tables of the chunk: warp per source, lane = region index
+        for (int t = warp; t < ngroups * SM_TG; t += SM_WARPS) {
+            int4 sw = make_int4(0, 0, 0, 0);
+            if (t < T) sw = SW[q0 + t];
+            if (lane < SM_LS) {
+                const int k = lane;
+                double vx = 0.0, vy = 0.0, vz = 0.0;
+                if (t < T && k < L) {
+                    const double* w = W + (q0 + t) * 3 * P;
+                    const int kx = k - (sw.x - X0), ky = k - (sw.y - Y0), kz = k - (sw.z - Z0);
+                    if (kx >= 0 && kx < P) vx = __ldg(w + kx);
+                    if (ky >= 0 && ky < P) vy = __ldg(w + P + ky);
+                    if (kz >= 0 && kz < P) vz = __ldg(w + 2 * P + kz);
+                }
+                wx[t][k] = vx;
+                wy[t][k] = vy;
+                wz[t][k] = vz;
+            }
+            if (lane < C) fs[t * C + lane] = t < T ? STR[(q0 + t) * C + lane] : 0.0;
+        }
+        __syncthreads();
+        for (int c = 0; c < C; ++c) {
+            double acc[RBW][3][2];
+#pragma unroll
+            for (int j = 0; j < RBW; ++j)
+#pragma unroll
+                for (int nb = 0; nb < 3; ++nb) acc[j][nb][0] = acc[j][nb][1] = 0.0;
+            for (int grp = 0; grp < ngroups; ++grp) {
+#pragma unroll
+                for (int j = 0; j < RBW; ++j) {
+                    const int rb = warp + j * SM_WARPS;
+                    if (rb < RB) {
+                        const int row = rb * 8 + (lane >> 2);  // A / C row of this lane
+                        const int a = row / L, b = row - a * L;
+#pragma unroll
+                        for (int ks = 0; ks < SM_TG / 4; ++ks) {
+                            const int t = grp * SM_TG + ks * 4 + (lane & 3);
+                            const double af = (fs[t * C + c] * wx[t][a]) * wy[t][b];
+#pragma unroll
+                            for (int nb = 0; nb < 3; ++nb)
+                                dmma(acc[j][nb][0], acc[j][nb][1], af, wz[t][nb * 8 + (lane >> 2)]);
+                        }
+                    }
+                }
+            }
+            // add the region to the grid
+            double* oc = out + (int64_t)c * cs;
+#pragma unroll
+            for (int j = 0; j < RBW; ++j) {
+                const int rb = warp + j * SM_WARPS;
+                if (rb >= RB) continue;
+                const int row = rb * 8 + (lane >> 2);
+                if (row >= ROWS) continue;
+                const int a = row / L, b = row - a * L;
+                int gx = X0 + a, gy = Y0 + b;
+                if (g.d > 0) gx %= g.n[0]; else if (gx >= g.n[0]) continue;
+                if (g.d > 1) gy %= g.n[1]; else if (gy >= g.n[1]) continue;
+                double* col = oc + ((int64_t)gx * g.n[1] + gy) * g.n[2];
+#pragma unroll
+                for (int nb = 0; nb < 3; ++nb)
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+                        const int z = nb * 8 + 2 * (lane & 3) + h;
+                        if (z >= L) continue;
+                        int gz = Z0 + z;
+                        if (g.d > 2) gz %= g.n[2]; else if (gz >= g.n[2]) continue;
+                        const double v = acc[j][nb][h];
+                        if (v != 0.0) atomicAdd(col + gz, v);
+                    }
+            }
+        }
+    }
+}
+
 // Wide windows (20 < P <= 32, e.g. the Gaussian window of c4 at P = 32):
 // B = 8, region L = P + 7 <= 39, z padded to LS = 40 (5 n-blocks). The whole
 // tile's source tables stay in shared memory (up to WT_TMAX sources per pass),
@@ -283,6 +395,10 @@ void launch_spread_mma_bucket(const DevGrid& g, int P, const SpreadMmaShape& s, 
 int launch_spread_mma(const DevGrid& g, int P, const SpreadMmaShape& s, const double* W, const int4* SW,
                       const double* STR, int C, const int64_t* off, double* out, cudaStream_t st) {
     cudaMemsetAsync(out, 0, sizeof(double) * C * (size_t)g.n[0] * g.n[1] * g.n[2], st);
+    static const bool cached = [] {  // SEWALD_SPREAD_CACHED=0: per-group tables (A/B)
+        const char* e = getenv("SEWALD_SPREAD_CACHED");
+        return !(e && e[0] == '0');
+    }();
     for (int64_t a = 0; a < s.ntiles; a += (int64_t)1 << 30) {
         const int64_t n = std::min<int64_t>(s.ntiles - a, (int64_t)1 << 30);
         if (s.L > 23) {
@@ -292,6 +408,11 @@ int launch_spread_mma(const DevGrid& g, int P, const SpreadMmaShape& s, const do
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             kern<<<(unsigned)n, 32 * WT_WARPS, sm, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W, SW, STR, C, off,
                                                         out);
+        } else if (cached && C <= CT_CMAX) {
+            const size_t sm = cached_smem_bytes();
+            auto kern = s.L == 23 ? spread_tile_mma_cached_kernel<23> : spread_tile_mma_cached_kernel<19>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            kern<<<(unsigned)n, SM_THREADS, sm, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W, SW, STR, C, off, out);
         } else if (s.L == 23)
             spread_tile_mma_kernel<23><<<(unsigned)n, SM_THREADS, 0, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W,
                                                                            SW, STR, C, off, out);
