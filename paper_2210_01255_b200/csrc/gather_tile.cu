@@ -154,6 +154,10 @@ gather_tile_kernel(DevGrid g, int P, int B, int L, int ntx, int nty, int ntz, in
 // epilogue. Shared-memory traffic per tile drops ~15x against the per-target
 // tap loop.
 constexpr int MM_TG = 32;            // targets per group (4 n-blocks of 8)
+#ifndef SEWALD_GATHER_TMAX
+#define SEWALD_GATHER_TMAX 64
+#endif
+constexpr int MM_TMAX = SEWALD_GATHER_TMAX;  // targets whose taps are staged per tile chunk
 constexpr int MM_WARPS = 8;
 constexpr int MM_THREADS = 32 * MM_WARPS;
 
@@ -181,17 +185,20 @@ gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
     const int tx = (int)(tile / ((int64_t)ntz * nty));
     const int X0 = tx * B, Y0 = ty * B, Z0 = tz * B;
 
-    double* region = sm;                                   // [MM_RB*8][MM_LS] (rows >= 361 zero)
-    double* wz = region + MM_RB * 8 * MM_LS;               // [MM_TG][MM_LS]   Wz'[t][c]
-    double* wx = wz + MM_TG * MM_LS;                       // [MM_LS][MM_TG]   Wx'[a][t] (a = 19 zero)
-    double* wy = wx + MM_LS * MM_TG;                       // [MM_LS][MM_TG]   Wy'[b][t]
-    double* part = wy + MM_LS * MM_TG;                     // [MM_WARPS][MM_TG]
-    int* rowoff = reinterpret_cast<int*>(part + MM_WARPS * MM_TG);  // [361]
-    int* zoff = rowoff + MM_ROWS;                                  // [19]
-    int* tid = zoff + MM_L;                                        // [MM_TG] target ids
+    // Target taps of up to MM_TMAX targets (MM_TMAX / 32 groups) are staged once
+    // per tile chunk; each component's region is then loaded once and serves
+    // every group of the chunk.
+    double* region = sm;                                   // [MM_RB*8][MM_LS] (rows >= L*L zero)
+    double* wz = region + MM_RB * 8 * MM_LS;               // [MM_TMAX][MM_LS]   Wz'[t][c]
+    double* wx = wz + MM_TMAX * MM_LS;                     // [MM_LS][MM_TMAX]   Wx'[a][t] (a = L zero)
+    double* wy = wx + MM_LS * MM_TMAX;                     // [MM_LS][MM_TMAX]   Wy'[b][t]
+    double* part = wy + MM_LS * MM_TMAX;                   // [MM_WARPS][MM_TMAX]
+    int* rowoff = reinterpret_cast<int*>(part + MM_WARPS * MM_TMAX);  // [L*L]
+    int* zoff = rowoff + MM_ROWS;                                    // [L]
+    int* tid = zoff + MM_L;                                          // [MM_TMAX] target ids
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
-    // zero padding only: column c = 19 of every row and the rows >= 361 (never loaded)
+    // zero padding only: column c = L of every row and the rows >= L*L (never loaded)
     for (int e = threadIdx.x; e < MM_ROWS; e += MM_THREADS) region[e * MM_LS + MM_L] = 0.0;
     for (int e = threadIdx.x; e < (MM_RB * 8 - MM_ROWS) * MM_LS; e += MM_THREADS) region[MM_ROWS * MM_LS + e] = 0.0;
     for (int row = threadIdx.x; row < MM_ROWS; row += MM_THREADS) {
@@ -209,15 +216,14 @@ gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
         zoff[threadIdx.x] = ok ? gz : -1;
     }
     const int64_t cs = (int64_t)g.n[0] * g.n[1] * g.n[2];
-    const int ngroups = (int)((p1 - p0 + MM_TG - 1) / MM_TG);
 
-    for (int grp = 0; grp < ngroups; ++grp) {
-        const int64_t q0 = p0 + (int64_t)grp * MM_TG;
-        const int T = (int)min((int64_t)MM_TG, p1 - q0);
+    for (int64_t q0 = p0; q0 < p1; q0 += MM_TMAX) {
+        const int T = (int)min((int64_t)MM_TMAX, p1 - q0);
+        const int ngroups = (T + MM_TG - 1) / MM_TG;
         __syncthreads();
         // per-target taps placed at the target's offset in the region (warp per
         // target, lane = region index k)
-        for (int t = warp; t < MM_TG; t += MM_WARPS) {
+        for (int t = warp; t < ngroups * MM_TG; t += MM_WARPS) {
             int4 sw = make_int4(0, 0, 0, -1);
             if (t < T) sw = SW[q0 + t];
             if (lane < MM_LS) {
@@ -231,12 +237,11 @@ gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
                     if (kz >= 0 && kz < P) vz = __ldg(wt + 2 * P + kz);
                 }
                 wz[t * MM_LS + k] = vz;
-                wx[k * MM_TG + t] = vx;
-                wy[k * MM_TG + t] = vy;
+                wx[k * MM_TMAX + t] = vx;
+                wy[k * MM_TMAX + t] = vy;
             }
             if (lane == 0) tid[t] = sw.w;
         }
-        const int nblk = (T + 7) / 8;
         for (int c = 0; c < 3; ++c) {
             __syncthreads();
             const double* gc = grid + c * cs;
@@ -257,55 +262,59 @@ gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
             }
             asm volatile("cp.async.wait_all;\n" ::);
             __syncthreads();
-            // B fragments (k-steps x n-blocks): lane holds Wz'[k0 + lane%4][n0 + lane/4]
-            double bf[KS][4];
+            for (int grp = 0; grp < ngroups; ++grp) {
+                const int tg0 = grp * MM_TG;
+                const int nblk = (min(T - tg0, MM_TG) + 7) / 8;
+                // B fragments (k-steps x n-blocks): lane holds Wz'[k0 + lane%4][n0 + lane/4]
+                double bf[KS][4];
 #pragma unroll
-            for (int ks = 0; ks < KS; ++ks)
+                for (int ks = 0; ks < KS; ++ks)
+#pragma unroll
+                    for (int nb = 0; nb < 4; ++nb)
+                        bf[ks][nb] = wz[(tg0 + nb * 8 + (lane >> 2)) * MM_LS + ks * 4 + (lane & 3)];
+                double acc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
+                const int tc = tg0 + 2 * (lane & 3);  // this lane's two target columns within an n-block
+                for (int rb = warp; rb < MM_RB; rb += MM_WARPS) {
+                    const int row_a = rb * 8 + (lane >> 2);  // A-fragment row of this lane
+                    double af[KS];
+#pragma unroll
+                    for (int ks = 0; ks < KS; ++ks) af[ks] = region[row_a * MM_LS + ks * 4 + (lane & 3)];
+                    const int a = row_a / MM_L, b = row_a - a * MM_L;  // C rows = A rows (groupID)
+#pragma unroll
+                    for (int nb = 0; nb < 4; ++nb) {
+                        if (nb < nblk) {
+                            double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                            for (int ks = 0; ks < KS; ++ks) dmma_8x8x4(d0, d1, af[ks], bf[ks][nb]);
+                            const int t = nb * 8 + tc;
+                            const double2 vx = *reinterpret_cast<const double2*>(wx + a * MM_TMAX + t);
+                            const double2 vy = *reinterpret_cast<const double2*>(wy + b * MM_TMAX + t);
+                            acc[nb][0] = fma(d0, vx.x * vy.x, acc[nb][0]);
+                            acc[nb][1] = fma(d1, vx.y * vy.y, acc[nb][1]);
+                        }
+                    }
+                }
+                // reduce over the 8 lanes sharing a column pair (lane % 4)
 #pragma unroll
                 for (int nb = 0; nb < 4; ++nb)
-                    bf[ks][nb] = wz[(nb * 8 + (lane >> 2)) * MM_LS + ks * 4 + (lane & 3)];
-            double acc[4][2] = {{0, 0}, {0, 0}, {0, 0}, {0, 0}};
-            const int tc = 2 * (lane & 3);  // this lane's two target columns within an n-block
-            for (int rb = warp; rb < MM_RB; rb += MM_WARPS) {
-                const int row_a = rb * 8 + (lane >> 2);  // A-fragment row of this lane
-                double af[KS];
 #pragma unroll
-                for (int ks = 0; ks < KS; ++ks) af[ks] = region[row_a * MM_LS + ks * 4 + (lane & 3)];
-                const int a = row_a / MM_L, b = row_a - a * MM_L;  // C rows = A rows (groupID)
+                    for (int h = 0; h < 2; ++h)
 #pragma unroll
-                for (int nb = 0; nb < 4; ++nb) {
-                    if (nb < nblk) {
-                        double d0 = 0.0, d1 = 0.0;
+                        for (int s2 = 4; s2 < 32; s2 <<= 1) acc[nb][h] += __shfl_xor_sync(0xffffffffu, acc[nb][h], s2);
+                if (lane < 4) {
 #pragma unroll
-                        for (int ks = 0; ks < KS; ++ks) dmma_8x8x4(d0, d1, af[ks], bf[ks][nb]);
-                        const int t = nb * 8 + tc;
-                        const double2 vx = *reinterpret_cast<const double2*>(wx + a * MM_TG + t);
-                        const double2 vy = *reinterpret_cast<const double2*>(wy + b * MM_TG + t);
-                        acc[nb][0] = fma(d0, vx.x * vy.x, acc[nb][0]);
-                        acc[nb][1] = fma(d1, vx.y * vy.y, acc[nb][1]);
+                    for (int nb = 0; nb < 4; ++nb) {
+                        part[warp * MM_TMAX + tg0 + nb * 8 + 2 * lane] = acc[nb][0];
+                        part[warp * MM_TMAX + tg0 + nb * 8 + 2 * lane + 1] = acc[nb][1];
                     }
                 }
             }
-            // reduce over the 8 lanes sharing a column pair (lane % 4)
-#pragma unroll
-            for (int nb = 0; nb < 4; ++nb)
-#pragma unroll
-                for (int h = 0; h < 2; ++h)
-#pragma unroll
-                    for (int s = 4; s < 32; s <<= 1) acc[nb][h] += __shfl_xor_sync(0xffffffffu, acc[nb][h], s);
-            if (lane < 4) {
-#pragma unroll
-                for (int nb = 0; nb < 4; ++nb) {
-                    part[warp * MM_TG + nb * 8 + 2 * lane] = acc[nb][0];
-                    part[warp * MM_TG + nb * 8 + 2 * lane + 1] = acc[nb][1];
-                }
-            }
             __syncthreads();
-            if (threadIdx.x < T) {
+            for (int t = threadIdx.x; t < T; t += MM_THREADS) {
                 double v = 0.0;
 #pragma unroll
-                for (int w = 0; w < MM_WARPS; ++w) v += part[w * MM_TG + threadIdx.x];
-                double* dst = u + 3 * (int64_t)tid[threadIdx.x] + c;
+                for (int w = 0; w < MM_WARPS; ++w) v += part[w * MM_TMAX + t];
+                double* dst = u + 3 * (int64_t)tid[t] + c;
                 *dst = accumulate ? *dst + h3 * v : h3 * v;
             }
         }
@@ -314,8 +323,8 @@ gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
 
 size_t mma_smem_bytes(int L) {
     const int LS = (L + 4) & ~3, rows = L * L, rb = (rows + 7) / 8;
-    return sizeof(double) * ((size_t)rb * 8 * LS + MM_TG * LS + 2 * LS * MM_TG + MM_WARPS * MM_TG) +
-           sizeof(int) * (rows + L + MM_TG);
+    return sizeof(double) * ((size_t)rb * 8 * LS + MM_TMAX * LS + 2 * LS * MM_TMAX + MM_WARPS * MM_TMAX) +
+           sizeof(int) * (rows + L + MM_TMAX);
 }
 
 }  // namespace
