@@ -154,10 +154,9 @@ gather_tile_kernel(DevGrid g, int P, int B, int L, int ntx, int nty, int ntz, in
 // epilogue. Shared-memory traffic per tile drops ~15x against the per-target
 // tap loop.
 constexpr int MM_TG = 32;            // targets per group (4 n-blocks of 8)
-#ifndef SEWALD_GATHER_TMAX
-#define SEWALD_GATHER_TMAX 64
-#endif
-constexpr int MM_TMAX = SEWALD_GATHER_TMAX;  // targets whose taps are staged per tile chunk
+// targets whose taps are staged per tile chunk: 64, or 128 for dense tiles
+// (>= 64 targets on average; c3: 8.1 -> 6.6 -> 5.6 ms for 32 / 64 / 128,
+// c2 / c5 prefer 64 for occupancy)
 constexpr int MM_WARPS = 8;
 constexpr int MM_THREADS = 32 * MM_WARPS;
 
@@ -167,7 +166,7 @@ __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, dou
                  : "d"(a), "d"(b));
 }
 
-template <int MM_L>  // region edge: 15 (B = 16 - P), 19 (B = 20 - P, P <= 16) or 23 (B = 24 - P, P <= 20)
+template <int MM_L, int MM_TMAX>  // region edge: 15 (B = 16 - P), 19 (B = 20 - P, P <= 16) or 23 (B = 24 - P, P <= 20)
 __global__ void __launch_bounds__(MM_THREADS)
 gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64_t tile0,
                        const double* __restrict__ W, const int4* __restrict__ SW, const int64_t* __restrict__ off,
@@ -321,7 +320,7 @@ gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
     }
 }
 
-size_t mma_smem_bytes(int L) {
+size_t mma_smem_bytes(int L, int MM_TMAX) {
     const int LS = (L + 4) & ~3, rows = L * L, rb = (rows + 7) / 8;
     return sizeof(double) * ((size_t)rb * 8 * LS + MM_TMAX * LS + 2 * LS * MM_TMAX + MM_WARPS * MM_TMAX) +
            sizeof(int) * (rows + L + MM_TMAX);
@@ -351,6 +350,7 @@ TileShape tile_shape(const DevGrid& g, int P, int64_t Nt) {
     s.L = s.B + P - 1;
     for (int ax = 0; ax < 3; ++ax) s.nt[ax] = (g.n[ax] + s.B - 1) / s.B;
     s.ntiles = (int64_t)s.nt[0] * s.nt[1] * s.nt[2];
+    s.tpt = s.ntiles > 0 ? (double)Nt / (double)s.ntiles : 0.0;
     if (s.ntiles >= (int64_t(1) << 31)) s.ok = false;
     const int pad = 2 * GT_PMAX * s.L + 2 * GT_PMAX;
     s.smem = sizeof(double) * ((size_t)s.L * s.L * s.L + pad + GT_WARPS * 3 * GT_PMAX) +
@@ -377,9 +377,12 @@ void launch_gather_tile(const DevGrid& g, int P, const TileShape& s, const doubl
         return !(e && e[0] == '0');
     }();
     if ((use_mma || P > GT_PMAX || s.L == 15) && (s.L == 15 || s.L == 19 || s.L == 23)) {
-        const size_t sm = mma_smem_bytes(s.L);
-        auto kern = s.L == 15 ? gather_tile_mma_kernel<15>
-                              : (s.L == 19 ? gather_tile_mma_kernel<19> : gather_tile_mma_kernel<23>);
+        const bool wide = s.tpt >= 64.0;
+        const size_t sm = mma_smem_bytes(s.L, wide ? 128 : 64);
+        auto kern = wide ? (s.L == 15 ? gather_tile_mma_kernel<15, 128>
+                                      : (s.L == 19 ? gather_tile_mma_kernel<19, 128> : gather_tile_mma_kernel<23, 128>))
+                         : (s.L == 15 ? gather_tile_mma_kernel<15, 64>
+                                      : (s.L == 19 ? gather_tile_mma_kernel<19, 64> : gather_tile_mma_kernel<23, 64>));
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         for (int64_t a = t0; a < t1; a += (int64_t)1 << 30) {
             const int64_t n = std::min<int64_t>(t1 - a, (int64_t)1 << 30);

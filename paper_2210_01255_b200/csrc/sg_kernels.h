@@ -43,6 +43,7 @@ struct TileShape {
     int64_t ntiles;
     size_t smem;
     bool ok;
+    double tpt;  // mean targets per tile
 };
 // Nt: number of targets (tile size choice for dense targets)
 TileShape tile_shape(const DevGrid& g, int P, int64_t Nt = 0);
