@@ -22,6 +22,7 @@ int main(int argc, char** argv) {
     const int CS = argc > 5 ? atoi(argv[5]) : 32;  // i-cluster size; lanes l and l+CS.. share i
     const int W = argc > 6 ? atoi(argv[6]) : 4;    // blocks pooled by the windowed packer
     const double AX = argc > 7 ? atof(argv[7]) : 1.0;  // cell aspect w_x / w_yz (cell volume kept)
+    const int JB = argc > 8 ? atoi(argv[8]) : 32;      // j-block size (16: lanes l, l+16 share slot j)
     std::mt19937_64 rng(7);
     std::uniform_real_distribution<double> U(0.0, 1.0);
     std::vector<double> x(3 * (size_t)N);
@@ -110,16 +111,16 @@ int main(int argc, char** argv) {
                 int64_t rb = ((int64_t)cz * nc + cy) * ncx;
                 int64_t b0 = off[rb + cxl], b1 = off[rb + cxh + 1];
                 if (b0 < istart) b0 = istart;
-                for (int64_t jb = b0; jb < b1; jb += 32) {
-                    int cnt = (int)std::min<int64_t>(32, b1 - jb);
+                for (int64_t jb = b0; jb < b1; jb += JB) {
+                    int cnt = (int)std::min<int64_t>(JB, b1 - jb);
                     uint32_t m[32], A[32];
                     int degj[32] = {0};
                     int Eb = 0, maxl = 0;
                     for (int l = 0; l < 32; ++l) {
                         m[l] = 0;
                         const int64_t ia = istart + (l % CS);
-                        for (int s = 0; s < CS; ++s) {
-                            int j = (l + s) & 31;
+                        for (int s = 0; s < (JB < CS ? JB : CS); ++s) {
+                            int j = JB == 32 ? ((l + s) & 31) : ((l + s) % JB);
                             if (j >= cnt) continue;
                             int64_t jg = jb + j;
                             if (jg <= ia) continue;
