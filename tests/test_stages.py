@@ -265,3 +265,24 @@ def test_pipeline_uses_caller_table(S, ref):
     assert np.max(np.abs(u2 - u0)) > 1e-10 * np.max(np.abs(u0))  # the table made a difference
     # back to the engine's own table
     _close(S.se_fourier_potential(sysm, tg, p), u0, 1e-14)
+
+
+@pytest.mark.gpu
+def test_stage_empty_and_zero_inputs(S):
+    """Empty source / target sets and all-zero fields through the stage API:
+    exact zeros out, shapes as the reference's."""
+    for name, grid, plan, R in _cases(S):
+        d = grid.d
+        p = _params(S, 0, grid, plan, R)
+        sysm = S.SourceSystem(S.Kernel.stokeslet, S.Cell(tuple(grid.L)), d, np.zeros((0, 3)), np.zeros((0, 3)))
+        phi = S.spread(sysm, p)
+        assert phi.shape == (3,) + tuple(grid.M_ext) and not np.any(phi)
+        F = S.aft_forward(phi, grid, plan)
+        for k in ("far", "near", "zero"):
+            assert not np.any(getattr(F, k))
+        spec = S.ModifiedKernelSpec.optimal(S.Kernel.stokeslet, d, 1.0 if d == 3 else R)
+        Fs = S.scale(F, spec, p.xi, p.window, grid)
+        back = S.aft_inverse(Fs, grid, plan)
+        assert back.shape == (3,) + tuple(grid.M_ext) and not np.any(back)
+        u = S.gather(back, p, S.TargetSet(np.zeros((0, 3)), False))
+        assert u.shape == (0, 3)
