@@ -116,3 +116,25 @@ def test_oracle_reproduces_golden(ref):
     p = ref.RefParams.from_buffer_copy(bytes(g["params"]))
     u = ref.full_potential(p, g["x"], g["f"])
     assert np.array_equal(u, g["u"])
+
+
+def test_dropin_headers_self_contained(tmp_path):
+    """Every drop-in header (include/sewald/*.h, include/sewald_gpu.h) compiles
+    on its own, as the reference's headers do for its users."""
+    import glob
+    import os
+    import shutil
+    import subprocess
+    from conftest import ROOT
+    cxx = shutil.which("g++")
+    if not cxx:
+        pytest.skip("no g++")
+    hdrs = sorted(glob.glob(os.path.join(ROOT, "include", "sewald", "*.h*")))
+    assert hdrs
+    for h in hdrs + [os.path.join(ROOT, "include", "sewald_gpu.h")]:
+        rel = os.path.relpath(h, os.path.join(ROOT, "include"))
+        src = tmp_path / "tu.cpp"
+        src.write_text(f'#include "{rel}"\nint main() {{ return 0; }}\n')
+        r = subprocess.run([cxx, "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra", "-Werror",
+                            "-I", os.path.join(ROOT, "include"), str(src)], capture_output=True, text=True)
+        assert r.returncode == 0, (rel, r.stderr[-2000:])
