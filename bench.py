@@ -9,15 +9,20 @@ scale -> IFFT -> gather, plus the real-space cell-list sum and the self
 term) over the whole synthetic workload. `value` is measured with inputs
 resident in HBM through the device session (sort/bucketing included every
 step, as positions change in time stepping); `e2e` through the public API
-full_potential() with pinned host buffers (H2D of x,f and D2H of u inside
-the timed region). Multi-GPU (torchrun): every rank spreads 1/N of the
-sources, the grid is summed with an NCCL all-reduce, every rank solves the
-k-space part and evaluates 1/N of the targets (strong scaling: the
-workload is fixed as N grows).
+(full_potential on 1 GPU, parallel.full_potential_sharded on N) with pinned
+host buffers (H2D of the inputs and D2H of u inside the timed region).
+`--gpus N` without a torchrun environment re-launches itself under
+torch.distributed.run with N ranks (one per GPU, NCCL). Multi-GPU: every
+rank spreads 1/N of the sources, the grid is summed with an NCCL all-reduce
+(D = 0: slab-distributed solve), every rank evaluates 1/N of the targets
+(strong scaling: the workload is fixed as N grows).
 
-`--impl reference` times the reference's own CPU implementation (oracle/_ref,
-the unmodified reference compiled with shims) on bounded samples of the
-same workload, rank 0 only.
+`--impl reference` runs the reference's own CPU implementation
+(oracle/_ref: the unmodified reference sources compiled with shims) over the
+WHOLE workload once, on rank 0 only: se_fourier_potential single-threaded as
+shipped and realspace_potential on all host threads (its only parallel
+knob, realspace.h:40-41), assembled as realspace.cpp:205-219. That run is
+the measurement (steps = 1, warmup = 0); it imports only oracle/ modules.
 """
 from __future__ import annotations
 
@@ -132,17 +137,66 @@ def select(S, cfg, x, f, nu):
     return sysm, sel
 
 
+KERNEL_NAMES = {0: "stokeslet", 1: "stresslet", 2: "rotlet"}
+WINDOW_NAMES = {0: "kb", 1: "pkb", 2: "tg"}
+
+
+def config_dict(name, N, Nt, kind, d, xi, tol, M_ext, P, window, rc, ws):
+    """The `config` of both arms (identical for the same workload and N)."""
+    par = (f"targets+source-slices x{ws}, NCCL all-reduce of the grid" if d != 0 or ws == 1 else
+           f"targets+source-slices x{ws}, slab FFT (NCCL reduce-scatter, 2 all-to-all, all-gather)")
+    return {"workload": name, "N": int(N), "Nt": int(Nt), "kernel": KERNEL_NAMES[int(kind)], "d": int(d),
+            "xi": float(xi), "tol": float(tol), "M_ext": [int(v) for v in M_ext], "P": int(P),
+            "window": WINDOW_NAMES[int(window)], "rc": float(rc), "parallelism": par,
+            "l2": "GPU arm: flushed between steps (256 MB write inside the timed loop)"}
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def fixture_parity(u, cfg_index):
+    """rel-RMS of u against the reference's own full-size run stored in
+    tests/golden/fullsize_c<k>.npz (sampled targets) and the worst
+    all-target projection deviation (see tests/test_fullsize_parity.py)."""
+    path = os.path.join(ROOT, "tests", "golden", f"fullsize_c{cfg_index}.npz")
+    if not os.path.exists(path):
+        return None
+    g = np.load(path)
+    if int(g["Nt"]) != u.shape[0]:
+        return None
+    idx = g["idx"]
+    ref = g["u"]
+    rel = float(np.sqrt(np.mean(np.sum((u[idx] - ref) ** 2, 1)) / np.mean(np.sum(ref ** 2, 1))))
+    rng = np.random.default_rng(int(g["proj_seed"]))
+    pj = np.array([float(np.sum(rng.standard_normal(u.shape) * u)) for _ in range(len(g["proj_u"]))])
+    pdev = float(np.max(np.abs(pj - g["proj_u"])) / np.sqrt(float(g["ss_u"])))
+    return {"fixture": os.path.relpath(path, ROOT), "rel_rms_sampled": rel, "n_sampled": int(len(idx)),
+            "proj_dev_all_targets": pdev, "bar": 1e-12}
+
+
 # ---------------------------------------------------------------------------
-# CPU reference (oracle/_ref) on bounded samples
+# CPU reference (oracle/_ref)
 # ---------------------------------------------------------------------------
 
-def cpu_reference_sample(cfg, params_c, x, f, nu, xt, n_threads, sample=10000, seed=7, fft_seconds=None):
-    """Time the reference on a bounded sample of the workload and combine the
-    measured per-unit rates into the full-workload time:
-        T = T_fft(full grid) + N * t_spread + Nt * t_gather + Nt * t_realspace
-    t_spread / t_gather / t_realspace are measured on `sample` sources /
-    targets of the SAME workload (all N sources present for real space, so
-    the pair density is the full one). Returns (targets_per_s, detail)."""
+def cpu_reference_sample(cfg, params_c, x, f, nu, xt, n_threads, sample=10000, seed=7):
+    """cpu_baseline of the GPU arm (rank 0, N = 1; ~10-30 s of CPU work): the
+    reference's per-unit costs measured on `sample` sources / targets of the
+    SAME workload and combined into the whole workload's time
+        T = T_fixed + N t_spread + Nt t_gather + Nt t_realspace.
+    T_fixed is one reference flow_field call on a single source (grid zero,
+    FFT, scale, IFFT) plus the real-space cell-list build over all N sources;
+    the per-unit rates have those fixed costs subtracted (a 1-point call of
+    the same stage is timed and removed), so they are not inflated by the
+    sample size. Real space runs for the sampled targets against all N
+    sources on `n_threads` threads. This is a model of the full run, which
+    `bench.py --impl reference` measures directly."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import sewald_ref as R
 
@@ -154,87 +208,83 @@ def cpu_reference_sample(cfg, params_c, x, f, nu, xt, n_threads, sample=10000, s
     Nt = tx.shape[0]
     si = rng.choice(N, size=min(sample, N), replace=False)
     ti = rng.choice(Nt, size=min(sample, Nt), replace=False)
-    detail = {}
-    if fft_seconds is None:
-        t0 = time.perf_counter()
-        R.flow_field(p, x[:1], f[:1], None if nu is None else nu[:1])
-        fft_seconds = time.perf_counter() - t0
-    detail["fft_s"] = fft_seconds
-    t0 = time.perf_counter()
-    R.spread(p, x[si], f[si], None if nu is None else nu[si])
-    t_spread = (time.perf_counter() - t0) / len(si)
+    nus = lambda idx: None if nu is None else nu[idx]
+    clock = time.perf_counter
+    t0 = clock()
+    R.flow_field(p, x[:1], f[:1], nus(slice(0, 1)))
+    t_fft = clock() - t0
+    t0 = clock()
+    R.spread(p, x[:1], f[:1], nus(slice(0, 1)))
+    t_sp1 = clock() - t0
+    t0 = clock()
+    R.spread(p, x[si], f[si], nus(si))
+    t_spread = max(clock() - t0 - t_sp1, 0.0) / len(si)
     field = np.zeros((3, p.M_ext[0], p.M_ext[1], p.M_ext[2]))
-    t0 = time.perf_counter()
+    t0 = clock()
+    R.gather(p, field, tx[:1])
+    t_g1 = clock() - t0
+    t0 = clock()
     R.gather(p, field, tx[ti])
-    t_gather = (time.perf_counter() - t0) / len(ti)
-    # real space for sampled targets against ALL sources; same-point targets
-    # are nudged by 1e-9 so the (skipped) self pair does not hit r = 0.
-    # The fixed cell-list build over all N sources is timed with one target
-    # and removed, so the per-target rate is not inflated by the sample size.
+    t_gather = max(clock() - t0 - t_g1, 0.0) / len(ti)
+    # same-point targets are nudged by 1e-9 so the (skipped) self pair is not r = 0
     tt = tx[ti] + (1e-9 if same else 0.0)
-    t0 = time.perf_counter()
+    t0 = clock()
     R.realspace_potential(int(cfg.kind), cfg.d, cfg.L, x, f, nu, tt[:1], False, float(params_c.xi),
                           float(params_c.rc), False, 1)
-    t_fixed = time.perf_counter() - t0
-    t0 = time.perf_counter()
+    t_cells = clock() - t0
+    t0 = clock()
     R.realspace_potential(int(cfg.kind), cfg.d, cfg.L, x, f, nu, tt, False, float(params_c.xi),
                           float(params_c.rc), False, n_threads)
-    t_rs = max(time.perf_counter() - t0 - t_fixed, 0.0) / len(ti)
-    detail["cell_list_build_s"] = t_fixed
-    total = fft_seconds + t_fixed + N * t_spread + Nt * t_gather + Nt * t_rs
-    detail.update(spread_us_per_source=t_spread * 1e6, gather_us_per_target=t_gather * 1e6,
-                  realspace_us_per_target=t_rs * 1e6, full_workload_s=total,
-                  sample_sources=len(si), sample_targets=len(ti))
+    t_rs = max(clock() - t0 - t_cells, 0.0) / len(ti)
+    total = t_fft + t_cells + N * t_spread + Nt * t_gather + Nt * t_rs
+    detail = dict(fixed_fft_s=t_fft, cell_list_build_s=t_cells, spread_us_per_source=t_spread * 1e6,
+                  gather_us_per_target=t_gather * 1e6, realspace_us_per_target=t_rs * 1e6,
+                  modelled_full_workload_s=total, sample_sources=len(si), sample_targets=len(ti))
     return Nt / total, detail
 
 
-def run_reference(args, cfg):
-    import paper_2210_01255_b200 as S
-    from paper_2210_01255_b200.workloads import generate
-
+def run_reference(args, cfg_index):
+    """The reference arm: the unmodified reference (oracle/_ref) runs the whole
+    workload once on this host. Only oracle/ modules are imported (inputs:
+    oracle/baseline_inputs.py, the same bytes the GPU arm draws; parameters:
+    the reference's own select_parameters)."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import baseline_inputs as BI
     import sewald_ref as R
-    metric = "targets/sec"
     if not R.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libsewald_ref.so not built"}))
         return
-    x, f, nu, xt = generate(cfg)
-    sysm, sel = select(S, cfg, x, f, nu)
-    pc = sel.params.to_c()
+    wall0 = time.perf_counter()
+    cfg = BI.CONFIGS[cfg_index]
+    x, f, nu, xt = BI.generate(cfg_index)
+    same = xt is None
+    Nt = x.shape[0] if same else xt.shape[0]
+    Q = BI.source_quantity(cfg.kind, f, nu)
+    p, _ = R.select_parameters(cfg.kind, cfg.d, cfg.L, Q, cfg.xi, cfg.tol, False, 4, cfg.window, True)
     nthreads = os.cpu_count() or 1
     t0 = time.perf_counter()
-    _, det = cpu_reference_sample(cfg, pc, x, f, nu, xt, nthreads, sample=2000)
-    fft_s = det["fft_s"]
-    for _ in range(max(args.warmup - 1, 0)):
-        cpu_reference_sample(cfg, pc, x, f, nu, xt, nthreads, sample=2000, fft_seconds=fft_s)
-    vals, step_s = [], []
-    for k in range(args.steps):
-        s0 = time.perf_counter()
-        v, det = cpu_reference_sample(cfg, pc, x, f, nu, xt, nthreads, sample=5000, seed=11 + k,
-                                      fft_seconds=fft_s)
-        step_s.append(time.perf_counter() - s0)
-        vals.append(v)
-    value = float(np.median(vals))
-    Nt = cfg.N if cfg.Nt is None else cfg.Nt
+    u, _, _, secs = R.full_parts(p, x, f, nu, xt, same, precompute_0p=True, n_threads=nthreads)
+    run_s = time.perf_counter() - t0
+    value = Nt / run_s
     line = {
-        "impl": "reference", "metric": metric, "value": value, "unit": "targets/s",
-        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * Nt / value, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded uniform, BASELINE configs)",
-        "config": {"workload": cfg.name, "N": cfg.N, "Nt": Nt, "xi": cfg.xi, "tol": cfg.tol,
-                   "M": list(sel.params.grid.M_ext), "P": sel.params.window.P, "rc": sel.params.rc,
-                   "l2": "n/a (CPU)"},
+        "impl": "reference", "metric": "targets/sec", "value": value, "unit": "targets/s",
+        "n_gpus": ws, "steps": 1, "warmup": 0, "requested": {"steps": args.steps, "warmup": args.warmup},
+        "ms_per_step": 1e3 * run_s, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic (seeded uniform positions, N(0,1) strengths; BASELINE config)",
+        "config": config_dict(cfg.name, x.shape[0], Nt, cfg.kind, cfg.d, cfg.xi, cfg.tol, list(p.M_ext), p.P,
+                              p.win_kind, p.rc, ws),
         "cpu_baseline": {"value": value, "unit": "targets/s", "cores": nthreads, "kind": "reference",
-                         "sample": ("reference C++ (oracle/_ref) per-unit rates on 5000 sampled sources/targets "
-                                    "of the full workload (real space against all N sources on all cores; "
-                                    "spread/gather/FFT single-threaded as shipped) combined as "
-                                    "T = T_fft + T_cells + N t_spread + Nt t_gather + Nt t_realspace"),
-                         "detail": det},
+                         "cpu_model": cpu_model(),
+                         "sample": ("the whole workload, measured once: reference C++ (oracle/_ref) "
+                                    "se_fourier_potential single-threaded as shipped + realspace_potential on "
+                                    f"{nthreads} threads + self/zero-mode/gauge terms (realspace.cpp:205-219)"),
+                         "stage_s": secs},
         "e2e": {"value": value, "unit": "targets/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "wall_s": time.perf_counter() - t0,
+        "parity_vs_fixture": fixture_parity(u, cfg_index),
+        "wall_s": time.perf_counter() - wall0,
     }
     print(json.dumps(line))
 
@@ -325,6 +375,7 @@ def run_ours(args, cfg):
     ms_per_step = float(t.item()) / args.steps
     value = Nt / (ms_per_step * 1e-3)
     pairs = sess.pair_count(reset=True) / max(args.steps, 1)
+    u_step = u.cpu().numpy() if rank == 0 else None  # the last timed step's velocity (all targets)
 
     # per-stage device times (one instrumented step on the same stream)
     stages = {}
@@ -381,7 +432,7 @@ def run_ours(args, cfg):
         except Exception:
             pass
         hbm_peak = mp.get("hbm_gbs", 6650.0)
-        fl = FLOPS_PER_PAIR[(int(cfg.kind), bool(same and os.environ.get("SEWALD_RS_SYM", "1") != "0"))]
+        fl = FLOPS_PER_PAIR[(int(cfg.kind), bool(same and S.get_kernel_option(S.KernelOption.RS_SYM) != 0))]
         achieved = rs_pairs * fl / (rs_ms * 1e-3) / 1e12
         C = 9 if cfg.kind == S.Kernel.stresslet else 3
         vol = int(np.prod(params.grid.M_ext))
@@ -392,12 +443,8 @@ def run_ours(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded uniform positions, N(0,1) strengths; BASELINE config)",
-            "config": {"workload": cfg.name, "N": N, "Nt": Nt, "kernel": cfg.kind.name, "d": cfg.d,
-                       "xi": cfg.xi, "tol": cfg.tol, "M_ext": list(params.grid.M_ext),
-                       "P": params.window.P, "window": params.window.kind.name, "rc": params.rc,
-                       "parallelism": (f"targets+source-slices x{ws} (NCCL all-reduce of the grid)" if cfg.d != 0 or ws == 1 else
-                                       f"targets+source-slices x{ws}, slab FFT (NCCL reduce-scatter, 2 all-to-all, all-gather)"),
-                       "l2": "flushed between steps (256 MB write inside the timed loop)"},
+            "config": config_dict(cfg.name, N, Nt, cfg.kind, cfg.d, cfg.xi, cfg.tol, params.grid.M_ext,
+                                  params.window.P, params.window.kind, params.rc, ws),
             "roofline": {"kernel": "realspace", "bound": "fp64", "achieved": achieved, "peak": peak64,
                          "unit": "TFLOP/s", "frac": achieved / peak64,
                          "peak_source": "measured DFMA microbenchmark (sewald_gpu_fp64_peak)",
@@ -417,34 +464,58 @@ def run_ours(args, cfg):
             "clocks": clocks,
         }
 
-    # end-to-end through the public API with pinned host buffers (N=1 only)
-    if ws == 1 and not args.no_e2e and rank == 0:
+    # parity of the device-resident result against the reference's own run
+    if rank == 0 and line is not None:
+        torch.cuda.synchronize()
+        line["parity_vs_fixture"] = fixture_parity(u_step, cfg.index)
+
+    # end-to-end through the public API with pinned host buffers: full_potential
+    # on 1 GPU, parallel.full_potential_sharded on N (max over ranks)
+    if not args.no_e2e:
+        from paper_2210_01255_b200.parallel import full_potential_sharded
         pin = lambda a: torch.from_numpy(a).pin_memory().numpy() if a is not None else None
         px, pf, pnu = pin(x), pin(f), pin(nu)
         pxt = pin(xt)
         psys = S.SourceSystem(cfg.kind, S.Cell(cfg.L), cfg.d, px, pf, pnu)
         ptg = S.TargetSet.from_sources(psys) if same else S.TargetSet(pxt, False)
-        eng2 = S.default_engine(local)
         pout = torch.empty((Nt, 3), dtype=torch.float64).pin_memory().numpy()
-        S.full_potential(psys, ptg, params, engine=eng2, out=pout)  # warm (plans, buffers)
+        if ws == 1:
+            eng2 = S.default_engine(local)
+            call = lambda: S.full_potential(psys, ptg, params, engine=eng2, out=pout)
+            api = "paper_2210_01255_b200.full_potential (pinned host numpy in/out)"
+        else:
+            call = lambda: full_potential_sharded(psys, ptg, params, rank, ws, dist=dist, engine=engine, out=pout)
+            api = "paper_2210_01255_b200.parallel.full_potential_sharded (pinned host numpy in, rank 0 out)"
+        call()  # warm (plans, buffers)
         ts = []
         for _ in range(max(1, min(args.steps, 5))):
+            barrier()
             t0 = time.perf_counter()
-            uo = S.full_potential(psys, ptg, params, engine=eng2, out=pout)
-            ts.append(time.perf_counter() - t0)
+            uo = call()
+            torch.cuda.synchronize()
+            dt = torch.tensor([time.perf_counter() - t0], dtype=torch.float64, device=dev)
+            if ws > 1:
+                dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            ts.append(float(dt.item()))
         e2e_s = float(np.median(ts))
         h2d = x.nbytes + f.nbytes + (nu.nbytes if nu is not None else 0) + (xt.nbytes if xt is not None else 0)
-        line["e2e"] = {"value": Nt / e2e_s, "unit": "targets/s", "h2d_bytes_per_step": int(h2d),
-                       "d2h_bytes_per_step": int(uo.nbytes), "ms_per_call": e2e_s * 1e3,
-                       "api": "paper_2210_01255_b200.full_potential (pinned host numpy in/out)"}
+        if rank == 0:
+            line["e2e"] = {"value": Nt / e2e_s, "unit": "targets/s", "h2d_bytes_per_step": int(h2d) * ws,
+                           "d2h_bytes_per_step": int(pout.nbytes), "ms_per_call": e2e_s * 1e3,
+                           "api": api, "timing": "host wall clock per call, max over ranks, median of calls"}
+            par = fixture_parity(uo, cfg.index)
+            if par is not None:
+                line["e2e"]["parity_vs_fixture"] = par
 
     if ws == 1 and rank == 0 and not args.no_cpu_baseline:
         try:
             v, det = cpu_reference_sample(cfg, params.to_c(), x, f, nu, xt, os.cpu_count() or 1, sample=10000)
             line["cpu_baseline"] = {
                 "value": v, "unit": "targets/s", "cores": os.cpu_count() or 1, "kind": "reference",
-                "sample": ("reference C++ (oracle/_ref) on 10000 sampled sources/targets of this workload; "
-                           "T = T_fft + T_cells + N t_spread + Nt t_gather + Nt t_realspace (real space on all cores)"),
+                "cpu_model": cpu_model(), "modelled": True,
+                "sample": ("reference C++ (oracle/_ref) per-unit costs on 10000 sampled sources/targets of this "
+                           "workload, fixed costs removed; T = T_fixed + N t_spread + Nt t_gather + Nt t_realspace "
+                           "(real space on all cores). bench.py --impl reference measures the whole run."),
                 "detail": det}
         except Exception as e:  # pragma: no cover
             line["cpu_baseline"] = {"value": None, "unit": "targets/s", "cores": 0, "kind": "reference",
@@ -456,14 +527,30 @@ def run_ours(args, cfg):
         dist.destroy_process_group()
 
 
+def relaunch_distributed(n: int) -> int:
+    """`--gpus N` outside torchrun: run this script under torch.distributed.run
+    with N ranks on this node (rendezvous on 127.0.0.1)."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
-    from paper_2210_01255_b200.workloads import CONFIGS
-    cfg = CONFIGS[args.config]
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_distributed(args.gpus))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus and int(os.environ.get("RANK", "0")) == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; using {ws} ranks", file=sys.stderr)
     if args.impl == "reference":
-        run_reference(args, cfg)
+        run_reference(args, args.config)
     else:
-        run_ours(args, cfg)
+        from paper_2210_01255_b200.workloads import CONFIGS
+        run_ours(args, CONFIGS[args.config])
 
 
 if __name__ == "__main__":

@@ -136,6 +136,26 @@ int64_t sewald_gpu_launch_count(const sewald_gpu_ctx* ctx);
  * microbenchmark; roofline denominator for the fp64-bound kernels). */
 int sewald_gpu_fp64_peak(sewald_gpu_ctx* ctx, double* tflops);
 
+/* ---- kernel-choice switches (process-wide; diagnostics and tests) ------
+ * Defaults are the measured best and come from the SEWALD_* environment
+ * variables DESIGN.md §6b lists; setting one makes later calls on every
+ * context use it (sessions rebuild their orderings). Not part of the
+ * reference API: the reference has one CPU code path per stage. */
+enum {
+    SEWALD_OPT_RS_SYM = 0,        /* real space, targets == sources: 0 never pair-symmetric,
+                                     1 auto (large target sets), 2 always */
+    SEWALD_OPT_GATHER = 1,        /* -1 auto, 0 warp per target, 1 z-sweep, 2 tiles */
+    SEWALD_OPT_GATHER_MMA = 2,    /* tiled gather: 1 tensor-core form (P <= 16), 0 CUDA-core form */
+    SEWALD_OPT_GATHER_L = 3,      /* tiled gather region edge: 0 auto, 15 or 19 */
+    SEWALD_OPT_SPREAD_SWEEP = 4,  /* -1 auto (P <= 24), 0 off, 1 on */
+    SEWALD_OPT_SPREAD_MMA = 5,    /* 1 tensor-core spread for 15 <= P <= 32, 0 off */
+    SEWALD_OPT_SPREAD_MMA_L = 6,  /* tensor-core spread region edge for P <= 20: 23 or 19 */
+    SEWALD_OPT_SPREAD_CACHED = 7, /* tensor-core spread: 1 staged tables per chunk, 0 per group */
+    SEWALD_OPT_COUNT = 8
+};
+int sewald_gpu_set_option(int which, int value);
+int sewald_gpu_get_option(int which, int* value);
+
 /* ---- host-buffer entry points (drop-in path) ------------------------- */
 /* x, f: N*3 doubles; nu: N*3 (stresslet) or NULL; xt: Nt*3. When
  * same_as_sources != 0 the targets are the sources (xt may be NULL or x).

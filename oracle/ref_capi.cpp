@@ -353,9 +353,9 @@ int ref_full_potential(const sewald_params_c* p, const double* x, const double* 
 // real-space sum on n_threads workers (the reference's only parallel knob,
 // realspace.h:40-41). Used as the CPU baseline; stage wall times are kept
 // for ref_last_seconds.
-int ref_full_split(const sewald_params_c* p, const double* x, const double* f, const double* nu,
+int ref_full_parts(const sewald_params_c* p, const double* x, const double* f, const double* nu,
                    int64_t N, const double* xt, int64_t Nt, int same, int precompute_0p,
-                   int n_threads, double* u_out) {
+                   int n_threads, double* u_out, double* uf_out, double* ur_out) {
     return guarded([&] {
         using clk = std::chrono::steady_clock;
         EwaldParams e = from_c(p);
@@ -368,6 +368,8 @@ int ref_full_split(const sewald_params_c* p, const double* x, const double* f, c
         auto t1 = clk::now();
         const std::vector<Vec3> far = se_fourier_potential(s, t, e, opt);
         auto t2 = clk::now();
+        if (ur_out) out3(u, ur_out);
+        if (uf_out) out3(far, uf_out);
         for (std::size_t i = 0; i < u.size(); ++i) u[i] += far[i];
         if (t.same_as_sources)
             for (std::size_t i = 0; i < u.size(); ++i) u[i] += self_term(s.kind, e.xi, s.f[i]);
@@ -382,6 +384,14 @@ int ref_full_split(const sewald_params_c* p, const double* x, const double* f, c
         g_last_seconds[3] = std::chrono::duration<double>(t3 - t0).count();
         out3(u, u_out);
     });
+}
+
+// full_potential assembled as realspace.cpp:205-219 (u only).
+int ref_full_split(const sewald_params_c* p, const double* x, const double* f, const double* nu,
+                   int64_t N, const double* xt, int64_t Nt, int same, int precompute_0p,
+                   int n_threads, double* u_out) {
+    return ref_full_parts(p, x, f, nu, N, xt, Nt, same, precompute_0p, n_threads, u_out, nullptr,
+                          nullptr);
 }
 
 // precompute_0p (fourier.cpp:722-803): table of (2 M_ext)^3 complex values,

@@ -85,6 +85,7 @@ _SIGS = {
                                           C.c_double, C.c_double, C.c_int, C.c_int, DP]),
     "ref_full_potential": (C.c_int, [PP, DP, DP, DP, I64, DP, I64, C.c_int, C.c_int, DP]),
     "ref_full_split": (C.c_int, [PP, DP, DP, DP, I64, DP, I64, C.c_int, C.c_int, C.c_int, DP]),
+    "ref_full_parts": (C.c_int, [PP, DP, DP, DP, I64, DP, I64, C.c_int, C.c_int, C.c_int, DP, DP, DP]),
     "ref_precompute_0p": (C.c_int, [PP, DP, C.POINTER(C.c_int32)]),
     "ref_aft_forward": (C.c_int, [PP, DP, C.c_int, GP]),
     "ref_field_get": (C.c_int, [GP, IP32, DP, DP, DP]),
@@ -272,6 +273,22 @@ def full_split(p: RefParams, x, f, nu=None, xt=None, same=True, precompute_0p=Tr
     secs = np.zeros(4)
     lib().ref_last_seconds(_dp(secs))
     return out, dict(fourier=secs[0], realspace=secs[1], terms=secs[2], total=secs[3])
+
+
+def full_parts(p: RefParams, x, f, nu=None, xt=None, same=True, precompute_0p=True, n_threads=1):
+    """As full_split, also returning the two sums it adds: (u, u_F, u_R, seconds)
+    with u_F = se_fourier_potential (fourier.cpp:805-852) and u_R =
+    realspace_potential (realspace.cpp:166-203), starred when same."""
+    x, f, nu = _v3(x), _v3(f), _v3(nu)
+    xt, nt = _targets(x, xt, same)
+    out = np.zeros((nt, 3))
+    uf = np.zeros((nt, 3))
+    ur = np.zeros((nt, 3))
+    _chk(lib().ref_full_parts(C.byref(p), _dp(x), _dp(f), _dp(nu), x.shape[0], _dp(xt), nt, int(same),
+                              int(precompute_0p), int(n_threads), _dp(out), _dp(uf), _dp(ur)))
+    secs = np.zeros(4)
+    lib().ref_last_seconds(_dp(secs))
+    return out, uf, ur, dict(fourier=secs[0], realspace=secs[1], terms=secs[2], total=secs[3])
 
 
 def precompute_0p(p: RefParams) -> np.ndarray:

@@ -12,6 +12,7 @@ from .api import (Cell, DeviceError, DomainError, Engine, EstimateReport, EwaldP
                   gather, pkb_coefficients, realspace_potential, se_fourier_potential,
                   select_parameters, source_quantity, spread, strength_components, window_eval,
                   window_hat, ModifiedKernelSpec, FourierField, PrecomputedKernel0P, aft_forward,
-                  aft_inverse, scale, precompute_0p)
+                  aft_inverse, scale, precompute_0p, KernelOption, get_kernel_option,
+                  set_kernel_option, kernel_options)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

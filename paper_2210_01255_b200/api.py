@@ -16,6 +16,7 @@ Exceptions: InvalidArgument (std::invalid_argument), DomainError
 """
 from __future__ import annotations
 
+import contextlib
 import ctypes as C
 import enum
 import threading
@@ -290,6 +291,43 @@ def source_quantity(system: SourceSystem) -> float:
 # ---------------------------------------------------------------------------
 # device engine
 # ---------------------------------------------------------------------------
+
+
+class KernelOption(enum.IntEnum):
+    """Kernel-choice switches (include/sewald_gpu.h SEWALD_OPT_*): defaults
+    are the measured best; tests set them to pin every kernel family."""
+    RS_SYM = 0          # 0 never pair-symmetric, 1 auto, 2 always (targets == sources)
+    GATHER = 1          # -1 auto, 0 warp per target, 1 z-sweep, 2 tiles
+    GATHER_MMA = 2      # tiled gather: 1 tensor-core form, 0 CUDA-core form
+    GATHER_L = 3        # tiled gather region edge: 0 auto, 15, 19
+    SPREAD_SWEEP = 4    # -1 auto, 0 off, 1 on
+    SPREAD_MMA = 5      # 1 tensor-core spread (15 <= P <= 32), 0 off
+    SPREAD_MMA_L = 6    # 23 or 19
+    SPREAD_CACHED = 7   # 1 staged tables per chunk, 0 per group
+
+
+def get_kernel_option(which: KernelOption) -> int:
+    v = C.c_int()
+    _abi.raise_for(_abi.load().sewald_gpu_get_option(int(which), C.byref(v)), f"unknown option {which}")
+    return v.value
+
+
+def set_kernel_option(which: KernelOption, value: int) -> None:
+    code = _abi.load().sewald_gpu_set_option(int(which), int(value))
+    _abi.raise_for(code, f"bad value {value} for option {KernelOption(which).name}")
+
+
+@contextlib.contextmanager
+def kernel_options(**kw):
+    """with kernel_options(RS_SYM=2, GATHER=1): ... — set, then restore."""
+    old = {k: get_kernel_option(KernelOption[k]) for k in kw}
+    try:
+        for k, v in kw.items():
+            set_kernel_option(KernelOption[k], v)
+        yield
+    finally:
+        for k, v in old.items():
+            set_kernel_option(KernelOption[k], v)
 
 
 class Engine:
@@ -679,6 +717,10 @@ class Session:
         self.engine.check(self._lib.sewald_gpu_session_create(self.engine.ctx, C.byref(c), C.byref(h)))
         self.s = h
         self._keep = []
+        self._C = strength_components(Kernel(int(c.kind)))
+        self._N = 0
+        self._Nt = 0
+        self._same = True
 
     def close(self):
         if getattr(self, "s", None):
@@ -695,39 +737,76 @@ class Session:
         import torch
         self.engine.set_stream(torch.cuda.current_stream().cuda_stream)
 
-    @staticmethod
-    def _ptr(t):
+    def _ptr(self, t, name: str, doubles: Optional[int] = None, optional: bool = False):
+        """Device pointer of a float64 (or complex128) CUDA tensor on this
+        session's device holding exactly `doubles` doubles. The C-ABI reads
+        and writes these buffers as double, so any other dtype, device, layout
+        or size is refused here (InvalidArgument) instead of being
+        reinterpreted or overrun on the device."""
+        import torch
         if t is None:
-            return None
-        assert t.is_cuda and t.dtype.is_floating_point and t.is_contiguous()
+            if optional:
+                return None
+            raise _abi.InvalidArgument(f"{name}: a tensor is required")
+        if not isinstance(t, torch.Tensor):
+            raise _abi.InvalidArgument(f"{name}: expected a torch CUDA tensor, got {type(t).__name__}")
+        if t.dtype not in (torch.float64, torch.complex128):
+            raise _abi.InvalidArgument(f"{name}: dtype must be torch.float64 (got {t.dtype})")
+        if not t.is_cuda or (t.device.index if t.device.index is not None else 0) != self.engine.device:
+            raise _abi.InvalidArgument(f"{name}: must live on cuda:{self.engine.device} (got {t.device})")
+        if not t.is_contiguous():
+            raise _abi.InvalidArgument(f"{name}: must be contiguous")
+        n = t.numel() * (2 if t.dtype == torch.complex128 else 1)
+        if doubles is not None and n != doubles:
+            raise _abi.InvalidArgument(f"{name}: expected {doubles} doubles, got {n}")
         return C.c_void_p(t.data_ptr())
+
+    @staticmethod
+    def _rows(t, name: str) -> int:
+        if t is None or t.dim() != 2 or t.shape[1] != 3:
+            raise _abi.InvalidArgument(f"{name}: expected an (n, 3) tensor")
+        return int(t.shape[0])
 
     def set_sources(self, x, f, nu=None):
         self._sync_stream()
+        n = self._rows(x, "x")
+        px = self._ptr(x, "x", 3 * n)
+        pf = self._ptr(f, "f", 3 * n)
+        pn = self._ptr(nu, "nu", 3 * n, optional=True)
         self._keep = [x, f, nu]
-        self.engine.check(self._lib.sewald_gpu_session_set_sources(
-            self.s, self._ptr(x), self._ptr(f), self._ptr(nu), int(x.shape[0])))
+        self.engine.check(self._lib.sewald_gpu_session_set_sources(self.s, px, pf, pn, n))
+        self._N = n
+        if self._same:
+            self._Nt = n
 
     def set_targets(self, xt=None, same_as_sources: bool = True):
         self._sync_stream()
-        n = 0 if xt is None else int(xt.shape[0])
-        self.engine.check(self._lib.sewald_gpu_session_set_targets(self.s, self._ptr(xt), n, int(same_as_sources)))
+        n = 0 if xt is None else self._rows(xt, "xt")
+        p = None if xt is None else self._ptr(xt, "xt", 3 * n)
+        self.engine.check(self._lib.sewald_gpu_session_set_targets(self.s, p, n, int(same_as_sources)))
+        self._same = bool(same_as_sources)
+        self._Nt = self._N if same_as_sources else n
 
     def grid_size(self) -> int:
         return int(self._lib.sewald_gpu_session_grid_size(self.s))
 
+    def _flow_size(self) -> int:
+        return 3 * self.grid_size() // self._C
+
     def spread(self, i0: int, i1: int, grid=None):
         self._sync_stream()
-        self.engine.check(self._lib.sewald_gpu_session_spread(self.s, int(i0), int(i1), self._ptr(grid)))
+        g = self._ptr(grid, "grid", self.grid_size(), optional=True)
+        self.engine.check(self._lib.sewald_gpu_session_spread(self.s, int(i0), int(i1), g))
 
     def solve(self, grid=None, precompute_0p: bool = True):
         self._sync_stream()
-        self.engine.check(self._lib.sewald_gpu_session_solve(self.s, self._ptr(grid), int(precompute_0p)))
+        g = self._ptr(grid, "grid", self.grid_size(), optional=True)
+        self.engine.check(self._lib.sewald_gpu_session_solve(self.s, g, int(precompute_0p)))
 
     def evaluate(self, u, part: int = 0, nparts: int = 1, parts: int = 7):
         self._sync_stream()
-        self.engine.check(self._lib.sewald_gpu_session_evaluate(self.s, int(part), int(nparts), int(parts),
-                                                                self._ptr(u)))
+        pu = self._ptr(u, "u", 3 * self._Nt)
+        self.engine.check(self._lib.sewald_gpu_session_evaluate(self.s, int(part), int(nparts), int(parts), pu))
 
     # ---- slab-distributed D = 0 solve (parallel.d0_sharded_solve) ----------
     def d0_geometry(self, precompute_0p: bool = True) -> dict:
@@ -747,31 +826,42 @@ class Session:
 
     def d0_forward(self, grid_slab, xa: int, xb: int, kz_bounds, send, precompute_0p: bool = True):
         self._sync_stream()
+        g = self.d0_geometry(precompute_0p)
+        m, cc, h2 = g["m"], g["C"], g["h2"]
         w, arr = self._bounds(kz_bounds)
-        self.engine.check(self._lib.sewald_gpu_session_d0_forward(
-            self.s, int(precompute_0p), self._ptr(grid_slab), int(xa), int(xb), w, arr, C.c_void_p(send.data_ptr())))
+        pg = self._ptr(grid_slab, "grid_slab", cc * (xb - xa) * m[1] * m[2])
+        ps = self._ptr(send, "send", 2 * cc * (xb - xa) * m[1] * h2)
+        self.engine.check(self._lib.sewald_gpu_session_d0_forward(self.s, int(precompute_0p), pg, int(xa), int(xb),
+                                                                  w, arr, ps))
 
     def d0_middle(self, recv, x_bounds, ka: int, kb: int, send, precompute_0p: bool = True):
         self._sync_stream()
+        g = self.d0_geometry(precompute_0p)
+        m, cc = g["m"], g["C"]
         w, arr = self._bounds(x_bounds)
-        self.engine.check(self._lib.sewald_gpu_session_d0_middle(
-            self.s, int(precompute_0p), C.c_void_p(recv.data_ptr()), w, arr, int(ka), int(kb),
-            C.c_void_p(send.data_ptr())))
+        pr = self._ptr(recv, "recv", 2 * cc * m[0] * m[1] * (kb - ka))
+        ps = self._ptr(send, "send", 2 * 3 * (kb - ka) * m[0] * m[1])
+        self.engine.check(self._lib.sewald_gpu_session_d0_middle(self.s, int(precompute_0p), pr, w, arr, int(ka),
+                                                                 int(kb), ps))
 
     def d0_inverse(self, recv, xa: int, xb: int, kz_bounds, flow_slab, precompute_0p: bool = True):
         self._sync_stream()
+        g = self.d0_geometry(precompute_0p)
+        m, h2 = g["m"], g["h2"]
         w, arr = self._bounds(kz_bounds)
-        self.engine.check(self._lib.sewald_gpu_session_d0_inverse(
-            self.s, int(precompute_0p), C.c_void_p(recv.data_ptr()), int(xa), int(xb), w, arr,
-            self._ptr(flow_slab)))
+        pr = self._ptr(recv, "recv", 2 * 3 * h2 * (xb - xa) * m[1])
+        pf = self._ptr(flow_slab, "flow_slab", 3 * (xb - xa) * m[1] * m[2])
+        self.engine.check(self._lib.sewald_gpu_session_d0_inverse(self.s, int(precompute_0p), pr, int(xa), int(xb),
+                                                                  w, arr, pf))
 
     def set_flow(self, flow):
         self._sync_stream()
-        self.engine.check(self._lib.sewald_gpu_session_set_flow(self.s, self._ptr(flow)))
+        self.engine.check(self._lib.sewald_gpu_session_set_flow(self.s, self._ptr(flow, "flow", self._flow_size())))
 
     def pair_count(self, reset: bool = False) -> int:
         return int(self._lib.sewald_gpu_session_pair_count(self.s, int(reset)))
 
     def run(self, u, precompute_0p: bool = True):
         self._sync_stream()
-        self.engine.check(self._lib.sewald_gpu_session_run(self.s, int(precompute_0p), self._ptr(u)))
+        pu = self._ptr(u, "u", 3 * self._Nt)
+        self.engine.check(self._lib.sewald_gpu_session_run(self.s, int(precompute_0p), pu))

@@ -11,6 +11,7 @@
 #include "engine.h"
 #include "host_params.h"
 #include "aft_d0.h"
+#include "options.h"
 
 #include <cub/cub.cuh>
 
@@ -243,10 +244,7 @@ void build_cell_grid(sewald_gpu_session* s) {
         const char* e = getenv("SEWALD_RS_PPC");
         return e ? atof(e) : 0.0;
     }();
-    static const bool sym_on = [] {
-        const char* e = getenv("SEWALD_RS_SYM");
-        return !(e && e[0] == '0');
-    }();
+    const bool sym_on = option(SEWALD_OPT_RS_SYM) != 0;
     // pair-symmetric kernel (targets == sources): 28; separate targets: 40 (c4: 47.6 vs 49.3 ms)
     const double ppc = ppc_env > 0.0 ? ppc_env : (s->same && sym_on ? 28.0 : 40.0);
     double target_w;
@@ -300,7 +298,19 @@ void ensure_sums(sewald_gpu_session* s) {
     s->sums_ready = true;
 }
 
+// Orderings built under other kernel-choice switches are dropped (options.h).
+void sync_options(sewald_gpu_session* s) {
+    const int e = options_epoch();
+    if (s->opt_epoch == e) return;
+    s->opt_epoch = e;
+    s->sp_i0 = s->sp_i1 = -1;
+    s->cells_ready = false;
+    s->tg_ready = false;
+    s->tg_wpart = -1;
+}
+
 void ensure_spread_order(sewald_gpu_session* s, int64_t i0, int64_t i1) {
+    sync_options(s);
     if (s->sp_i0 == i0 && s->sp_i1 == i1) return;
     const int64_t n = i1 - i0;
     cudaStream_t st = s->ctx->stream;
@@ -308,16 +318,10 @@ void ensure_spread_order(sewald_gpu_session* s, int64_t i0, int64_t i1) {
     s->sweep = sweep_shape(s->g, s->p.P);
     // z-sweep for P <= 24 (c1-c3, c5); the 8x8x16 tile kernel wins for the
     // widest windows (c4, P = 32: 25 ms vs 42 ms). SEWALD_SPREAD_SWEEP=0/1 forces.
-    static const int sweep_mode = [] {
-        const char* e = getenv("SEWALD_SPREAD_SWEEP");
-        return e && e[0] ? (e[0] == '0' ? 0 : 1) : -1;
-    }();
+    const int sweep_mode = option(SEWALD_OPT_SPREAD_SWEEP);
     if (sweep_mode == 0 || (sweep_mode < 0 && s->p.P > 24)) s->sweep.ok = false;
     // tensor-core tiles for P <= 16 (SEWALD_SPREAD_MMA=0 disables)
-    static const bool mma_enabled = [] {
-        const char* e = getenv("SEWALD_SPREAD_MMA");
-        return !(e && e[0] == '0');
-    }();
+    const bool mma_enabled = option(SEWALD_OPT_SPREAD_MMA) != 0;
     s->sm_shape = spread_mma_shape(s->g, s->p.P);
     s->sp_mode = (mma_enabled && s->sm_shape.ok) ? 2 : (s->sweep.ok ? 1 : 0);
     const int64_t nb = s->sp_mode == 2 ? s->sm_shape.ntiles
@@ -352,6 +356,7 @@ void ensure_spread_order(sewald_gpu_session* s, int64_t i0, int64_t i1) {
 }
 
 void ensure_cells(sewald_gpu_session* s) {
+    sync_options(s);
     if (s->cells_ready) return;
     cudaStream_t st = s->ctx->stream;
     build_cell_grid(s);
@@ -433,14 +438,8 @@ void ensure_gather_weights(sewald_gpu_session* s, int mode, int part, int nparts
 }
 
 int ensure_gather_order(sewald_gpu_session* s, int part, int nparts) {
-    static const int forced = [] {
-        const char* e = getenv("SEWALD_GATHER");
-        if (!e) return -1;
-        if (!strcmp(e, "warp")) return 0;
-        if (!strcmp(e, "sweep")) return 1;
-        if (!strcmp(e, "tile")) return 2;
-        return -1;
-    }();
+    sync_options(s);
+    const int forced = option(SEWALD_OPT_GATHER);
     const SweepShape sh = sweep_shape(s->g, s->p.P);
     const TileShape ts = tile_shape(s->g, s->p.P, s->Nt);
     int mode = forced >= 0 ? forced : (s->p.P > 20 ? 1 : 2);
@@ -720,16 +719,19 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
     const int64_t t0 = std::min<int64_t>(32 * c0, Nt), t1 = std::min<int64_t>(32 * c1, Nt);
     if (t1 <= t0) return;
     const uint32_t* torder = target_order(s);
-    static const bool sym_enabled = [] {
-        const char* e = getenv("SEWALD_RS_SYM");
-        return !(e && e[0] == '0');
-    }();
+    // SEWALD_RS_SYM: 0 = never the pair-symmetric kernel, "force" = always
+    // when targets are the sources (tests pin it at small N), else automatic.
+    const int sym_mode = option(SEWALD_OPT_RS_SYM);
     // Small target sets (fewer 32-target groups than resident warps) take the
     // non-symmetric kernel with each group's rows split over several warps and
     // a fixed-order combination: the whole GPU works on them and the result is
     // independent of scheduling (no reactions, no atomics).
-    const int rs_split = realspace_split(t1 - t0);
-    const bool use_sym = (parts & 2) && s->same && sym_enabled && rs_split == 1;
+    // The choice is made once for the whole partition (from the smallest part,
+    // ncl / nparts clusters), so every part and rank runs the same kernel: the
+    // symmetric kernel's half rule assigns each pair to the part holding its
+    // lower index, which is only complete when all parts use it.
+    const int rs_split = realspace_split(32 * std::max<int64_t>(1, ncl / nparts));
+    const bool use_sym = (parts & 2) && s->same && sym_mode != 0 && (rs_split == 1 || sym_mode == 2);
     // The pair-symmetric real-space sum adds reactions to any particle, and
     // multi-part evaluation is combined by summing the per-part outputs: in
     // both cases the whole output is zeroed here and every stage accumulates.
@@ -1048,19 +1050,36 @@ int sewald_gpu_gather(sewald_gpu_ctx* ctx, const sewald_params_c* p, const doubl
                       const double* xt, int64_t Nt, double* u_out) {
     if (!ctx) return SEWALD_EINVAL;
     return ctx_guard(ctx, [&] {
+        // The stage function runs the same gather kernel the pipeline picks
+        // (tiles / tensor-core tiles / z-sweep / warp per target, options.h),
+        // on the caller's grid and targets, without the epilogue terms.
         sewald_gpu_session* s = cached_session(ctx, *p);
         const int64_t vol = (int64_t)s->g.n[0] * s->g.n[1] * s->g.n[2];
         double* flow = static_cast<double*>(s->flow.ensure(sizeof(double) * 3 * vol));
         cuda_check(cudaMemcpyAsync(flow, grid, sizeof(double) * 3 * vol, cudaMemcpyDefault, ctx->stream), "grid in");
-        double* dx = static_cast<double*>(ctx->hxt.ensure(sizeof(double) * 3 * std::max<int64_t>(Nt, 1)));
         double* du = static_cast<double*>(ctx->hu.ensure(sizeof(double) * 3 * std::max<int64_t>(Nt, 1)));
+        // the cached session's sources stay; its targets become xt
+        session_set_targets(s, xt, Nt, false);
         if (Nt > 0) {
-            cuda_check(cudaMemcpyAsync(dx, xt, sizeof(double) * 3 * Nt, cudaMemcpyDefault, ctx->stream), "xt in");
-            launch_stencil_bounds(s->g, s->p.P, dx, Nt, s->flags.as<int>() + FLAG_GATHER_BOX, ctx->stream);
+            check_flag(s, FLAG_TGT_NONFINITE, SEWALD_EINVAL, "target coordinates must be finite");
+            launch_stencil_bounds(s->g, s->p.P, s->xt.as<double>(), Nt, s->flags.as<int>() + FLAG_GATHER_BOX,
+                                  ctx->stream);
             check_flag(s, FLAG_GATHER_BOX, SEWALD_EINVAL,
                        "point too close to the extended box boundary; free-direction padding is too small");
             const double h3 = s->p.h * s->p.h * s->p.h;
-            launch_gather(s->g, s->w, flow, dx, nullptr, Nt, h3, 0, du, ctx->stream);
+            const int gmode = ensure_gather_order(s, 0, 1);
+            if (gmode == 1) {
+                cuda_check(cudaMemsetAsync(du, 0, sizeof(double) * 3 * Nt, ctx->stream), "u zero");
+                launch_gather_sweep(s->g, s->p.P, s->tg_w.as<double>(), s->tg_sw.as<int4>(), s->tg_off.as<int64_t>(),
+                                    sweep_shape(s->g, s->p.P), 0, 1, flow, h3, du, ctx->stream);
+            } else if (gmode == 2) {
+                launch_gather_tile(s->g, s->p.P, tile_shape(s->g, s->p.P, Nt), s->tg_w.as<double>(),
+                                   s->tg_sw.as<int4>(), s->tg_off.as<int64_t>(), 0, 1, flow, h3, 0, du, ctx->stream);
+            } else {
+                launch_gather(s->g, s->w, flow, s->xt.as<double>(), nullptr, Nt, h3, 0, du, ctx->stream);
+            }
+            ++ctx->launches;
+            cuda_check(cudaGetLastError(), "gather launch");
             cuda_check(cudaMemcpyAsync(u_out, du, sizeof(double) * 3 * Nt, cudaMemcpyDefault, ctx->stream), "u out");
         }
         cuda_check(cudaStreamSynchronize(ctx->stream), "gather sync");

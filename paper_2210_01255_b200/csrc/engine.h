@@ -86,6 +86,7 @@ struct sewald_gpu_session {
     bool tg_ready = false;
     int tg_mode = 0;  // 1: z-sweep gather, 2: tiled gather
     int tg_wpart = -1;  // part of the targets whose taps are current (0: all)
+    int opt_epoch = 0;  // options_epoch() the orderings were built under
     sewald_b200::DevBuf tg_keys, tg_keys2, tg_vals, tg_order, tg_off, tg_w, tg_sw;
     // grids
     sewald_b200::DevBuf grid, flow;

@@ -14,6 +14,7 @@
 // results are written without atomics.
 #include "device_common.cuh"
 #include "sg_kernels.h"
+#include "options.h"
 
 #include <algorithm>
 #include <cstdlib>
@@ -337,10 +338,7 @@ TileShape tile_shape(const DevGrid& g, int P, int64_t Nt) {
     // per target and a tile's region is loaded once per component.
     s.ok = P <= 20;
     s.B = P <= GT_PMAX ? std::max(1, 20 - P) : std::max(1, 24 - P);
-    static const int forced_l = [] {
-        const char* e = getenv("SEWALD_GATHER_L");
-        return e ? atoi(e) : 0;
-    }();
+    const int forced_l = option(SEWALD_OPT_GATHER_L);
     if (P <= 15) {
         const double cells = (double)g.n[0] * g.n[1] * g.n[2];
         const int b15 = 16 - P;
@@ -372,10 +370,7 @@ void launch_gather_tile(const DevGrid& g, int P, const TileShape& s, const doubl
                         double* u, cudaStream_t st) {
     const int64_t t0 = s.ntiles * part / nparts, t1 = s.ntiles * (part + 1) / nparts;
     if (t1 <= t0) return;
-    static const bool use_mma = [] {
-        const char* e = getenv("SEWALD_GATHER_MMA");
-        return !(e && e[0] == '0');
-    }();
+    const bool use_mma = option(SEWALD_OPT_GATHER_MMA) != 0;
     if ((use_mma || P > GT_PMAX || s.L == 15) && (s.L == 15 || s.L == 19 || s.L == 23)) {
         const bool wide = s.tpt >= 64.0;
         const size_t sm = mma_smem_bytes(s.L, wide ? 128 : 64);

@@ -13,6 +13,7 @@
 // instruction) and added to the grid with fp64 RED. The grid is zeroed first.
 #include "device_common.cuh"
 #include "sg_kernels.h"
+#include "options.h"
 
 #include <algorithm>
 #include <cstdlib>
@@ -356,10 +357,7 @@ spread_tile_mma_wide_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, 
 
 SpreadMmaShape spread_mma_shape(const DevGrid& g, int P) {
     SpreadMmaShape s{};
-    static const int Lenv = [] {
-        const char* e = getenv("SEWALD_SPREAD_MMA_L");
-        return e ? atoi(e) : 23;
-    }();
+    const int Lenv = option(SEWALD_OPT_SPREAD_MMA_L);
     s.L = Lenv == 19 ? 19 : 23;
     if (P > 20 && P <= 32) {  // wide windows: B = 8, L = P + 7 (spread_tile_mma_wide_kernel)
         s.ok = (int64_t)g.n[0] * g.n[1] * g.n[2] < (int64_t(1) << 31);
@@ -395,10 +393,7 @@ void launch_spread_mma_bucket(const DevGrid& g, int P, const SpreadMmaShape& s, 
 int launch_spread_mma(const DevGrid& g, int P, const SpreadMmaShape& s, const double* W, const int4* SW,
                       const double* STR, int C, const int64_t* off, double* out, cudaStream_t st) {
     cudaMemsetAsync(out, 0, sizeof(double) * C * (size_t)g.n[0] * g.n[1] * g.n[2], st);
-    static const bool cached = [] {  // SEWALD_SPREAD_CACHED=0: per-group tables (A/B)
-        const char* e = getenv("SEWALD_SPREAD_CACHED");
-        return !(e && e[0] == '0');
-    }();
+    const bool cached = option(SEWALD_OPT_SPREAD_CACHED) != 0;  // 0: per-group tables (A/B)
     for (int64_t a = 0; a < s.ntiles; a += (int64_t)1 << 30) {
         const int64_t n = std::min<int64_t>(s.ntiles - a, (int64_t)1 << 30);
         if (s.L > 23) {

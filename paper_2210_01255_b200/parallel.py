@@ -168,3 +168,64 @@ def d0_sharded_solve(session, grid, rank: int, world: int, dist, precompute_0p: 
     flow = torch.cat([outs[q][:, :sl.nx(q)] for q in range(world)], dim=1).contiguous()
     session.set_flow(flow)
     return flow
+
+
+# ---------------------------------------------------------------------------
+# Multi-GPU public entry point (host arrays in, host array out)
+# ---------------------------------------------------------------------------
+
+_SESSIONS = {}
+
+
+def full_potential_sharded(system, targets, params, rank: int, world: int, dist=None, engine=None, out=None,
+                           precompute_0p: bool = True, group=None):
+    """full_potential (realspace.h:46-47) on `world` GPUs, one process each.
+
+    Every rank calls it with the same host arrays (as it would call the
+    reference's full_potential); rank r uploads the inputs (the real-space sum
+    needs every source), spreads its 1/W slice of the sources, the grids are
+    summed (all-reduce; for D = 0 the slab-distributed solve), rank r evaluates
+    its 1/W of the cell-ordered targets, and the per-rank outputs are summed
+    onto rank 0 (reduce), which copies the velocity to `out` (host, e.g.
+    pinned). Returns u on rank 0 and None elsewhere. With world == 1 no
+    collective is issued."""
+    import numpy as np
+    import torch
+
+    from .api import Cell, Session, _system_arrays, _vec3, default_engine, InvalidArgument
+
+    if world > 1 and dist is None:
+        raise InvalidArgument("world > 1 needs torch.distributed")
+    eng = engine or default_engine()
+    dev = torch.device("cuda", eng.device)
+    x, f, nu = _system_arrays(system, params)
+    same = bool(targets.same_as_sources)
+    xt = None if same else _vec3(targets.x, "targets")
+    key = (id(eng), bytes(params.to_c()), tuple(float(v) for v in system.cell.L))
+    sess = _SESSIONS.get(key)
+    if sess is None:
+        _SESSIONS.clear()
+        sess = Session(params, Cell(tuple(system.cell.L)), eng)
+        _SESSIONS[key] = sess
+    T = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev, non_blocking=True)
+    dx, df, dnu, dxt = T(x), T(f), T(nu), T(xt)
+    sess.set_sources(dx, df, dnu)
+    sess.set_targets(dxt, same)
+    nt = x.shape[0] if same else xt.shape[0]
+    grid = torch.empty(sess.grid_size(), dtype=torch.float64, device=dev)
+    u = torch.empty((nt, 3), dtype=torch.float64, device=dev)
+    reduce_sum = None
+    if world > 1:
+        reduce_sum = lambda t: dist.all_reduce(t, group=group)
+    slab = dist if (world > 1 and int(params.d) == 0) else None
+    sharded_step(sess, x.shape[0], grid, u, rank, world, all_reduce=reduce_sum, precompute_0p=precompute_0p,
+                 gather_result=False, slab_dist=slab)
+    if world > 1:
+        dist.reduce(u, dst=0, group=group)
+    if rank != 0:
+        torch.cuda.current_stream().synchronize()
+        return None
+    if out is None:
+        out = np.empty((nt, 3))
+    torch.from_numpy(out).copy_(u)  # D2H (synchronous)
+    return out

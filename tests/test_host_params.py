@@ -138,3 +138,17 @@ def test_dropin_headers_self_contained(tmp_path):
         r = subprocess.run([cxx, "-std=c++20", "-fsyntax-only", "-Wall", "-Wextra", "-Werror",
                             "-I", os.path.join(ROOT, "include"), str(src)], capture_output=True, text=True)
         assert r.returncode == 0, (rel, r.stderr[-2000:])
+
+
+def test_kernel_options_roundtrip(S):
+    """Kernel-choice switches (sewald_gpu_set_option): host-only, no GPU call."""
+    old = S.get_kernel_option(S.KernelOption.RS_SYM)
+    with S.kernel_options(RS_SYM=2, GATHER=1, GATHER_L=15):
+        assert S.get_kernel_option(S.KernelOption.RS_SYM) == 2
+        assert S.get_kernel_option(S.KernelOption.GATHER) == 1
+        assert S.get_kernel_option(S.KernelOption.GATHER_L) == 15
+    assert S.get_kernel_option(S.KernelOption.RS_SYM) == old
+    with pytest.raises(S.InvalidArgument):
+        S.set_kernel_option(S.KernelOption.GATHER_L, 17)
+    with pytest.raises(S.InvalidArgument):
+        S.set_kernel_option(S.KernelOption.RS_SYM, 5)
