@@ -31,6 +31,18 @@ void cufft_check(cufftResult r, const char* what) {
         throw EngineError(SEWALD_ECUFFT, std::string(what) + ": cuFFT error " + std::to_string((int)r));
 }
 
+HostFlags::~HostFlags() {
+    if (p) cudaFreeHost(p);
+}
+
+int* HostFlags::get() {
+    if (!p) {
+        cuda_check(cudaMallocHost(reinterpret_cast<void**>(&p), sizeof(int) * 16), "pinned flags");
+        std::memset(p, 0, sizeof(int) * 16);
+    }
+    return p;
+}
+
 DevBuf::~DevBuf() {
     if (ptr) cudaFree(ptr);
 }
@@ -205,6 +217,23 @@ void check_flag(sewald_gpu_session* s, int which, int code, const char* msg) {
 enum { FLAG_SRC_NONFINITE = 0, FLAG_TGT_NONFINITE = 1, FLAG_SPREAD_BOX = 2, FLAG_GATHER_BOX = 3,
        FLAG_SINGULAR = 4, NFLAGS = 8 };
 
+// The input checks of one call (non-finite sources and targets) are read
+// together, once, by the first stage that consumes the inputs: one D2H and
+// one stream synchronisation instead of one per stage.
+void check_inputs(sewald_gpu_session* s) {
+    if (s->inputs_checked) return;
+    int* h = s->hflags.get();
+    cuda_check(cudaMemcpyAsync(h, s->flags.as<int>(), sizeof(int) * 2, cudaMemcpyDeviceToHost, s->ctx->stream),
+               "flag read");
+    cuda_check(cudaStreamSynchronize(s->ctx->stream), "flag sync");
+    if (h[FLAG_SRC_NONFINITE] || h[FLAG_TGT_NONFINITE]) {
+        cuda_check(cudaMemsetAsync(s->flags.as<int>(), 0, sizeof(int) * 2, s->ctx->stream), "flag reset");
+        if (h[FLAG_SRC_NONFINITE]) throw EngineError(SEWALD_EINVAL, "non-finite source position");
+        throw EngineError(SEWALD_EINVAL, "target coordinates must be finite");
+    }
+    s->inputs_checked = true;
+}
+
 void build_cell_grid(sewald_gpu_session* s) {
     const sewald_params_c& p = s->p;
     CellGrid cg{};
@@ -343,8 +372,10 @@ void ensure_spread_order(sewald_gpu_session* s, int64_t i0, int64_t i1) {
         launch_spread_bucket(s->g, s->p.P, s->x.as<double>() + 3 * i0, n, s->shape,
                              s->sp_keys.as<uint32_t>(), s->sp_vals.as<uint32_t>(), bad, st);
     ++s->ctx->launches;
-    check_flag(s, FLAG_SPREAD_BOX, SEWALD_EINVAL,
-               "point too close to the extended box boundary; free-direction padding is too small");
+    // a finite point always has an in-range stencil on a periodic axis
+    if (s->p.d < 3)
+        check_flag(s, FLAG_SPREAD_BOX, SEWALD_EINVAL,
+                   "point too close to the extended box boundary; free-direction padding is too small");
     if (n > 0) {
         sort_pairs(s, s->sp_keys.as<uint32_t>(), s->sp_keys2.as<uint32_t>(), s->sp_vals.as<uint32_t>(),
                    s->sp_order.as<uint32_t>(), n, bits_for((uint64_t)nb + 1));
@@ -625,6 +656,7 @@ void session_set_sources(sewald_gpu_session* s, const double* x, const double* f
     s->cells_ready = false;
     s->sums_ready = false;
     s->tg_ready = false;
+    s->inputs_checked = false;
     if (s->same) s->Nt = N;
 }
 
@@ -632,6 +664,7 @@ void session_set_targets(sewald_gpu_session* s, const double* xt, int64_t Nt, bo
     if (s->same != same) s->cells_ready = false;  // the cell width depends on the kernel (build_cell_grid)
     s->same = same;
     s->tg_ready = false;
+    s->inputs_checked = false;
     if (same) {
         s->Nt = s->N;
         return;
@@ -649,7 +682,7 @@ void session_set_targets(sewald_gpu_session* s, const double* xt, int64_t Nt, bo
 
 void session_spread(sewald_gpu_session* s, int64_t i0, int64_t i1, double* grid) {
     if (i0 < 0 || i1 > s->N || i0 > i1) throw EngineError(SEWALD_EINVAL, "bad source range");
-    check_flag(s, FLAG_SRC_NONFINITE, SEWALD_EINVAL, "non-finite source position");
+    check_inputs(s);
     ensure_spread_order(s, i0, i1);
     cudaStream_t st = s->ctx->stream;
     const int64_t vol = (int64_t)s->g.n[0] * s->g.n[1] * s->g.n[2];
@@ -709,7 +742,7 @@ void session_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p
 
 void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, double* u) {
     if (nparts < 1 || part < 0 || part >= nparts) throw EngineError(SEWALD_EINVAL, "bad target partition");
-    check_flag(s, FLAG_TGT_NONFINITE, SEWALD_EINVAL, "target coordinates must be finite");
+    check_inputs(s);
     cudaStream_t st = s->ctx->stream;
     ensure_target_order(s);
     const int64_t Nt = s->Nt;
@@ -913,8 +946,15 @@ void host_pipeline(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* 
         tm.mark();
     }
     tm.mark();  // 6
+    int* hf = s->hflags.get();
+    cuda_check(cudaMemcpyAsync(hf + FLAG_SINGULAR, s->flags.as<int>() + FLAG_SINGULAR, sizeof(int),
+                               cudaMemcpyDeviceToHost, ctx->stream), "flag read");
     cuda_check(cudaStreamSynchronize(ctx->stream), "pipeline sync");
-    check_flag(s, FLAG_SINGULAR, SEWALD_EDOMAIN, "real-space kernel is singular at the origin");
+    if (hf[FLAG_SINGULAR]) {  // read with the result: no extra synchronisation
+        hf[FLAG_SINGULAR] = 0;
+        cuda_check(cudaMemsetAsync(s->flags.as<int>() + FLAG_SINGULAR, 0, sizeof(int), ctx->stream), "flag reset");
+        throw EngineError(SEWALD_EDOMAIN, "real-space kernel is singular at the origin");
+    }
     sewald_timings_c& T = ctx->timings;
     T = sewald_timings_c{};
     T.h2d_ms = tm.ms(0, 1);
@@ -1061,7 +1101,7 @@ int sewald_gpu_gather(sewald_gpu_ctx* ctx, const sewald_params_c* p, const doubl
         // the cached session's sources stay; its targets become xt
         session_set_targets(s, xt, Nt, false);
         if (Nt > 0) {
-            check_flag(s, FLAG_TGT_NONFINITE, SEWALD_EINVAL, "target coordinates must be finite");
+            check_inputs(s);
             launch_stencil_bounds(s->g, s->p.P, s->xt.as<double>(), Nt, s->flags.as<int>() + FLAG_GATHER_BOX,
                                   ctx->stream);
             check_flag(s, FLAG_GATHER_BOX, SEWALD_EINVAL,

@@ -33,6 +33,13 @@ struct DevBuf {
     template <class T> T* as() const { return static_cast<T*>(ptr); }
 };
 
+// Pinned host copy of the session's device status flags (one D2H per check).
+struct HostFlags {
+    int* p = nullptr;
+    ~HostFlags();
+    int* get();
+};
+
 struct FourierPlanD3;   // cuFFT plans + k tables for the fully periodic path
 struct FourierPlanAFT;  // zero-padded / upsampled free-direction path (d < 3)
 struct AftDeleter {
@@ -92,6 +99,8 @@ struct sewald_gpu_session {
     sewald_b200::DevBuf grid, flow;
     // global sums: f (3), q.nu (1), x (q.nu) (3); partials
     sewald_b200::DevBuf sums, partials, flags, pair_counter, work_counter, rs_scratch;
+    sewald_b200::HostFlags hflags;
+    bool inputs_checked = false;  // non-finite source / target flags read since the last upload
     bool sums_ready = false;
     std::unique_ptr<sewald_b200::FourierPlanD3> d3;
     std::unique_ptr<sewald_b200::FourierPlanAFT, sewald_b200::AftDeleter> aft;

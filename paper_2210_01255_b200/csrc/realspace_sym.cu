@@ -113,6 +113,122 @@ __device__ __forceinline__ void pair_both(const Screened& sc, double xi2, double
     }
 }
 
+// The same pair split in two halves so that two pairs can be in flight per
+// lane (SEWALD_SYM_ILP = 2): the scalar coefficients of a pair, then its
+// contribution to one side. sign = +1 for the target (separation r), -1 for
+// the source's reaction (separation -r: the odd kernels change sign).
+template <int KIND>
+struct PairCoef {
+    double a, b;
+};
+
+template <int KIND>
+__device__ __forceinline__ PairCoef<KIND> pair_coef(const Screened& sc, double xi2, double n2) {
+    PairCoef<KIND> c;
+    if (KIND == SEWALD_STOKESLET) {
+        c.a = sc.Ey * (sc.R - sc.cx);
+        c.b = sc.Ey * (sc.iy * sc.iy) * (sc.R + sc.cx);
+    } else if (KIND == SEWALD_ROTLET) {
+        c.a = sc.Ey * (sc.iy * sc.iy) * (sc.R + sc.cx);
+        c.b = 0.0;
+    } else {
+        const double iy2 = sc.iy * sc.iy;
+        const double x2 = xi2 * n2;
+        c.a = -2.0 * sc.Ey * (iy2 * iy2) * (3.0 * sc.R + (3.0 + 2.0 * x2) * sc.cx);
+        c.b = 2.0 * xi2 * sc.Ey * sc.cx;
+    }
+    return c;
+}
+
+template <int KIND, bool REACTION>
+__device__ __forceinline__ void pair_apply(const PairCoef<KIND>& c, double r0, double r1, double r2,
+                                           const double* s, double* u) {
+    if (KIND == SEWALD_STOKESLET) {
+        const double bs = c.b * (r0 * s[0] + r1 * s[1] + r2 * s[2]);
+        u[0] = fma(c.a, s[0], fma(bs, r0, u[0]));
+        u[1] = fma(c.a, s[1], fma(bs, r1, u[1]));
+        u[2] = fma(c.a, s[2], fma(bs, r2, u[2]));
+    } else if (KIND == SEWALD_ROTLET) {
+        const double cc = REACTION ? -c.a : c.a;
+        u[0] = fma(cc, s[1] * r2 - s[2] * r1, u[0]);
+        u[1] = fma(cc, s[2] * r0 - s[0] * r2, u[1]);
+        u[2] = fma(cc, s[0] * r1 - s[1] * r0, u[2]);
+    } else {
+        const double rq = r0 * s[0] + r1 * s[1] + r2 * s[2];
+        const double rv = r0 * s[3] + r1 * s[4] + r2 * s[5];
+        const double w = fma(c.a * rq, rv, c.b * s[6]);
+        const double cv = c.b * rv, cq = c.b * rq;
+        if (REACTION) {
+            u[0] = fma(-cq, s[3], fma(-cv, s[0], fma(-w, r0, u[0])));
+            u[1] = fma(-cq, s[4], fma(-cv, s[1], fma(-w, r1, u[1])));
+            u[2] = fma(-cq, s[5], fma(-cv, s[2], fma(-w, r2, u[2])));
+        } else {
+            u[0] = fma(cq, s[3], fma(cv, s[0], fma(w, r0, u[0])));
+            u[1] = fma(cq, s[4], fma(cv, s[1], fma(w, r1, u[1])));
+            u[2] = fma(cq, s[5], fma(cv, s[2], fma(w, r2, u[2])));
+        }
+    }
+}
+
+#ifndef SEWALD_SYM_ILP
+#define SEWALD_SYM_ILP 1
+#endif
+// Blocks with fewer candidate pairs than this go through the pooled path
+// (0 = rotation steps only). c2: rotation only 67.6 ms; pooled below
+// 192 / 256 / 384 pairs (mode 2): 63.3 / 62.7-63.0 / 63.5 ms.
+#ifndef SEWALD_SYM_POOL
+#define SEWALD_SYM_POOL 256
+#endif
+// Pooled pairs accumulate: 0 both sides with shared-memory atomics (the j
+// side in the block's reaction slots), 1 both sides with global fp64 RED,
+// 2 i side shared, j side global (modes 1, 2 skip the block's reaction flush).
+// c2 at 256: mode 0 67.0 ms, mode 1 63.4 ms, mode 2 63.0 ms.
+#ifndef SEWALD_SYM_POOL_MODE
+#define SEWALD_SYM_POOL_MODE 2
+#endif
+// exp table copies (lane-interleaved, conflict-free lookups): 16 copies
+// measured slower at c2 (69.0 vs 67.6 ms), so one copy.
+#ifndef SEWALD_EXP_REP
+#define SEWALD_EXP_REP 1
+#endif
+
+// One branch-free pair slot of a step: separation, acceptance, screened
+// coefficients (zero for lanes without an accepted pair).
+template <int KIND, int NS, bool SHORT>
+struct SlotEval {
+    double r0, r1, r2;
+    PairCoef<KIND> c;
+    double sj[NS];
+    bool acc;
+};
+
+template <int KIND, int RS, int NS, bool SHORT>
+__device__ __forceinline__ void slot_eval(SlotEval<KIND, NS, SHORT>& e, const double* rec, double xs0, double xs1,
+                                          double xs2, bool in, double rc2, double xi, double xi2,
+                                          const double* exp_tab, bool& coincident) {
+    const double2 xy = *reinterpret_cast<const double2*>(rec);
+    const double2 zs0 = *reinterpret_cast<const double2*>(rec + 2);
+    e.r0 = xs0 - xy.x;
+    e.r1 = xs1 - xy.y;
+    e.r2 = xs2 - zs0.x;
+    const double n2 = __dadd_rn(__dadd_rn(__dmul_rn(e.r0, e.r0), __dmul_rn(e.r1, e.r1)), __dmul_rn(e.r2, e.r2));
+    bool acc = in && n2 < rc2;
+    coincident |= acc && n2 == 0.0;
+    acc = acc && n2 != 0.0;
+    e.acc = acc;
+    const double n2e = acc ? n2 : 0.25 * rc2;
+    e.sj[0] = zs0.y;
+#pragma unroll
+    for (int c = 1; c < NS; c += 2) {
+        const double2 v = *reinterpret_cast<const double2*>(rec + 3 + c);
+        e.sj[c] = v.x;
+        if (c + 1 < NS) e.sj[c + 1] = v.y;
+    }
+    Screened sc = screened<SHORT, SEWALD_EXP_REP>(n2e, xi, xi2, exp_tab);
+    sc.Ey = acc ? sc.Ey : 0.0;
+    e.c = pair_coef<KIND>(sc, xi2, n2e);
+}
+
 template <int KIND, int S, bool SHORT>
 __global__ void __launch_bounds__(SYM_THREADS, SEWALD_SYM_MINB)
 realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed,
@@ -131,14 +247,30 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     __shared__ __align__(16) double jrec_all[SYM_WARPS][32][RS];
     __shared__ long long jid_all[SYM_WARPS][32];
     __shared__ float4 jf_all[SYM_WARPS][32];  // fp32 positions for the candidate pass
-    __shared__ double exp_tab[32];
-    if (threadIdx.x < 32) exp_tab[threadIdx.x] = c_exp2_tab32[threadIdx.x];
+    // 2^(j/32) table, replicated SEWALD_EXP_REP times (lane-interleaved: conflict-free lookups)
+    __shared__ double exp_tab_rep[32 * SEWALD_EXP_REP];
+#if SEWALD_SYM_POOL > 0
+    // sparse-block pool (see below): the cluster's records, its pooled
+    // i-side sums and the block's candidate queue, per warp
+    constexpr int IS = (3 + NS + 1) | 1;  // odd stride (in doubles): random il hit distinct banks; last: index
+    __shared__ double irec_all[SYM_WARPS][32][IS];
+    __shared__ double ipool_all[SYM_WARPS][32][3];
+    __shared__ unsigned short queue_all[SYM_WARPS][SEWALD_SYM_POOL];
+#endif
+    for (int t = threadIdx.x; t < 32 * SEWALD_EXP_REP; t += SYM_THREADS) exp_tab_rep[t] = c_exp2_tab32[t / SEWALD_EXP_REP];
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const double* exp_tab = exp_tab_rep + (lane % SEWALD_EXP_REP);
     double(*jrec)[RS] = jrec_all[warp];
     long long* jid = jid_all[warp];
     float4* jf = jf_all[warp];
+#if SEWALD_SYM_POOL > 0
+    double(*irec)[IS] = irec_all[warp];
+    double(*ipool)[3] = ipool_all[warp];
+    unsigned short* queue = queue_all[warp];
+    const unsigned lanemask_lt = (1u << lane) - 1u;
+#endif
     unsigned long long npairs = 0;  // flushed per cluster from the 32-bit step counter
     // Persistent warps: clusters are taken from a global counter, so the
     // uneven per-cluster work (row geometry, half rule) does not leave SMs
@@ -167,6 +299,17 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
         for (int c = 0; c < NS; ++c) fa[c] = q[4 + c];
     }
 
+#if SEWALD_SYM_POOL > 0
+    __syncwarp();
+    irec[lane][0] = xa0;
+    irec[lane][1] = xa1;
+    irec[lane][2] = xa2;
+#pragma unroll
+    for (int c = 0; c < NS; ++c) irec[lane][3 + c] = fa[c];
+    irec[lane][IS - 1] = __longlong_as_double(valid ? ida : 0);
+    ipool[lane][0] = ipool[lane][1] = ipool[lane][2] = 0.0;
+    __syncwarp();
+#endif
     double lo[3] = {valid ? xa0 : 1e300, valid ? xa1 : 1e300, valid ? xa2 : 1e300};
     double hi[3] = {valid ? xa0 : -1e300, valid ? xa1 : -1e300, valid ? xa2 : -1e300};
 #pragma unroll
@@ -287,6 +430,134 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                     }
                     unsigned steps = __reduce_or_sync(0xffffffffu, m);
                     bool coincident = false;
+                    bool pooled = false;
+#if SEWALD_SYM_POOL > 0
+                    // Sparse block (few candidates, spread over many rotations): the
+                    // rotation steps would run mostly idle lanes. Its candidate pairs
+                    // are queued instead (rotation-major, so a batch rarely repeats a
+                    // particle) and evaluated 32 at a time, one pair per lane; both
+                    // sides accumulate with shared-memory atomics (i side: the
+                    // cluster's pool, added to the lane sums at the end; j side: the
+                    // block's reaction slots, flushed as for the rotation steps).
+                    const int ncand = __reduce_add_sync(0xffffffffu, __popc(m));
+                    pooled = ncand < SEWALD_SYM_POOL;
+                    if (pooled) {
+                        int base = 0;
+                        unsigned st = steps;
+                        while (st) {
+                            const int s = 31 - __clz(st);
+                            st ^= 1u << s;
+                            const bool on = (m >> s) & 1u;
+                            const unsigned act = __ballot_sync(0xffffffffu, on);
+                            if (on)
+                                queue[base + __popc(act & lanemask_lt)] =
+                                    (unsigned short)((lane << 5) | ((lane + s) & 31));
+                            base += __popc(act);
+                        }
+                        __syncwarp();
+                        for (int k0 = 0; k0 < ncand; k0 += 32) {
+                            const int k = k0 + lane;
+                            const bool in = k < ncand;
+                            const int e = in ? queue[k] : 0;
+                            const int il = e >> 5, j = e & 31;
+                            const double* ir = irec[il];
+                            const double ys0 = ir[0] - shx, ys1 = ir[1] - shy, ys2 = ir[2] - shz;
+                            double fi[NS];
+#pragma unroll
+                            for (int c = 0; c < NS; ++c) fi[c] = ir[3 + c];
+                            SlotEval<KIND, NS, SHORT> ev;
+                            double* rec = jrec[j];
+                            slot_eval<KIND, RS, NS, SHORT>(ev, rec, ys0, ys1, ys2, in, rc2, a.xi, xi2, exp_tab,
+                                                          coincident);
+                            if (ev.acc) {
+                                double ui[3] = {0.0, 0.0, 0.0}, uj[3] = {0.0, 0.0, 0.0};
+                                pair_apply<KIND, false>(ev.c, ev.r0, ev.r1, ev.r2, ev.sj, ui);
+                                pair_apply<KIND, true>(ev.c, ev.r0, ev.r1, ev.r2, fi, uj);
+#if SEWALD_SYM_POOL_MODE == 1
+                                // global fp64 RED on both sides (no shared-memory CAS loops)
+                                double* di = u + 3 * __double_as_longlong(irec[il][IS - 1]);
+                                double* dj = u + 3 * jid[j];
+#pragma unroll
+                                for (int c = 0; c < 3; ++c) {
+                                    atomicAdd(di + c, ui[c]);
+                                    atomicAdd(dj + c, uj[c]);
+                                }
+#elif SEWALD_SYM_POOL_MODE == 2
+                                // i side: the cluster's shared pool; j side: global fp64 RED
+                                double* dj = u + 3 * jid[j];
+#pragma unroll
+                                for (int c = 0; c < 3; ++c) {
+                                    atomicAdd(&ipool[il][c], ui[c]);
+                                    atomicAdd(dj + c, uj[c]);
+                                }
+#else
+#pragma unroll
+                                for (int c = 0; c < 3; ++c) {
+                                    atomicAdd(&ipool[il][c], ui[c]);
+                                    atomicAdd(&rec[RO + c], uj[c]);
+                                }
+#endif
+                                npairs32 += 2u;
+                            }
+                        }
+                        steps = 0u;  // the rotation loop below has nothing left
+                    }
+#endif
+#if SEWALD_SYM_ILP == 2
+                    // Two steps in flight per lane: their scalar math is independent
+                    // (hides the fp64 dependency latency); the reactions are applied
+                    // one step after the other with a warp barrier between, since
+                    // lane l's slot in the second step can be another lane's slot in
+                    // the first.
+                    while (BF && steps) {
+                        const int s1 = 31 - __clz(steps);
+                        steps ^= 1u << s1;
+                        const int j1 = (lane + s1) & 31;
+                        if (steps == 0u) {
+                            SlotEval<KIND, NS, SHORT> e;
+                            double* rec = jrec[j1];
+                            slot_eval<KIND, RS, NS, SHORT>(e, rec, xs0, xs1, xs2, (m >> s1) & 1u, rc2, a.xi, xi2,
+                                                          exp_tab, coincident);
+                            pair_apply<KIND, false>(e.c, e.r0, e.r1, e.r2, e.sj, ua);
+                            const double2 r01 = *reinterpret_cast<const double2*>(rec + RO);
+                            double ub[3] = {r01.x, r01.y, rec[RO + 2]};
+                            pair_apply<KIND, true>(e.c, e.r0, e.r1, e.r2, fa, ub);
+                            *reinterpret_cast<double2*>(rec + RO) = make_double2(ub[0], ub[1]);
+                            rec[RO + 2] = ub[2];
+                            npairs32 += e.acc ? 2u : 0u;
+                            break;
+                        }
+                        const int s2 = 31 - __clz(steps);
+                        steps ^= 1u << s2;
+                        const int j2 = (lane + s2) & 31;
+                        SlotEval<KIND, NS, SHORT> e1, e2;
+                        double* rec1 = jrec[j1];
+                        double* rec2 = jrec[j2];
+                        slot_eval<KIND, RS, NS, SHORT>(e1, rec1, xs0, xs1, xs2, (m >> s1) & 1u, rc2, a.xi, xi2,
+                                                      exp_tab, coincident);
+                        slot_eval<KIND, RS, NS, SHORT>(e2, rec2, xs0, xs1, xs2, (m >> s2) & 1u, rc2, a.xi, xi2,
+                                                      exp_tab, coincident);
+                        pair_apply<KIND, false>(e1.c, e1.r0, e1.r1, e1.r2, e1.sj, ua);
+                        pair_apply<KIND, false>(e2.c, e2.r0, e2.r1, e2.r2, e2.sj, ua);
+                        {
+                            const double2 r01 = *reinterpret_cast<const double2*>(rec1 + RO);
+                            double ub[3] = {r01.x, r01.y, rec1[RO + 2]};
+                            pair_apply<KIND, true>(e1.c, e1.r0, e1.r1, e1.r2, fa, ub);
+                            *reinterpret_cast<double2*>(rec1 + RO) = make_double2(ub[0], ub[1]);
+                            rec1[RO + 2] = ub[2];
+                        }
+                        __syncwarp();
+                        {
+                            const double2 r01 = *reinterpret_cast<const double2*>(rec2 + RO);
+                            double ub[3] = {r01.x, r01.y, rec2[RO + 2]};
+                            pair_apply<KIND, true>(e2.c, e2.r0, e2.r1, e2.r2, fa, ub);
+                            *reinterpret_cast<double2*>(rec2 + RO) = make_double2(ub[0], ub[1]);
+                            rec2[RO + 2] = ub[2];
+                        }
+                        __syncwarp();
+                        npairs32 += (e1.acc ? 2u : 0u) + (e2.acc ? 2u : 0u);
+                    }
+#endif
                     while (steps) {
                         const int s = 31 - __clz(steps);  // highest step first: one FLO
                         steps ^= 1u << s;
@@ -315,7 +586,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                                 sj[c] = v.x;
                                 if (c + 1 < NS) sj[c + 1] = v.y;
                             }
-                            Screened sc = screened<SHORT>(n2e, a.xi, xi2, exp_tab);
+                            Screened sc = screened<SHORT, SEWALD_EXP_REP>(n2e, a.xi, xi2, exp_tab);
                             sc.Ey = acc ? sc.Ey : 0.0;
                             const double2 r01 = *reinterpret_cast<const double2*>(rec + RO);
                             double ub[3] = {r01.x, r01.y, rec[RO + 2]};
@@ -349,7 +620,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                                         sj[c] = v.x;
                                         if (c + 1 < NS) sj[c + 1] = v.y;
                                     }
-                                    const Screened sc = screened<SHORT>(n2, a.xi, xi2, exp_tab);
+                                    const Screened sc = screened<SHORT, SEWALD_EXP_REP>(n2, a.xi, xi2, exp_tab);
                                     const double2 r01 = *reinterpret_cast<const double2*>(rec + RO);
                                     double ub[3] = {r01.x, r01.y, rec[RO + 2]};
                                     pair_both<KIND>(sc, xi2, n2, r0, r1, r2, sj, fa, ua, ub);
@@ -362,7 +633,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                     }
                     if (coincident) atomicExch(err, 1);
                     __syncwarp();
-                    if (lane < cnt) {
+                    if (lane < cnt && !(SEWALD_SYM_POOL_MODE != 0 && pooled)) {
                         double* dst = u + 3 * jid[lane];
                         atomicAdd(dst, jrec[lane][RO]);
                         atomicAdd(dst + 1, jrec[lane][RO + 1]);
@@ -373,6 +644,12 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
         }
     }
     npairs += npairs32;
+#if SEWALD_SYM_POOL > 0
+    __syncwarp();
+    ua[0] += ipool[lane][0];
+    ua[1] += ipool[lane][1];
+    ua[2] += ipool[lane][2];
+#endif
     if (valid) {
         double* dst = u + 3 * ida;
         atomicAdd(dst, ua[0]);

@@ -80,7 +80,10 @@ __device__ __forceinline__ double exp_neg(double y) {
 
 // e^{-y} for y >= 0 via 2^(j/32) table (tab: shared-memory copy of
 // c_exp2_tab32) and a degree-6 polynomial: 9 fp64 FMAs instead of 16.
-template <bool CLAMP = true>
+// STRIDE > 1: the table is replicated STRIDE times, interleaved, and `tab`
+// points at the calling lane's copy (lane % STRIDE), so a warp's random
+// indices fall in distinct shared-memory banks.
+template <bool CLAMP = true, int STRIDE = 1>
 __device__ __forceinline__ double exp_neg_tab(double y, const double* tab) {
     // callers that guarantee y <= 49 (x <= 7, the SHORT real-space kernels) skip the clamp
     if (CLAMP) y = fmin(y, 700.0);
@@ -95,7 +98,7 @@ __device__ __forceinline__ double exp_neg_tab(double y, const double* tab) {
     for (int i = 5; i >= 0; --i) p = fma(p, f, c_exp6[i]);
     const int m = n >> 5;  // n = 32 m + j, n <= 0
     // scale by 2^m in the exponent field (y <= 700 keeps the result normal)
-    const double v = p * tab[n & 31];
+    const double v = p * tab[(n & 31) * STRIDE];
     return __hiloint2double(__double2hiint(v) + (m << 20), __double2loint(v));
 }
 
@@ -137,15 +140,23 @@ struct Screened {
     double iy, Ey, R, cx, E;
 };
 
-template <bool SHORT = false>
+template <bool SHORT = false, int STRIDE = 1>
 __device__ __forceinline__ Screened screened(double n2, double xi, double xi2, const double* exp_tab = nullptr) {
     Screened s;
     s.iy = rsqrt_nr(n2);
     const double r = n2 * s.iy;
     const double x = xi * r;
-    s.E = exp_tab ? exp_neg_tab<!SHORT>(xi2 * n2, exp_tab) : exp_neg(xi2 * n2);
+#ifdef SEWALD_PROBE_NOEXP  // timing probe builds only (wrong results)
+    s.E = 1.0 / (1.0 + 0.0 * n2);
+#else
+    s.E = exp_tab ? exp_neg_tab<!SHORT, STRIDE>(xi2 * n2, exp_tab) : exp_neg(xi2 * n2);
+#endif
     s.Ey = s.E * s.iy;
+#ifdef SEWALD_PROBE_NOERFCX
+    s.R = x;
+#else
     s.R = erfcx_rat<SHORT>(x);
+#endif
     s.cx = c_misc[4] * x;
     return s;
 }

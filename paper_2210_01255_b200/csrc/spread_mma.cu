@@ -358,7 +358,7 @@ spread_tile_mma_wide_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, 
 SpreadMmaShape spread_mma_shape(const DevGrid& g, int P) {
     SpreadMmaShape s{};
     const int Lenv = option(SEWALD_OPT_SPREAD_MMA_L);
-    s.L = Lenv == 19 ? 19 : 23;
+    s.L = (Lenv == 19 && P <= 19) ? 19 : 23;  // the region must hold a P-wide stencil (B >= 1)
     if (P > 20 && P <= 32) {  // wide windows: B = 8, L = P + 7 (spread_tile_mma_wide_kernel)
         s.ok = (int64_t)g.n[0] * g.n[1] * g.n[2] < (int64_t(1) << 31);
         s.B = 8;

@@ -209,7 +209,7 @@ def test_spread_family(S, ref, family, P, d, kind, window):
 
 @pytest.mark.oracle
 @pytest.mark.parametrize("family", list(GATHER_FAMILIES))
-@pytest.mark.parametrize("P", [8, 12, 15, 16, 18, 20, 24, 32])
+@pytest.mark.parametrize("P", [8, 12, 14, 16, 18, 20, 24, 32])
 @pytest.mark.parametrize("d", [3, 2, 1, 0])
 def test_gather_family(S, ref, family, P, d):
     """sewald_gpu_gather runs the kernel the pipeline would pick (or the
