@@ -507,6 +507,16 @@ def run_ours(args, cfg):
             if par is not None:
                 line["e2e"]["parity_vs_fixture"] = par
 
+    # the C++ drop-in path (sewald::full_potential, pageable std::vector in/out), config 2 only
+    exe = os.path.join(ROOT, "paper_2210_01255_b200", "lib", "bench_dropin")
+    if ws == 1 and rank == 0 and not args.no_e2e and cfg.index == 2 and os.path.exists(exe):
+        try:
+            r = subprocess.run([exe, str(N), str(max(1, min(args.steps, 5)))], capture_output=True, text=True,
+                               timeout=600)
+            line["e2e_cpp"] = json.loads(r.stdout.strip().splitlines()[-1])
+        except Exception as e:  # pragma: no cover
+            line["e2e_cpp"] = {"unavailable": str(e)[:200]}
+
     if ws == 1 and rank == 0 and not args.no_cpu_baseline:
         try:
             v, det = cpu_reference_sample(cfg, params.to_c(), x, f, nu, xt, os.cpu_count() or 1, sample=10000)
