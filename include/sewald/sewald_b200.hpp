@@ -348,4 +348,13 @@ std::vector<Vec3> realspace_potential(const SourceSystem& system, const TargetSe
 std::vector<Vec3> full_potential(const SourceSystem& system, const TargetSet& targets,
                                  const EwaldParams& params, const SePipelineOptions& opt = {});
 
+// ---- B200 extension (not in the reference API) -------------------------------------
+namespace b200 {
+// full_potential / se_fourier_potential on these GPUs of this node (one
+// process, NVLink peer memory; include/sewald_gpu.h sewald_gpu_multi_*).
+// Fewer than two entries: one GPU (the default; SEWALD_DEVICES="0,1,..."
+// sets the initial list).
+void use_devices(const std::vector<int>& devices);
+}  // namespace b200
+
 }  // namespace sewald

@@ -156,6 +156,27 @@ enum {
 int sewald_gpu_set_option(int which, int value);
 int sewald_gpu_get_option(int which, int* value);
 
+/* ---- multi-GPU context (one process, several GPUs of one node) --------
+ * Replaces the reference's only parallel knob (realspace_potential's
+ * n_threads, realspace.h:40-41) for callers without MPI/torch: the sources
+ * are spread in 1/W slices, the grids summed over NVLink peer memory, and
+ * each GPU evaluates 1/W of the targets. dev_ids may repeat a
+ * device (tests on one GPU); distinct devices need peer access (ECUDA
+ * otherwise). Arguments and results as sewald_gpu_full_potential. */
+typedef struct sewald_gpu_multi sewald_gpu_multi;
+int sewald_gpu_multi_create(int n_gpus, const int* dev_ids, sewald_gpu_multi** out);
+void sewald_gpu_multi_destroy(sewald_gpu_multi* m);
+const char* sewald_gpu_multi_last_error(const sewald_gpu_multi* m);
+int sewald_gpu_multi_size(const sewald_gpu_multi* m);
+/* The single-device context of member d (e.g. for sewald_gpu_set_table0p). */
+sewald_gpu_ctx* sewald_gpu_multi_context(sewald_gpu_multi* m, int d);
+int sewald_gpu_multi_full_potential(sewald_gpu_multi* m, const sewald_params_c* p, const double* x,
+                                    const double* f, const double* nu, int64_t N, const double* xt, int64_t Nt,
+                                    int same_as_sources, int precompute_0p, double* u_out);
+int sewald_gpu_multi_fourier_potential(sewald_gpu_multi* m, const sewald_params_c* p, const double* x,
+                                       const double* f, const double* nu, int64_t N, const double* xt, int64_t Nt,
+                                       int same_as_sources, int precompute_0p, double* u_out);
+
 /* ---- host-buffer entry points (drop-in path) ------------------------- */
 /* x, f: N*3 doubles; nu: N*3 (stresslet) or NULL; xt: Nt*3. When
  * same_as_sources != 0 the targets are the sources (xt may be NULL or x).

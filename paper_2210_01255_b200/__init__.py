@@ -13,6 +13,6 @@ from .api import (Cell, DeviceError, DomainError, Engine, EstimateReport, EwaldP
                   select_parameters, source_quantity, spread, strength_components, window_eval,
                   window_hat, ModifiedKernelSpec, FourierField, PrecomputedKernel0P, aft_forward,
                   aft_inverse, scale, precompute_0p, KernelOption, get_kernel_option,
-                  set_kernel_option, kernel_options)
+                  set_kernel_option, kernel_options, MultiEngine)
 
 __all__ = [n for n in dir() if not n.startswith("_")]

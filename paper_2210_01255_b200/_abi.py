@@ -90,6 +90,15 @@ _SIGS = [
     ("sewald_gpu_fp64_peak", C.c_int, [VP, DP]),
     ("sewald_gpu_launch_count", I64, [VP]),
     ("sewald_gpu_set_option", C.c_int, [C.c_int, C.c_int]),
+    ("sewald_gpu_multi_create", C.c_int, [C.c_int, IP, C.POINTER(VP)]),
+    ("sewald_gpu_multi_destroy", None, [VP]),
+    ("sewald_gpu_multi_last_error", C.c_char_p, [VP]),
+    ("sewald_gpu_multi_size", C.c_int, [VP]),
+    ("sewald_gpu_multi_context", VP, [VP, C.c_int]),
+    ("sewald_gpu_multi_full_potential", C.c_int, [VP, C.POINTER(sewald_params_c), DP, DP, DP, I64, DP, I64,
+                                                  C.c_int, C.c_int, DP]),
+    ("sewald_gpu_multi_fourier_potential", C.c_int, [VP, C.POINTER(sewald_params_c), DP, DP, DP, I64, DP, I64,
+                                                     C.c_int, C.c_int, DP]),
     ("sewald_gpu_get_option", C.c_int, [C.c_int, IP]),
     ("sewald_gpu_session_pair_count", I64, [VP, C.c_int]),
     ("sewald_gpu_full_potential", C.c_int, [VP, C.POINTER(sewald_params_c), DP, DP, DP, I64, DP, I64,

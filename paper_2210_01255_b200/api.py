@@ -382,6 +382,72 @@ _engines: dict = {}
 _elock = threading.Lock()
 
 
+class MultiEngine:
+    """Several GPUs of this node driven from one process (sewald_gpu_multi_*):
+    sources spread in 1/W slices, grids summed over NVLink peer memory, each
+    GPU evaluates 1/W of the targets. `devices` may repeat a device (tests on
+    one GPU). full_potential / se_fourier_potential take the same arguments as
+    the module functions."""
+
+    def __init__(self, devices: Sequence[int]):
+        self._lib = _abi.load()
+        devs = [int(d) for d in devices]
+        if not devs:
+            raise InvalidArgument("at least one device")
+        arr = (C.c_int * len(devs))(*devs)
+        h = C.c_void_p()
+        code = self._lib.sewald_gpu_multi_create(len(devs), arr, C.byref(h))
+        if code != _abi.OK:
+            _abi.raise_for(code, f"sewald_gpu_multi_create({devs}) failed (devices or peer access unavailable)")
+        self.m = h
+        self.devices = devs
+        self._lock = threading.Lock()
+
+    def close(self):
+        if getattr(self, "m", None):
+            self._lib.sewald_gpu_multi_destroy(self.m)
+            self.m = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _run(self, entry, system, targets, params, opt, out):
+        x, f, nu = _system_arrays(system, params)
+        if not (float(params.xi) > 0.0):
+            raise InvalidArgument("xi must be positive")
+        same = bool(targets.same_as_sources)
+        xt = x if same else _vec3(targets.x, "targets")
+        nt = xt.shape[0]
+        u = _out_array(out, nt)
+        c = _params_for(system, params)
+        with self._lock:
+            if int(params.d) == 0 and opt.precompute_0p:
+                tab = opt.table
+                for d in range(len(self.devices)):
+                    ctx = self._lib.sewald_gpu_multi_context(self.m, d)
+                    if tab is None:
+                        code = self._lib.sewald_gpu_set_table0p(ctx, C.byref(c), None, None)
+                    else:
+                        tb = np.ascontiguousarray(np.asarray(tab.table, dtype=np.complex128).ravel())
+                        tn = (C.c_int32 * 3)(*[int(v) for v in tab.n])
+                        code = self._lib.sewald_gpu_set_table0p(ctx, C.byref(c), tn, _cdp(tb))
+                    _abi.raise_for(code, self._lib.sewald_gpu_last_error(ctx).decode())
+            code = getattr(self._lib, entry)(self.m, C.byref(c), _dp(x), _dp(f), _dp(nu), x.shape[0], _dp(xt), nt,
+                                             int(same), int(bool(opt.precompute_0p)), _dp(u))
+            _abi.raise_for(code, self._lib.sewald_gpu_multi_last_error(self.m).decode())
+        return u
+
+    def full_potential(self, system, targets, params, opt=None, out=None):
+        return self._run("sewald_gpu_multi_full_potential", system, targets, params, opt or SePipelineOptions(), out)
+
+    def se_fourier_potential(self, system, targets, params, opt=None, out=None):
+        return self._run("sewald_gpu_multi_fourier_potential", system, targets, params, opt or SePipelineOptions(),
+                         out)
+
+
 def default_engine(device: int = 0) -> Engine:
     with _elock:
         e = _engines.get(device)

@@ -11,6 +11,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -30,6 +31,40 @@ sewald_gpu_ctx* context() {
         return c;
     }();
     return ctx;
+}
+
+// Several GPUs for full_potential / se_fourier_potential: sewald::b200::use_devices
+// or SEWALD_DEVICES="0,1,2,3" (read once); one device otherwise.
+std::vector<int> g_devices;
+bool g_devices_set = false;
+sewald_gpu_multi* g_multi = nullptr;
+
+std::vector<int> env_devices() {
+    std::vector<int> d;
+    const char* e = getenv("SEWALD_DEVICES");
+    if (!e) return d;
+    std::string s(e);
+    size_t pos = 0;
+    while (pos < s.size()) {
+        size_t q = s.find(',', pos);
+        if (q == std::string::npos) q = s.size();
+        if (q > pos) d.push_back(std::atoi(s.substr(pos, q - pos).c_str()));
+        pos = q + 1;
+    }
+    return d;
+}
+
+sewald_gpu_multi* multi_context() {
+    if (!g_devices_set) {
+        g_devices = env_devices();
+        g_devices_set = true;
+    }
+    if (g_devices.size() < 2) return nullptr;
+    if (!g_multi) {
+        if (sewald_gpu_multi_create(static_cast<int>(g_devices.size()), g_devices.data(), &g_multi) != SEWALD_OK)
+            throw std::runtime_error("sewald: cannot open the multi-GPU context (peer access between the devices?)");
+    }
+    return g_multi;
 }
 
 void rethrow(int rc, const char* msg) {
@@ -598,6 +633,23 @@ std::vector<Vec3> pipeline(bool full, const SourceSystem& s, const TargetSet& t,
             throw std::invalid_argument("kernel table storage is inconsistent");
         check_ctx(sewald_gpu_set_table0p(context(), &p, tn, opt.table ? Z(opt.table->table) : nullptr));
     }
+    if (sewald_gpu_multi* m = multi_context()) {
+        if (e.d == 0 && opt.precompute_0p) {
+            const int32_t tn[3] = {opt.table ? opt.table->n[0] : 0, opt.table ? opt.table->n[1] : 0,
+                                   opt.table ? opt.table->n[2] : 0};
+            for (int d = 0; d < sewald_gpu_multi_size(m); ++d) {
+                sewald_gpu_ctx* c = sewald_gpu_multi_context(m, d);
+                rethrow(sewald_gpu_set_table0p(c, &p, tn, opt.table ? Z(opt.table->table) : nullptr),
+                        sewald_gpu_last_error(c));
+            }
+        }
+        auto fm = full ? sewald_gpu_multi_full_potential : sewald_gpu_multi_fourier_potential;
+        rethrow(fm(m, &p, D(s.x), D(s.f), nu, static_cast<int64_t>(s.size()), t.same_as_sources ? nullptr : D(t.x),
+                   static_cast<int64_t>(nt), t.same_as_sources ? 1 : 0, opt.precompute_0p ? 1 : 0,
+                   reinterpret_cast<double*>(u.data())),
+                sewald_gpu_multi_last_error(m));
+        return u;
+    }
     auto fn = full ? sewald_gpu_full_potential : sewald_gpu_fourier_potential;
     check_ctx(fn(context(), &p, D(s.x), D(s.f), nu, static_cast<int64_t>(s.size()),
                  t.same_as_sources ? nullptr : D(t.x), static_cast<int64_t>(nt), t.same_as_sources ? 1 : 0,
@@ -606,6 +658,20 @@ std::vector<Vec3> pipeline(bool full, const SourceSystem& s, const TargetSet& t,
 }
 
 }  // namespace
+
+namespace b200 {
+
+void use_devices(const std::vector<int>& devices) {
+    std::lock_guard<std::mutex> lk(g_mu);
+    if (g_multi) {
+        sewald_gpu_multi_destroy(g_multi);
+        g_multi = nullptr;
+    }
+    g_devices = devices;
+    g_devices_set = true;
+}
+
+}  // namespace b200
 
 std::vector<Vec3> se_fourier_potential(const SourceSystem& system, const TargetSet& targets,
                                        const EwaldParams& params, const SePipelineOptions& opt) {

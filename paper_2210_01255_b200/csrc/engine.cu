@@ -750,7 +750,11 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
     const int64_t ncl = (Nt + 31) / 32;
     const int64_t c0 = ncl * part / nparts, c1 = ncl * (part + 1) / nparts;
     const int64_t t0 = std::min<int64_t>(32 * c0, Nt), t1 = std::min<int64_t>(32 * c1, Nt);
-    if (t1 <= t0) return;
+    // A part may own no 32-target cluster (more parts than clusters) and still
+    // own gather tiles (the tiled / swept gathers split the tiles, not the
+    // clusters): it then contributes its gather share only.
+    const bool has_targets = t1 > t0;
+    if (Nt == 0) return;
     const uint32_t* torder = target_order(s);
     // SEWALD_RS_SYM: 0 = never the pair-symmetric kernel, "force" = always
     // when targets are the sources (tests pin it at small N), else automatic.
@@ -773,7 +777,7 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
         cuda_check(cudaMemsetAsync(u, 0, sizeof(double) * 3 * Nt, st), "u zero");
         first = false;
     }
-    if (parts & 2) {
+    if ((parts & 2) && has_targets) {
         if (!(s->p.xi > 0.0)) throw EngineError(SEWALD_EINVAL, "split parameter must be positive");
         if (!(s->p.rc > 0.0)) throw EngineError(SEWALD_EINVAL, "cell list cutoff must be positive");
         RealspaceArgs a{};
@@ -819,14 +823,14 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
             launch_gather_tile(s->g, s->p.P, tile_shape(s->g, s->p.P, s->Nt), s->tg_w.as<double>(), s->tg_sw.as<int4>(),
                                s->tg_off.as<int64_t>(), part, nparts, s->flow.as<double>(), h3, first ? 0 : 1, u,
                                st);
-        } else {
+        } else if (has_targets) {
             launch_gather(s->g, s->w, s->flow.as<double>(), target_positions(s), torder + t0, t1 - t0, h3,
                           first ? 0 : 1, u, st);
         }
         ++s->ctx->launches;
         first = false;
     }
-    if (parts & 4 || (parts & 1)) {
+    if ((parts & 4 || (parts & 1)) && has_targets) {
         ensure_sums(s);
         EpilogueArgs e{};
         e.kind = s->p.kind;
@@ -858,6 +862,45 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
         ++s->ctx->launches;
     }
     cuda_check(cudaGetLastError(), "evaluate launch");
+}
+
+// The context's host-buffer session, rebuilt when the parameters change.
+sewald_gpu_session* cached_session(sewald_gpu_ctx* ctx, const sewald_params_c& p) {
+    if (ctx->cached && std::memcmp(&ctx->cached_params, &p, sizeof(p)) == 0) return ctx->cached.get();
+    ctx->cached.reset();
+    auto s = std::make_unique<sewald_gpu_session>();
+    session_init(s.get(), ctx, p);
+    ctx->cached = std::move(s);
+    ctx->cached_params = p;
+    return ctx->cached.get();
+}
+
+// Free-axis stencil bound of the targets (the reference's gather check,
+// fourier.cpp:176-181), d < 3 only: one flag read.
+void session_check_target_box(sewald_gpu_session* s) {
+    if (s->p.d >= 3 || s->Nt == 0) return;
+    launch_stencil_bounds(s->g, s->p.P, target_positions(s), s->Nt, s->flags.as<int>() + FLAG_GATHER_BOX,
+                          s->ctx->stream);
+    check_flag(s, FLAG_GATHER_BOX, SEWALD_EINVAL,
+               "point too close to the extended box boundary; free-direction padding is too small");
+}
+
+// Starts the read of the real-space singularity flag (r = 0 between distinct
+// points) into pinned memory; session_finish_singular throws after the
+// caller's stream synchronisation if it was set.
+void session_read_singular(sewald_gpu_session* s) {
+    int* hf = s->hflags.get();
+    cuda_check(cudaMemcpyAsync(hf + FLAG_SINGULAR, s->flags.as<int>() + FLAG_SINGULAR, sizeof(int),
+                               cudaMemcpyDeviceToHost, s->ctx->stream), "flag read");
+}
+
+void session_finish_singular(sewald_gpu_session* s) {
+    int* hf = s->hflags.get();
+    if (hf[FLAG_SINGULAR]) {
+        hf[FLAG_SINGULAR] = 0;
+        cuda_check(cudaMemsetAsync(s->flags.as<int>() + FLAG_SINGULAR, 0, sizeof(int), s->ctx->stream), "flag reset");
+        throw EngineError(SEWALD_EDOMAIN, "real-space kernel is singular at the origin");
+    }
 }
 
 }  // namespace sewald_b200
@@ -892,16 +935,6 @@ int ctx_guard(sewald_gpu_ctx* ctx, F&& fn) {
     }
 }
 
-sewald_gpu_session* cached_session(sewald_gpu_ctx* ctx, const sewald_params_c& p) {
-    if (ctx->cached && std::memcmp(&ctx->cached_params, &p, sizeof(p)) == 0) return ctx->cached.get();
-    ctx->cached.reset();
-    auto s = std::make_unique<sewald_gpu_session>();
-    session_init(s.get(), ctx, p);
-    ctx->cached = std::move(s);
-    ctx->cached_params = p;
-    return ctx->cached.get();
-}
-
 void host_pipeline(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* x, const double* f,
                    const double* nu, int64_t N, const double* xt, int64_t Nt, int same, int use_table,
                    int parts, double* u_out) {
@@ -931,12 +964,7 @@ void host_pipeline(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* 
     }
     if (nt > 0) {
         ensure_target_order(s);
-        if ((parts & 1) && s->p.d < 3) {
-            launch_stencil_bounds(s->g, s->p.P, target_positions(s), nt, s->flags.as<int>() + FLAG_GATHER_BOX,
-                                  ctx->stream);
-            check_flag(s, FLAG_GATHER_BOX, SEWALD_EINVAL,
-                       "point too close to the extended box boundary; free-direction padding is too small");
-        }
+        if (parts & 1) session_check_target_box(s);
         tm.mark();  // 4
         session_evaluate(s, 0, 1, parts, du);
         tm.mark();  // 5
@@ -946,15 +974,9 @@ void host_pipeline(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* 
         tm.mark();
     }
     tm.mark();  // 6
-    int* hf = s->hflags.get();
-    cuda_check(cudaMemcpyAsync(hf + FLAG_SINGULAR, s->flags.as<int>() + FLAG_SINGULAR, sizeof(int),
-                               cudaMemcpyDeviceToHost, ctx->stream), "flag read");
+    session_read_singular(s);  // read with the result: no extra synchronisation
     cuda_check(cudaStreamSynchronize(ctx->stream), "pipeline sync");
-    if (hf[FLAG_SINGULAR]) {  // read with the result: no extra synchronisation
-        hf[FLAG_SINGULAR] = 0;
-        cuda_check(cudaMemsetAsync(s->flags.as<int>() + FLAG_SINGULAR, 0, sizeof(int), ctx->stream), "flag reset");
-        throw EngineError(SEWALD_EDOMAIN, "real-space kernel is singular at the origin");
-    }
+    session_finish_singular(s);
     sewald_timings_c& T = ctx->timings;
     T = sewald_timings_c{};
     T.h2d_ms = tm.ms(0, 1);

@@ -123,6 +123,10 @@ void session_set_targets(sewald_gpu_session* s, const double* xt, int64_t Nt, bo
 void session_spread(sewald_gpu_session* s, int64_t i0, int64_t i1, double* grid);
 void session_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p);
 void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, double* u);
+sewald_gpu_session* cached_session(sewald_gpu_ctx* ctx, const sewald_params_c& p);
+void session_check_target_box(sewald_gpu_session* s);
+void session_read_singular(sewald_gpu_session* s);
+void session_finish_singular(sewald_gpu_session* s);
 
 // Fourier solve for d < 3 (aft.cu): grid (C comps, real) -> s->flow (3 comps).
 void aft_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p);
