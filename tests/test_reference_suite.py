@@ -7,7 +7,7 @@ GPU box); the same sources linked with the reference library give the check
 counts below (`make -C oracle check`), so a pass with the same count is the
 reference suite passing on the B200 engine.
 
-test_fourier and test_realspace drive spread / aft_forward / scale /
+All 8 implemented suites are built. test_fourier and test_realspace drive spread / aft_forward / scale /
 aft_inverse / gather / se_fourier_potential / realspace_potential /
 full_potential on the GPU; the others exercise the host layer (parameters,
 windows, kernel tensors, modified kernels) and need no device.
@@ -24,7 +24,7 @@ REF_BIN = os.path.join(ROOT, "oracle", "_ref")
 
 # checks / test cases of the reference's own build of the same sources
 EXPECTED = {
-    "domain": (33, 7), "kernels": (5047, 14), "modified_kernels": (1232, 12), "window": (221, 7),
+    "domain": (33, 7), "specfun": (563, 14), "kernels": (5047, 14), "modified_kernels": (1232, 12), "window": (221, 7),
     "estimates": (1689, 13), "fourier": (72, 23), "realspace": (568, 20),
 }
 
@@ -42,7 +42,7 @@ def _run(name):
     assert (checks, cases) == EXPECTED[name], (checks, cases)
 
 
-@pytest.mark.parametrize("name", ["domain", "kernels", "modified_kernels", "window", "estimates"])
+@pytest.mark.parametrize("name", ["domain", "specfun", "kernels", "modified_kernels", "window", "estimates"])
 def test_reference_host_suites(name):
     _run(name)
 
