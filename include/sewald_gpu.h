@@ -151,7 +151,8 @@ enum {
     SEWALD_OPT_SPREAD_MMA = 5,    /* 1 tensor-core spread for 15 <= P <= 32, 0 off */
     SEWALD_OPT_SPREAD_MMA_L = 6,  /* tensor-core spread region edge for P <= 20: 23 or 19 */
     SEWALD_OPT_SPREAD_CACHED = 7, /* tensor-core spread: 1 staged tables per chunk, 0 per group */
-    SEWALD_OPT_COUNT = 8
+    SEWALD_OPT_SPREAD_ROWSWEEP = 8, /* tensor-core spread, P <= 20: 1 row-sweep CTAs (several per SM) */
+    SEWALD_OPT_COUNT = 9
 };
 int sewald_gpu_set_option(int which, int value);
 int sewald_gpu_get_option(int which, int* value);

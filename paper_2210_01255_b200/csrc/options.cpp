@@ -42,6 +42,9 @@ int env_default(int which) {
         case SEWALD_OPT_SPREAD_CACHED:
             e = env("SEWALD_SPREAD_CACHED");
             return (e && e[0] == '0') ? 0 : 1;
+        case SEWALD_OPT_SPREAD_ROWSWEEP:
+            e = env("SEWALD_SPREAD_ROWSWEEP");
+            return (e && e[0] == '1') ? 1 : 0;
     }
     return 0;
 }
@@ -56,6 +59,7 @@ bool valid(int which, int v) {
         case SEWALD_OPT_SPREAD_MMA: return v == 0 || v == 1;
         case SEWALD_OPT_SPREAD_MMA_L: return v == 19 || v == 23;
         case SEWALD_OPT_SPREAD_CACHED: return v == 0 || v == 1;
+        case SEWALD_OPT_SPREAD_ROWSWEEP: return v == 0 || v == 1;
     }
     return false;
 }

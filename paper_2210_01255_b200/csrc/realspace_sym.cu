@@ -588,11 +588,23 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                             }
                             Screened sc = screened<SHORT, SEWALD_EXP_REP>(n2e, a.xi, xi2, exp_tab);
                             sc.Ey = acc ? sc.Ey : 0.0;
+#if defined(SEWALD_PROBE_NOREACT)  // timing probes only (wrong results)
+                            {
+                                const PairCoef<KIND> pc = pair_coef<KIND>(sc, xi2, n2e);
+                                pair_apply<KIND, false>(pc, r0, r1, r2, sj, ua);
+                            }
+#elif defined(SEWALD_PROBE_WONLY)
+                            double ub[3] = {0.0, 0.0, 0.0};
+                            pair_both<KIND>(sc, xi2, n2e, r0, r1, r2, sj, fa, ua, ub);
+                            *reinterpret_cast<double2*>(rec + RO) = make_double2(ub[0], ub[1]);
+                            rec[RO + 2] = ub[2];
+#else
                             const double2 r01 = *reinterpret_cast<const double2*>(rec + RO);
                             double ub[3] = {r01.x, r01.y, rec[RO + 2]};
                             pair_both<KIND>(sc, xi2, n2e, r0, r1, r2, sj, fa, ua, ub);
                             *reinterpret_cast<double2*>(rec + RO) = make_double2(ub[0], ub[1]);
                             rec[RO + 2] = ub[2];
+#endif
                             npairs32 += acc ? 2u : 0u;
                         } else {
                             bool acc = (m >> s) & 1u;

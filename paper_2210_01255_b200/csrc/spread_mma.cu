@@ -265,13 +265,24 @@ spread_tile_mma_cached_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz
 constexpr int WT_TMAX = 128;
 constexpr int WT_LS = 40;
 constexpr int WT_WARPS = 16;
+#ifndef SEWALD_SPREAD_RS_WARPS
+#define SEWALD_SPREAD_RS_WARPS 8
+#endif
+#ifndef SEWALD_SPREAD_RS_MINB
+#define SEWALD_SPREAD_RS_MINB 2
+#endif
 
-template <int L>
-__global__ void __launch_bounds__(32 * WT_WARPS)
+// Also used for 15 <= P <= 20 (L = 23 / 19, LS = 24) as the row-sweep form
+// (SEWALD_OPT_SPREAD_ROWSWEEP): few registers per warp, so several tile
+// CTAs share an SM and one's table staging overlaps another's MMAs.
+template <int L, int LS = WT_LS, int NW = WT_WARPS, int MINB = 1>
+__global__ void __launch_bounds__(32 * NW, MINB)
 spread_tile_mma_wide_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64_t tile0,
                             const double* __restrict__ W, const int4* __restrict__ SW,
                             const double* __restrict__ STR, int C, const int64_t* __restrict__ off,
                             double* __restrict__ out) {
+    constexpr int WT_LS = LS;
+    constexpr int WT_WARPS = NW;
     constexpr int ROWS = L * L;
     constexpr int RB = (ROWS + 7) / 8;
     constexpr int NB = WT_LS / 8;
@@ -403,6 +414,13 @@ int launch_spread_mma(const DevGrid& g, int P, const SpreadMmaShape& s, const do
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             kern<<<(unsigned)n, 32 * WT_WARPS, sm, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W, SW, STR, C, off,
                                                         out);
+        } else if (option(SEWALD_OPT_SPREAD_ROWSWEEP)) {
+            const size_t sm = sizeof(double) * 4 * WT_TMAX * 24;
+            auto kern = s.L == 23 ? spread_tile_mma_wide_kernel<23, 24, SEWALD_SPREAD_RS_WARPS, SEWALD_SPREAD_RS_MINB>
+                                  : spread_tile_mma_wide_kernel<19, 24, SEWALD_SPREAD_RS_WARPS, SEWALD_SPREAD_RS_MINB>;
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            kern<<<(unsigned)n, 32 * SEWALD_SPREAD_RS_WARPS, sm, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W, SW,
+                                                                      STR, C, off, out);
         } else if (cached && C <= CT_CMAX) {
             const size_t sm = cached_smem_bytes();
             auto kern = s.L == 23 ? spread_tile_mma_cached_kernel<23> : spread_tile_mma_cached_kernel<19>;

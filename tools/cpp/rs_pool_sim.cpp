@@ -58,6 +58,9 @@ int main(int argc, char** argv) {
     const int NTH = 9;
     const int TH[NTH] = {32, 64, 96, 128, 192, 256, 320, 410, 512};
     double Sd[NTH] = {0}, Ps[NTH] = {0}, Pb[NTH] = {0}, Pl[NTH] = {0};
+    const int NK = 6;
+    const int KT[NK] = {4, 8, 12, 16, 20, 24};
+    double Sk[NK] = {0}, Pk[NK] = {0}, Bk[NK] = {0};  // steps kept, pooled pairs, pooled batches (per block)
     struct Ent { uint32_t a, v; int blk; };
     std::vector<Ent> win;
     int win_blocks = 0;
@@ -181,6 +184,15 @@ int main(int argc, char** argv) {
                     for (int j = 0; j < 32; ++j) maxj = std::max(maxj, degj[j]);
                     E += Eb;
                     S_cur += __builtin_popcount(OR);
+                    for (int q = 0; q < NK; ++q) {
+                        int kept = 0, pp = 0;
+                        for (int s2 = 0; s2 < 32; ++s2) {
+                            const int c = __builtin_popcount(A[s2]);
+                            if (!c) continue;
+                            if (c >= KT[q]) ++kept; else pp += c;
+                        }
+                        Sk[q] += kept; Pk[q] += pp; Bk[q] += (pp + 31) / 32;
+                    }
                     for (int q = 0; q < NTH; ++q) {
                         if (Eb < TH[q]) { Ps[q] += Eb; Pb[q] += (Eb + 31) / 32; Pl[q] += maxl; } else Sd[q] += __builtin_popcount(OR);
                     }
@@ -213,6 +225,9 @@ int main(int argc, char** argv) {
     for (int q = 0; q < NTH; ++q)
         printf("per-block batches, < %3d pairs: cost (ovh 1.2/1.5) %.3f %.3f  (pooled batches/cluster %.1f)\n", TH[q],
                (Sd[q] + 1.2 * Pb[q]) / S_cur, (Sd[q] + 1.5 * Pb[q]) / S_cur, Pb[q] / nclusters);
+    for (int q = 0; q < NK; ++q)
+        printf("steps with < %2d lanes pooled (per block): kept steps %.3f, pooled pairs %.3f -> cost (ovh 1.2/1.5) %.3f %.3f\n",
+               KT[q], Sk[q] / S_cur, Pk[q] / E, (Sk[q] + 1.2 * Bk[q]) / S_cur, (Sk[q] + 1.5 * Bk[q]) / S_cur);
     for (int q = 0; q < NTH; ++q)
         printf("per-lane candidate steps (max lane degree), < %3d pairs: cost (ovh 1.0/1.1/1.2) %.3f %.3f %.3f\n", TH[q],
                (Sd[q] + Pl[q]) / S_cur, (Sd[q] + 1.1 * Pl[q]) / S_cur, (Sd[q] + 1.2 * Pl[q]) / S_cur);
