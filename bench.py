@@ -336,13 +336,13 @@ def run_ours(args, cfg):
     l2 = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)  # 256 MB > 126 MB L2
     i0, i1 = N * rank // ws, N * (rank + 1) // ws
 
-    from paper_2210_01255_b200.parallel import sharded_step
+    from paper_2210_01255_b200.parallel import sharded_step, use_slabs
 
     def step():
         sess.set_sources(dx, df, dnu)
         sess.set_targets(dxt, same)
         sharded_step(sess, N, grid, u, rank, ws, all_reduce=dist.all_reduce if ws > 1 else None,
-                     slab_dist=dist if (ws > 1 and cfg.d == 0) else None)
+                     slab_dist=dist if use_slabs(cfg.d, ws) else None)
 
     def barrier():
         if ws > 1:

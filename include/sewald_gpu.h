@@ -319,7 +319,10 @@ int sewald_gpu_session_solve(sewald_gpu_session* s, const double* grid_dev, int 
  * zero-mode / gauge terms. */
 int sewald_gpu_session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts,
                                 double* u_dev);
-/* ---- slab-distributed D = 0 solve (one rank of `world`) -------
+/* ---- slab-distributed D = 0 / D = 3 solve (one rank of `world`) -
+ * D = 3 runs the same stages on the unpadded periodic box (n = M) with the
+ * periodic operator (G(0) = 0) in place of the free-space one. */
+/* ---- (D = 0 details) ------------------------------------------------------
  * Replaces se_fourier_potential's single-box transform (fourier.cpp:311-520,
  * :668-720) by x-slabs of the M_ext box for the z transforms and kz-slabs of
  * the half spectrum for the (x, y) transforms and the scale, with two

@@ -713,8 +713,26 @@ void session_set_table0p(sewald_gpu_session* s, const int32_t n[3], const double
         s->user_table_src = nullptr;
         return;
     }
-    if (s->has_user_table && s->user_table_src == table) return;  // same table object as before
     if (s->p.d != 0) throw EngineError(SEWALD_EINVAL, "precomputed kernels apply to d = 0 only");
+    // Re-upload unless it is the same table: same address and size AND the
+    // same values at 4096 sampled entries (a new table allocated at a freed
+    // one's address differs there; the table can be GBs, so the full content
+    // is not compared on every call).
+    const int64_t cnt = (int64_t)n[0] * n[1] * n[2];
+    uint64_t fp = 1469598103934665603ull ^ (uint64_t)cnt;
+    cudaPointerAttributes attr{};
+    const bool host_mem = cudaPointerGetAttributes(&attr, table) != cudaSuccess || attr.type == cudaMemoryTypeHost ||
+                          attr.type == cudaMemoryTypeUnregistered;
+    cudaGetLastError();
+    if (!host_mem) fp = ~s->user_table_fp;  // device memory: always copied (device to device)
+    for (int k = 0; k < 4096 && cnt > 0 && host_mem; ++k) {
+        const int64_t i = (int64_t)((__int128)cnt * k / 4096);
+        uint64_t w[2];
+        std::memcpy(w, table + 2 * i, sizeof(w));
+        fp = (fp ^ w[0]) * 1099511628211ull;
+        fp = (fp ^ w[1]) * 1099511628211ull;
+    }
+    if (s->has_user_table && s->user_table_src == table && s->user_table_fp == fp) return;
     // the table path pads with s0 = 2 (fourier.cpp:819-821), so the table must
     // live on the (2 M_ext)^3 mode grid (fourier.cpp:672-673)
     for (int ax = 0; ax < 3; ++ax)
@@ -726,13 +744,57 @@ void session_set_table0p(sewald_gpu_session* s, const int32_t n[3], const double
     cuda_check(cudaStreamSynchronize(s->ctx->stream), "table in");
     s->has_user_table = true;
     s->user_table_src = table;
+    s->user_table_fp = fp;
     s->aft.reset();  // the next table-path solve rebuilds its plan with this table
 }
 
-// ---- slab-distributed D = 0 solve: stage wrappers ------------------
+// ---- slab-distributed solve: stage wrappers -------------------------
+// D = 0: the padded-box real transforms of D0Real. D = 3: the same machinery on
+// the unpadded periodic box (n = M, wavenumbers 2 pi m / L, Nyquist at -pi/h)
+// with the plain periodic operator (modified_coeffs at d = 3: G(0) = 0,
+// modified_kernels.cpp:250-252) and its Hermitian Nyquist part, i.e. the
+// same per-mode operator as the single-GPU D = 3 solve (kspace.cu).
+
+struct D3Slab {
+    D0Real d;
+    D0ScaleArgs sa{};
+    DevBuf tables;
+    ModSpec spec{};
+};
+
+void D3SlabDeleter::operator()(D3Slab* p) const { delete p; }
+
+static D3Slab& d3_slab(sewald_gpu_session* s) {
+    if (s->slab3) return *s->slab3;
+    const sewald_params_c& p = s->p;
+    cudaStream_t st = s->ctx->stream;
+    std::unique_ptr<D3Slab, D3SlabDeleter> D(new D3Slab());
+    int m[3];
+    for (int ax = 0; ax < 3; ++ax) m[ax] = p.M_ext[ax];
+    D->d.setup(m, m, s->C, st);
+    D->spec = make_modspec(p.kind, 3, p.R);
+    std::vector<double> k0 = wavenumbers(m[0], p.h), k1 = wavenumbers(m[1], p.h), k2 = wavenumbers(m[2], p.h);
+    std::vector<double> w0 = window_hat_table(p, k0), w1 = window_hat_table(p, k1), w2 = window_hat_table(p, k2);
+    std::vector<double> tab;
+    for (auto* v : {&k0, &w0, &k1, &w1, &k2, &w2}) tab.insert(tab.end(), v->begin(), v->end());
+    double* t = upload(D->tables, tab, st);
+    size_t o = 0;
+    const double* dk0 = t + o; o += k0.size();
+    const double* dw0 = t + o; o += w0.size();
+    const double* dk1 = t + o; o += k1.size();
+    const double* dw1 = t + o; o += w1.size();
+    const double* dk2 = t + o; o += k2.size();
+    const double* dw2 = t + o;
+    const int64_t vol = (int64_t)m[0] * m[1] * m[2];
+    D->sa = D0ScaleArgs{0, 0, 0, 0, 0, dk0, dk1, dk2, dw0, dw1, dw2, 1.0 / static_cast<double>(vol)};
+    cuda_check(cudaStreamSynchronize(st), "d3 slab prepare");
+    s->slab3 = std::move(D);
+    return *s->slab3;
+}
 
 static D0Real& d0_plan(sewald_gpu_session* s, bool use_table) {
-    if (s->p.d != 0) throw EngineError(SEWALD_EINVAL, "slab-distributed solve is the D=0 path");
+    if (s->p.d == 3) return d3_slab(s).d;
+    if (s->p.d != 0) throw EngineError(SEWALD_EINVAL, "the slab-distributed solve covers D = 0 and D = 3");
     prepare(s, use_table);
     FourierPlanAFT& A = *s->aft;
     if (!A.d0r) throw EngineError(SEWALD_EINVAL, "slab-distributed solve needs the real-transform D=0 path");
@@ -758,6 +820,12 @@ void aft_d0_slab_forward(sewald_gpu_session* s, bool use_table, const double* gr
 void aft_d0_slab_middle(sewald_gpu_session* s, bool use_table, const void* recv, const SlabBounds& xbd, int ka,
                         int kb, void* send) {
     D0Real& D = d0_plan(s, use_table);
+    if (s->p.d == 3) {
+        D3Slab& P = d3_slab(s);
+        s->ctx->launches += D.slab_middle(static_cast<const cuDoubleComplex*>(recv), xbd, ka, kb, P.spec, s->p.kind,
+                                          s->p.xi, P.sa, false, static_cast<cuDoubleComplex*>(send), s->ctx->stream);
+        return;
+    }
     FourierPlanAFT& A = *s->aft;
     s->ctx->launches += D.slab_middle(static_cast<const cuDoubleComplex*>(recv), xbd, ka, kb, A.spec, s->p.kind,
                                       s->p.xi, A.d0sa, A.table_path, static_cast<cuDoubleComplex*>(send),

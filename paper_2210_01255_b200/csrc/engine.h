@@ -45,6 +45,10 @@ struct FourierPlanAFT;  // zero-padded / upsampled free-direction path (d < 3)
 struct AftDeleter {
     void operator()(FourierPlanAFT* p) const;
 };
+struct D3Slab;  // slab-distributed D = 3 solve (aft.cu)
+struct D3SlabDeleter {
+    void operator()(D3Slab* p) const;
+};
 
 }  // namespace sewald_b200
 
@@ -104,11 +108,13 @@ struct sewald_gpu_session {
     bool sums_ready = false;
     std::unique_ptr<sewald_b200::FourierPlanD3> d3;
     std::unique_ptr<sewald_b200::FourierPlanAFT, sewald_b200::AftDeleter> aft;
+    std::unique_ptr<sewald_b200::D3Slab, sewald_b200::D3SlabDeleter> slab3;
     // D = 0 kernel table supplied by the caller (SePipelineOptions::table,
     // fourier.h:76-79); used instead of building one when set
     sewald_b200::DevBuf user_table0p;
     bool has_user_table = false;
-    const void* user_table_src = nullptr;  // caller's pointer (re-upload skipped when unchanged)
+    const void* user_table_src = nullptr;  // caller's pointer and sampled-content fingerprint:
+    uint64_t user_table_fp = 0;            // the re-upload is skipped only when both are unchanged
 };
 
 namespace sewald_b200 {

@@ -14,7 +14,18 @@ grid), solve(grid, precompute_0p), evaluate(u, part, nparts, parts).
 """
 from __future__ import annotations
 
+import os
 from typing import Callable, Optional
+
+# D = 3 grids are slab-distributed too when SEWALD_SLAB_D3=1; by default they
+# are all-reduced and solved on every rank (the whole D = 3 k-space step is
+# 0.16 ms at c2).
+SLAB_D3 = os.environ.get("SEWALD_SLAB_D3", "0") == "1"
+
+
+def use_slabs(d: int, world: int) -> bool:
+    """Whether the k-space step of a world-rank run is slab-distributed."""
+    return world > 1 and (d == 0 or (d == 3 and SLAB_D3))
 
 
 def slice_bounds(n: int, rank: int, world: int):
@@ -30,7 +41,7 @@ def sharded_step(session, n_sources: int, grid, u, rank: int, world: int,
     """One distributed full-potential step. Each rank's evaluate() output
     holds its part's contributions (zero elsewhere); with gather_result the
     outputs are summed so every rank ends with the full velocity field.
-    With `slab_dist` (torch.distributed) the D = 0 solve is slab-distributed
+    With `slab_dist` (torch.distributed) the D = 0 / D = 3 solve is slab-distributed
     (d0_sharded_solve) instead of replicated after a grid all-reduce."""
     i0, i1 = slice_bounds(n_sources, rank, world)
     session.spread(i0, i1, grid)
@@ -217,7 +228,7 @@ def full_potential_sharded(system, targets, params, rank: int, world: int, dist=
     reduce_sum = None
     if world > 1:
         reduce_sum = lambda t: dist.all_reduce(t, group=group)
-    slab = dist if (world > 1 and int(params.d) == 0) else None
+    slab = dist if use_slabs(int(params.d), world) else None
     sharded_step(sess, x.shape[0], grid, u, rank, world, all_reduce=reduce_sum, precompute_0p=precompute_0p,
                  gather_result=False, slab_dist=slab)
     if world > 1:

@@ -430,22 +430,24 @@ def test_full_size_c2_realspace_subset(S, ref):
 
 
 @pytest.mark.parametrize("world", [2, 3])
-@pytest.mark.parametrize("kind,table", [(0, True), (1, True), (2, False)])
-def test_d0_slab_solve_emulated(S, world, kind, table):
-    """Slab-distributed D = 0 solve (x-slabs -> all-to-all -> kz-slabs -> all-to-all
-    back -> all-gather), ranks run in sequence in one process with the
-    exchanges done by slicing: the Fourier velocity equals the single-GPU solve."""
+@pytest.mark.parametrize("d,kind,table", [(0, 0, True), (0, 1, True), (0, 2, False),
+                                          (3, 0, False), (3, 1, False), (3, 2, False)])
+def test_slab_solve_emulated(S, world, d, kind, table):
+    """Slab-distributed D = 0 and D = 3 solves (x-slabs -> all-to-all ->
+    kz-slabs -> all-to-all back -> all-gather), ranks run in sequence in one
+    process with the exchanges done by slicing: the Fourier velocity equals the
+    single-GPU solve (D = 3 there: the D2Z / Z2D path of kspace.cu)."""
     import torch
     from paper_2210_01255_b200.parallel import (D0Slabs, d0_stage_forward, d0_stage_inverse, d0_stage_middle,
                                                 emulate_all_to_all)
-    rng = np.random.default_rng(900 + kind + 10 * world)
+    rng = np.random.default_rng(900 + kind + 10 * world + d)
     N = 3000
-    L = (2.0, 1.0, 1.0)
+    L = (2.0, 1.0, 1.0) if d == 0 else (1.0, 1.0, 1.0)
     x = rng.random((N, 3)) * np.asarray(L)
     f = rng.standard_normal((N, 3))
     nu = rng.standard_normal((N, 3)) if kind == 1 else None
-    sysm = S.SourceSystem(S.Kernel(kind), S.Cell(L), 0, x, f, nu)
-    sel = S.select_parameters(sysm.kind, 0, sysm.cell, S.source_quantity(sysm), 9.0, S.ToleranceSpec(1e-8))
+    sysm = S.SourceSystem(S.Kernel(kind), S.Cell(L), d, x, f, nu)
+    sel = S.select_parameters(sysm.kind, d, sysm.cell, S.source_quantity(sysm), 9.0, S.ToleranceSpec(1e-8))
     dev = torch.device("cuda", 0)
     T = lambda a: None if a is None else torch.from_numpy(np.ascontiguousarray(a)).to(dev)
     sess = S.Session(sel.params, sysm.cell)

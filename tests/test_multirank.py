@@ -122,9 +122,9 @@ class FakeD0Session:
     layouts as include/sewald_gpu.h) with a fixed real, even k-space
     operator, so d0_sharded_solve's collectives can run on gloo (tests only)."""
 
-    def __init__(self, m, C):
+    def __init__(self, m, C, pad=2):
         self.m, self.C = m, C
-        self.n = tuple(2 * v for v in m)
+        self.n = tuple(pad * v for v in m)  # pad 2: D = 0 box; pad 1: the periodic D = 3 box
         self.h2 = self.n[2] // 2 + 1
         k = [np.fft.fftfreq(v) * v for v in self.n]
         kz = np.arange(self.h2)
@@ -175,7 +175,7 @@ class FakeD0Session:
         self.flow = flow.numpy().copy()
 
 
-def _d0_worker(rank, world, port, outdir):
+def _d0_worker(rank, world, port, outdir, pad=2):
     import sys
     sys.path.insert(0, ROOT)
     import torch
@@ -184,8 +184,8 @@ def _d0_worker(rank, world, port, outdir):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    m, C = (11, 6, 5), 9
-    sess = FakeD0Session(m, C)
+    m, C = ((11, 6, 5), 9) if pad == 2 else ((12, 6, 8), 3)
+    sess = FakeD0Session(m, C, pad)
     rng = np.random.default_rng(40 + rank)  # per-rank partial grids, summed by the solve
     grid = torch.from_numpy(rng.standard_normal(C * m[0] * m[1] * m[2]))
     d0_sharded_solve(sess, grid, rank, world, dist)
@@ -197,12 +197,15 @@ def _d0_worker(rank, world, port, outdir):
     dist.destroy_process_group()
 
 
-def test_d0_sharded_solve_gloo_world2(tmp_path):
-    """d0_sharded_solve with real collectives (gloo, world 2): grid reduction
-    to x-slabs, two all-to-alls, all-gather of the flow slabs."""
+@pytest.mark.parametrize("world,pad", [(2, 2), (3, 2), (2, 1), (3, 1)])
+def test_sharded_solve_gloo(tmp_path, world, pad):
+    """d0_sharded_solve with real collectives (gloo, world 2 and 3): grid
+    reduction to x-slabs, two all-to-alls, all-gather of the flow slabs; on the
+    zero-padded D = 0 box (pad 2) and the unpadded periodic D = 3 box (pad 1)."""
     import torch.multiprocessing as mp
     port = _free_port()
-    mp.start_processes(_d0_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True, start_method="spawn")
+    mp.start_processes(_d0_worker, args=(world, port, str(tmp_path), pad), nprocs=world, join=True,
+                       start_method="spawn")
     flow = np.load(tmp_path / "flow.npy")
     ref = np.load(tmp_path / "ref.npy")
     assert np.max(np.abs(flow - ref)) < 1e-12 * np.max(np.abs(ref))

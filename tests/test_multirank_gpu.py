@@ -4,7 +4,8 @@ of the multi-GPU code path on a one-GPU box; NCCL needs one GPU per rank).
 Each rank runs parallel.sharded_step with a real device Session; the summed
 result must equal the single-process full_potential. Covers the replicated
 solve (D = 3, grid all-reduce + symmetric real-space reactions) and the
-slab-distributed D = 0 solve (reduce -> all-to-all -> all-to-all -> all-gather)."""
+slab-distributed D = 0 and D = 3 solves (reduce -> all-to-all -> all-to-all ->
+all-gather), world sizes 2 and 3."""
 import os
 import socket
 
@@ -33,7 +34,7 @@ def _system(d, kind, N):
     return L, x, f, nu
 
 
-def _worker(rank, world, port, outdir, d, kind, N):
+def _worker(rank, world, port, outdir, d, kind, N, slab=None):
     import sys
     sys.path.insert(0, ROOT)
     import torch
@@ -53,8 +54,9 @@ def _worker(rank, world, port, outdir, d, kind, N):
     sess.set_targets(None, True)
     grid = torch.zeros(sess.grid_size(), dtype=torch.float64, device=dev)
     u = torch.zeros((N, 3), dtype=torch.float64, device=dev)
+    use_slab = (d == 0) if slab is None else slab
     sharded_step(sess, N, grid, u, rank, world, all_reduce=dist.all_reduce,
-                 slab_dist=dist if d == 0 else None)
+                 slab_dist=dist if use_slab else None)
     torch.cuda.synchronize()
     if rank == 0:
         np.save(os.path.join(outdir, "u.npy"), u.cpu().numpy())
@@ -63,11 +65,14 @@ def _worker(rank, world, port, outdir, d, kind, N):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("d,kind", [(3, 0), (0, 0), (0, 1), (2, 2)])
-def test_sharded_step_two_ranks_gpu(tmp_path, d, kind):
+@pytest.mark.parametrize("d,kind,slab,world", [(3, 0, False, 2), (0, 0, True, 2), (0, 1, True, 2), (2, 2, False, 2),
+                                               (3, 0, True, 2), (3, 1, True, 3), (3, 2, True, 3)])
+def test_sharded_step_ranks_gpu(tmp_path, d, kind, slab, world):
+    """slab: the k-space step slab-distributed (reduce-scatter, two all-to-alls,
+    all-gather) instead of a grid all-reduce and a replicated solve."""
     import torch.multiprocessing as mp
     port = _free_port()
-    mp.start_processes(_worker, args=(2, port, str(tmp_path), d, kind, 3000), nprocs=2, join=True,
+    mp.start_processes(_worker, args=(world, port, str(tmp_path), d, kind, 3000, slab), nprocs=world, join=True,
                        start_method="spawn")
     u = np.load(tmp_path / "u.npy")
     uref = np.load(tmp_path / "uref.npy")
