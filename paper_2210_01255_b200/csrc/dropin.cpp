@@ -182,9 +182,8 @@ void validate_system(const SourceSystem& s) {
     } else if (!s.nu.empty()) {
         throw std::invalid_argument("orientations only apply to the stresslet");
     }
-    for (const Vec3& p : s.x)
-        for (double c : p)
-            if (!std::isfinite(c)) throw std::invalid_argument("non-finite source position");
+    // non-finite positions: checked on the device by the first stage that
+    // reads them (finite_check_kernel), same std::invalid_argument message
 }
 
 double source_quantity(const SourceSystem& s) {

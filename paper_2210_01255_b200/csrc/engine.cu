@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <thread>
 
 namespace sewald_b200 {
 
@@ -30,6 +31,62 @@ void cufft_check(cufftResult r, const char* what) {
     if (r != CUFFT_SUCCESS)
         throw EngineError(SEWALD_ECUFFT, std::string(what) + ": cuFFT error " + std::to_string((int)r));
 }
+
+PinnedBuf::~PinnedBuf() {
+    if (ptr) cudaFreeHost(ptr);
+}
+
+void* PinnedBuf::ensure(size_t n) {
+    if (n <= bytes) return ptr;
+    if (ptr) cudaFreeHost(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    cuda_check(cudaMallocHost(&ptr, n), "pinned staging");
+    bytes = n;
+    return ptr;
+}
+
+namespace {
+
+// memcpy on up to 8 host threads (pageable <-> pinned staging: one thread
+// copies ~5-10 GB/s; a 1e6-point input array is 24 MB).
+void parallel_memcpy(void* dst, const void* src, size_t n) {
+    const size_t chunk = size_t(4) << 20;
+    unsigned t = (unsigned)std::min<size_t>(8, (n + chunk - 1) / chunk);
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    t = std::max(1u, std::min(t, hw));
+    if (t <= 1) {
+        std::memcpy(dst, src, n);
+        return;
+    }
+    std::vector<std::thread> th;
+    for (unsigned k = 1; k < t; ++k)
+        th.emplace_back([=] {
+            const size_t a = n * k / t, b = n * (k + 1) / t;
+            std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
+        });
+    std::memcpy(dst, src, n / t);
+    for (auto& x : th) x.join();
+}
+
+bool is_pageable(const void* p) {
+    cudaPointerAttributes a{};
+    const cudaError_t e = cudaPointerGetAttributes(&a, p);
+    cudaGetLastError();
+    return e != cudaSuccess || a.type == cudaMemoryTypeUnregistered;
+}
+
+// A pageable host array is staged into pinned memory with parallel host
+// copies so its H2D copy runs asynchronously at full link speed; pinned and
+// device arrays are used as they are.
+const double* stage_in(PinnedBuf& buf, const double* src, size_t count) {
+    if (!src || count == 0 || !is_pageable(src)) return src;
+    double* dst = static_cast<double*>(buf.ensure(sizeof(double) * count));
+    parallel_memcpy(dst, src, sizeof(double) * count);
+    return dst;
+}
+
+}  // namespace
 
 HostFlags::~HostFlags() {
     if (p) cudaFreeHost(p);
@@ -945,12 +1002,17 @@ void host_pipeline(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* 
     StageTimer tm(ctx);
     const int64_t launches0 = ctx->launches;
     tm.mark();
+    x = stage_in(ctx->px, x, 3 * (size_t)N);
+    f = stage_in(ctx->pf, f, 3 * (size_t)N);
+    nu = stage_in(ctx->pnu, nu, 3 * (size_t)N);
+    if (!same) xt = stage_in(ctx->pxt, xt, 3 * (size_t)Nt);
     session_set_targets(s, xt, Nt, same != 0);
     session_set_sources(s, x, f, nu, N);
     if (!same) session_set_targets(s, xt, Nt, false);
     tm.mark();  // 1: after H2D
     const int64_t nt = s->Nt;
     double* du = static_cast<double*>(ctx->hu.ensure(sizeof(double) * 3 * std::max<int64_t>(nt, 1)));
+    double* out_stage = nullptr;
     if (parts & 1) {
         const int64_t vol = (int64_t)s->g.n[0] * s->g.n[1] * s->g.n[2];
         double* grid = static_cast<double*>(s->grid.ensure(sizeof(double) * s->C * vol));
@@ -968,7 +1030,13 @@ void host_pipeline(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* 
         tm.mark();  // 4
         session_evaluate(s, 0, 1, parts, du);
         tm.mark();  // 5
-        cuda_check(cudaMemcpyAsync(u_out, du, sizeof(double) * 3 * nt, cudaMemcpyDefault, ctx->stream), "u copy");
+        if (is_pageable(u_out)) {  // through pinned staging, copied out after the synchronisation
+            out_stage = static_cast<double*>(ctx->pu.ensure(sizeof(double) * 3 * nt));
+            cuda_check(cudaMemcpyAsync(out_stage, du, sizeof(double) * 3 * nt, cudaMemcpyDeviceToHost, ctx->stream),
+                       "u copy");
+        } else {
+            cuda_check(cudaMemcpyAsync(u_out, du, sizeof(double) * 3 * nt, cudaMemcpyDefault, ctx->stream), "u copy");
+        }
     } else {
         tm.mark();
         tm.mark();
@@ -977,6 +1045,7 @@ void host_pipeline(sewald_gpu_ctx* ctx, const sewald_params_c* p, const double* 
     session_read_singular(s);  // read with the result: no extra synchronisation
     cuda_check(cudaStreamSynchronize(ctx->stream), "pipeline sync");
     session_finish_singular(s);
+    if (out_stage) parallel_memcpy(u_out, out_stage, sizeof(double) * 3 * nt);
     sewald_timings_c& T = ctx->timings;
     T = sewald_timings_c{};
     T.h2d_ms = tm.ms(0, 1);

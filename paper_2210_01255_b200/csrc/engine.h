@@ -40,6 +40,14 @@ struct HostFlags {
     int* get();
 };
 
+// Grow-only pinned host buffer (staging of pageable caller buffers).
+struct PinnedBuf {
+    void* ptr = nullptr;
+    size_t bytes = 0;
+    ~PinnedBuf();
+    void* ensure(size_t n);
+};
+
 struct FourierPlanD3;   // cuFFT plans + k tables for the fully periodic path
 struct FourierPlanAFT;  // zero-padded / upsampled free-direction path (d < 3)
 struct AftDeleter {
@@ -65,6 +73,8 @@ struct sewald_gpu_ctx {
     sewald_params_c cached_params{};
     // staging for host-buffer entry points
     sewald_b200::DevBuf hx, hf, hnu, hxt, hu;
+    // pinned staging of pageable host inputs / output (parallel host copies)
+    sewald_b200::PinnedBuf px, pf, pnu, pxt, pu;
 };
 
 struct sewald_gpu_session {
