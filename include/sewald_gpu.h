@@ -152,7 +152,9 @@ enum {
     SEWALD_OPT_SPREAD_MMA_L = 6,  /* tensor-core spread region edge for P <= 20: 23 or 19 */
     SEWALD_OPT_SPREAD_CACHED = 7, /* tensor-core spread: 1 staged tables per chunk, 0 per group */
     SEWALD_OPT_SPREAD_ROWSWEEP = 8, /* tensor-core spread, P <= 20: 1 row-sweep CTAs (several per SM) */
-    SEWALD_OPT_COUNT = 9
+    SEWALD_OPT_SPREAD_FUSED = 9,  /* tensor-core spread tiles (3 components): 1 taps evaluated in the
+                                     kernel, 0 read from a taps array written by a separate kernel */
+    SEWALD_OPT_COUNT = 10
 };
 int sewald_gpu_set_option(int which, int value);
 int sewald_gpu_get_option(int which, int* value);

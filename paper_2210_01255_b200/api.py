@@ -305,6 +305,7 @@ class KernelOption(enum.IntEnum):
     SPREAD_MMA_L = 6    # 23 or 19
     SPREAD_CACHED = 7   # 1 staged tables per chunk, 0 per group
     SPREAD_ROWSWEEP = 8  # 1 row-sweep tensor-core spread CTAs for P <= 20
+    SPREAD_FUSED = 9    # 1 tensor-core spread tiles evaluate their taps in the kernel
 
 
 def get_kernel_option(which: KernelOption) -> int:

@@ -743,6 +743,16 @@ void session_spread(sewald_gpu_session* s, int64_t i0, int64_t i1, double* grid)
     ensure_spread_order(s, i0, i1);
     cudaStream_t st = s->ctx->stream;
     const int64_t vol = (int64_t)s->g.n[0] * s->g.n[1] * s->g.n[2];
+    if (s->sp_mode == 2 && spread_mma_fused_ok(s->sm_shape, s->C)) {
+        void* fsrc = s->fused_arg.ensure(fused_src_bytes());
+        s->ctx->launches += launch_spread_mma_fused(s->g, s->w, s->p.P, s->sm_shape, s->x.as<double>() + 3 * i0,
+                                                    s->f.as<double>() + 3 * i0,
+                                                    s->stresslet ? s->nu.as<double>() + 3 * i0 : nullptr,
+                                                    s->sp_order.as<uint32_t>(), s->C, s->sp_off.as<int64_t>(), grid,
+                                                    fsrc, st);
+        cuda_check(cudaGetLastError(), "spread launch");
+        return;
+    }
     if (s->sp_mode == 2 || s->sweep.ok) {
         const int64_t n = i1 - i0;
         const int P = s->p.P;

@@ -45,6 +45,9 @@ int env_default(int which) {
         case SEWALD_OPT_SPREAD_ROWSWEEP:
             e = env("SEWALD_SPREAD_ROWSWEEP");
             return (e && e[0] == '1') ? 1 : 0;
+        case SEWALD_OPT_SPREAD_FUSED:
+            e = env("SEWALD_SPREAD_FUSED");
+            return (e && e[0] == '0') ? 0 : 1;
     }
     return 0;
 }
@@ -60,6 +63,7 @@ bool valid(int which, int v) {
         case SEWALD_OPT_SPREAD_MMA_L: return v == 19 || v == 23;
         case SEWALD_OPT_SPREAD_CACHED: return v == 0 || v == 1;
         case SEWALD_OPT_SPREAD_ROWSWEEP: return v == 0 || v == 1;
+        case SEWALD_OPT_SPREAD_FUSED: return v == 0 || v == 1;
     }
     return false;
 }

@@ -66,6 +66,13 @@ void launch_spread_mma_bucket(const DevGrid& g, int P, const SpreadMmaShape& s, 
                               uint32_t* keys, uint32_t* vals, int* bad, cudaStream_t st);
 int launch_spread_mma(const DevGrid& g, int P, const SpreadMmaShape& s, const double* W, const int4* SW,
                       const double* STR, int C, const int64_t* off, double* out, cudaStream_t st);
+// Same tiles with the taps evaluated in the kernel (no taps array); fsrc_dev:
+// fused_src_bytes() of device scratch for the kernel's argument block.
+bool spread_mma_fused_ok(const SpreadMmaShape& s, int C);
+size_t fused_src_bytes();
+int launch_spread_mma_fused(const DevGrid& g, const DevWindow& w, int P, const SpreadMmaShape& s, const double* x,
+                            const double* f, const double* nu, const uint32_t* order, int C, const int64_t* off,
+                            double* out, void* fsrc_dev, cudaStream_t st);
 
 struct SweepShape {
     int nbx, nby, nseg;

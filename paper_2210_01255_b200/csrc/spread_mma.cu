@@ -153,12 +153,27 @@ constexpr int CT_CMAX = 9;
 
 size_t cached_smem_bytes() { return sizeof(double) * (size_t)CT_TMAX * (3 * SM_LS + CT_CMAX); }
 
-template <int L>
+// Fused taps (FUSED = true): the chunk's window taps are evaluated here from
+// the positions (fourier.cpp:168-188, same expression as the taps kernel)
+// instead of being read from a taps array written by a separate kernel: no
+// 3 P doubles per source through HBM and one launch less per spread. One
+// thread per (axis, source), axis-major, so a warp's PKB coefficient reads
+// are uniform. Measured at c2 (C = 3): 4.31 vs 4.40 ms with the taps kernel;
+// c3 (C = 9): 12.7 vs 12.2 ms, so it is the default for 3 components only.
+struct FusedSrc {
+    const double* x;        // positions of the spread slice (AoS)
+    const double* f;        // strengths
+    const double* nu;       // stresslet orientations or null
+    const uint32_t* order;  // bucket-sorted -> slice index
+    DevWindow win;
+};
+
+template <int L, bool FUSED = false>
 __global__ void __launch_bounds__(SM_THREADS)
 spread_tile_mma_cached_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64_t tile0,
                               const double* __restrict__ W, const int4* __restrict__ SW,
                               const double* __restrict__ STR, int C, const int64_t* __restrict__ off,
-                              double* __restrict__ out) {
+                              double* __restrict__ out, const FusedSrc* __restrict__ fsrc) {
     constexpr int ROWS = L * L;
     constexpr int RB = (ROWS + 7) / 8;
     constexpr int RBW = (RB + SM_WARPS - 1) / SM_WARPS;  // row blocks per warp
@@ -182,25 +197,62 @@ spread_tile_mma_cached_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz
         const int T = (int)min((int64_t)CT_TMAX, p1 - q0);
         const int ngroups = (T + SM_TG - 1) / SM_TG;
         __syncthreads();
-        // tables of the chunk: warp per source, lane = region index
-        for (int t = warp; t < ngroups * SM_TG; t += SM_WARPS) {
-            int4 sw = make_int4(0, 0, 0, 0);
-            if (t < T) sw = SW[q0 + t];
-            if (lane < SM_LS) {
-                const int k = lane;
-                double vx = 0.0, vy = 0.0, vz = 0.0;
-                if (t < T && k < L) {
-                    const double* w = W + (q0 + t) * 3 * P;
-                    const int kx = k - (sw.x - X0), ky = k - (sw.y - Y0), kz = k - (sw.z - Z0);
-                    if (kx >= 0 && kx < P) vx = __ldg(w + kx);
-                    if (ky >= 0 && ky < P) vy = __ldg(w + P + ky);
-                    if (kz >= 0 && kz < P) vz = __ldg(w + 2 * P + kz);
-                }
-                wx[t][k] = vx;
-                wy[t][k] = vy;
-                wz[t][k] = vz;
+        if (FUSED) {
+            // zero the chunk's tables, then one thread per (axis, source) writes
+            // the P taps at the source's offset in the region
+            const int rows = ngroups * SM_TG;
+            for (int e = threadIdx.x; e < rows * SM_LS; e += SM_THREADS) {
+                (&wx[0][0])[e] = 0.0;
+                (&wy[0][0])[e] = 0.0;
+                (&wz[0][0])[e] = 0.0;
             }
-            if (lane < C) fs[t * C + lane] = t < T ? STR[(q0 + t) * C + lane] : 0.0;
+            for (int e = threadIdx.x; e < rows * C; e += SM_THREADS) {
+                const int t = e / C, c = e - t * C;
+                double v = 0.0;
+                if (t < T) {
+                    const int64_t i = fsrc->order[q0 + t];
+                    if (C == 3) {
+                        v = fsrc->f[3 * i + c];
+                    } else {  // stresslet: q_l nu_m (fourier.cpp:253-258)
+                        const int l = c / 3, m = c - 3 * l;
+                        v = fsrc->f[3 * i + l] * fsrc->nu[3 * i + m];
+                    }
+                }
+                fs[e] = v;
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < 3 * T; e += SM_THREADS) {
+                const int ax = e / T, t = e - ax * T;
+                const int64_t i = fsrc->order[q0 + t];
+                int j0;
+                double rel;
+                stencil_origin(g, P, ax, fsrc->x[3 * i + ax], j0, rel);
+                const int sw = ax < g.d ? wrap_index(j0, g.n[ax]) : j0;
+                const int o = sw - (ax == 0 ? X0 : (ax == 1 ? Y0 : Z0));
+                double* row = ax == 0 ? wx[t] : (ax == 1 ? wy[t] : wz[t]);
+                for (int p = 0; p < P; ++p) row[o + p] = window_eval(fsrc->win, ((double)(j0 + p) - rel) * g.h);
+            }
+        } else {
+            // tables of the chunk: warp per source, lane = region index
+            for (int t = warp; t < ngroups * SM_TG; t += SM_WARPS) {
+                int4 sw = make_int4(0, 0, 0, 0);
+                if (t < T) sw = SW[q0 + t];
+                if (lane < SM_LS) {
+                    const int k = lane;
+                    double vx = 0.0, vy = 0.0, vz = 0.0;
+                    if (t < T && k < L) {
+                        const double* w = W + (q0 + t) * 3 * P;
+                        const int kx = k - (sw.x - X0), ky = k - (sw.y - Y0), kz = k - (sw.z - Z0);
+                        if (kx >= 0 && kx < P) vx = __ldg(w + kx);
+                        if (ky >= 0 && ky < P) vy = __ldg(w + P + ky);
+                        if (kz >= 0 && kz < P) vz = __ldg(w + 2 * P + kz);
+                    }
+                    wx[t][k] = vx;
+                    wy[t][k] = vy;
+                    wz[t][k] = vz;
+                }
+                if (lane < C) fs[t * C + lane] = t < T ? STR[(q0 + t) * C + lane] : 0.0;
+            }
         }
         __syncthreads();
         for (int c = 0; c < C; ++c) {
@@ -401,6 +453,30 @@ void launch_spread_mma_bucket(const DevGrid& g, int P, const SpreadMmaShape& s, 
     launch_tile_bucket(g, P, ts, x, N, keys, vals, bad, st);
 }
 
+bool spread_mma_fused_ok(const SpreadMmaShape& s, int C) {
+    return s.ok && s.L <= 23 && C == 3 && option(SEWALD_OPT_SPREAD_CACHED) != 0 &&
+           !option(SEWALD_OPT_SPREAD_ROWSWEEP) && option(SEWALD_OPT_SPREAD_FUSED) != 0;
+}
+
+int launch_spread_mma_fused(const DevGrid& g, const DevWindow& w, int P, const SpreadMmaShape& s, const double* x,
+                            const double* f, const double* nu, const uint32_t* order, int C, const int64_t* off,
+                            double* out, void* fsrc_dev, cudaStream_t st) {
+    cudaMemsetAsync(out, 0, sizeof(double) * C * (size_t)g.n[0] * g.n[1] * g.n[2], st);
+    FusedSrc h{x, f, nu, order, w};
+    cudaMemcpyAsync(fsrc_dev, &h, sizeof(FusedSrc), cudaMemcpyHostToDevice, st);
+    const size_t sm = cached_smem_bytes();
+    auto kern = s.L == 23 ? spread_tile_mma_cached_kernel<23, true> : spread_tile_mma_cached_kernel<19, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    for (int64_t a = 0; a < s.ntiles; a += (int64_t)1 << 30) {
+        const int64_t n = std::min<int64_t>(s.ntiles - a, (int64_t)1 << 30);
+        kern<<<(unsigned)n, SM_THREADS, sm, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, nullptr, nullptr, nullptr, C,
+                                                  off, out, static_cast<const FusedSrc*>(fsrc_dev));
+    }
+    return 1;
+}
+
+size_t fused_src_bytes() { return sizeof(FusedSrc); }
+
 int launch_spread_mma(const DevGrid& g, int P, const SpreadMmaShape& s, const double* W, const int4* SW,
                       const double* STR, int C, const int64_t* off, double* out, cudaStream_t st) {
     cudaMemsetAsync(out, 0, sizeof(double) * C * (size_t)g.n[0] * g.n[1] * g.n[2], st);
@@ -425,7 +501,8 @@ int launch_spread_mma(const DevGrid& g, int P, const SpreadMmaShape& s, const do
             const size_t sm = cached_smem_bytes();
             auto kern = s.L == 23 ? spread_tile_mma_cached_kernel<23> : spread_tile_mma_cached_kernel<19>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-            kern<<<(unsigned)n, SM_THREADS, sm, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W, SW, STR, C, off, out);
+            kern<<<(unsigned)n, SM_THREADS, sm, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W, SW, STR, C, off, out,
+                                                      nullptr);
         } else if (s.L == 23)
             spread_tile_mma_kernel<23><<<(unsigned)n, SM_THREADS, 0, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W,
                                                                            SW, STR, C, off, out);
