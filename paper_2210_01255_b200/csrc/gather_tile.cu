@@ -321,6 +321,145 @@ gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
     }
 }
 
+// Wide windows (20 < P <= 32, c4's Gaussian window at P = 32): B = L - P + 1
+// with L = 31 / 35 / 39. The L^3 region no longer fits in shared memory, so
+// the A fragments (grid values G[(a,b)][c]) are read straight from the grid
+// (L2-resident) per row block, and every n-block of the chunk's targets
+// consumes them while they sit in registers; the B fragments (z taps) and the
+// epilogue tables stay in shared memory. Same contraction as above.
+constexpr int WG_TMAX = 64;
+
+template <int MM_L>
+__global__ void __launch_bounds__(MM_THREADS, 2)
+gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64_t tile0,
+                       const double* __restrict__ W, const int4* __restrict__ SW, const int64_t* __restrict__ off,
+                       const double* __restrict__ grid, double h3, int accumulate, double* __restrict__ u) {
+    constexpr int LS = (MM_L + 4) & ~3;  // K = LS = 4 x KS (columns >= L are zero taps)
+    constexpr int KS = LS / 4;
+    constexpr int ROWS = MM_L * MM_L;
+    constexpr int RB = (ROWS + 7) / 8;
+    constexpr int NBMAX = WG_TMAX / 8;
+    extern __shared__ __align__(16) double sm[];
+    const int64_t tile = tile0 + blockIdx.x;
+    const int64_t p0 = off[tile], p1 = off[tile + 1];
+    if (p0 >= p1) return;
+    const int tz = (int)(tile % ntz);
+    const int ty = (int)((tile / ntz) % nty);
+    const int tx = (int)(tile / ((int64_t)ntz * nty));
+    const int X0 = tx * B, Y0 = ty * B, Z0 = tz * B;
+    double* wz = sm;                                   // [WG_TMAX][LS]   Wz'[t][c]
+    double* wx = wz + WG_TMAX * LS;                    // [LS][WG_TMAX]   Wx'[a][t]
+    double* wy = wx + LS * WG_TMAX;                    // [LS][WG_TMAX]   Wy'[b][t]
+    double* part = wy + LS * WG_TMAX;                  // [MM_WARPS][WG_TMAX]
+    int* rowoff = reinterpret_cast<int*>(part + MM_WARPS * WG_TMAX);  // [ROWS]
+    int* zoff = rowoff + ROWS;                                      // [LS]
+    int* tid = zoff + LS;                                           // [WG_TMAX]
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    for (int row = threadIdx.x; row < ROWS; row += MM_THREADS) {
+        const int i = row / MM_L, j = row - i * MM_L;
+        int gx = X0 + i, gy = Y0 + j;
+        bool ok = true;
+        if (g.d > 0) gx %= g.n[0]; else ok = gx < g.n[0];
+        if (g.d > 1) gy %= g.n[1]; else ok = ok && gy < g.n[1];
+        rowoff[row] = ok ? (gx * g.n[1] + gy) * g.n[2] : -1;
+    }
+    for (int k = threadIdx.x; k < LS; k += MM_THREADS) {
+        int gz = Z0 + k;
+        bool ok = k < MM_L;
+        if (g.d > 2) gz %= g.n[2]; else ok = ok && gz < g.n[2];
+        zoff[k] = ok ? gz : -1;
+    }
+    const int64_t cs = (int64_t)g.n[0] * g.n[1] * g.n[2];
+
+    for (int64_t q0 = p0; q0 < p1; q0 += WG_TMAX) {
+        const int T = (int)min((int64_t)WG_TMAX, p1 - q0);
+        const int nblk = (T + 7) / 8;
+        __syncthreads();
+        for (int t = warp; t < nblk * 8; t += MM_WARPS) {
+            int4 sw = make_int4(0, 0, 0, -1);
+            if (t < T) sw = SW[q0 + t];
+            for (int k = lane; k < LS; k += 32) {
+                double vz = 0.0, vx = 0.0, vy = 0.0;
+                if (t < T && k < MM_L) {
+                    const double* wt = W + (q0 + t) * 3 * P;
+                    const int kx = k - (sw.x - X0), ky = k - (sw.y - Y0), kz = k - (sw.z - Z0);
+                    if (kx >= 0 && kx < P) vx = __ldg(wt + kx);
+                    if (ky >= 0 && ky < P) vy = __ldg(wt + P + ky);
+                    if (kz >= 0 && kz < P) vz = __ldg(wt + 2 * P + kz);
+                }
+                wz[t * LS + k] = vz;
+                wx[k * WG_TMAX + t] = vx;
+                wy[k * WG_TMAX + t] = vy;
+            }
+            if (lane == 0) tid[t] = sw.w;
+        }
+        __syncthreads();
+        for (int c = 0; c < 3; ++c) {
+            const double* gc = grid + c * cs;
+            double acc[NBMAX][2];
+#pragma unroll
+            for (int nb = 0; nb < NBMAX; ++nb) acc[nb][0] = acc[nb][1] = 0.0;
+            const int tcol = 2 * (lane & 3);
+            for (int rb = warp; rb < RB; rb += MM_WARPS) {
+                const int row_a = rb * 8 + (lane >> 2);
+                const int ro = row_a < ROWS ? rowoff[row_a] : -1;
+                double af[KS];
+#pragma unroll
+                for (int ks = 0; ks < KS; ++ks) {
+                    const int zo = zoff[ks * 4 + (lane & 3)];
+                    af[ks] = (ro >= 0 && zo >= 0) ? __ldg(gc + ro + zo) : 0.0;
+                }
+                const int a = row_a / MM_L, b = row_a - a * MM_L;  // rows >= L*L: a >= L (zero taps)
+#pragma unroll
+                for (int nb = 0; nb < NBMAX; ++nb) {
+                    if (nb < nblk) {
+                        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                        for (int ks = 0; ks < KS; ++ks)
+                            dmma_8x8x4(d0, d1, af[ks], wz[(nb * 8 + (lane >> 2)) * LS + ks * 4 + (lane & 3)]);
+                        if (a < LS) {
+                            const int t = nb * 8 + tcol;
+                            const double2 vx = *reinterpret_cast<const double2*>(wx + a * WG_TMAX + t);
+                            const double2 vy = *reinterpret_cast<const double2*>(wy + b * WG_TMAX + t);
+                            acc[nb][0] = fma(d0, vx.x * vy.x, acc[nb][0]);
+                            acc[nb][1] = fma(d1, vx.y * vy.y, acc[nb][1]);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int nb = 0; nb < NBMAX; ++nb)
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+#pragma unroll
+                    for (int s2 = 4; s2 < 32; s2 <<= 1) acc[nb][h] += __shfl_xor_sync(0xffffffffu, acc[nb][h], s2);
+            if (lane < 4) {
+#pragma unroll
+                for (int nb = 0; nb < NBMAX; ++nb) {
+                    part[warp * WG_TMAX + nb * 8 + 2 * lane] = acc[nb][0];
+                    part[warp * WG_TMAX + nb * 8 + 2 * lane + 1] = acc[nb][1];
+                }
+            }
+            __syncthreads();
+            for (int t = threadIdx.x; t < T; t += MM_THREADS) {
+                double v = 0.0;
+#pragma unroll
+                for (int w = 0; w < MM_WARPS; ++w) v += part[w * WG_TMAX + t];
+                double* dst = u + 3 * (int64_t)tid[t] + c;
+                *dst = accumulate ? *dst + h3 * v : h3 * v;
+            }
+            __syncthreads();
+        }
+    }
+}
+
+size_t wide_smem_bytes(int L) {
+    const int LS = (L + 4) & ~3;
+    return sizeof(double) * ((size_t)3 * WG_TMAX * LS + MM_WARPS * WG_TMAX) +
+           sizeof(int) * ((size_t)L * L + LS + WG_TMAX);
+}
+
 size_t mma_smem_bytes(int L, int MM_TMAX) {
     const int LS = (L + 4) & ~3, rows = L * L, rb = (rows + 7) / 8;
     return sizeof(double) * ((size_t)rb * 8 * LS + MM_TMAX * LS + 2 * LS * MM_TMAX + MM_WARPS * MM_TMAX) +
@@ -338,6 +477,17 @@ TileShape tile_shape(const DevGrid& g, int P, int64_t Nt) {
     // per target and a tile's region is loaded once per component.
     s.ok = P <= 20;
     s.B = P <= GT_PMAX ? std::max(1, 20 - P) : std::max(1, 24 - P);
+    if (P > 20 && P <= 32) {  // wide-window tensor-core tiles (gather_wide_mma_kernel)
+        s.L = P <= 24 ? 31 : (P <= 28 ? 35 : 39);
+        s.B = s.L - P + 1;
+        for (int ax = 0; ax < 3; ++ax) s.nt[ax] = (g.n[ax] + s.B - 1) / s.B;
+        s.ntiles = (int64_t)s.nt[0] * s.nt[1] * s.nt[2];
+        s.tpt = s.ntiles > 0 ? (double)Nt / (double)s.ntiles : 0.0;
+        s.smem = wide_smem_bytes(s.L);
+        s.ok = option(SEWALD_OPT_GATHER_WIDE) != 0 && s.ntiles < (int64_t(1) << 31) &&
+               (int64_t)g.n[0] * g.n[1] * g.n[2] < (int64_t(1) << 31);
+        return s;
+    }
     const int forced_l = option(SEWALD_OPT_GATHER_L);
     if (P <= 15) {
         const double cells = (double)g.n[0] * g.n[1] * g.n[2];
@@ -371,6 +521,17 @@ void launch_gather_tile(const DevGrid& g, int P, const TileShape& s, const doubl
     const int64_t t0 = s.ntiles * part / nparts, t1 = s.ntiles * (part + 1) / nparts;
     if (t1 <= t0) return;
     const bool use_mma = option(SEWALD_OPT_GATHER_MMA) != 0;
+    if (s.L >= 31) {
+        auto kern = s.L == 31 ? gather_wide_mma_kernel<31>
+                              : (s.L == 35 ? gather_wide_mma_kernel<35> : gather_wide_mma_kernel<39>);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s.smem);
+        for (int64_t a = t0; a < t1; a += (int64_t)1 << 30) {
+            const int64_t n = std::min<int64_t>(t1 - a, (int64_t)1 << 30);
+            kern<<<(unsigned)n, MM_THREADS, s.smem, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W, SW, off, grid,
+                                                          h3, accumulate, u);
+        }
+        return;
+    }
     if ((use_mma || P > GT_PMAX || s.L == 15) && (s.L == 15 || s.L == 19 || s.L == 23)) {
         const bool wide = s.tpt >= 64.0;
         const size_t sm = mma_smem_bytes(s.L, wide ? 128 : 64);

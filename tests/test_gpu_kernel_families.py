@@ -181,6 +181,7 @@ GATHER_FAMILIES = {
     "tile_mma": dict(GATHER=2, GATHER_MMA=1),
     "tile_mma_L15": dict(GATHER=2, GATHER_MMA=1, GATHER_L=15),
     "tile_cuda": dict(GATHER=2, GATHER_MMA=0),
+    "sweep_wide_off": dict(GATHER=-1, GATHER_WIDE=0),
 }
 
 
