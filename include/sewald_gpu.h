@@ -154,7 +154,9 @@ enum {
     SEWALD_OPT_SPREAD_ROWSWEEP = 8, /* tensor-core spread, P <= 20: 1 row-sweep CTAs (several per SM) */
     SEWALD_OPT_SPREAD_FUSED = 9,  /* tensor-core spread tiles (3 components): 1 taps evaluated in the
                                      kernel, 0 read from a taps array written by a separate kernel */
-    SEWALD_OPT_GATHER_WIDE = 10,  /* 20 < P <= 32: 1 tensor-core tiles (A fragments from the grid), 0 z-sweep */
+    SEWALD_OPT_GATHER_WIDE = 10,  /* tensor-core gather tiles with the A fragments read from the grid into
+                                     registers: 2 every width (default), 1 only 20 < P <= 32, 0 never
+                                     (shared-memory region tiles for P <= 20, z-sweep above) */
     SEWALD_OPT_COUNT = 11
 };
 int sewald_gpu_set_option(int which, int value);

@@ -306,7 +306,7 @@ class KernelOption(enum.IntEnum):
     SPREAD_CACHED = 7   # 1 staged tables per chunk, 0 per group
     SPREAD_ROWSWEEP = 8  # 1 row-sweep tensor-core spread CTAs for P <= 20
     SPREAD_FUSED = 9    # 1 tensor-core spread tiles evaluate their taps in the kernel
-    GATHER_WIDE = 10    # 20 < P <= 32: 1 tensor-core gather tiles, 0 z-sweep
+    GATHER_WIDE = 10    # register-A gather tiles: 2 every width, 1 only 20 < P <= 32, 0 never
 
 
 def get_kernel_option(which: KernelOption) -> int:

@@ -321,16 +321,25 @@ gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
     }
 }
 
-// Wide windows (20 < P <= 32, c4's Gaussian window at P = 32): B = L - P + 1
-// with L = 31 / 35 / 39. The L^3 region no longer fits in shared memory, so
-// the A fragments (grid values G[(a,b)][c]) are read straight from the grid
-// (L2-resident) per row block, and every n-block of the chunk's targets
-// consumes them while they sit in registers; the B fragments (z taps) and the
-// epilogue tables stay in shared memory. Same contraction as above.
-constexpr int WG_TMAX = 64;
+// Register-A form (default for every width): the A fragments (grid values
+// G[(a,b)][c]) are read straight from the L2-resident grid per row block and
+// every n-block of the chunk's targets consumes them from registers; the B
+// fragments (z taps) and the epilogue tables stay in shared memory. No region
+// staging, no cp.async phase between barriers. Wide windows (20 < P <= 32,
+// c4's Gaussian window at P = 32: B = L - P + 1, L = 31 / 35 / 39) need it, as
+// the L^3 region does not fit in shared memory: c4 17.3 -> 9.1 ms against the
+// z-sweep; for L = 19 / 23 it beats the shared-region kernel above too
+// (c2 3.68 -> 3.24 ms, c3 5.62 -> 4.50, c5 13.8 -> 11.9).
+#ifndef SEWALD_WG_TMAX
+#define SEWALD_WG_TMAX 64
+#endif
+#ifndef SEWALD_WG_MINB
+#define SEWALD_WG_MINB 3
+#endif
+constexpr int WG_TMAX = SEWALD_WG_TMAX;
 
 template <int MM_L>
-__global__ void __launch_bounds__(MM_THREADS, 2)
+__global__ void __launch_bounds__(MM_THREADS, SEWALD_WG_MINB)
 gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64_t tile0,
                        const double* __restrict__ W, const int4* __restrict__ SW, const int64_t* __restrict__ off,
                        const double* __restrict__ grid, double h3, int accumulate, double* __restrict__ u) {
@@ -521,14 +530,20 @@ void launch_gather_tile(const DevGrid& g, int P, const TileShape& s, const doubl
     const int64_t t0 = s.ntiles * part / nparts, t1 = s.ntiles * (part + 1) / nparts;
     if (t1 <= t0) return;
     const bool use_mma = option(SEWALD_OPT_GATHER_MMA) != 0;
-    if (s.L >= 31) {
+    const bool wide_all = option(SEWALD_OPT_GATHER_WIDE) == 2 && (s.L == 15 || s.L == 19 || s.L == 23);
+    if (s.L >= 31 || wide_all) {
         auto kern = s.L == 31 ? gather_wide_mma_kernel<31>
-                              : (s.L == 35 ? gather_wide_mma_kernel<35> : gather_wide_mma_kernel<39>);
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s.smem);
+                              : (s.L == 35 ? gather_wide_mma_kernel<35>
+                                           : (s.L == 39 ? gather_wide_mma_kernel<39>
+                                                        : (s.L == 15 ? gather_wide_mma_kernel<15>
+                                                                     : (s.L == 19 ? gather_wide_mma_kernel<19>
+                                                                                  : gather_wide_mma_kernel<23>))));
+        const size_t smw = wide_smem_bytes(s.L);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
         for (int64_t a = t0; a < t1; a += (int64_t)1 << 30) {
             const int64_t n = std::min<int64_t>(t1 - a, (int64_t)1 << 30);
-            kern<<<(unsigned)n, MM_THREADS, s.smem, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W, SW, off, grid,
-                                                          h3, accumulate, u);
+            kern<<<(unsigned)n, MM_THREADS, smw, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W, SW, off, grid,
+                                                       h3, accumulate, u);
         }
         return;
     }

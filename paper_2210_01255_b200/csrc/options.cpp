@@ -50,7 +50,7 @@ int env_default(int which) {
             return (e && e[0] == '0') ? 0 : 1;
         case SEWALD_OPT_GATHER_WIDE:
             e = env("SEWALD_GATHER_WIDE");
-            return (e && e[0] == '0') ? 0 : 1;
+            return e ? atoi(e) : 2;
     }
     return 0;
 }
@@ -67,7 +67,7 @@ bool valid(int which, int v) {
         case SEWALD_OPT_SPREAD_CACHED: return v == 0 || v == 1;
         case SEWALD_OPT_SPREAD_ROWSWEEP: return v == 0 || v == 1;
         case SEWALD_OPT_SPREAD_FUSED: return v == 0 || v == 1;
-        case SEWALD_OPT_GATHER_WIDE: return v == 0 || v == 1;
+        case SEWALD_OPT_GATHER_WIDE: return v >= 0 && v <= 2;
     }
     return false;
 }
