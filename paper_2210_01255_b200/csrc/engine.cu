@@ -845,7 +845,10 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
         cuda_check(cudaMemsetAsync(u, 0, sizeof(double) * 3 * Nt, st), "u zero");
         first = false;
     }
-    if ((parts & 2) && has_targets) {
+    // the pair-symmetric kernel takes interleaved clusters (below): part p has
+    // work iff p < ncl; the other kernels take the contiguous target range
+    const bool rs_work = use_sym ? (int64_t)part < ncl : has_targets;
+    if ((parts & 2) && rs_work) {
         if (!(s->p.xi > 0.0)) throw EngineError(SEWALD_EINVAL, "split parameter must be positive");
         if (!(s->p.rc > 0.0)) throw EngineError(SEWALD_EINVAL, "cell list cutoff must be positive");
         RealspaceArgs a{};
@@ -864,7 +867,15 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
         const double rpad = a.rc + std::ldexp(ext, -18);
         a.thresh_f = (float)(rpad * rpad * (1.0 + std::ldexp(1.0, -16)));
         if (use_sym) {
-            launch_realspace_sym(s->cg, a, s->packed.as<double>(), Nt, s->c_off.as<int64_t>(), c0, c1, u,
+            // Parts take every nparts-th cluster (not a contiguous range): the half
+            // rule gives the clusters near the start of the cell order (low z)
+            // the periodic-wrap pairs of both ends, so contiguous ranges would
+            // load the first part with up to ~1.5x the average (measured 55 / 45 %
+            // of the pairs for two parts at c2); interleaved parts sample every
+            // z layer. The epilogue keeps the contiguous target range: each is a
+            // partition of its own work and the outputs are summed.
+            launch_realspace_sym(s->cg, a, s->packed.as<double>(), Nt, s->c_off.as<int64_t>(),
+                                 nparts > 1 ? part : 0, ncl, nparts, u,
                                  s->pair_counter.as<unsigned long long>(), s->flags.as<int>() + FLAG_SINGULAR,
                                  static_cast<unsigned long long*>(s->work_counter.ensure(sizeof(unsigned long long))),
                                  st);

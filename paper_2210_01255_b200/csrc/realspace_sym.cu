@@ -232,7 +232,7 @@ __device__ __forceinline__ void slot_eval(SlotEval<KIND, NS, SHORT>& e, const do
 template <int KIND, int S, bool SHORT>
 __global__ void __launch_bounds__(SYM_THREADS, SEWALD_SYM_MINB)
 realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed,
-                     const int64_t* __restrict__ cell_off, int64_t N, int64_t c0, int64_t c1,
+                     const int64_t* __restrict__ cell_off, int64_t N, int64_t c0, int64_t c1, int64_t cstride,
                      double* __restrict__ u, unsigned long long* __restrict__ pair_count, int* __restrict__ err,
                      unsigned long long* __restrict__ work) {
     constexpr int NS = Strength<KIND>::n;
@@ -278,7 +278,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     for (;;) {
     long long next = 0;
     if (lane == 0) next = (long long)atomicAdd(work, 1ull);
-    const int64_t cl = c0 + __shfl_sync(0xffffffffu, next, 0);
+    const int64_t cl = c0 + cstride * __shfl_sync(0xffffffffu, next, 0);
     if (cl >= c1) break;
 
     const int64_t istart = cl * 32;
@@ -679,9 +679,9 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
 }  // namespace
 
 void launch_realspace_sym(const CellGrid& cg, const RealspaceArgs& a, const double* packed, int64_t N,
-                          const int64_t* cell_off, int64_t c0, int64_t c1, double* u,
+                          const int64_t* cell_off, int64_t c0, int64_t c1, int64_t cstride, double* u,
                           unsigned long long* pair_count, int* err, unsigned long long* work, cudaStream_t st) {
-    if (c1 <= c0) return;
+    if (c1 <= c0 || cstride < 1) return;
     cudaMemsetAsync(work, 0, sizeof(unsigned long long), st);
     int dev = 0, sms = 148, per_sm = 4;
     cudaGetDevice(&dev);
@@ -703,14 +703,15 @@ void launch_realspace_sym(const CellGrid& cg, const RealspaceArgs& a, const doub
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(
             &per_sm, shrt ? realspace_sym_kernel<SEWALD_STOKESLET, 8, true> : realspace_sym_kernel<SEWALD_STOKESLET, 8, false>,
             SYM_THREADS, 0);
-    const int64_t need = (c1 - c0 + SYM_WARPS - 1) / SYM_WARPS;
+    const int64_t count = (c1 - c0 + cstride - 1) / cstride;
+    const int64_t need = (count + SYM_WARPS - 1) / SYM_WARPS;
     const unsigned blocks = (unsigned)std::min<int64_t>(need, (int64_t)sms * std::max(per_sm, 1));
 #define SEWALD_SYM_LAUNCH(K, S)                                                                            \
     if (shrt)                                                                                              \
-        realspace_sym_kernel<K, S, true><<<blocks, SYM_THREADS, 0, st>>>(cg, a, packed, cell_off, N, c0, c1, u, \
+        realspace_sym_kernel<K, S, true><<<blocks, SYM_THREADS, 0, st>>>(cg, a, packed, cell_off, N, c0, c1, cstride, u, \
                                                                           pair_count, err, work);          \
     else                                                                                                   \
-        realspace_sym_kernel<K, S, false><<<blocks, SYM_THREADS, 0, st>>>(cg, a, packed, cell_off, N, c0, c1, u, \
+        realspace_sym_kernel<K, S, false><<<blocks, SYM_THREADS, 0, st>>>(cg, a, packed, cell_off, N, c0, c1, cstride, u, \
                                                                            pair_count, err, work);
     switch (a.kind) {
         case SEWALD_STOKESLET: SEWALD_SYM_LAUNCH(SEWALD_STOKESLET, 8) break;

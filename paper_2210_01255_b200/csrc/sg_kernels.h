@@ -133,10 +133,11 @@ void launch_realspace(const CellGrid& cg, const RealspaceArgs& a, const double* 
 int realspace_split(int64_t Nt);
 
 // Symmetric real-space sum for targets == sources (realspace_sym.cu):
-// i-clusters [c0, c1) of 32 cell-ordered particles; u (original order) must
-// be zeroed beforehand and receives contributions of every particle.
+// i-clusters c0, c0 + cstride, ... < c1 of 32 cell-ordered particles; u
+// (original order) must be zeroed beforehand and receives contributions of
+// every particle.
 void launch_realspace_sym(const CellGrid& cg, const RealspaceArgs& a, const double* packed, int64_t N,
-                          const int64_t* cell_off, int64_t c0, int64_t c1, double* u,
+                          const int64_t* cell_off, int64_t c0, int64_t c1, int64_t cstride, double* u,
                           unsigned long long* pair_count, int* err, unsigned long long* work, cudaStream_t st);
 
 // ---- k space (kspace.cu) ---------------------------------------------------

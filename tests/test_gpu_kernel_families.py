@@ -251,3 +251,34 @@ def test_spread_family_golden(S, family):
         with S.kernel_options(**SPREAD_FAMILIES[family]):
             grid = S.spread(sysm, params)
         assert np.max(np.abs(grid - g["grid"])) <= 1e-14 * np.max(np.abs(g["grid"])), (family, name)
+
+
+def test_partition_pair_balance(S):
+    """Multi-part pair-symmetric real space takes interleaved clusters: every
+    part gets the same share of the pairs (contiguous ranges gave the first
+    part the periodic-wrap pairs of both ends), and the parts' pairs add up to
+    the single-part count."""
+    import torch
+    N = 300_000
+    rng = np.random.default_rng(8450)
+    x = rng.random((N, 3))
+    f = rng.standard_normal((N, 3))
+    sysm = S.SourceSystem(S.Kernel.stokeslet, S.Cell((1, 1, 1)), 3, x, f)
+    p = S.select_parameters(sysm.kind, 3, sysm.cell, S.source_quantity(sysm), 25.0, S.ToleranceSpec(1e-8)).params
+    dev = torch.device("cuda", 0)
+    T = lambda a: torch.from_numpy(np.ascontiguousarray(a)).to(dev)
+    sess = S.Session(p, sysm.cell)
+    sess.set_sources(T(x), T(f))
+    sess.set_targets(None, True)
+    u = torch.zeros((N, 3), dtype=torch.float64, device=dev)
+    with S.kernel_options(RS_SYM=2):
+        sess.pair_count(reset=True)
+        sess.evaluate(u, 0, 1, 2)
+        total = sess.pair_count(reset=True)
+        counts = []
+        for r in range(8):
+            sess.evaluate(u, r, 8, 2)
+            counts.append(sess.pair_count(reset=True))
+    sess.close()
+    assert sum(counts) == total
+    assert max(counts) / min(counts) < 1.05, counts
