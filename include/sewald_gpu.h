@@ -157,7 +157,8 @@ enum {
     SEWALD_OPT_GATHER_WIDE = 10,  /* tensor-core gather tiles with the A fragments read from the grid into
                                      registers: 2 every width (default), 1 only 20 < P <= 32, 0 never
                                      (shared-memory region tiles for P <= 20, z-sweep above) */
-    SEWALD_OPT_COUNT = 11
+    SEWALD_OPT_GATHER_FUSED = 11, /* register-A gather tiles: 1 taps evaluated in the kernel, 0 taps array */
+    SEWALD_OPT_COUNT = 12
 };
 int sewald_gpu_set_option(int which, int value);
 int sewald_gpu_get_option(int which, int* value);

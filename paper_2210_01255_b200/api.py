@@ -307,6 +307,7 @@ class KernelOption(enum.IntEnum):
     SPREAD_ROWSWEEP = 8  # 1 row-sweep tensor-core spread CTAs for P <= 20
     SPREAD_FUSED = 9    # 1 tensor-core spread tiles evaluate their taps in the kernel
     GATHER_WIDE = 10    # register-A gather tiles: 2 every width, 1 only 20 < P <= 32, 0 never
+    GATHER_FUSED = 11   # register-A gather tiles evaluate their taps in the kernel
 
 
 def get_kernel_option(which: KernelOption) -> int:

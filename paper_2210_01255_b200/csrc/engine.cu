@@ -510,6 +510,8 @@ const uint32_t* target_order(sewald_gpu_session* s) {
 void ensure_gather_weights(sewald_gpu_session* s, int mode, int part, int nparts) {
     const int key = nparts == 1 ? 0 : part * 4096 + nparts;
     if (s->tg_wpart == key) return;
+    // the fused tensor-core tiles evaluate their taps themselves
+    if (mode == 2 && gather_tile_fused_ok(tile_shape(s->g, s->p.P, s->Nt))) return;
     const SweepShape sh = sweep_shape(s->g, s->p.P);
     const TileShape ts = tile_shape(s->g, s->p.P, s->Nt);
     const int64_t nt = mode == 1 ? (int64_t)sh.nbx * sh.nby : ts.ntiles;
@@ -899,9 +901,14 @@ void session_evaluate(sewald_gpu_session* s, int part, int nparts, int parts, do
             launch_gather_sweep(s->g, s->p.P, s->tg_w.as<double>(), s->tg_sw.as<int4>(), s->tg_off.as<int64_t>(),
                                 sweep_shape(s->g, s->p.P), part, nparts, s->flow.as<double>(), h3, u, st);
         } else if (gmode == 2) {
-            launch_gather_tile(s->g, s->p.P, tile_shape(s->g, s->p.P, s->Nt), s->tg_w.as<double>(), s->tg_sw.as<int4>(),
-                               s->tg_off.as<int64_t>(), part, nparts, s->flow.as<double>(), h3, first ? 0 : 1, u,
-                               st);
+            const TileShape ts = tile_shape(s->g, s->p.P, s->Nt);
+            if (gather_tile_fused_ok(ts))
+                launch_gather_tile_fused(s->g, s->w, s->p.P, ts, target_positions(s), s->tg_order.as<uint32_t>(),
+                                         s->tg_off.as<int64_t>(), part, nparts, s->flow.as<double>(), h3,
+                                         first ? 0 : 1, u, s->fused_garg.ensure(fused_tgt_bytes()), st);
+            else
+                launch_gather_tile(s->g, s->p.P, ts, s->tg_w.as<double>(), s->tg_sw.as<int4>(), s->tg_off.as<int64_t>(),
+                                   part, nparts, s->flow.as<double>(), h3, first ? 0 : 1, u, st);
         } else if (has_targets) {
             launch_gather(s->g, s->w, s->flow.as<double>(), target_positions(s), torder + t0, t1 - t0, h3,
                           first ? 0 : 1, u, st);
@@ -1226,8 +1233,14 @@ int sewald_gpu_gather(sewald_gpu_ctx* ctx, const sewald_params_c* p, const doubl
                 launch_gather_sweep(s->g, s->p.P, s->tg_w.as<double>(), s->tg_sw.as<int4>(), s->tg_off.as<int64_t>(),
                                     sweep_shape(s->g, s->p.P), 0, 1, flow, h3, du, ctx->stream);
             } else if (gmode == 2) {
-                launch_gather_tile(s->g, s->p.P, tile_shape(s->g, s->p.P, Nt), s->tg_w.as<double>(),
-                                   s->tg_sw.as<int4>(), s->tg_off.as<int64_t>(), 0, 1, flow, h3, 0, du, ctx->stream);
+                const TileShape ts = tile_shape(s->g, s->p.P, Nt);
+                if (gather_tile_fused_ok(ts))
+                    launch_gather_tile_fused(s->g, s->w, s->p.P, ts, s->xt.as<double>(), s->tg_order.as<uint32_t>(),
+                                             s->tg_off.as<int64_t>(), 0, 1, flow, h3, 0, du,
+                                             s->fused_garg.ensure(fused_tgt_bytes()), ctx->stream);
+                else
+                    launch_gather_tile(s->g, s->p.P, ts, s->tg_w.as<double>(), s->tg_sw.as<int4>(),
+                                       s->tg_off.as<int64_t>(), 0, 1, flow, h3, 0, du, ctx->stream);
             } else {
                 launch_gather(s->g, s->w, flow, s->xt.as<double>(), nullptr, Nt, h3, 0, du, ctx->stream);
             }

@@ -113,7 +113,7 @@ struct sewald_gpu_session {
     sewald_b200::DevBuf grid, flow;
     // global sums: f (3), q.nu (1), x (q.nu) (3); partials
     sewald_b200::DevBuf sums, partials, flags, pair_counter, work_counter, rs_scratch;
-    sewald_b200::DevBuf fused_arg;  // argument block of the fused-taps spread kernel
+    sewald_b200::DevBuf fused_arg, fused_garg;  // argument blocks of the fused-taps spread / gather kernels
     sewald_b200::HostFlags hflags;
     bool inputs_checked = false;  // non-finite source / target flags read since the last upload
     bool sums_ready = false;

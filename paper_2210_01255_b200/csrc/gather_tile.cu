@@ -338,11 +338,20 @@ gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
 #endif
 constexpr int WG_TMAX = SEWALD_WG_TMAX;
 
-template <int MM_L>
+// Targets' taps evaluated in the kernel (FUSED): positions + bucket order
+// instead of the taps array of a separate kernel.
+struct FusedTgt {
+    const double* x;        // target positions (AoS)
+    const uint32_t* order;  // bucket-sorted -> target index
+    DevWindow win;
+};
+
+template <int MM_L, bool FUSED = false>
 __global__ void __launch_bounds__(MM_THREADS, SEWALD_WG_MINB)
 gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64_t tile0,
                        const double* __restrict__ W, const int4* __restrict__ SW, const int64_t* __restrict__ off,
-                       const double* __restrict__ grid, double h3, int accumulate, double* __restrict__ u) {
+                       const double* __restrict__ grid, double h3, int accumulate, double* __restrict__ u,
+                       const FusedTgt* __restrict__ ftg) {
     constexpr int LS = (MM_L + 4) & ~3;  // K = LS = 4 x KS (columns >= L are zero taps)
     constexpr int KS = LS / 4;
     constexpr int ROWS = MM_L * MM_L;
@@ -385,6 +394,31 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
         const int T = (int)min((int64_t)WG_TMAX, p1 - q0);
         const int nblk = (T + 7) / 8;
         __syncthreads();
+        if (FUSED) {
+            for (int e = threadIdx.x; e < nblk * 8 * LS; e += MM_THREADS) wz[e] = 0.0;
+            for (int e = threadIdx.x; e < LS * WG_TMAX; e += MM_THREADS) {
+                wx[e] = 0.0;
+                wy[e] = 0.0;
+            }
+            for (int t = threadIdx.x; t < nblk * 8; t += MM_THREADS) tid[t] = t < T ? (int)ftg->order[q0 + t] : -1;
+            __syncthreads();
+            for (int e = threadIdx.x; e < 3 * T; e += MM_THREADS) {
+                const int ax = e / T, t = e - ax * T;
+                const int64_t i = ftg->order[q0 + t];
+                int j0;
+                double rel;
+                stencil_origin(g, P, ax, ftg->x[3 * i + ax], j0, rel);
+                const int sw = ax < g.d ? wrap_index(j0, g.n[ax]) : j0;
+                const int o = sw - (ax == 0 ? X0 : (ax == 1 ? Y0 : Z0));
+                for (int p = 0; p < P; ++p) {
+                    const double v = window_eval(ftg->win, ((double)(j0 + p) - rel) * g.h);
+                    const int k = o + p;
+                    if (ax == 2) wz[t * LS + k] = v;
+                    else if (ax == 0) wx[k * WG_TMAX + t] = v;
+                    else wy[k * WG_TMAX + t] = v;
+                }
+            }
+        } else
         for (int t = warp; t < nblk * 8; t += MM_WARPS) {
             int4 sw = make_int4(0, 0, 0, -1);
             if (t < T) sw = SW[q0 + t];
@@ -463,6 +497,22 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
     }
 }
 
+size_t wide_smem_bytes(int L);
+
+template <int L>
+void launch_wide_fused(const DevGrid& g, int P, const TileShape& s, int64_t t0, int64_t t1, const int64_t* off,
+                       const double* grid, double h3, int accumulate, double* u, const FusedTgt* arg,
+                       cudaStream_t st) {
+    auto kern = gather_wide_mma_kernel<L, true>;
+    const size_t smw = wide_smem_bytes(L);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
+    for (int64_t a = t0; a < t1; a += (int64_t)1 << 30) {
+        const int64_t n = std::min<int64_t>(t1 - a, (int64_t)1 << 30);
+        kern<<<(unsigned)n, MM_THREADS, smw, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, nullptr, nullptr, off,
+                                                   grid, h3, accumulate, u, arg);
+    }
+}
+
 size_t wide_smem_bytes(int L) {
     const int LS = (L + 4) & ~3;
     return sizeof(double) * ((size_t)3 * WG_TMAX * LS + MM_WARPS * WG_TMAX) +
@@ -524,6 +574,31 @@ void launch_tile_bucket(const DevGrid& g, int P, const TileShape& s, const doubl
                                                                      keys, vals, bad);
 }
 
+bool gather_tile_fused_ok(const TileShape& s) {
+    return s.ok && option(SEWALD_OPT_GATHER_FUSED) != 0 &&
+           (s.L >= 31 || (option(SEWALD_OPT_GATHER_WIDE) == 2 && (s.L == 15 || s.L == 19 || s.L == 23)));
+}
+
+size_t fused_tgt_bytes() { return sizeof(FusedTgt); }
+
+void launch_gather_tile_fused(const DevGrid& g, const DevWindow& w, int P, const TileShape& s, const double* xt,
+                              const uint32_t* order, const int64_t* off, int part, int nparts, const double* grid,
+                              double h3, int accumulate, double* u, void* arg_dev, cudaStream_t st) {
+    const int64_t t0 = s.ntiles * part / nparts, t1 = s.ntiles * (part + 1) / nparts;
+    if (t1 <= t0) return;
+    FusedTgt h{xt, order, w};
+    cudaMemcpyAsync(arg_dev, &h, sizeof(FusedTgt), cudaMemcpyHostToDevice, st);
+    const FusedTgt* a = static_cast<const FusedTgt*>(arg_dev);
+    switch (s.L) {
+        case 15: launch_wide_fused<15>(g, P, s, t0, t1, off, grid, h3, accumulate, u, a, st); break;
+        case 19: launch_wide_fused<19>(g, P, s, t0, t1, off, grid, h3, accumulate, u, a, st); break;
+        case 23: launch_wide_fused<23>(g, P, s, t0, t1, off, grid, h3, accumulate, u, a, st); break;
+        case 31: launch_wide_fused<31>(g, P, s, t0, t1, off, grid, h3, accumulate, u, a, st); break;
+        case 35: launch_wide_fused<35>(g, P, s, t0, t1, off, grid, h3, accumulate, u, a, st); break;
+        default: launch_wide_fused<39>(g, P, s, t0, t1, off, grid, h3, accumulate, u, a, st); break;
+    }
+}
+
 void launch_gather_tile(const DevGrid& g, int P, const TileShape& s, const double* W, const int4* SW,
                         const int64_t* off, int part, int nparts, const double* grid, double h3, int accumulate,
                         double* u, cudaStream_t st) {
@@ -540,10 +615,11 @@ void launch_gather_tile(const DevGrid& g, int P, const TileShape& s, const doubl
                                                                                   : gather_wide_mma_kernel<23>))));
         const size_t smw = wide_smem_bytes(s.L);
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smw);
+        const FusedTgt* ftg_null = nullptr;
         for (int64_t a = t0; a < t1; a += (int64_t)1 << 30) {
             const int64_t n = std::min<int64_t>(t1 - a, (int64_t)1 << 30);
             kern<<<(unsigned)n, MM_THREADS, smw, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W, SW, off, grid,
-                                                       h3, accumulate, u);
+                                                       h3, accumulate, u, ftg_null);
         }
         return;
     }

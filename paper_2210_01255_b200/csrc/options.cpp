@@ -51,6 +51,9 @@ int env_default(int which) {
         case SEWALD_OPT_GATHER_WIDE:
             e = env("SEWALD_GATHER_WIDE");
             return e ? atoi(e) : 2;
+        case SEWALD_OPT_GATHER_FUSED:
+            e = env("SEWALD_GATHER_FUSED");
+            return (e && e[0] == '1') ? 1 : 0;
     }
     return 0;
 }
@@ -68,6 +71,7 @@ bool valid(int which, int v) {
         case SEWALD_OPT_SPREAD_ROWSWEEP: return v == 0 || v == 1;
         case SEWALD_OPT_SPREAD_FUSED: return v == 0 || v == 1;
         case SEWALD_OPT_GATHER_WIDE: return v >= 0 && v <= 2;
+        case SEWALD_OPT_GATHER_FUSED: return v == 0 || v == 1;
     }
     return false;
 }

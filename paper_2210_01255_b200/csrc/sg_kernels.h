@@ -52,6 +52,13 @@ void launch_tile_bucket(const DevGrid& g, int P, const TileShape& s, const doubl
 void launch_gather_tile(const DevGrid& g, int P, const TileShape& s, const double* W, const int4* SW,
                         const int64_t* off, int part, int nparts, const double* grid, double h3, int accumulate,
                         double* u, cudaStream_t st);
+// Register-A tensor-core gather tiles with the taps evaluated in the kernel
+// (no taps array); arg_dev: fused_tgt_bytes() of device scratch.
+bool gather_tile_fused_ok(const TileShape& s);
+size_t fused_tgt_bytes();
+void launch_gather_tile_fused(const DevGrid& g, const DevWindow& w, int P, const TileShape& s, const double* xt,
+                              const uint32_t* order, const int64_t* off, int part, int nparts, const double* grid,
+                              double h3, int accumulate, double* u, void* arg_dev, cudaStream_t st);
 
 // Tensor-core spread (spread_mma.cu): sources bucketed by the B^3 block of
 // their stencil start, region L^3 (L = B + P - 1) per block as a DMMA GEMM.

@@ -182,6 +182,7 @@ GATHER_FAMILIES = {
     "tile_mma_L15": dict(GATHER=2, GATHER_MMA=1, GATHER_L=15),
     "tile_cuda": dict(GATHER=2, GATHER_MMA=0),
     "tile_smem_region": dict(GATHER=2, GATHER_WIDE=0),
+    "tile_fused_taps": dict(GATHER=2, GATHER_FUSED=1),
     "tile_regA_wide_only": dict(GATHER=2, GATHER_WIDE=1),
     "sweep_wide_off": dict(GATHER=-1, GATHER_WIDE=0),
 }
