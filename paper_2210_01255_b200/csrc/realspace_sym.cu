@@ -186,6 +186,14 @@ __device__ __forceinline__ void pair_apply(const PairCoef<KIND>& c, double r0, d
 #ifndef SEWALD_SYM_POOL_MODE
 #define SEWALD_SYM_POOL_MODE 2
 #endif
+// j-block records loaded with 16-byte loads (c2 62.9 -> 61.3 ms, c3 118.9 ->
+// 117.9, c5 72.4 -> 71.1 against 8-byte loads). A fully coalesced block load
+// (lane l reading chunks l, l + 32, ... and scattering the fields) measured
+// 74.6 ms: the per-lane field selection diverges four ways.
+#ifndef SEWALD_SYM_VEC
+#define SEWALD_SYM_VEC 1
+#endif
+
 // exp table copies (lane-interleaved, conflict-free lookups): 16 copies
 // measured slower at c2 (69.0 vs 67.6 ms), so one copy.
 #ifndef SEWALD_EXP_REP
@@ -377,6 +385,26 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                 for (int64_t jb = b0; jb < b1; jb += 32) {
                     const int cnt = (int)min((int64_t)32, b1 - jb);
                     __syncwarp();
+#if SEWALD_SYM_VEC
+                    if (lane < cnt) {
+                        // 16-byte loads of the lane's record (S doubles, 16-byte aligned):
+                        // half the load instructions and L1 sectors of 8-byte loads
+                        const double2* q2 = reinterpret_cast<const double2*>(packed + (jb + lane) * S);
+                        double* rec = jrec[lane];
+                        const double2 xy = __ldg(q2), zi = __ldg(q2 + 1);
+                        rec[0] = xy.x;
+                        rec[1] = xy.y;
+                        rec[2] = zi.x;
+                        jid[lane] = __double_as_longlong(zi.y);
+                        jf[lane] = make_float4((float)xy.x, (float)xy.y, (float)zi.x, 0.0f);
+#pragma unroll
+                        for (int c = 0; c < NS; c += 2) {
+                            const double2 v = __ldg(q2 + 2 + c / 2);
+                            rec[3 + c] = v.x;
+                            if (c + 1 < NS) rec[4 + c] = v.y;
+                        }
+                    } else {
+#else
                     if (lane < cnt) {
                         const double* q = packed + (jb + lane) * S;
                         double* rec = jrec[lane];
@@ -388,6 +416,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
 #pragma unroll
                         for (int c = 0; c < NS; ++c) rec[3 + c] = q[4 + c];
                     } else {
+#endif
                         // unused slots: far away in fp32 (never candidates) and
                         // finite in fp64 (branch-free steps read them)
                         jf[lane] = make_float4(1e30f, 1e30f, 1e30f, 0.0f);
