@@ -175,16 +175,23 @@ __device__ __forceinline__ void pair_apply(const PairCoef<KIND>& c, double r0, d
 #endif
 // Blocks with fewer candidate pairs than this go through the pooled path
 // (0 = rotation steps only). c2: rotation only 67.6 ms; pooled below
-// 192 / 256 / 384 pairs (mode 2): 63.3 / 62.7-63.0 / 63.5 ms.
+// 192 / 256 / 384 pairs (mode 2): 63.3 / 62.7-63.0 / 63.5 ms; mode 3 at
+// 256 / 384 / 512: c2 59.1 / 58.3 / 59.0, c3 116.0 / 112.3 / 112.5,
+// c5 67.0 / 66.3 / 68.0.
 #ifndef SEWALD_SYM_POOL
-#define SEWALD_SYM_POOL 256
+#define SEWALD_SYM_POOL 384
 #endif
 // Pooled pairs accumulate: 0 both sides with shared-memory atomics (the j
 // side in the block's reaction slots), 1 both sides with global fp64 RED,
-// 2 i side shared, j side global (modes 1, 2 skip the block's reaction flush).
-// c2 at 256: mode 0 67.0 ms, mode 1 63.4 ms, mode 2 63.0 ms.
+// 2 i side shared, j side global (modes 1, 2 skip the block's reaction flush),
+// 3 as 2 but the queue lane-major and the i side segment-summed per batch
+// (plain shared adds): mode 2's fp64 CAS loops retried ~5 times per batch
+// (rotation-major batches of a sparse block repeat the few busy i particles)
+// and drew 16 % of the kernel's stall samples.
+// c2 at 256: mode 0 67.0 ms, mode 1 63.4 ms, mode 2 63.0 ms (61.4 with the
+// 16-byte record loads), mode 3 58.9 ms; c3 117.9 -> 115.6, c5 70.8 -> 66.8.
 #ifndef SEWALD_SYM_POOL_MODE
-#define SEWALD_SYM_POOL_MODE 2
+#define SEWALD_SYM_POOL_MODE 3
 #endif
 // j-block records loaded with 16-byte loads (c2 62.9 -> 61.3 ms, c3 118.9 ->
 // 117.9, c5 72.4 -> 71.1 against 8-byte loads). A fully coalesced block load
@@ -471,6 +478,26 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                     const int ncand = __reduce_add_sync(0xffffffffu, __popc(m));
                     pooled = ncand < SEWALD_SYM_POOL;
                     if (pooled) {
+#if SEWALD_SYM_POOL_MODE == 3
+                        // lane-major queue: each i particle's pairs are consecutive,
+                        // so a batch holds runs of equal il (segment-summed below)
+                        {
+                            const int cntm = __popc(m);
+                            int off = cntm;
+#pragma unroll
+                            for (int d = 1; d < 32; d <<= 1) {
+                                const int t = __shfl_up_sync(0xffffffffu, off, d);
+                                if (lane >= d) off += t;
+                            }
+                            off -= cntm;
+                            unsigned mm = m;
+                            while (mm) {
+                                const int s = __ffs(mm) - 1;
+                                mm &= mm - 1u;
+                                queue[off++] = (unsigned short)((lane << 5) | ((lane + s) & 31));
+                            }
+                        }
+#else
                         int base = 0;
                         unsigned st = steps;
                         while (st) {
@@ -483,6 +510,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                                     (unsigned short)((lane << 5) | ((lane + s) & 31));
                             base += __popc(act);
                         }
+#endif
                         __syncwarp();
                         for (int k0 = 0; k0 < ncand; k0 += 32) {
                             const int k = k0 + lane;
@@ -498,7 +526,41 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                             double* rec = jrec[j];
                             slot_eval<KIND, RS, NS, SHORT>(ev, rec, ys0, ys1, ys2, in, rc2, a.xi, xi2, exp_tab,
                                                           coincident);
+#if SEWALD_SYM_POOL_MODE == 3
+                            {
+                                // i side: segmented sum over the batch's runs of equal il
+                                // (one plain shared add per run, no CAS loops); j side:
+                                // global fp64 RED
+                                double ui[3] = {0.0, 0.0, 0.0};
+                                if (ev.acc) {
+                                    double uj[3] = {0.0, 0.0, 0.0};
+                                    pair_apply<KIND, false>(ev.c, ev.r0, ev.r1, ev.r2, ev.sj, ui);
+                                    pair_apply<KIND, true>(ev.c, ev.r0, ev.r1, ev.r2, fi, uj);
+                                    double* dj = u + 3 * jid[j];
+#pragma unroll
+                                    for (int c = 0; c < 3; ++c) atomicAdd(dj + c, uj[c]);
+                                    npairs32 += 2u;
+                                }
+                                const unsigned same = __match_any_sync(0xffffffffu, in ? il : 32 + lane);
+                                const int first = __ffs(same) - 1;
+                                const int runmax = __reduce_max_sync(0xffffffffu, __popc(same));
+                                for (int d = 1; d < runmax; d <<= 1) {
+#pragma unroll
+                                    for (int c = 0; c < 3; ++c) {
+                                        const double t = __shfl_up_sync(0xffffffffu, ui[c], d);
+                                        if (lane - d >= first) ui[c] += t;
+                                    }
+                                }
+                                if (in && lane == 31 - __clz(same)) {
+#pragma unroll
+                                    for (int c = 0; c < 3; ++c) ipool[il][c] += ui[c];
+                                }
+                                __syncwarp();
+                            }
+                            if (false) {
+#else
                             if (ev.acc) {
+#endif
                                 double ui[3] = {0.0, 0.0, 0.0}, uj[3] = {0.0, 0.0, 0.0};
                                 pair_apply<KIND, false>(ev.c, ev.r0, ev.r1, ev.r2, ev.sj, ui);
                                 pair_apply<KIND, true>(ev.c, ev.r0, ev.r1, ev.r2, fi, uj);
