@@ -181,18 +181,23 @@ __device__ __forceinline__ void pair_apply(const PairCoef<KIND>& c, double r0, d
 #ifndef SEWALD_SYM_POOL
 #define SEWALD_SYM_POOL 384
 #endif
-// Pooled pairs accumulate: 0 both sides with shared-memory atomics (the j
-// side in the block's reaction slots), 1 both sides with global fp64 RED,
-// 2 i side shared, j side global (modes 1, 2 skip the block's reaction flush),
-// 3 as 2 but the queue lane-major and the i side segment-summed per batch
-// (plain shared adds): mode 2's fp64 CAS loops retried ~5 times per batch
-// (rotation-major batches of a sparse block repeat the few busy i particles)
-// and drew 16 % of the kernel's stall samples.
-// c2 at 256: mode 0 67.0 ms, mode 1 63.4 ms, mode 2 63.0 ms (61.4 with the
-// 16-byte record loads), mode 3 58.9 ms; c3 117.9 -> 115.6, c5 70.8 -> 66.8.
-#ifndef SEWALD_SYM_POOL_MODE
-#define SEWALD_SYM_POOL_MODE 3
+// Rotation steps of denser blocks with fewer than SEWALD_SYM_SPLIT active
+// lanes are pooled too (0 = off): 6 / 9 / 12 lanes measured c2 58.2 / 58.3 /
+// 58.4, c3 108.7 / 108.4 / 107.9, c5 66.0 / 65.7 / 65.6 against 56.7 / 108.2 /
+// 64.4 ms without (4 more registers, and the pooled pair costs ~2.5 lane-slots).
+#ifndef SEWALD_SYM_SPLIT
+#define SEWALD_SYM_SPLIT 0
 #endif
+#define SEWALD_SYM_QMAX (SEWALD_SYM_POOL > 32 * SEWALD_SYM_SPLIT ? SEWALD_SYM_POOL : 32 * SEWALD_SYM_SPLIT)
+// Pooled pairs: history at c2 (pool threshold 256). Both sides with shared
+// fp64 atomics (CAS loops; j side in the block's reaction slots) 67.0 ms; both
+// sides with global fp64 RED 63.4; i side shared CAS, j side global RED 63.0
+// (61.4 with the 16-byte record loads) — there the CAS loops retried ~5 times
+// per batch (rotation-major batches of a sparse block repeat the few busy i
+// particles) and drew 16 % of the kernel's stall samples; lane-major queue
+// with the segmented i-side sum (below) 58.9 (c3 117.9 -> 115.6, c5 70.8 ->
+// 66.8). Pooling whole blocks whose rotation steps would be < 40 / 55 / 70 %
+// occupied: c2 58.4 / 59.8 / 63.3 against 58.2 ms (threshold only).
 // j-block records loaded with 16-byte loads (c2 62.9 -> 61.3 ms, c3 118.9 ->
 // 117.9, c5 72.4 -> 71.1 against 8-byte loads). A fully coalesced block load
 // (lane l reading chunks l, l + 32, ... and scattering the fields) measured
@@ -267,10 +272,10 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
 #if SEWALD_SYM_POOL > 0
     // sparse-block pool (see below): the cluster's records, its pooled
     // i-side sums and the block's candidate queue, per warp
-    constexpr int IS = (3 + NS + 1) | 1;  // odd stride (in doubles): random il hit distinct banks; last: index
+    constexpr int IS = (3 + NS) | 1;  // odd stride (in doubles): random il hit distinct banks
     __shared__ double irec_all[SYM_WARPS][32][IS];
     __shared__ double ipool_all[SYM_WARPS][32][3];
-    __shared__ unsigned short queue_all[SYM_WARPS][SEWALD_SYM_POOL];
+    __shared__ unsigned short queue_all[SYM_WARPS][SEWALD_SYM_QMAX];
 #endif
     for (int t = threadIdx.x; t < 32 * SEWALD_EXP_REP; t += SYM_THREADS) exp_tab_rep[t] = c_exp2_tab32[t / SEWALD_EXP_REP];
     __syncthreads();
@@ -284,7 +289,6 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     double(*irec)[IS] = irec_all[warp];
     double(*ipool)[3] = ipool_all[warp];
     unsigned short* queue = queue_all[warp];
-    const unsigned lanemask_lt = (1u << lane) - 1u;
 #endif
     unsigned long long npairs = 0;  // flushed per cluster from the 32-bit step counter
     // Persistent warps: clusters are taken from a global counter, so the
@@ -321,7 +325,6 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     irec[lane][2] = xa2;
 #pragma unroll
     for (int c = 0; c < NS; ++c) irec[lane][3 + c] = fa[c];
-    irec[lane][IS - 1] = __longlong_as_double(valid ? ida : 0);
     ipool[lane][0] = ipool[lane][1] = ipool[lane][2] = 0.0;
     __syncwarp();
 #endif
@@ -466,23 +469,46 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                     }
                     unsigned steps = __reduce_or_sync(0xffffffffu, m);
                     bool coincident = false;
-                    bool pooled = false;
 #if SEWALD_SYM_POOL > 0
-                    // Sparse block (few candidates, spread over many rotations): the
-                    // rotation steps would run mostly idle lanes. Its candidate pairs
-                    // are queued instead (rotation-major, so a batch rarely repeats a
-                    // particle) and evaluated 32 at a time, one pair per lane; both
-                    // sides accumulate with shared-memory atomics (i side: the
-                    // cluster's pool, added to the lane sums at the end; j side: the
-                    // block's reaction slots, flushed as for the rotation steps).
-                    const int ncand = __reduce_add_sync(0xffffffffu, __popc(m));
-                    pooled = ncand < SEWALD_SYM_POOL;
-                    if (pooled) {
-#if SEWALD_SYM_POOL_MODE == 3
-                        // lane-major queue: each i particle's pairs are consecutive,
-                        // so a batch holds runs of equal il (segment-summed below)
+                    // Pooled pairs: every pair of a sparse block (fewer than
+                    // SEWALD_SYM_POOL candidates, spread over many rotations) and, in
+                    // denser blocks, the pairs of rotation steps with fewer than
+                    // SEWALD_SYM_SPLIT active lanes: those steps would run mostly
+                    // idle lanes. The pairs are queued lane-major (each i particle's
+                    // pairs consecutive) and evaluated 32 at a time, one pair per
+                    // lane: the i side is summed over each batch's runs of equal i
+                    // particle (one plain shared add per run into the cluster's pool,
+                    // added to the lane sums at the end), the j side goes to global
+                    // memory with fp64 RED.
+                    unsigned mp = m;
+                    int np = __reduce_add_sync(0xffffffffu, __popc(m));
+                    if (np >= SEWALD_SYM_POOL) {
+#if SEWALD_SYM_SPLIT > 0
+                        // active lanes per rotation step: 32 x 32 bit transpose of the
+                        // masks (lane k ends up with the lane bits of step 31 - k)
+                        unsigned x = m, msk = 0x0000FFFFu;
+#pragma unroll
+                        for (int jj = 16; jj > 0; jj >>= 1, msk ^= msk << jj) {
+                            const unsigned y = __shfl_xor_sync(0xffffffffu, x, jj);
+                            if (lane & jj)
+                                x ^= ((y ^ (x >> jj)) & msk) << jj;
+                            else
+                                x ^= (x ^ (y >> jj)) & msk;
+                        }
+                        const unsigned sparse =
+                            __brev(__ballot_sync(0xffffffffu, __popc(x) < SEWALD_SYM_SPLIT)) & steps;
+                        mp = m & sparse;
+                        np = sparse ? __reduce_add_sync(0xffffffffu, __popc(mp)) : 0;
+                        steps &= ~sparse;
+#else
+                        np = 0;
+#endif
+                    } else {
+                        steps = 0u;  // the rotation loop below has nothing left
+                    }
+                    if (np > 0) {
                         {
-                            const int cntm = __popc(m);
+                            const int cntm = __popc(mp);
                             int off = cntm;
 #pragma unroll
                             for (int d = 1; d < 32; d <<= 1) {
@@ -490,31 +516,17 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                                 if (lane >= d) off += t;
                             }
                             off -= cntm;
-                            unsigned mm = m;
+                            unsigned mm = mp;
                             while (mm) {
                                 const int s = __ffs(mm) - 1;
                                 mm &= mm - 1u;
                                 queue[off++] = (unsigned short)((lane << 5) | ((lane + s) & 31));
                             }
                         }
-#else
-                        int base = 0;
-                        unsigned st = steps;
-                        while (st) {
-                            const int s = 31 - __clz(st);
-                            st ^= 1u << s;
-                            const bool on = (m >> s) & 1u;
-                            const unsigned act = __ballot_sync(0xffffffffu, on);
-                            if (on)
-                                queue[base + __popc(act & lanemask_lt)] =
-                                    (unsigned short)((lane << 5) | ((lane + s) & 31));
-                            base += __popc(act);
-                        }
-#endif
                         __syncwarp();
-                        for (int k0 = 0; k0 < ncand; k0 += 32) {
+                        for (int k0 = 0; k0 < np; k0 += 32) {
                             const int k = k0 + lane;
-                            const bool in = k < ncand;
+                            const bool in = k < np;
                             const int e = in ? queue[k] : 0;
                             const int il = e >> 5, j = e & 31;
                             const double* ir = irec[il];
@@ -523,77 +535,37 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
 #pragma unroll
                             for (int c = 0; c < NS; ++c) fi[c] = ir[3 + c];
                             SlotEval<KIND, NS, SHORT> ev;
-                            double* rec = jrec[j];
-                            slot_eval<KIND, RS, NS, SHORT>(ev, rec, ys0, ys1, ys2, in, rc2, a.xi, xi2, exp_tab,
+                            slot_eval<KIND, RS, NS, SHORT>(ev, jrec[j], ys0, ys1, ys2, in, rc2, a.xi, xi2, exp_tab,
                                                           coincident);
-#if SEWALD_SYM_POOL_MODE == 3
-                            {
-                                // i side: segmented sum over the batch's runs of equal il
-                                // (one plain shared add per run, no CAS loops); j side:
-                                // global fp64 RED
-                                double ui[3] = {0.0, 0.0, 0.0};
-                                if (ev.acc) {
-                                    double uj[3] = {0.0, 0.0, 0.0};
-                                    pair_apply<KIND, false>(ev.c, ev.r0, ev.r1, ev.r2, ev.sj, ui);
-                                    pair_apply<KIND, true>(ev.c, ev.r0, ev.r1, ev.r2, fi, uj);
-                                    double* dj = u + 3 * jid[j];
-#pragma unroll
-                                    for (int c = 0; c < 3; ++c) atomicAdd(dj + c, uj[c]);
-                                    npairs32 += 2u;
-                                }
-                                const unsigned same = __match_any_sync(0xffffffffu, in ? il : 32 + lane);
-                                const int first = __ffs(same) - 1;
-                                const int runmax = __reduce_max_sync(0xffffffffu, __popc(same));
-                                for (int d = 1; d < runmax; d <<= 1) {
-#pragma unroll
-                                    for (int c = 0; c < 3; ++c) {
-                                        const double t = __shfl_up_sync(0xffffffffu, ui[c], d);
-                                        if (lane - d >= first) ui[c] += t;
-                                    }
-                                }
-                                if (in && lane == 31 - __clz(same)) {
-#pragma unroll
-                                    for (int c = 0; c < 3; ++c) ipool[il][c] += ui[c];
-                                }
-                                __syncwarp();
-                            }
-                            if (false) {
-#else
+                            double ui[3] = {0.0, 0.0, 0.0};
                             if (ev.acc) {
-#endif
-                                double ui[3] = {0.0, 0.0, 0.0}, uj[3] = {0.0, 0.0, 0.0};
+                                double uj[3] = {0.0, 0.0, 0.0};
                                 pair_apply<KIND, false>(ev.c, ev.r0, ev.r1, ev.r2, ev.sj, ui);
                                 pair_apply<KIND, true>(ev.c, ev.r0, ev.r1, ev.r2, fi, uj);
-#if SEWALD_SYM_POOL_MODE == 1
-                                // global fp64 RED on both sides (no shared-memory CAS loops)
-                                double* di = u + 3 * __double_as_longlong(irec[il][IS - 1]);
                                 double* dj = u + 3 * jid[j];
 #pragma unroll
-                                for (int c = 0; c < 3; ++c) {
-                                    atomicAdd(di + c, ui[c]);
-                                    atomicAdd(dj + c, uj[c]);
-                                }
-#elif SEWALD_SYM_POOL_MODE == 2
-                                // i side: the cluster's shared pool; j side: global fp64 RED
-                                double* dj = u + 3 * jid[j];
-#pragma unroll
-                                for (int c = 0; c < 3; ++c) {
-                                    atomicAdd(&ipool[il][c], ui[c]);
-                                    atomicAdd(dj + c, uj[c]);
-                                }
-#else
-#pragma unroll
-                                for (int c = 0; c < 3; ++c) {
-                                    atomicAdd(&ipool[il][c], ui[c]);
-                                    atomicAdd(&rec[RO + c], uj[c]);
-                                }
-#endif
+                                for (int c = 0; c < 3; ++c) atomicAdd(dj + c, uj[c]);
                                 npairs32 += 2u;
                             }
+                            const unsigned same = __match_any_sync(0xffffffffu, in ? il : 32 + lane);
+                            const int first = __ffs(same) - 1;
+                            const int runmax = __reduce_max_sync(0xffffffffu, __popc(same));
+                            for (int d = 1; d < runmax; d <<= 1) {
+#pragma unroll
+                                for (int c = 0; c < 3; ++c) {
+                                    const double t = __shfl_up_sync(0xffffffffu, ui[c], d);
+                                    if (lane - d >= first) ui[c] += t;
+                                }
+                            }
+                            if (in && lane == 31 - __clz(same)) {
+#pragma unroll
+                                for (int c = 0; c < 3; ++c) ipool[il][c] += ui[c];
+                            }
+                            __syncwarp();
                         }
-                        steps = 0u;  // the rotation loop below has nothing left
                     }
 #endif
+                    const bool rotated = steps != 0u;  // reaction slots written: flush below
 #if SEWALD_SYM_ILP == 2
                     // Two steps in flight per lane: their scalar math is independent
                     // (hides the fp64 dependency latency); the reactions are applied
@@ -736,7 +708,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                     }
                     if (coincident) atomicExch(err, 1);
                     __syncwarp();
-                    if (lane < cnt && !(SEWALD_SYM_POOL_MODE != 0 && pooled)) {
+                    if (rotated && lane < cnt) {
                         double* dst = u + 3 * jid[lane];
                         atomicAdd(dst, jrec[lane][RO]);
                         atomicAdd(dst + 1, jrec[lane][RO + 1]);
