@@ -158,7 +158,11 @@ enum {
                                      registers: 2 every width (default), 1 only 20 < P <= 32, 0 never
                                      (shared-memory region tiles for P <= 20, z-sweep above) */
     SEWALD_OPT_GATHER_FUSED = 11, /* register-A gather tiles: 1 taps evaluated in the kernel, 0 taps array */
-    SEWALD_OPT_COUNT = 12
+    SEWALD_OPT_SPREAD_SORT = 12,  /* tensor-core spread tiles (P <= 20): 1 points of a tile ordered by their
+                                     (x, y) stencil offset and MMA steps that cannot reach a row block
+                                     skipped, 0 tile order only */
+    SEWALD_OPT_GATHER_SORT = 13,  /* register-A gather tiles: the same ordering and skipping for targets */
+    SEWALD_OPT_COUNT = 14
 };
 int sewald_gpu_set_option(int which, int value);
 int sewald_gpu_get_option(int which, int* value);

@@ -308,6 +308,8 @@ class KernelOption(enum.IntEnum):
     SPREAD_FUSED = 9    # 1 tensor-core spread tiles evaluate their taps in the kernel
     GATHER_WIDE = 10    # register-A gather tiles: 2 every width, 1 only 20 < P <= 32, 0 never
     GATHER_FUSED = 11   # register-A gather tiles evaluate their taps in the kernel
+    SPREAD_SORT = 12    # tensor-core spread tiles: points ordered by (x, y) offset, unreachable MMA steps skipped
+    GATHER_SORT = 13    # register-A gather tiles: the same for targets
 
 
 def get_kernel_option(which: KernelOption) -> int:

@@ -419,6 +419,7 @@ void ensure_spread_order(sewald_gpu_session* s, int64_t i0, int64_t i1) {
     s->sp_order.ensure(sizeof(uint32_t) * std::max<int64_t>(n, 1));
     s->sp_off.ensure(sizeof(int64_t) * (nb + 1));
     int* bad = s->flags.as<int>() + FLAG_SPREAD_BOX;
+    const int sub = s->sp_mode == 2 ? s->sm_shape.sub : 0;
     if (s->sp_mode == 2)
         launch_spread_mma_bucket(s->g, s->p.P, s->sm_shape, s->x.as<double>() + 3 * i0, n, s->sp_keys.as<uint32_t>(),
                                  s->sp_vals.as<uint32_t>(), bad, st);
@@ -435,9 +436,9 @@ void ensure_spread_order(sewald_gpu_session* s, int64_t i0, int64_t i1) {
                    "point too close to the extended box boundary; free-direction padding is too small");
     if (n > 0) {
         sort_pairs(s, s->sp_keys.as<uint32_t>(), s->sp_keys2.as<uint32_t>(), s->sp_vals.as<uint32_t>(),
-                   s->sp_order.as<uint32_t>(), n, bits_for((uint64_t)nb + 1));
+                   s->sp_order.as<uint32_t>(), n, bits_for((uint64_t)nb + 1) + sub);
     }
-    launch_bucket_offsets(s->sp_keys2.as<uint32_t>(), n, (int)nb, s->sp_off.as<int64_t>(), st);
+    launch_bucket_offsets(s->sp_keys2.as<uint32_t>(), n, (int)nb, s->sp_off.as<int64_t>(), st, sub);
     ++s->ctx->launches;
     s->sp_i0 = i0;
     s->sp_i1 = i1;

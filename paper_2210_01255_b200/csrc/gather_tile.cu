@@ -29,10 +29,10 @@ constexpr int GT_PMAX = 16;
 
 __global__ void tile_bucket_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, const double* __restrict__ x,
                                    int64_t N, uint32_t* __restrict__ keys, uint32_t* __restrict__ vals,
-                                   int* __restrict__ bad) {
+                                   int* __restrict__ bad, int sub) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= N) return;
-    int t[3];
+    int t[3], l[3];
     const int nt[3] = {ntx, nty, ntz};
     for (int ax = 0; ax < 3; ++ax) {
         int j0;
@@ -45,8 +45,13 @@ __global__ void tile_bucket_kernel(DevGrid g, int P, int B, int ntx, int nty, in
             j0 = 0;
         }
         t[ax] = min(j0 / B, nt[ax] - 1);
+        l[ax] = min(j0 - t[ax] * B, 7);
     }
-    keys[i] = (uint32_t)(((int64_t)t[0] * nty + t[1]) * ntz + t[2]);
+    // sub = 6: the low bits order a tile's points by the (x, y) offset of their
+    // stencil start inside the tile (the spread skips MMA steps whose points
+    // cannot reach a row block)
+    const uint32_t lo = sub ? (uint32_t)((l[0] << 3) | l[1]) : 0u;
+    keys[i] = ((uint32_t)(((int64_t)t[0] * nty + t[1]) * ntz + t[2]) << sub) | lo;
     vals[i] = (uint32_t)i;
 }
 
@@ -568,10 +573,10 @@ TileShape tile_shape(const DevGrid& g, int P, int64_t Nt) {
 }
 
 void launch_tile_bucket(const DevGrid& g, int P, const TileShape& s, const double* x, int64_t N, uint32_t* keys,
-                        uint32_t* vals, int* bad, cudaStream_t st) {
+                        uint32_t* vals, int* bad, cudaStream_t st, int sub) {
     if (N == 0) return;
     tile_bucket_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], x, N,
-                                                                     keys, vals, bad);
+                                                                     keys, vals, bad, sub);
 }
 
 bool gather_tile_fused_ok(const TileShape& s) {

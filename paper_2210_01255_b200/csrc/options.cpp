@@ -54,6 +54,12 @@ int env_default(int which) {
         case SEWALD_OPT_GATHER_FUSED:
             e = env("SEWALD_GATHER_FUSED");
             return (e && e[0] == '1') ? 1 : 0;
+        case SEWALD_OPT_SPREAD_SORT:
+            e = env("SEWALD_SPREAD_SORT");
+            return (e && e[0] == '0') ? 0 : 1;
+        case SEWALD_OPT_GATHER_SORT:
+            e = env("SEWALD_GATHER_SORT");
+            return (e && e[0] == '0') ? 0 : 1;
     }
     return 0;
 }
@@ -72,6 +78,8 @@ bool valid(int which, int v) {
         case SEWALD_OPT_SPREAD_FUSED: return v == 0 || v == 1;
         case SEWALD_OPT_GATHER_WIDE: return v >= 0 && v <= 2;
         case SEWALD_OPT_GATHER_FUSED: return v == 0 || v == 1;
+        case SEWALD_OPT_SPREAD_SORT: return v == 0 || v == 1;
+        case SEWALD_OPT_GATHER_SORT: return v == 0 || v == 1;
     }
     return false;
 }

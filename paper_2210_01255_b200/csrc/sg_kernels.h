@@ -48,7 +48,7 @@ struct TileShape {
 // Nt: number of targets (tile size choice for dense targets)
 TileShape tile_shape(const DevGrid& g, int P, int64_t Nt = 0);
 void launch_tile_bucket(const DevGrid& g, int P, const TileShape& s, const double* x, int64_t N, uint32_t* keys,
-                        uint32_t* vals, int* bad, cudaStream_t st);
+                        uint32_t* vals, int* bad, cudaStream_t st, int sub = 0);
 void launch_gather_tile(const DevGrid& g, int P, const TileShape& s, const double* W, const int4* SW,
                         const int64_t* off, int part, int nparts, const double* grid, double h3, int accumulate,
                         double* u, cudaStream_t st);
@@ -67,6 +67,7 @@ struct SpreadMmaShape {
     int nt[3];
     int64_t ntiles;
     bool ok;
+    int sub;  // low key bits ordering a tile's points by their (x, y) stencil offset (0 or 6)
 };
 SpreadMmaShape spread_mma_shape(const DevGrid& g, int P);
 void launch_spread_mma_bucket(const DevGrid& g, int P, const SpreadMmaShape& s, const double* x, int64_t N,

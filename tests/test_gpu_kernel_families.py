@@ -168,6 +168,8 @@ def test_partition_kernel_choice_consistent(S):
 SPREAD_FAMILIES = {
     "mma": dict(SPREAD_MMA=1, SPREAD_SWEEP=-1),
     "mma_taps_kernel": dict(SPREAD_MMA=1, SPREAD_SWEEP=-1, SPREAD_FUSED=0),
+    "mma_unsorted": dict(SPREAD_MMA=1, SPREAD_SWEEP=-1, SPREAD_SORT=0),
+    "mma_taps_unsorted": dict(SPREAD_MMA=1, SPREAD_SWEEP=-1, SPREAD_FUSED=0, SPREAD_SORT=0),
     "mma_rowsweep": dict(SPREAD_MMA=1, SPREAD_SWEEP=-1, SPREAD_ROWSWEEP=1),
     "mma_L19": dict(SPREAD_MMA=1, SPREAD_MMA_L=19, SPREAD_SWEEP=-1),
     "mma_pergroup": dict(SPREAD_MMA=1, SPREAD_CACHED=0, SPREAD_SWEEP=-1),

@@ -1,4 +1,5 @@
-for c in 2 3 5; do for v in var_s6 var_s9 var_s12 MAIN var_s6 var_s9 var_s12 MAIN; do
-  if [ $v = MAIN ]; then L=paper_2210_01255_b200/lib/libsewald_gpu.so; else L=paper_2210_01255_b200/lib/$v/libsewald_gpu.so; fi
-  echo "c$c $v $(SEWALD_LIB=$L timeout 300 python tools/rs_time.py $c 7 2>&1 | tail -1)"
-done; done
+# A/B timing of variant builds (see tools/README.md)
+for c in 2 3; do
+  python tools/sg_time.py $c 7 "" SPREAD_SORT=0
+  SEWALD_LIB=paper_2210_01255_b200/lib/var_base/libsewald_gpu.so python tools/sg_time.py $c 7 ""
+done
