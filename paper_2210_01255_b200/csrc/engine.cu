@@ -555,16 +555,22 @@ int ensure_gather_order(sewald_gpu_session* s, int part, int nparts) {
     s->tg_w.ensure(sizeof(double) * 3 * s->p.P * n);
     s->tg_sw.ensure(sizeof(int4) * n);
     int* bad = s->flags.as<int>() + FLAG_GATHER_BOX;
+    // register-A tiles: a tile's targets ordered by their x stencil offset (n-blocks skip rows they cannot reach)
+    const int sub = (mode == 2 && gather_tile_regA(ts) && option(SEWALD_OPT_GATHER_SORT) != 0 &&
+                     ts.ntiles < (int64_t(1) << 26))
+                        ? 6
+                        : 0;
     if (mode == 1)
         launch_sweep_bucket(s->g, s->p.P, xt, Nt, sh, s->tg_keys.as<uint32_t>(), s->tg_vals.as<uint32_t>(), bad, st);
     else
-        launch_tile_bucket(s->g, s->p.P, ts, xt, Nt, s->tg_keys.as<uint32_t>(), s->tg_vals.as<uint32_t>(), bad, st);
+        launch_tile_bucket(s->g, s->p.P, ts, xt, Nt, s->tg_keys.as<uint32_t>(), s->tg_vals.as<uint32_t>(), bad, st,
+                           sub);
     check_flag(s, FLAG_GATHER_BOX, SEWALD_EINVAL,
                "point too close to the extended box boundary; free-direction padding is too small");
     if (Nt > 0)
         sort_pairs(s, s->tg_keys.as<uint32_t>(), s->tg_keys2.as<uint32_t>(), s->tg_vals.as<uint32_t>(),
-                   s->tg_order.as<uint32_t>(), Nt, bits_for((uint64_t)nkeys + 1));
-    launch_bucket_offsets(s->tg_keys2.as<uint32_t>(), Nt, (int)nkeys, s->tg_off.as<int64_t>(), st);
+                   s->tg_order.as<uint32_t>(), Nt, bits_for((uint64_t)nkeys + 1) + sub);
+    launch_bucket_offsets(s->tg_keys2.as<uint32_t>(), Nt, (int)nkeys, s->tg_off.as<int64_t>(), st, sub);
     s->ctx->launches += 2;
     s->tg_ready = true;
     s->tg_mode = mode;

@@ -335,6 +335,10 @@ gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
 // the L^3 region does not fit in shared memory: c4 17.3 -> 9.1 ms against the
 // z-sweep; for L = 19 / 23 it beats the shared-region kernel above too
 // (c2 3.68 -> 3.24 ms, c3 5.62 -> 4.50, c5 13.8 -> 11.9).
+// With a tile's targets ordered by their x stencil offset
+// (SEWALD_OPT_GATHER_SORT) each row block visits only the n-blocks whose x
+// windows reach it (and loads no A fragments when none does): c2 2.90 ->
+// 2.84 ms, c3 4.35 -> 3.71, c4 9.12 -> 7.94, c5 10.62 -> 9.81.
 #ifndef SEWALD_WG_TMAX
 #define SEWALD_WG_TMAX 64
 #endif
@@ -377,6 +381,9 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
     int* rowoff = reinterpret_cast<int*>(part + MM_WARPS * WG_TMAX);  // [ROWS]
     int* zoff = rowoff + ROWS;                                      // [LS]
     int* tid = zoff + LS;                                           // [WG_TMAX]
+    int* ox = tid + WG_TMAX;                                        // [WG_TMAX] x offset of each target
+    int* nbmin = ox + WG_TMAX;                                      // [LS] first / last n-block reaching row a
+    int* nbmax = nbmin + LS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
     for (int row = threadIdx.x; row < ROWS; row += MM_THREADS) {
@@ -399,6 +406,10 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
         const int T = (int)min((int64_t)WG_TMAX, p1 - q0);
         const int nblk = (T + 7) / 8;
         __syncthreads();
+        if (threadIdx.x < LS) {
+            nbmin[threadIdx.x] = 1 << 20;
+            nbmax[threadIdx.x] = -1;
+        }
         if (FUSED) {
             for (int e = threadIdx.x; e < nblk * 8 * LS; e += MM_THREADS) wz[e] = 0.0;
             for (int e = threadIdx.x; e < LS * WG_TMAX; e += MM_THREADS) {
@@ -415,6 +426,7 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
                 stencil_origin(g, P, ax, ftg->x[3 * i + ax], j0, rel);
                 const int sw = ax < g.d ? wrap_index(j0, g.n[ax]) : j0;
                 const int o = sw - (ax == 0 ? X0 : (ax == 1 ? Y0 : Z0));
+                if (ax == 0) ox[t] = o;
                 for (int p = 0; p < P; ++p) {
                     const double v = window_eval(ftg->win, ((double)(j0 + p) - rel) * g.h);
                     const int k = o + p;
@@ -440,7 +452,25 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
                 wx[k * WG_TMAX + t] = vx;
                 wy[k * WG_TMAX + t] = vy;
             }
-            if (lane == 0) tid[t] = sw.w;
+            if (lane == 0) {
+                tid[t] = sw.w;
+                if (t < T) ox[t] = sw.x - X0;
+            }
+        }
+        __syncthreads();
+        // n-blocks (8 targets) whose x windows reach region row a: a contiguous
+        // range when the targets are ordered by x offset (SEWALD_OPT_GATHER_SORT),
+        // a conservative cover otherwise
+        for (int nb = threadIdx.x; nb < nblk; nb += MM_THREADS) {
+            int lo = 1 << 20, hi = -(1 << 20);
+            for (int t = 8 * nb; t < min(8 * nb + 8, T); ++t) {
+                lo = min(lo, ox[t]);
+                hi = max(hi, ox[t] + P - 1);
+            }
+            for (int a = max(lo, 0); a <= min(hi, MM_L - 1); ++a) {
+                atomicMin(&nbmin[a], nb);
+                atomicMax(&nbmax[a], nb);
+            }
         }
         __syncthreads();
         for (int c = 0; c < 3; ++c) {
@@ -450,6 +480,9 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
             for (int nb = 0; nb < NBMAX; ++nb) acc[nb][0] = acc[nb][1] = 0.0;
             const int tcol = 2 * (lane & 3);
             for (int rb = warp; rb < RB; rb += MM_WARPS) {
+                const int a_lo = (rb * 8) / MM_L, a_hi = min(rb * 8 + 7, ROWS - 1) / MM_L;
+                const int nb_lo = min(nbmin[a_lo], nbmin[a_hi]), nb_hi = max(nbmax[a_lo], nbmax[a_hi]);
+                if (nb_lo > nb_hi) continue;  // no target of the chunk reaches these rows
                 const int row_a = rb * 8 + (lane >> 2);
                 const int ro = row_a < ROWS ? rowoff[row_a] : -1;
                 double af[KS];
@@ -461,7 +494,7 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
                 const int a = row_a / MM_L, b = row_a - a * MM_L;  // rows >= L*L: a >= L (zero taps)
 #pragma unroll
                 for (int nb = 0; nb < NBMAX; ++nb) {
-                    if (nb < nblk) {
+                    if (nb >= nb_lo && nb <= nb_hi) {
                         double d0 = 0.0, d1 = 0.0;
 #pragma unroll
                         for (int ks = 0; ks < KS; ++ks)
@@ -521,7 +554,7 @@ void launch_wide_fused(const DevGrid& g, int P, const TileShape& s, int64_t t0, 
 size_t wide_smem_bytes(int L) {
     const int LS = (L + 4) & ~3;
     return sizeof(double) * ((size_t)3 * WG_TMAX * LS + MM_WARPS * WG_TMAX) +
-           sizeof(int) * ((size_t)L * L + LS + WG_TMAX);
+           sizeof(int) * ((size_t)L * L + 3 * LS + 2 * WG_TMAX);
 }
 
 size_t mma_smem_bytes(int L, int MM_TMAX) {
@@ -577,6 +610,10 @@ void launch_tile_bucket(const DevGrid& g, int P, const TileShape& s, const doubl
     if (N == 0) return;
     tile_bucket_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], x, N,
                                                                      keys, vals, bad, sub);
+}
+
+bool gather_tile_regA(const TileShape& s) {
+    return s.ok && (s.L >= 31 || (option(SEWALD_OPT_GATHER_WIDE) == 2 && (s.L == 15 || s.L == 19 || s.L == 23)));
 }
 
 bool gather_tile_fused_ok(const TileShape& s) {

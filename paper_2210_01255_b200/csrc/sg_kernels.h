@@ -55,6 +55,8 @@ void launch_gather_tile(const DevGrid& g, int P, const TileShape& s, const doubl
 // Register-A tensor-core gather tiles with the taps evaluated in the kernel
 // (no taps array); arg_dev: fused_tgt_bytes() of device scratch.
 bool gather_tile_fused_ok(const TileShape& s);
+// the tiles run the register-A tensor-core kernel (gather_wide_mma_kernel)
+bool gather_tile_regA(const TileShape& s);
 size_t fused_tgt_bytes();
 void launch_gather_tile_fused(const DevGrid& g, const DevWindow& w, int P, const TileShape& s, const double* xt,
                               const uint32_t* order, const int64_t* off, int part, int nparts, const double* grid,

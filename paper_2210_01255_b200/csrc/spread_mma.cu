@@ -358,7 +358,9 @@ spread_tile_mma_cached_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz
     }
 }
 
-// Wide windows (20 < P <= 32, e.g. the Gaussian window of c4 at P = 32):
+// Wide windows (20 < P <= 32, e.g. the Gaussian window of c4 at P = 32;
+// with SEWALD_OPT_SPREAD_SORT each row block visits only the k-steps that
+// reach it, c4 9.55 -> 8.50 ms):
 // B = 8, region L = P + 7 <= 39, z padded to LS = 40 (5 n-blocks). The whole
 // tile's source tables stay in shared memory (up to WT_TMAX sources per pass),
 // each warp owns whole row blocks and sweeps all sources for them with every
@@ -393,6 +395,9 @@ spread_tile_mma_wide_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, 
     double(*wx)[WT_LS] = reinterpret_cast<double(*)[WT_LS]>(wsm + WT_TMAX * WT_LS);      // wx_t(a)
     double(*wy)[WT_LS] = reinterpret_cast<double(*)[WT_LS]>(wsm + 2 * WT_TMAX * WT_LS);  // wy_t(b)
     double(*wz)[WT_LS] = reinterpret_cast<double(*)[WT_LS]>(wsm + 3 * WT_TMAX * WT_LS);  // wz_t(z)
+    int* ox = reinterpret_cast<int*>(wsm + 4 * WT_TMAX * WT_LS);  // [WT_TMAX] x offset of each point
+    int* kmin = ox + WT_TMAX;                                      // [WT_LS] first / last k-step reaching row a
+    int* kmax = kmin + WT_LS;
 
     const int64_t tile = tile0 + blockIdx.x;
     const int64_t p0 = off[tile], p1 = off[tile + 1];
@@ -408,9 +413,14 @@ spread_tile_mma_wide_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, 
         const int T = (int)min((int64_t)WT_TMAX, p1 - q0);
         const int T4 = (T + 3) & ~3;
         __syncthreads();
+        if (threadIdx.x < WT_LS) {
+            kmin[threadIdx.x] = 1 << 20;
+            kmax[threadIdx.x] = -1;
+        }
         for (int t = warp; t < T4; t += WT_WARPS) {
             int4 sw = make_int4(0, 0, 0, 0);
             if (t < T) sw = SW[q0 + t];
+            if (lane == 0 && t < T) ox[t] = sw.x - X0;
             for (int k = lane; k < WT_LS; k += 32) {
                 double vx = 0.0, vy = 0.0, vz = 0.0;
                 if (t < T && k < L) {
@@ -423,6 +433,20 @@ spread_tile_mma_wide_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, 
                 wx[t][k] = vx;
                 wy[t][k] = vy;
                 wz[t][k] = vz;
+            }
+        }
+        __syncthreads();
+        // k-steps whose points' x windows reach region row a (contiguous when the
+        // points are ordered by x offset, SEWALD_OPT_SPREAD_SORT)
+        for (int k = threadIdx.x; k < T4 / 4; k += 32 * WT_WARPS) {
+            int lo = 1 << 20, hi = -(1 << 20);
+            for (int q = 4 * k; q < min(4 * k + 4, T); ++q) {
+                lo = min(lo, ox[q]);
+                hi = max(hi, ox[q] + P - 1);
+            }
+            for (int a = max(lo, 0); a <= min(hi, L - 1); ++a) {
+                atomicMin(&kmin[a], k);
+                atomicMax(&kmax[a], k);
             }
         }
         for (int c = 0; c < C; ++c) {
@@ -439,7 +463,9 @@ spread_tile_mma_wide_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, 
                 double acc[NB][2];
 #pragma unroll
                 for (int nb = 0; nb < NB; ++nb) acc[nb][0] = acc[nb][1] = 0.0;
-                for (int ks = 0; ks < T4 / 4; ++ks) {
+                const int a_lo = (rb * 8) / L, a_hi = min(rb * 8 + 7, ROWS - 1) / L;
+                const int kb = min(kmin[a_lo], kmin[a_hi]), ke = max(kmax[a_lo], kmax[a_hi]);
+                for (int ks = kb; ks <= ke; ++ks) {
                     const int t = ks * 4 + (lane & 3);
                     const double af = wxf[t][a] * wy[t][b];
 #pragma unroll
@@ -479,6 +505,7 @@ SpreadMmaShape spread_mma_shape(const DevGrid& g, int P) {
         for (int ax = 0; ax < 3; ++ax) s.nt[ax] = (g.n[ax] + s.B - 1) / s.B;
         s.ntiles = (int64_t)s.nt[0] * s.nt[1] * s.nt[2];
         if (s.ntiles >= (int64_t(1) << 31)) s.ok = false;
+        s.sub = (option(SEWALD_OPT_SPREAD_SORT) != 0 && s.ntiles < (int64_t(1) << 26)) ? 6 : 0;
         return s;
     }
     // The region work is fixed by L (L^2 x 24 per 32 sources) while the sweep's
@@ -537,14 +564,14 @@ int launch_spread_mma(const DevGrid& g, int P, const SpreadMmaShape& s, const do
     for (int64_t a = 0; a < s.ntiles; a += (int64_t)1 << 30) {
         const int64_t n = std::min<int64_t>(s.ntiles - a, (int64_t)1 << 30);
         if (s.L > 23) {
-            const size_t sm = sizeof(double) * 4 * WT_TMAX * WT_LS;
+            const size_t sm = sizeof(double) * 4 * WT_TMAX * WT_LS + sizeof(int) * (WT_TMAX + 2 * WT_LS);
             auto kern = s.L <= 31 ? spread_tile_mma_wide_kernel<31>
                                   : (s.L <= 35 ? spread_tile_mma_wide_kernel<35> : spread_tile_mma_wide_kernel<39>);
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             kern<<<(unsigned)n, 32 * WT_WARPS, sm, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W, SW, STR, C, off,
                                                         out);
         } else if (option(SEWALD_OPT_SPREAD_ROWSWEEP)) {
-            const size_t sm = sizeof(double) * 4 * WT_TMAX * 24;
+            const size_t sm = sizeof(double) * 4 * WT_TMAX * 24 + sizeof(int) * (WT_TMAX + 2 * 24);
             auto kern = s.L == 23 ? spread_tile_mma_wide_kernel<23, 24, SEWALD_SPREAD_RS_WARPS, SEWALD_SPREAD_RS_MINB>
                                   : spread_tile_mma_wide_kernel<19, 24, SEWALD_SPREAD_RS_WARPS, SEWALD_SPREAD_RS_MINB>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);

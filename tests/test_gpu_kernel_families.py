@@ -171,6 +171,7 @@ SPREAD_FAMILIES = {
     "mma_unsorted": dict(SPREAD_MMA=1, SPREAD_SWEEP=-1, SPREAD_SORT=0),
     "mma_taps_unsorted": dict(SPREAD_MMA=1, SPREAD_SWEEP=-1, SPREAD_FUSED=0, SPREAD_SORT=0),
     "mma_rowsweep": dict(SPREAD_MMA=1, SPREAD_SWEEP=-1, SPREAD_ROWSWEEP=1),
+    "mma_rowsweep_unsorted": dict(SPREAD_MMA=1, SPREAD_SWEEP=-1, SPREAD_ROWSWEEP=1, SPREAD_SORT=0),
     "mma_L19": dict(SPREAD_MMA=1, SPREAD_MMA_L=19, SPREAD_SWEEP=-1),
     "mma_pergroup": dict(SPREAD_MMA=1, SPREAD_CACHED=0, SPREAD_SWEEP=-1),
     "sweep": dict(SPREAD_MMA=0, SPREAD_SWEEP=1),
@@ -186,6 +187,8 @@ GATHER_FAMILIES = {
     "tile_smem_region": dict(GATHER=2, GATHER_WIDE=0),
     "tile_fused_taps": dict(GATHER=2, GATHER_FUSED=1),
     "tile_regA_wide_only": dict(GATHER=2, GATHER_WIDE=1),
+    "tile_regA_unsorted": dict(GATHER=2, GATHER_SORT=0),
+    "tile_fused_unsorted": dict(GATHER=2, GATHER_FUSED=1, GATHER_SORT=0),
     "sweep_wide_off": dict(GATHER=-1, GATHER_WIDE=0),
 }
 
