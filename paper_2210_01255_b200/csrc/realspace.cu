@@ -31,7 +31,17 @@ namespace {
 
 constexpr int RS_THREADS = 128;
 constexpr int RS_WARPS = 4;
-constexpr int WCHUNK = 64;
+#ifndef SEWALD_RS_CHUNK
+#define SEWALD_RS_CHUNK 64
+#endif
+constexpr int WCHUNK = SEWALD_RS_CHUNK;  // 64 or 128 (mask path)
+// candidate sources of a chunk as a per-lane 64-bit mask (1) or a per-lane
+// byte queue in shared memory (0): c4 47.9 -> 43.2 ms (no per-candidate
+// stores in the fp32 pass, no queue reads in the fp64 pass; same pair order).
+// 128-source chunks (two masks) measured slower: 56.9 ms.
+#ifndef SEWALD_RS_MASK
+#define SEWALD_RS_MASK 1
+#endif
 
 __device__ __forceinline__ int floor_div(int a, int b) {
     int q = a / b;
@@ -148,9 +158,12 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
                  const double* __restrict__ tfolded, const uint32_t* __restrict__ torder, int64_t Nt,
                  double* __restrict__ u, int accumulate, unsigned long long* __restrict__ pair_count,
                  int* __restrict__ err, int split, double* __restrict__ scratch) {
-    __shared__ __align__(16) double src_all[RS_WARPS][WCHUNK * S];
-    __shared__ float4 srcf_all[RS_WARPS][WCHUNK];
-    __shared__ uint8_t queue_all[RS_WARPS][WCHUNK][32];
+    constexpr int CH = S > 8 ? 64 : WCHUNK;  // stresslet records: 64 (static shared-memory limit)
+    __shared__ __align__(16) double src_all[RS_WARPS][CH * S];
+    __shared__ float4 srcf_all[RS_WARPS][CH];
+#if !SEWALD_RS_MASK
+    __shared__ uint8_t queue_all[RS_WARPS][CH][32];
+#endif
     __shared__ double exp_tab[32];
     if (threadIdx.x < 32) exp_tab[threadIdx.x] = c_exp2_tab32[threadIdx.x];
     __syncthreads();
@@ -158,7 +171,9 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     double* src = src_all[warp];
     float4* srcf = srcf_all[warp];
+#if !SEWALD_RS_MASK
     uint8_t(*queue)[32] = queue_all[warp];
+#endif
 
     // work item = (32-target group, row part): small target sets split each
     // group's neighbour rows over `split` warps; the parts' sums are added in
@@ -244,17 +259,54 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
                 const bool primary = (sx == 0) && (sy == 0) && (sz == 0);
                 // fp32 image of this target relative to the row piece's shift
                 const float tf0 = (float)(xt0 - shx), tf1 = (float)(xt1 - shy), tf2 = (float)(xt2 - shz);
-                for (int64_t base = b0; base < b1; base += WCHUNK) {
-                    const int cnt = (int)min((int64_t)WCHUNK, b1 - base);
+                for (int64_t base = b0; base < b1; base += CH) {
+                    const int cnt = (int)min((int64_t)CH, b1 - base);
                     __syncwarp();
                     {
                         const double2* g2 = reinterpret_cast<const double2*>(packed + base * S);
                         double2* s2 = reinterpret_cast<double2*>(src);
                         for (int e = lane; e < cnt * (S / 2); e += 32) s2[e] = __ldg(g2 + e);
+#if SEWALD_RS_MASK
+                        // slots past the chunk: far away in fp32 (never candidates)
+                        for (int e = lane; e < CH; e += 32)
+                            srcf[e] = e < cnt ? __ldg(packedf + base + e) : make_float4(1e30f, 1e30f, 1e30f, 0.0f);
+#else
                         for (int e = lane; e < cnt; e += 32) srcf[e] = __ldg(packedf + base + e);
+#endif
                     }
                     __syncwarp();
                     if (!valid) continue;
+#if SEWALD_RS_MASK
+                    // Pass 1 (fp32, conservative): this lane's candidate sources as a
+                    // 64-bit mask (no per-candidate stores; slots past cnt are far away).
+                    constexpr int NM = CH / 64;
+                    unsigned long long cm[NM];
+                    const int cnt8 = (cnt + 7) & ~7;
+#pragma unroll
+                    for (int h = 0; h < NM; ++h) {
+                        cm[h] = 0ull;
+                        const int kend = min(cnt8 - 64 * h, 64);
+#pragma unroll 8
+                        for (int kk = 0; kk < kend; ++kk) {
+                            const float4 q = srcf[64 * h + kk];
+                            const float d0 = tf0 - q.x, d1 = tf1 - q.y, d2 = tf2 - q.z;
+                            const float dd = fmaf(d2, d2, fmaf(d1, d1, d0 * d0));
+                            cm[h] |= (unsigned long long)(dd < a.thresh_f) << kk;
+                        }
+                    }
+                    // Pass 2 (fp64, exact reference test + kernel) on the candidates.
+                    for (;;) {
+                        int k;
+                        if (cm[0]) {
+                            k = __ffsll((long long)cm[0]) - 1;
+                            cm[0] &= cm[0] - 1ull;
+                        } else if (NM > 1 && cm[NM - 1]) {
+                            k = 64 * (NM - 1) + __ffsll((long long)cm[NM - 1]) - 1;
+                            cm[NM - 1] &= cm[NM - 1] - 1ull;
+                        } else {
+                            break;
+                        }
+#else
                     // Pass 1 (fp32, conservative): queue candidate sources.
                     int nq = 0;
                     for (int k = 0; k < cnt; ++k) {
@@ -266,6 +318,7 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
                     // Pass 2 (fp64, exact reference test + kernel) on queued pairs.
                     for (int j = 0; j < nq; ++j) {
                         const int k = queue[j][lane];
+#endif
                         const double* q = src + k * S;
                         const double r0 = (xt0 - q[0]) - shx;
                         const double r1 = (xt1 - q[1]) - shy;

@@ -1,5 +1,5 @@
 # A/B timing of variant builds (see tools/README.md)
-python tools/sg_time.py 4 7 "" SPREAD_SORT=0
-SEWALD_LIB=paper_2210_01255_b200/lib/var_base/libsewald_gpu.so python tools/sg_time.py 4 7 ""
-python tools/sg_time.py 2 5 "" SPREAD_ROWSWEEP=1 SPREAD_ROWSWEEP=1,SPREAD_SORT=0
-python -m pytest tests -m gpu -x -q -k "spread or gather or family or families or fullsize" 2>&1 | tail -2
+for v in MAIN var_c128 MAIN var_c128; do
+  if [ $v = MAIN ]; then L=paper_2210_01255_b200/lib/libsewald_gpu.so; else L=paper_2210_01255_b200/lib/$v/libsewald_gpu.so; fi
+  echo "c4 $v $(SEWALD_LIB=$L timeout 300 python tools/rs_time.py 4 5 2>&1 | tail -1)"
+done
