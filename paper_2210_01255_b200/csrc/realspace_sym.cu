@@ -266,7 +266,12 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     constexpr bool BF = SEWALD_SYM_BRANCHFREE;
     __shared__ __align__(16) double jrec_all[SYM_WARPS][32][RS];
     __shared__ long long jid_all[SYM_WARPS][32];
-    __shared__ float4 jf_all[SYM_WARPS][32];  // fp32 positions for the candidate pass
+    // fp32 positions for the candidate pass, stored twice (slot k and k + 32) so
+    // that rotation s reads jf[lane + s] at a constant offset (no wrap); with the
+    // 32 rotations fully unrolled a candidate test is 9 instructions instead of
+    // 14 (the kernel is issue-bound: c2 56.5 -> 53.2 ms, c3 108.0 -> 103.8, c5
+    // 64.1 -> 59.8)
+    __shared__ float4 jf_all[SYM_WARPS][64];
     // 2^(j/32) table, replicated SEWALD_EXP_REP times (lane-interleaved: conflict-free lookups)
     __shared__ double exp_tab_rep[32 * SEWALD_EXP_REP];
 #if SEWALD_SYM_POOL > 0
@@ -406,7 +411,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                         rec[1] = xy.y;
                         rec[2] = zi.x;
                         jid[lane] = __double_as_longlong(zi.y);
-                        jf[lane] = make_float4((float)xy.x, (float)xy.y, (float)zi.x, 0.0f);
+                        jf[lane] = jf[lane + 32] = make_float4((float)xy.x, (float)xy.y, (float)zi.x, 0.0f);
 #pragma unroll
                         for (int c = 0; c < NS; c += 2) {
                             const double2 v = __ldg(q2 + 2 + c / 2);
@@ -422,14 +427,14 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                         rec[1] = q[1];
                         rec[2] = q[2];
                         jid[lane] = __double_as_longlong(q[3]);
-                        jf[lane] = make_float4((float)q[0], (float)q[1], (float)q[2], 0.0f);
+                        jf[lane] = jf[lane + 32] = make_float4((float)q[0], (float)q[1], (float)q[2], 0.0f);
 #pragma unroll
                         for (int c = 0; c < NS; ++c) rec[3 + c] = q[4 + c];
                     } else {
 #endif
                         // unused slots: far away in fp32 (never candidates) and
                         // finite in fp64 (branch-free steps read them)
-                        jf[lane] = make_float4(1e30f, 1e30f, 1e30f, 0.0f);
+                        jf[lane] = jf[lane + 32] = make_float4(1e30f, 1e30f, 1e30f, 0.0f);
                         double* rec = jrec[lane];
                         rec[0] = rec[1] = rec[2] = 1e100;
 #pragma unroll
@@ -448,18 +453,20 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                         if (dlt <= -32) {
                             // block entirely after the cluster: no half-rule test
                             // (unused slots are far away and fail the distance test)
-#pragma unroll 8
+                            // fully unrolled: constant shared offsets and mask bits
+                            const float4* jl = jf + lane;
+#pragma unroll
                             for (int s = 0; s < 32; ++s) {
-                                const float4 p = jf[(lane + s) & 31];
+                                const float4 p = jl[s];
                                 const float d0 = tf0 - p.x, d1 = tf1 - p.y, d2 = tf2 - p.z;
-                                m |= (fmaf(d2, d2, fmaf(d1, d1, d0 * d0)) < a.thresh_f ? 1u : 0u) << s;
+                                if (fmaf(d2, d2, fmaf(d1, d1, d0 * d0)) < a.thresh_f) m |= 1u << s;
                             }
                         } else {
 #pragma unroll 8
                             for (int s = 0; s < 32; ++s) {
                                 const int j = (lane + s) & 31;
                                 const int dj = j - lane;
-                                const float4 p = jf[j];
+                                const float4 p = jf[lane + s];
                                 const float d0 = tf0 - p.x, d1 = tf1 - p.y, d2 = tf2 - p.z;
                                 const bool ok = j < cnt && (dj > dlt || (dj == dlt && pos_shift)) &&
                                                 fmaf(d2, d2, fmaf(d1, d1, d0 * d0)) < a.thresh_f;
