@@ -185,6 +185,11 @@ __device__ __forceinline__ void pair_apply(const PairCoef<KIND>& c, double r0, d
 // lanes are pooled too (0 = off): 6 / 9 / 12 lanes measured c2 58.2 / 58.3 /
 // 58.4, c3 108.7 / 108.4 / 107.9, c5 66.0 / 65.7 / 65.6 against 56.7 / 108.2 /
 // 64.4 ms without (4 more registers, and the pooled pair costs ~2.5 lane-slots).
+// pooled pairs' i side: 0 segmented sum into the cluster's pool, 1 global RED
+// (c2 53.1 -> 52.9, c3 103.8 -> 101.8, c5 60.2 -> 61.0 ms: kept at 0)
+#ifndef SEWALD_SYM_POOL_IRED
+#define SEWALD_SYM_POOL_IRED 0
+#endif
 #ifndef SEWALD_SYM_SPLIT
 #define SEWALD_SYM_SPLIT 0
 #endif
@@ -330,6 +335,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     irec[lane][2] = xa2;
 #pragma unroll
     for (int c = 0; c < NS; ++c) irec[lane][3 + c] = fa[c];
+    irec[lane][IS - 1] = __longlong_as_double(valid ? ida : 0);  // index (pad slot)
     ipool[lane][0] = ipool[lane][1] = ipool[lane][2] = 0.0;
     __syncwarp();
 #endif
@@ -554,6 +560,13 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                                 for (int c = 0; c < 3; ++c) atomicAdd(dj + c, uj[c]);
                                 npairs32 += 2u;
                             }
+#if SEWALD_SYM_POOL_IRED
+                            if (ev.acc) {  // i side with global fp64 RED as well (no scan)
+                                double* di = u + 3 * __double_as_longlong(irec[il][IS - 1]);
+#pragma unroll
+                                for (int c = 0; c < 3; ++c) atomicAdd(di + c, ui[c]);
+                            }
+#else
                             const unsigned same = __match_any_sync(0xffffffffu, in ? il : 32 + lane);
                             const int first = __ffs(same) - 1;
                             const int runmax = __reduce_max_sync(0xffffffffu, __popc(same));
@@ -569,6 +582,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                                 for (int c = 0; c < 3; ++c) ipool[il][c] += ui[c];
                             }
                             __syncwarp();
+#endif
                         }
                     }
 #endif
