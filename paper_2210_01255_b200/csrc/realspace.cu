@@ -39,6 +39,11 @@ constexpr int WCHUNK = SEWALD_RS_CHUNK;  // 64 or 128 (mask path)
 // byte queue in shared memory (0): c4 47.9 -> 43.2 ms (no per-candidate
 // stores in the fp32 pass, no queue reads in the fp64 pass; same pair order).
 // 128-source chunks (two masks) measured slower: 56.9 ms.
+// rows / chunks no target of the warp can reach are skipped before staging
+// (c4 43.3 -> 40.6 ms)
+#ifndef SEWALD_RS_BLOCKTEST
+#define SEWALD_RS_BLOCKTEST 1
+#endif
 #ifndef SEWALD_RS_MASK
 #define SEWALD_RS_MASK 1
 #endif
@@ -259,8 +264,29 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
                 const bool primary = (sx == 0) && (sy == 0) && (sz == 0);
                 // fp32 image of this target relative to the row piece's shift
                 const float tf0 = (float)(xt0 - shx), tf1 = (float)(xt1 - shy), tf2 = (float)(xt2 - shz);
+#if SEWALD_RS_BLOCKTEST
+                // per-target distance to the row's (y, z) slab and to each chunk's
+                // x range: rows and chunks no target of the warp can reach are
+                // skipped before staging (the bounding box reaches more)
+                const double ylo_f = cg.origin[1] + jy * cg.w[1], zlo_f = cg.origin[2] + jz * cg.w[2];
+                const double ys = xt1 - shy, zs = xt2 - shz, xsx = xt0 - shx;
+                const double ey = fmax(0.0, fmax(ylo_f - ys, ys - (ylo_f + cg.w[1])));
+                const double ez = fmax(0.0, fmax(zlo_f - zs, zs - (zlo_f + cg.w[2])));
+                const double lat_l = ey * ey + ez * ez;
+                const bool row_near = valid && lat_l < rcm2;
+                if (!__any_sync(0xffffffffu, row_near)) continue;
+                const double subw = cg.w[0] / (double)(1 << cg.sub);  // x order holds up to a sub-cell
+#endif
                 for (int64_t base = b0; base < b1; base += CH) {
                     const int cnt = (int)min((int64_t)CH, b1 - base);
+#if SEWALD_RS_BLOCKTEST
+                    {
+                        const double xb0 = __ldg(packed + base * S) - subw;
+                        const double xb1 = __ldg(packed + (base + cnt - 1) * S) + subw;
+                        const double ex = fmax(0.0, fmax(xb0 - xsx, xsx - xb1));
+                        if (!__any_sync(0xffffffffu, row_near && fma(ex, ex, lat_l) < rcm2)) continue;
+                    }
+#endif
                     __syncwarp();
                     {
                         const double2* g2 = reinterpret_cast<const double2*>(packed + base * S);
