@@ -310,6 +310,7 @@ class KernelOption(enum.IntEnum):
     GATHER_FUSED = 11   # register-A gather tiles evaluate their taps in the kernel
     SPREAD_SORT = 12    # tensor-core spread tiles: points ordered by (x, y) offset, unreachable MMA steps skipped
     GATHER_SORT = 13    # register-A gather tiles: the same for targets
+    D0_YFUSED = 14      # D = 0 solve: fused y transform + scale + inverse y transform (read at plan build)
 
 
 def get_kernel_option(which: KernelOption) -> int:

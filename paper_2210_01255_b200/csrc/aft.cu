@@ -649,9 +649,11 @@ void aft_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p) {
         cuDoubleComplex* z = A.zero.as<cuDoubleComplex>();
         real_to_padded_kernel<<<grid_for(C * zvol), 256, 0, st>>>(grid, C, A.n[0], A.n[1], A.n[2], A.nz[0], A.nz[1],
                                                                   A.nz[2], z);
+        cufftSetStream(A.p_box, st);
         cufft_check(cufftExecZ2Z(A.p_box, z, z, CUFFT_FORWARD), "d0 forward");
         launch_scale_class(p.kind, A.spec, A.cb_zero, p.xi, z,
                            A.table_path ? A.table0p.as<cuDoubleComplex>() : nullptr, st);
+        cufftSetStream(A.p_box, st);
         cufft_check(cufftExecZ2Z(A.p_box, z, z, CUFFT_INVERSE), "d0 inverse");
         padded_to_real_kernel<<<grid_for(3 * (int64_t)A.n[0] * A.n[1] * A.n[2]), 256, 0, st>>>(
             z, A.nz[0], A.nz[1], A.nz[2], A.n[0], A.n[1], A.n[2], zvol, flow);
@@ -672,6 +674,7 @@ void aft_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p) {
     // forward: h^3 phi (normalisation folded into scale), periodic FFTs
     real_to_padded_kernel<<<grid_for(C * vol), 256, 0, st>>>(grid, C, A.n[0], A.n[1], A.n[2], A.n[0], A.n[1],
                                                              A.n[2], far);
+    cufftSetStream(A.p_per, st);
     for (int c = 0; c < C; ++c)
         cufft_check(cufftExecZ2Z(A.p_per, far + c * vol, far + c * vol, CUFFT_FORWARD), "per forward");
     // save the zero / near rows' free blocks, zero padded
@@ -681,8 +684,11 @@ void aft_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p) {
         class_rows_kernel<<<grid_for((int64_t)C * A.R * q1 * q2), 256, 0, st>>>(far, A.nrows, b1, b2, near, A.R, q1,
                                                                                 q2, A.rows_near.as<int>(), C, 0);
     // free transforms: all rows unpadded, zero and near rows padded
+    cufftSetStream(A.p_far, st);
     cufft_check(cufftExecZ2Z(A.p_far, far, far, CUFFT_FORWARD), "far forward");
+    cufftSetStream(A.p_zero, st);
     cufft_check(cufftExecZ2Z(A.p_zero, zero, zero, CUFFT_FORWARD), "zero forward");
+    if (A.R > 0) cufftSetStream(A.p_near, st);
     if (A.R > 0) cufft_check(cufftExecZ2Z(A.p_near, near, near, CUFFT_FORWARD), "near forward");
     // scale each class (far rows of other classes are left unscaled and
     // overwritten on inversion, as in the reference)
@@ -690,14 +696,18 @@ void aft_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p) {
     launch_scale_class(p.kind, A.spec, A.cb_zero, p.xi, zero, nullptr, st);
     if (A.R > 0) launch_scale_class(p.kind, A.spec, A.cb_near, p.xi, near, nullptr, st);
     // inverse: free directions, class rows overwrite, periodic, real part
+    cufftSetStream(A.p_far, st);
     cufft_check(cufftExecZ2Z(A.p_far, far, far, CUFFT_INVERSE), "far inverse");
+    cufftSetStream(A.p_zero, st);
     cufft_check(cufftExecZ2Z(A.p_zero, zero, zero, CUFFT_INVERSE), "zero inverse");
+    if (A.R > 0) cufftSetStream(A.p_near, st);
     if (A.R > 0) cufft_check(cufftExecZ2Z(A.p_near, near, near, CUFFT_INVERSE), "near inverse");
     class_rows_kernel<<<grid_for((int64_t)3 * z1 * z2), 256, 0, st>>>(far, A.nrows, b1, b2, zero, 1, z1, z2,
                                                                        A.rows_zero.as<int>(), 3, 1);
     if (A.R > 0)
         class_rows_kernel<<<grid_for((int64_t)3 * A.R * q1 * q2), 256, 0, st>>>(far, A.nrows, b1, b2, near, A.R, q1,
                                                                                 q2, A.rows_near.as<int>(), 3, 1);
+    cufftSetStream(A.p_per, st);
     for (int c = 0; c < 3; ++c)
         cufft_check(cufftExecZ2Z(A.p_per, far + c * vol, far + c * vol, CUFFT_INVERSE), "per inverse");
     padded_to_real_kernel<<<grid_for(3 * vol), 256, 0, st>>>(far, A.n[0], A.n[1], A.n[2], A.n[0], A.n[1], A.n[2], vol,
@@ -988,6 +998,7 @@ void stage_aft_forward(sewald_gpu_ctx* ctx, const sewald_params_c& p, const doub
         cuDoubleComplex* z = A.zero.as<cuDoubleComplex>();
         real_to_padded_kernel<<<grid_for(C * bvol), 256, 0, st>>>(df, C, A.n[0], A.n[1], A.n[2], A.nz[0], A.nz[1],
                                                                   A.nz[2], z, h3);
+        cufftSetStream(A.p_box, st);
         cufft_check(cufftExecZ2Z(A.p_box, z, z, CUFFT_FORWARD), "stage box forward");
         d2h(d == 3 ? far : zero, z, 2 * C * bvol, st);
         ctx->launches += 2;
@@ -1001,6 +1012,7 @@ void stage_aft_forward(sewald_gpu_ctx* ctx, const sewald_params_c& p, const doub
         cuDoubleComplex* dnear = A.near.as<cuDoubleComplex>();
         real_to_padded_kernel<<<grid_for(C * vol), 256, 0, st>>>(df, C, A.n[0], A.n[1], A.n[2], A.n[0], A.n[1],
                                                                  A.n[2], dfar, h3);
+        cufftSetStream(A.p_per, st);
         for (int c = 0; c < C; ++c)
             cufft_check(cufftExecZ2Z(A.p_per, dfar + c * vol, dfar + c * vol, CUFFT_FORWARD), "stage per forward");
         class_rows_kernel<<<grid_for((int64_t)C * z1 * z2), 256, 0, st>>>(dfar, A.nrows, b1, b2, dzero, 1, z1, z2,
@@ -1008,8 +1020,11 @@ void stage_aft_forward(sewald_gpu_ctx* ctx, const sewald_params_c& p, const doub
         if (A.R > 0)
             class_rows_kernel<<<grid_for((int64_t)C * A.R * q1 * q2), 256, 0, st>>>(
                 dfar, A.nrows, b1, b2, dnear, A.R, q1, q2, A.rows_near.as<int>(), C, 0);
+        cufftSetStream(A.p_far, st);
         cufft_check(cufftExecZ2Z(A.p_far, dfar, dfar, CUFFT_FORWARD), "stage far forward");
+        cufftSetStream(A.p_zero, st);
         cufft_check(cufftExecZ2Z(A.p_zero, dzero, dzero, CUFFT_FORWARD), "stage zero forward");
+        if (A.R > 0) cufftSetStream(A.p_near, st);
         if (A.R > 0) cufft_check(cufftExecZ2Z(A.p_near, dnear, dnear, CUFFT_FORWARD), "stage near forward");
         d2h(far, dfar, 2 * g.far_len, st);
         d2h(zero, dzero, 2 * g.zero_len, st);
@@ -1035,6 +1050,7 @@ void stage_aft_inverse(sewald_gpu_ctx* ctx, const sewald_params_c& p, const sewa
         const int64_t bvol = cells3(A.nz);
         cuDoubleComplex* z = A.zero.as<cuDoubleComplex>();
         h2d(z, d == 3 ? far : zero, 2 * C * bvol, st);
+        cufftSetStream(A.p_box, st);
         cufft_check(cufftExecZ2Z(A.p_box, z, z, CUFFT_INVERSE), "stage box inverse");
         padded_to_real_kernel<<<grid_for(C * svol), 256, 0, st>>>(z, A.nz[0], A.nz[1], A.nz[2], A.n[0], A.n[1],
                                                                   A.n[2], bvol, dfield, C,
@@ -1058,20 +1074,24 @@ void stage_aft_inverse(sewald_gpu_ctx* ctx, const sewald_params_c& p, const sewa
             inv_near /= g.n_near[ax];
         }
         for (int ax = 0; ax < d; ++ax) inv_per /= p.M[ax];
+        cufftSetStream(A.p_far, st);
         cufft_check(cufftExecZ2Z(A.p_far, dfar, dfar, CUFFT_INVERSE), "stage far inverse");
         scale_complex_kernel<<<grid_for(C * vol), 256, 0, st>>>(dfar, C * vol, inv_free);
+        cufftSetStream(A.p_zero, st);
         cufft_check(cufftExecZ2Z(A.p_zero, dzero, dzero, CUFFT_INVERSE), "stage zero inverse");
         scale_complex_kernel<<<grid_for(g.zero_len), 256, 0, st>>>(dzero, g.zero_len, inv_zero);
         class_rows_kernel<<<grid_for((int64_t)C * z1 * z2), 256, 0, st>>>(dfar, A.nrows, b1, b2, dzero, 1, z1, z2,
                                                                            A.rows_zero.as<int>(), C, 1);
         ctx->launches += 5;
         if (A.R > 0) {
+            cufftSetStream(A.p_near, st);
             cufft_check(cufftExecZ2Z(A.p_near, dnear, dnear, CUFFT_INVERSE), "stage near inverse");
             scale_complex_kernel<<<grid_for(g.near_len), 256, 0, st>>>(dnear, g.near_len, inv_near);
             class_rows_kernel<<<grid_for((int64_t)C * A.R * q1 * q2), 256, 0, st>>>(
                 dfar, A.nrows, b1, b2, dnear, A.R, q1, q2, A.rows_near.as<int>(), C, 1);
             ctx->launches += 3;
         }
+        cufftSetStream(A.p_per, st);
         for (int c = 0; c < C; ++c)
             cufft_check(cufftExecZ2Z(A.p_per, dfar + c * vol, dfar + c * vol, CUFFT_INVERSE), "stage per inverse");
         padded_to_real_kernel<<<grid_for(C * vol), 256, 0, st>>>(dfar, A.n[0], A.n[1], A.n[2], A.n[0], A.n[1], A.n[2],

@@ -28,6 +28,10 @@
 #include "engine.h"
 #include "aft_d0.h"
 #include "modified_kernels.cuh"
+#include "options.h"
+
+#include <cmath>
+#include <vector>
 
 #include <algorithm>
 
@@ -59,15 +63,16 @@ __global__ void d0_extract_kernel(const double* __restrict__ R, int64_t lines, i
 
 // Per (c, y) pair: Z[x][kz] (x < m0, stride m1 h2) <-> T[kz][y][x] (x fastest,
 // plane n1 n0). grid (ceil(h2/32), ceil(m0/32), C*m1), block (32, 8).
+// rows: y rows of a T plane (n1, or m1 for the compact layout of the fused y path)
 template <bool FWD>
 __global__ void d0_transpose_kernel(cuDoubleComplex* __restrict__ Z, cuDoubleComplex* __restrict__ T, int m0, int m1,
-                                    int n0, int n1, int h2) {
+                                    int n0, int rows, int h2) {
     __shared__ cuDoubleComplex tile[32][33];
     const int cy = blockIdx.z;
     const int c = cy / m1, y = cy - c * m1;
     const int64_t zrow = (int64_t)m1 * h2;  // Z stride between x
     cuDoubleComplex* zs = Z + ((int64_t)c * m0 * m1 + y) * h2;
-    const int64_t plane = (int64_t)n0 * n1;
+    const int64_t plane = (int64_t)n0 * rows;
     cuDoubleComplex* ts = T + (int64_t)c * h2 * plane + (int64_t)y * n0;
     const int kz0 = blockIdx.x * 32, x0 = blockIdx.y * 32;
     if (FWD) {
@@ -177,6 +182,242 @@ __global__ void d0_scale_kernel(ModSpec spec, D0ScaleArgs a, double xi, cuDouble
     }
 }
 
+// ---------------------------------------------------------------------------
+// Fused y path: per (kz, pair of x columns) block, the m1 data rows of every
+// input component are loaded (rows m1..N-1 are the zero padding), transformed
+// along y (length N, radix-8/4/2 Stockham in shared memory), scaled exactly
+// as d0_scale_kernel does, transformed back for the 3 flow components and the
+// m1 rows the inverse z pass needs are stored. Replaces the forward y pass,
+// the scale kernel and the inverse y pass (three HBM round trips of the
+// padded slices) by one; the x passes then run over the m1 data rows only.
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+// multiply by -i (forward) or +i (inverse)
+template <bool INV>
+__device__ __forceinline__ double2 cmi(double2 a) {
+    return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft4(double2& a0, double2& a1, double2& a2, double2& a3) {
+    const double2 t0 = cadd(a0, a2), t1 = csub(a0, a2), t2 = cadd(a1, a3), t3 = cmi<INV>(csub(a1, a3));
+    a0 = cadd(t0, t2);
+    a2 = csub(t0, t2);
+    a1 = cadd(t1, t3);
+    a3 = csub(t1, t3);
+}
+
+template <int R, bool INV>
+__device__ __forceinline__ void dft(double2* a) {
+    if (R == 2) {
+        const double2 t = a[0];
+        a[0] = cadd(t, a[1]);
+        a[1] = csub(t, a[1]);
+    } else if (R == 4) {
+        dft4<INV>(a[0], a[1], a[2], a[3]);
+    } else {
+        constexpr double h = 0.70710678118654752440;
+        double2 e0 = a[0], e1 = a[2], e2 = a[4], e3 = a[6];
+        double2 o0 = a[1], o1 = a[3], o2 = a[5], o3 = a[7];
+        dft4<INV>(e0, e1, e2, e3);
+        dft4<INV>(o0, o1, o2, o3);
+        // o_k *= W8^(+-k)
+        o1 = cmul(o1, make_double2(h, INV ? h : -h));
+        o2 = cmi<INV>(o2);
+        o3 = cmul(o3, make_double2(-h, INV ? h : -h));
+        a[0] = cadd(e0, o0);
+        a[4] = csub(e0, o0);
+        a[1] = cadd(e1, o1);
+        a[5] = csub(e1, o1);
+        a[2] = cadd(e2, o2);
+        a[6] = csub(e2, o2);
+        a[3] = cadd(e3, o3);
+        a[7] = csub(e3, o3);
+    }
+}
+
+// One Stockham stage (radix R, input subsequence length NS) on S sequences of
+// length N in shared memory, in place: every thread loads its butterflies,
+// the block synchronises, then writes them back.
+template <int N, int R, int NS, bool INV, int THREADS, int SMAX>
+__device__ __forceinline__ void fft_stage(double2* buf, int S, const double2* __restrict__ tw) {
+    constexpr int NB = N / R;                                 // butterflies per sequence
+    constexpr int BPT = (SMAX * NB + THREADS - 1) / THREADS;  // per thread (upper bound)
+    const int total = S * NB;
+    double2 a[BPT][R];
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+        const int b = threadIdx.x + q * THREADS;
+        if (b < total) {
+            const int s = b / NB, i = b - s * NB;
+            const double2* x = buf + s * N;
+#pragma unroll
+            for (int r = 0; r < R; ++r) a[q][r] = x[i + r * NB];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < BPT; ++q) {
+        const int b = threadIdx.x + q * THREADS;
+        if (b < total) {
+            const int s = b / NB, i = b - s * NB;
+            const int j = i % NS;
+            if (NS > 1) {
+#pragma unroll
+                for (int r = 1; r < R; ++r) {
+                    double2 w = __ldg(tw + j * r * (N / (NS * R)));
+                    if (INV) w.y = -w.y;
+                    a[q][r] = cmul(a[q][r], w);
+                }
+            }
+            dft<R, INV>(a[q]);
+            double2* y = buf + s * N + (i / NS) * NS * R + j;
+#pragma unroll
+            for (int r = 0; r < R; ++r) y[r * NS] = a[q][r];
+        }
+    }
+    __syncthreads();
+}
+
+template <int N, int NS, bool INV, int THREADS, int SMAX>
+__device__ __forceinline__ void fft_all(double2* buf, int S, const double2* __restrict__ tw) {
+    if constexpr (NS < N) {
+        constexpr int REM = N / NS;
+        constexpr int R = REM % 8 == 0 ? 8 : (REM % 4 == 0 ? 4 : 2);
+        fft_stage<N, R, NS, INV, THREADS, SMAX>(buf, S, tw);
+        fft_all<N, NS * R, INV, THREADS, SMAX>(buf, S, tw);
+    }
+}
+
+constexpr int YF_COLS = 2;  // x columns per block (32-byte row segments: full sectors)
+
+template <int KIND, int N>
+struct YFusedCfg {
+    static constexpr int NC = KIND == SEWALD_STRESSLET ? 9 : 3;
+    static constexpr int SIN = NC * YF_COLS;                      // input sequences
+    // one radix-8 butterfly per thread and stage (capped at 1024 threads)
+    static constexpr int THREADS = SIN * (N / 8) >= 1024 ? 1024 : SIN * (N / 8);
+    static constexpr size_t SMEM = sizeof(double2) * (size_t)SIN * N;
+};
+
+template <int KIND, int N>
+__global__ void __launch_bounds__(YFusedCfg<KIND, N>::THREADS, YFusedCfg<KIND, N>::THREADS <= 512 ? 2 : 1)
+d0_yfused_kernel(ModSpec spec, D0ScaleArgs a, double xi, int m1, cuDoubleComplex* __restrict__ data,
+                 const cuDoubleComplex* __restrict__ Th, const double2* __restrict__ tw) {
+    using Cfg = YFusedCfg<KIND, N>;
+    constexpr int NC = Cfg::NC, SIN = Cfg::SIN, THREADS = Cfg::THREADS;
+    constexpr int NG = 3 * NC;
+    extern __shared__ double2 yb[];  // [c][col][y]
+    const int kx0 = blockIdx.x * YF_COLS;
+    const int kzl = blockIdx.y;  // kz of this launch (a.kz0 + kzl globally)
+    const int64_t rowbase = (int64_t)kzl * m1;
+    // load the data rows, zero the padding
+    for (int e = threadIdx.x; e < SIN * N; e += THREADS) {
+        const int col = e % YF_COLS;
+        const int t = e / YF_COLS;
+        const int y = t % N, c = t / N;
+        double2 v = make_double2(0.0, 0.0);
+        if (y < m1 && kx0 + col < a.n0) {
+            const cuDoubleComplex g = data[c * a.cstride + (rowbase + y) * a.n0 + kx0 + col];
+            v = make_double2(g.x, g.y);
+        }
+        yb[(c * YF_COLS + col) * N + y] = v;
+    }
+    __syncthreads();
+    fft_all<N, 1, false, THREADS, SIN>(yb, SIN, tw);
+    // scale (d0_scale_kernel per (col, ky)): 3 outputs into sequences 0..2
+    const int kz = a.kz0 + kzl;
+    for (int e = threadIdx.x; e < YF_COLS * N; e += THREADS) {
+        const int col = e / N, ky = e - col * N;
+        const int kx = kx0 + col;
+        if (kx >= a.n0) continue;
+        const double k0 = a.k0[kx], k1 = a.k1[ky], k2 = a.k2[kz];
+        const double wp = a.w0[kx] * a.w1[ky] * a.w2[kz];
+        const double kk = k0 * k0 + k1 * k1 + k2 * k2;
+        const double q = kk / (4.0 * xi * xi);
+        const double g = exp(-q);
+        const double scr = KIND == SEWALD_ROTLET ? g : g * (1.0 + q);
+        const double fac = scr / (wp * wp) * a.norm;
+        const bool table = Th != nullptr;
+        double re[NG], im[NG];
+        d0_operator<KIND>(spec, table, k0, k1, k2, re, im);
+        const bool nx = (a.n0 % 2 == 0) && kx == a.n0 / 2;
+        const bool ny = (a.n1 % 2 == 0) && ky == a.n1 / 2;
+        const bool nz = (a.n2 % 2 == 0) && kz == a.n2 / 2;
+        if (nx || ny || nz) {
+            double re2[NG], im2[NG];
+            d0_operator<KIND>(spec, table, nx ? -k0 : k0, ny ? -k1 : k1, nz ? -k2 : k2, re2, im2);
+#pragma unroll
+            for (int q2 = 0; q2 < NG; ++q2) {
+                re[q2] = 0.5 * (re[q2] + re2[q2]);
+                im[q2] = 0.5 * (im[q2] + im2[q2]);
+            }
+        }
+        if (table) {
+            const cuDoubleComplex tv = Th[((int64_t)kz * a.n1 + ky) * a.n0 + kx];
+#pragma unroll
+            for (int q2 = 0; q2 < NG; ++q2) {
+                const double x = re[q2], y = im[q2];
+                re[q2] = x * tv.x - y * tv.y;
+                im[q2] = x * tv.y + y * tv.x;
+            }
+        }
+        double2 in[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) in[c] = yb[(c * YF_COLS + col) * N + ky];
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            double ar = 0.0, ai = 0.0;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                ar += re[NC * j + c] * in[c].x - im[NC * j + c] * in[c].y;
+                ai += re[NC * j + c] * in[c].y + im[NC * j + c] * in[c].x;
+            }
+            yb[(j * YF_COLS + col) * N + ky] = make_double2(fac * ar, fac * ai);
+        }
+    }
+    __syncthreads();
+    fft_all<N, 1, true, THREADS, SIN>(yb, 3 * YF_COLS, tw);
+    for (int e = threadIdx.x; e < 3 * YF_COLS * m1; e += THREADS) {
+        const int col = e % YF_COLS;
+        const int t = e / YF_COLS;
+        const int y = t % m1, j = t / m1;
+        if (kx0 + col >= a.n0) continue;
+        const double2 v = yb[(j * YF_COLS + col) * N + y];
+        data[j * a.cstride + (rowbase + y) * a.n0 + kx0 + col] = make_cuDoubleComplex(v.x, v.y);
+    }
+}
+
+template <int KIND, int N>
+void launch_yfused(const ModSpec& spec, const D0ScaleArgs& sa, double xi, int m1, int nkz, cuDoubleComplex* data,
+                   const cuDoubleComplex* th, const double2* tw, cudaStream_t st) {
+    using Cfg = YFusedCfg<KIND, N>;
+    auto kern = d0_yfused_kernel<KIND, N>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    const dim3 grid((unsigned)((sa.n0 + YF_COLS - 1) / YF_COLS), (unsigned)nkz);
+    kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(spec, sa, xi, m1, data, th, tw);
+}
+
+template <int KIND>
+void launch_yfused_n(int N, const ModSpec& spec, const D0ScaleArgs& sa, double xi, int m1, int nkz,
+                     cuDoubleComplex* data, const cuDoubleComplex* th, const double2* tw, cudaStream_t st) {
+    switch (N) {
+        case 256: launch_yfused<KIND, 256>(spec, sa, xi, m1, nkz, data, th, tw, st); break;
+        case 512: launch_yfused<KIND, 512>(spec, sa, xi, m1, nkz, data, th, tw, st); break;
+        default: launch_yfused<KIND, 1024>(spec, sa, xi, m1, nkz, data, th, tw, st); break;
+    }
+}
+
+bool yfused_ok(int n1, int C) {
+    if (!(n1 == 256 || n1 == 512 || n1 == 1024)) return false;
+    // shared memory: C x 2 columns x n1 complex
+    return (size_t)C * YF_COLS * n1 * sizeof(double2) <= 200 * 1024;
+}
+
 void fft_check(cufftResult r, const char* what) {
     if (r != CUFFT_SUCCESS) throw EngineError(SEWALD_ECUFFT, std::string("cuFFT: ") + what);
 }
@@ -194,13 +435,25 @@ void D0Real::setup(const int m_[3], const int n_[3], int C_, cudaStream_t st) {
     }
     C = C_;
     h2 = n[2] / 2 + 1;
+    yfused = option(SEWALD_OPT_D0_YFUSED) != 0 && yfused_ok(n[1], C);
     const int64_t lines_in = (int64_t)C * m[0] * m[1], lines_out = (int64_t)3 * m[0] * m[1];
     R.ensure(sizeof(double) * lines_in * n[2]);
     Z.ensure(sizeof(cuDoubleComplex) * lines_in * h2);
-    const int64_t slab = (int64_t)h2 * n[0] * n[1];
+    // [c][kz][y][x] planes: all n1 rows, or the m1 data rows for the fused y path
+    const int64_t slab = (int64_t)h2 * n[0] * (yfused ? m[1] : n[1]);
     Tin.ensure(sizeof(cuDoubleComplex) * C * slab);
     Tout.ensure(sizeof(cuDoubleComplex) * C * slab);
     cuda_check(cudaMemsetAsync(Tin.ptr, 0, sizeof(cuDoubleComplex) * C * slab, st), "d0 Tin zero");
+    if (yfused) {  // exp(-2 pi i k / n1), k < n1
+        std::vector<double2> h(n[1]);
+        for (int k = 0; k < n[1]; ++k) {
+            const long double ang = -2.0L * 3.14159265358979323846264338327950288L * k / n[1];
+            h[k] = make_double2((double)cosl(ang), (double)sinl(ang));
+        }
+        tw.ensure(sizeof(double2) * n[1]);
+        cuda_check(cudaMemcpyAsync(tw.ptr, h.data(), sizeof(double2) * n[1], cudaMemcpyHostToDevice, st), "d0 tw");
+        cuda_check(cudaStreamSynchronize(st), "d0 tw");
+    }
 
     size_t ws = 0, w = 0;
     auto mk = [&](cufftHandle& h, int rank, const int* nl, const int* inem, long long is, long long id,
@@ -221,10 +474,17 @@ void D0Real::setup(const int m_[3], const int n_[3], int C_, cudaStream_t st) {
     int e_n2[1] = {n[2]}, e_h2[1] = {h2};
     mk(pz_f, 1, n + 2, e_n2, 1, n[2], e_h2, 1, h2, CUFFT_D2Z, lines_in);
     mk(pz_i, 1, n + 2, e_h2, 1, h2, e_n2, 1, n[2], CUFFT_Z2D, lines_out);
-    const int64_t plane = (int64_t)n[0] * n[1];
-    const int nyx[2] = {n[1], n[0]};  // [y][x] slices, x fastest
-    mk(pxy_f, 2, nyx, nyx, 1, plane, nyx, 1, plane, CUFFT_Z2Z, (long long)C * h2);
-    mk(pxy_i, 2, nyx, nyx, 1, plane, nyx, 1, plane, CUFFT_Z2Z, (long long)3 * h2);
+    if (yfused) {
+        // x transforms of the m1 data rows of every (c, kz) plane (contiguous rows)
+        const int e_n0[1] = {n[0]};
+        mk(px_f, 1, n, e_n0, 1, n[0], e_n0, 1, n[0], CUFFT_Z2Z, (long long)C * h2 * m[1]);
+        mk(px_i, 1, n, e_n0, 1, n[0], e_n0, 1, n[0], CUFFT_Z2Z, (long long)3 * h2 * m[1]);
+    } else {
+        const int64_t plane = (int64_t)n[0] * n[1];
+        const int nyx[2] = {n[1], n[0]};  // [y][x] slices, x fastest
+        mk(pxy_f, 2, nyx, nyx, 1, plane, nyx, 1, plane, CUFFT_Z2Z, (long long)C * h2);
+        mk(pxy_i, 2, nyx, nyx, 1, plane, nyx, 1, plane, CUFFT_Z2Z, (long long)3 * h2);
+    }
     work.ensure(std::max<size_t>(ws, 16));
     for (auto h : plans) fft_check(cufftSetWorkArea(h, work.ptr), "work area");
 }
@@ -239,7 +499,8 @@ void D0Real::build_herm_table(const cuDoubleComplex* full, cudaStream_t st) {
 int D0Real::solve(const double* grid, const ModSpec& spec, int kind, double xi, const D0ScaleArgs& sa_in, bool table,
                   double* flow, cudaStream_t st) {
     const int64_t lines_in = (int64_t)C * m[0] * m[1], lines_out = (int64_t)3 * m[0] * m[1];
-    const int64_t slab = (int64_t)h2 * n[0] * n[1];
+    const int rows = yfused ? m[1] : n[1];  // y rows of a T plane
+    const int64_t slab = (int64_t)h2 * n[0] * rows;
     double* r = R.as<double>();
     cuDoubleComplex* z = Z.as<cuDoubleComplex>();
     cuDoubleComplex* ti = Tin.as<cuDoubleComplex>();
@@ -247,12 +508,10 @@ int D0Real::solve(const double* grid, const ModSpec& spec, int kind, double xi, 
     int launches = 0;
     // forward
     d0_pad_z_kernel<<<blocks_for(lines_in * n[2]), 256, 0, st>>>(grid, lines_in, m[2], n[2], r);
+    cufftSetStream(pz_f, st);
     fft_check(cufftExecD2Z(pz_f, r, z), "d0 z forward");
     const dim3 tb(32, 8), tg((h2 + 31) / 32, (m[0] + 31) / 32, C * m[1]);
-    d0_transpose_kernel<true><<<tg, tb, 0, st>>>(z, ti, m[0], m[1], n[0], n[1], h2);
-    fft_check(cufftExecZ2Z(pxy_f, ti, to, CUFFT_FORWARD), "d0 xy forward");
-    launches += 2;  // own kernels only (cuFFT launches are library work)
-    // scale
+    d0_transpose_kernel<true><<<tg, tb, 0, st>>>(z, ti, m[0], m[1], n[0], rows, h2);
     D0ScaleArgs sa = sa_in;
     sa.n0 = n[0];
     sa.n1 = n[1];
@@ -261,18 +520,40 @@ int D0Real::solve(const double* grid, const ModSpec& spec, int kind, double xi, 
     sa.kz0 = 0;
     sa.cstride = slab;
     const cuDoubleComplex* th = table ? Th.as<cuDoubleComplex>() : nullptr;
-    const unsigned sb = (unsigned)((slab + 127) / 128);
-    switch (kind) {
-        case SEWALD_STOKESLET: d0_scale_kernel<SEWALD_STOKESLET><<<sb, 128, 0, st>>>(spec, sa, xi, to, th); break;
-        case SEWALD_ROTLET: d0_scale_kernel<SEWALD_ROTLET><<<sb, 128, 0, st>>>(spec, sa, xi, to, th); break;
-        default: d0_scale_kernel<SEWALD_STRESSLET><<<sb, 128, 0, st>>>(spec, sa, xi, to, th); break;
+    if (yfused) {
+        // x forward over the data rows, fused y transform / scale / inverse y, x inverse
+        cufftSetStream(px_f, st);
+        fft_check(cufftExecZ2Z(px_f, ti, to, CUFFT_FORWARD), "d0 x forward");
+        const double2* twp = tw.as<double2>();
+        switch (kind) {
+            case SEWALD_STOKESLET:
+                launch_yfused_n<SEWALD_STOKESLET>(n[1], spec, sa, xi, m[1], h2, to, th, twp, st);
+                break;
+            case SEWALD_ROTLET: launch_yfused_n<SEWALD_ROTLET>(n[1], spec, sa, xi, m[1], h2, to, th, twp, st); break;
+            default: launch_yfused_n<SEWALD_STRESSLET>(n[1], spec, sa, xi, m[1], h2, to, th, twp, st); break;
+        }
+        cufftSetStream(px_i, st);
+        fft_check(cufftExecZ2Z(px_i, to, to, CUFFT_INVERSE), "d0 x inverse");
+        launches += 3;  // own kernels only (cuFFT launches are library work)
+    } else {
+        cufftSetStream(pxy_f, st);
+        fft_check(cufftExecZ2Z(pxy_f, ti, to, CUFFT_FORWARD), "d0 xy forward");
+        launches += 2;
+        const unsigned sb = (unsigned)((slab + 127) / 128);
+        switch (kind) {
+            case SEWALD_STOKESLET: d0_scale_kernel<SEWALD_STOKESLET><<<sb, 128, 0, st>>>(spec, sa, xi, to, th); break;
+            case SEWALD_ROTLET: d0_scale_kernel<SEWALD_ROTLET><<<sb, 128, 0, st>>>(spec, sa, xi, to, th); break;
+            default: d0_scale_kernel<SEWALD_STRESSLET><<<sb, 128, 0, st>>>(spec, sa, xi, to, th); break;
+        }
+        ++launches;
+        // inverse (3 flow components)
+        cufftSetStream(pxy_i, st);
+        fft_check(cufftExecZ2Z(pxy_i, to, to, CUFFT_INVERSE), "d0 xy inverse");
     }
-    ++launches;
-    // inverse (3 flow components)
-    fft_check(cufftExecZ2Z(pxy_i, to, to, CUFFT_INVERSE), "d0 xy inverse");
     const dim3 tgi((h2 + 31) / 32, (m[0] + 31) / 32, 3 * m[1]);
-    d0_transpose_kernel<false><<<tgi, tb, 0, st>>>(z, to, m[0], m[1], n[0], n[1], h2);
+    d0_transpose_kernel<false><<<tgi, tb, 0, st>>>(z, to, m[0], m[1], n[0], rows, h2);
     ++launches;
+    cufftSetStream(pz_i, st);
     fft_check(cufftExecZ2D(pz_i, z, r), "d0 z inverse");
     d0_extract_kernel<<<blocks_for(lines_out * m[2]), 256, 0, st>>>(r, lines_out, m[2], n[2], flow);
     ++launches;
@@ -419,6 +700,7 @@ int D0Real::slab_forward(const double* grid_slab, int xa, int xb, const SlabBoun
     double* r = slab.R.as<double>();
     cuDoubleComplex* z = slab.Z.as<cuDoubleComplex>();
     d0_pad_z_kernel<<<blocks_for(lines * n[2]), 256, 0, st>>>(grid_slab, lines, m[2], n[2], r);
+    cufftSetStream(slab.pz_f, st);
     fft_check(cufftExecD2Z(slab.pz_f, r, z), "slab z forward");
     d0_pack_fwd_kernel<<<blocks_for(lines * h2), 256, 0, st>>>(z, C, nxs, m[1], h2, kzb, send);
     cuda_check(cudaGetLastError(), "slab forward");
@@ -436,6 +718,7 @@ int D0Real::slab_middle(const cuDoubleComplex* recv, const SlabBounds& xbd, int 
     cuDoubleComplex* to = slab.Tout.as<cuDoubleComplex>();
     const int64_t nin = (int64_t)C * nk * m[0] * m[1];
     d0_unpack_mid_kernel<<<blocks_for(nin), 256, 0, st>>>(recv, C, m[0], m[1], n[0], n[1], nk, xbd, ti);
+    cufftSetStream(slab.pxy_f, st);
     fft_check(cufftExecZ2Z(slab.pxy_f, ti, to, CUFFT_FORWARD), "slab xy forward");
     D0ScaleArgs sa = sa_in;
     sa.n0 = n[0];
@@ -451,6 +734,7 @@ int D0Real::slab_middle(const cuDoubleComplex* recv, const SlabBounds& xbd, int 
         case SEWALD_ROTLET: d0_scale_kernel<SEWALD_ROTLET><<<sb, 128, 0, st>>>(spec, sa, xi, to, th); break;
         default: d0_scale_kernel<SEWALD_STRESSLET><<<sb, 128, 0, st>>>(spec, sa, xi, to, th); break;
     }
+    cufftSetStream(slab.pxy_i, st);
     fft_check(cufftExecZ2Z(slab.pxy_i, to, to, CUFFT_INVERSE), "slab xy inverse");
     const int64_t nout = (int64_t)3 * nk * m[0] * m[1];
     d0_pack_mid_kernel<<<blocks_for(nout), 256, 0, st>>>(to, m[0], m[1], n[0], n[1], nk, xbd, send);
@@ -467,6 +751,7 @@ int D0Real::slab_inverse(const cuDoubleComplex* recv, int xa, int xb, const Slab
     cuDoubleComplex* z = slab.Z.as<cuDoubleComplex>();
     double* r = slab.R.as<double>();
     d0_unpack_inv_kernel<<<blocks_for(lines * h2), 256, 0, st>>>(recv, nxs, m[1], h2, kzb, z);
+    cufftSetStream(slab.pz_i, st);
     fft_check(cufftExecZ2D(slab.pz_i, z, r), "slab z inverse");
     d0_extract_kernel<<<blocks_for(lines * m[2]), 256, 0, st>>>(r, lines, m[2], n[2], flow_slab);
     cuda_check(cudaGetLastError(), "slab inverse");

@@ -43,7 +43,11 @@ struct D0Real {
     int m[3]{}, n[3]{}, C = 3, h2 = 0;
     std::vector<cufftHandle> plans;
     cufftHandle pz_f = 0, pz_i = 0, pxy_f = 0, pxy_i = 0;
-    DevBuf R, Z, Tin, Tout, Th, work;
+    // fused y path (n1 a power of two, 256..1024): x passes over the m1 data rows
+    // only, y transform + scale + inverse y transform in one kernel per column set
+    bool yfused = false;
+    cufftHandle px_f = 0, px_i = 0;
+    DevBuf R, Z, Tin, Tout, Th, work, tw;
     D0SlabPlan slab;
     ~D0Real();
     // m: input/output box (M_ext), n: padded transform box

@@ -808,11 +808,16 @@ void session_solve(sewald_gpu_session* s, const double* grid, bool precompute_0p
     FourierPlanD3& P = *s->d3;
     cudaStream_t st = s->ctx->stream;
     cuDoubleComplex* spec = P.spec.as<cuDoubleComplex>();
+    // cuFFT plans keep the stream they were last given; the context's stream
+    // can change between calls (Session follows torch's current stream), so
+    // every execution sets it (here and in aft.cu / aft_d0.cu)
+    cufftSetStream(P.fwd, st);
     cufft_check(cufftExecD2Z(P.fwd, const_cast<double*>(grid), spec), "exec D2Z");
     const int64_t hvol = (int64_t)P.n[0] * P.n[1] * (P.n[2] / 2 + 1);
     launch_scale_periodic(s->p.kind, P.n[0], P.n[1], P.n[2], s->p.xi, 1.0 / (double)vol, P.kt, spec,
                           hvol, st);
     ++s->ctx->launches;
+    cufftSetStream(P.inv, st);
     cufft_check(cufftExecZ2D(P.inv, spec, s->flow.as<double>()), "exec Z2D");
     cuda_check(cudaGetLastError(), "solve launch");
 }

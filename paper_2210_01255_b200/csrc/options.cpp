@@ -60,6 +60,9 @@ int env_default(int which) {
         case SEWALD_OPT_GATHER_SORT:
             e = env("SEWALD_GATHER_SORT");
             return (e && e[0] == '0') ? 0 : 1;
+        case SEWALD_OPT_D0_YFUSED:
+            e = env("SEWALD_D0_YFUSED");
+            return (e && e[0] == '1') ? 1 : 0;
     }
     return 0;
 }
@@ -80,6 +83,7 @@ bool valid(int which, int v) {
         case SEWALD_OPT_GATHER_FUSED: return v == 0 || v == 1;
         case SEWALD_OPT_SPREAD_SORT: return v == 0 || v == 1;
         case SEWALD_OPT_GATHER_SORT: return v == 0 || v == 1;
+        case SEWALD_OPT_D0_YFUSED: return v == 0 || v == 1;
     }
     return false;
 }

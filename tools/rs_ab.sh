@@ -1,5 +1,4 @@
-# A/B timing of variant builds (see tools/README.md)
-for c in 4 1; do for v in var_nbt MAIN var_nbt MAIN; do
-  if [ $v = MAIN ]; then L=paper_2210_01255_b200/lib/libsewald_gpu.so; else L=paper_2210_01255_b200/lib/$v/libsewald_gpu.so; fi
-  echo "c$c $v $(SEWALD_LIB=$L timeout 300 python tools/rs_time.py $c 5 2>&1 | tail -1)"
-done; done
+M="tests/test_multi_device.py::test_multi_matches_single_and_reference[stokeslet_d0-2]"
+mapfile -t IDS < tools/ids.txt
+for k in 4 5 6 7; do echo "id$k+slab"; python -m pytest -m gpu -x -q "${IDS[@]:$k:1}" "${IDS[@]:8:12}" "$M" 2>&1 | tail -1; done
+echo "4-7"; python -m pytest -m gpu -x -q "${IDS[@]:4:4}" "$M" 2>&1 | tail -1
