@@ -164,7 +164,7 @@ enum {
     SEWALD_OPT_GATHER_SORT = 13,  /* register-A gather tiles: the same ordering and skipping for targets */
     SEWALD_OPT_D0_YFUSED = 14,    /* D = 0 solve: 1 x transforms over the data rows only and the y transform,
                                      scale and inverse y transform fused in one kernel (padded y a power of
-                                     two, 256..1024), 0 batched 2-D transforms + scale kernel (default); read
+                                     two, 256..1024; default), 0 batched 2-D transforms + scale kernel; read
                                      when a session builds its D = 0 plan */
     SEWALD_OPT_COUNT = 15
 };

@@ -183,7 +183,9 @@ __global__ void d0_scale_kernel(ModSpec spec, D0ScaleArgs a, double xi, cuDouble
 }
 
 // ---------------------------------------------------------------------------
-// Fused y path: per (kz, pair of x columns) block, the m1 data rows of every
+// Fused y path (SEWALD_OPT_D0_YFUSED, default; c5: solve 17.6 -> 12.8 ms,
+// the kernel 5.9 ms, shared-memory and barrier bound): per (kz, pair of x
+// columns) block, the m1 data rows of every
 // input component are loaded (rows m1..N-1 are the zero padding), transformed
 // along y (length N, radix-8/4/2 Stockham in shared memory), scaled exactly
 // as d0_scale_kernel does, transformed back for the 3 flow components and the
@@ -240,11 +242,31 @@ __device__ __forceinline__ void dft(double2* a) {
     }
 }
 
+// Shared-memory position of element a of a sequence: one pad slot per 8
+// elements, so the stride-8 (NS = 1) and strided-group writes of the Stockham
+// stages and the contiguous reads stay free of bank conflicts (16-byte
+// elements: 8 lanes per wavefront).
+__device__ __forceinline__ int ypad(int a) { return a + (a >> 3); }
+template <int N>
+constexpr int yseq() { return N + N / 8; }
+
+// Radix of the Stockham stage that starts at subsequence length NS (8 while
+// it divides, then 4 / 2), and the offset of that stage's twiddle table in the
+// per-stage tables [r - 1][j] = W_N^(j r N / (NS R)) (r-major: the lanes of a
+// warp read consecutive j, free of bank conflicts).
+constexpr int stage_radix(int N, int NS) { return (N / NS) % 8 == 0 ? 8 : ((N / NS) % 4 == 0 ? 4 : 2); }
+constexpr int tw_offset(int N, int NS) {
+    int off = 0;
+    for (int ns = 1; ns < NS; ns *= stage_radix(N, ns))
+        if (ns > 1) off += (stage_radix(N, ns) - 1) * ns;
+    return off;
+}
+
 // One Stockham stage (radix R, input subsequence length NS) on S sequences of
 // length N in shared memory, in place: every thread loads its butterflies,
 // the block synchronises, then writes them back.
 template <int N, int R, int NS, bool INV, int THREADS, int SMAX>
-__device__ __forceinline__ void fft_stage(double2* buf, int S, const double2* __restrict__ tw) {
+__device__ __forceinline__ void fft_stage(double2* buf, int S, const double2* tw) {
     constexpr int NB = N / R;                                 // butterflies per sequence
     constexpr int BPT = (SMAX * NB + THREADS - 1) / THREADS;  // per thread (upper bound)
     const int total = S * NB;
@@ -254,9 +276,9 @@ __device__ __forceinline__ void fft_stage(double2* buf, int S, const double2* __
         const int b = threadIdx.x + q * THREADS;
         if (b < total) {
             const int s = b / NB, i = b - s * NB;
-            const double2* x = buf + s * N;
+            const double2* x = buf + s * yseq<N>();
 #pragma unroll
-            for (int r = 0; r < R; ++r) a[q][r] = x[i + r * NB];
+            for (int r = 0; r < R; ++r) a[q][r] = x[ypad(i + r * NB)];
         }
     }
     __syncthreads();
@@ -267,70 +289,88 @@ __device__ __forceinline__ void fft_stage(double2* buf, int S, const double2* __
             const int s = b / NB, i = b - s * NB;
             const int j = i % NS;
             if (NS > 1) {
+                const double2* tws = tw + tw_offset(N, NS) + j;
 #pragma unroll
                 for (int r = 1; r < R; ++r) {
-                    double2 w = __ldg(tw + j * r * (N / (NS * R)));
+                    double2 w = tws[(r - 1) * NS];
                     if (INV) w.y = -w.y;
                     a[q][r] = cmul(a[q][r], w);
                 }
             }
             dft<R, INV>(a[q]);
-            double2* y = buf + s * N + (i / NS) * NS * R + j;
+            double2* y = buf + s * yseq<N>();
+            const int o = (i / NS) * NS * R + j;
 #pragma unroll
-            for (int r = 0; r < R; ++r) y[r * NS] = a[q][r];
+            for (int r = 0; r < R; ++r) y[ypad(o + r * NS)] = a[q][r];
         }
     }
     __syncthreads();
 }
 
 template <int N, int NS, bool INV, int THREADS, int SMAX>
-__device__ __forceinline__ void fft_all(double2* buf, int S, const double2* __restrict__ tw) {
+__device__ __forceinline__ void fft_all(double2* buf, int S, const double2* tw) {
     if constexpr (NS < N) {
-        constexpr int REM = N / NS;
-        constexpr int R = REM % 8 == 0 ? 8 : (REM % 4 == 0 ? 4 : 2);
+        constexpr int R = stage_radix(N, NS);
         fft_stage<N, R, NS, INV, THREADS, SMAX>(buf, S, tw);
         fft_all<N, NS * R, INV, THREADS, SMAX>(buf, S, tw);
     }
 }
 
-constexpr int YF_COLS = 2;  // x columns per block (32-byte row segments: full sectors)
+#ifndef SEWALD_YF_COLS
+#define SEWALD_YF_COLS 2
+#endif
+constexpr int YF_COLS = SEWALD_YF_COLS;  // x columns per block (2: 32-byte row segments, full sectors)
 
 template <int KIND, int N>
 struct YFusedCfg {
     static constexpr int NC = KIND == SEWALD_STRESSLET ? 9 : 3;
     static constexpr int SIN = NC * YF_COLS;                      // input sequences
-    // one radix-8 butterfly per thread and stage (capped at 1024 threads)
-    static constexpr int THREADS = SIN * (N / 8) >= 1024 ? 1024 : SIN * (N / 8);
-    static constexpr size_t SMEM = sizeof(double2) * (size_t)SIN * N;
+    // one radix-8 butterfly per thread and stage, two above 512 threads
+    static constexpr int THREADS = SIN * (N / 8) <= 512 ? SIN * (N / 8) : SIN * (N / 16);
+    // + twiddles + the table values of the block's (col, ky) points
+    static constexpr size_t SMEM = sizeof(double2) * ((size_t)SIN * (N + N / 8) + N + YF_COLS * N);
 };
 
 template <int KIND, int N>
-__global__ void __launch_bounds__(YFusedCfg<KIND, N>::THREADS, YFusedCfg<KIND, N>::THREADS <= 512 ? 2 : 1)
+__global__ void __launch_bounds__(YFusedCfg<KIND, N>::THREADS, YFusedCfg<KIND, N>::THREADS <= 384 ? 2 : 1)
 d0_yfused_kernel(ModSpec spec, D0ScaleArgs a, double xi, int m1, cuDoubleComplex* __restrict__ data,
                  const cuDoubleComplex* __restrict__ Th, const double2* __restrict__ tw) {
     using Cfg = YFusedCfg<KIND, N>;
     constexpr int NC = Cfg::NC, SIN = Cfg::SIN, THREADS = Cfg::THREADS;
     constexpr int NG = 3 * NC;
-    extern __shared__ double2 yb[];  // [c][col][y]
+    extern __shared__ double2 yb[];  // [c][col][y] (padded), twiddles, table values [col][ky]
+    double2* tws = yb + SIN * yseq<N>();
+    double2* ths = tws + N;
     const int kx0 = blockIdx.x * YF_COLS;
     const int kzl = blockIdx.y;  // kz of this launch (a.kz0 + kzl globally)
+    const int kz = a.kz0 + kzl;
     const int64_t rowbase = (int64_t)kzl * m1;
-    // load the data rows, zero the padding
+    // every global read of the block as asynchronous copies into shared memory
+    // (all in flight at once), the zero padding with plain stores
+    auto cp16 = [](void* dst, const void* src) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(src));
+    };
+    for (int k = threadIdx.x; k < N; k += THREADS) cp16(tws + k, tw + k);
+    if (Th)
+        for (int e = threadIdx.x; e < YF_COLS * N; e += THREADS) {
+            const int col = e % YF_COLS, ky = e / YF_COLS;
+            if (kx0 + col < a.n0) cp16(ths + col * N + ky, Th + ((int64_t)kz * a.n1 + ky) * a.n0 + kx0 + col);
+        }
     for (int e = threadIdx.x; e < SIN * N; e += THREADS) {
         const int col = e % YF_COLS;
         const int t = e / YF_COLS;
         const int y = t % N, c = t / N;
-        double2 v = make_double2(0.0, 0.0);
-        if (y < m1 && kx0 + col < a.n0) {
-            const cuDoubleComplex g = data[c * a.cstride + (rowbase + y) * a.n0 + kx0 + col];
-            v = make_double2(g.x, g.y);
-        }
-        yb[(c * YF_COLS + col) * N + y] = v;
+        double2* dst = yb + (c * YF_COLS + col) * yseq<N>() + ypad(y);
+        if (y < m1 && kx0 + col < a.n0)
+            cp16(dst, data + c * a.cstride + (rowbase + y) * a.n0 + kx0 + col);
+        else
+            *dst = make_double2(0.0, 0.0);
     }
+    asm volatile("cp.async.wait_all;\n" ::);
     __syncthreads();
-    fft_all<N, 1, false, THREADS, SIN>(yb, SIN, tw);
+    fft_all<N, 1, false, THREADS, SIN>(yb, SIN, tws);
     // scale (d0_scale_kernel per (col, ky)): 3 outputs into sequences 0..2
-    const int kz = a.kz0 + kzl;
     for (int e = threadIdx.x; e < YF_COLS * N; e += THREADS) {
         const int col = e / N, ky = e - col * N;
         const int kx = kx0 + col;
@@ -358,7 +398,7 @@ d0_yfused_kernel(ModSpec spec, D0ScaleArgs a, double xi, int m1, cuDoubleComplex
             }
         }
         if (table) {
-            const cuDoubleComplex tv = Th[((int64_t)kz * a.n1 + ky) * a.n0 + kx];
+            const double2 tv = ths[col * N + ky];
 #pragma unroll
             for (int q2 = 0; q2 < NG; ++q2) {
                 const double x = re[q2], y = im[q2];
@@ -368,7 +408,7 @@ d0_yfused_kernel(ModSpec spec, D0ScaleArgs a, double xi, int m1, cuDoubleComplex
         }
         double2 in[NC];
 #pragma unroll
-        for (int c = 0; c < NC; ++c) in[c] = yb[(c * YF_COLS + col) * N + ky];
+        for (int c = 0; c < NC; ++c) in[c] = yb[(c * YF_COLS + col) * yseq<N>() + ypad(ky)];
 #pragma unroll
         for (int j = 0; j < 3; ++j) {
             double ar = 0.0, ai = 0.0;
@@ -377,17 +417,17 @@ d0_yfused_kernel(ModSpec spec, D0ScaleArgs a, double xi, int m1, cuDoubleComplex
                 ar += re[NC * j + c] * in[c].x - im[NC * j + c] * in[c].y;
                 ai += re[NC * j + c] * in[c].y + im[NC * j + c] * in[c].x;
             }
-            yb[(j * YF_COLS + col) * N + ky] = make_double2(fac * ar, fac * ai);
+            yb[(j * YF_COLS + col) * yseq<N>() + ypad(ky)] = make_double2(fac * ar, fac * ai);
         }
     }
     __syncthreads();
-    fft_all<N, 1, true, THREADS, SIN>(yb, 3 * YF_COLS, tw);
+    fft_all<N, 1, true, THREADS, SIN>(yb, 3 * YF_COLS, tws);
     for (int e = threadIdx.x; e < 3 * YF_COLS * m1; e += THREADS) {
         const int col = e % YF_COLS;
         const int t = e / YF_COLS;
         const int y = t % m1, j = t / m1;
         if (kx0 + col >= a.n0) continue;
-        const double2 v = yb[(j * YF_COLS + col) * N + y];
+        const double2 v = yb[(j * YF_COLS + col) * yseq<N>() + ypad(y)];
         data[j * a.cstride + (rowbase + y) * a.n0 + kx0 + col] = make_cuDoubleComplex(v.x, v.y);
     }
 }
@@ -415,7 +455,7 @@ void launch_yfused_n(int N, const ModSpec& spec, const D0ScaleArgs& sa, double x
 bool yfused_ok(int n1, int C) {
     if (!(n1 == 256 || n1 == 512 || n1 == 1024)) return false;
     // shared memory: C x 2 columns x n1 complex
-    return (size_t)C * YF_COLS * n1 * sizeof(double2) <= 200 * 1024;
+    return ((size_t)C * YF_COLS * (n1 + n1 / 8) + n1 + YF_COLS * n1) * sizeof(double2) <= 200 * 1024;
 }
 
 void fft_check(cufftResult r, const char* what) {
@@ -444,12 +484,20 @@ void D0Real::setup(const int m_[3], const int n_[3], int C_, cudaStream_t st) {
     Tin.ensure(sizeof(cuDoubleComplex) * C * slab);
     Tout.ensure(sizeof(cuDoubleComplex) * C * slab);
     cuda_check(cudaMemsetAsync(Tin.ptr, 0, sizeof(cuDoubleComplex) * C * slab, st), "d0 Tin zero");
-    if (yfused) {  // exp(-2 pi i k / n1), k < n1
-        std::vector<double2> h(n[1]);
-        for (int k = 0; k < n[1]; ++k) {
-            const long double ang = -2.0L * 3.14159265358979323846264338327950288L * k / n[1];
-            h[k] = make_double2((double)cosl(ang), (double)sinl(ang));
+    if (yfused) {  // per-stage twiddle tables (stage_radix / tw_offset order), padded to n1 entries
+        const int N = n[1];
+        std::vector<double2> h;
+        for (int ns = 1; ns < N; ns *= stage_radix(N, ns)) {
+            const int R = stage_radix(N, ns);
+            if (ns == 1) continue;
+            for (int r = 1; r < R; ++r)
+                for (int j = 0; j < ns; ++j) {
+                    const long double ang =
+                        -2.0L * 3.14159265358979323846264338327950288L * ((long long)j * r * (N / (ns * R))) / N;
+                    h.push_back(make_double2((double)cosl(ang), (double)sinl(ang)));
+                }
         }
+        h.resize(N, make_double2(0.0, 0.0));
         tw.ensure(sizeof(double2) * n[1]);
         cuda_check(cudaMemcpyAsync(tw.ptr, h.data(), sizeof(double2) * n[1], cudaMemcpyHostToDevice, st), "d0 tw");
         cuda_check(cudaStreamSynchronize(st), "d0 tw");

@@ -62,7 +62,7 @@ int env_default(int which) {
             return (e && e[0] == '0') ? 0 : 1;
         case SEWALD_OPT_D0_YFUSED:
             e = env("SEWALD_D0_YFUSED");
-            return (e && e[0] == '1') ? 1 : 0;
+            return (e && e[0] == '0') ? 0 : 1;
     }
     return 0;
 }
