@@ -40,8 +40,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # DRAM bytes (read + write) per launch of the dominant kernel from one
-# `ncu --set full` capture of the same bench command (profiles/r2_ncu_realspace_sym_v2.txt).
-TRAFFIC_BYTES = {"c2_stokeslet_d3_N1e6": 99_097_600 + 6_298_624}
+# `ncu --set full` capture of the kernel at the same workload (profiles/r2_ncu_realspace_sym_v4.txt).
+TRAFFIC_BYTES = {"c2_stokeslet_d3_N1e6": 98_096_128 + 3_664_128}
 
 # Algorithmic fp64 flops per accepted (directed) real-space pair of the
 # implemented evaluation, keyed (kernel, symmetric): ncu thread-level
