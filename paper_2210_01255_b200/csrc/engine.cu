@@ -331,8 +331,6 @@ void build_cell_grid(sewald_gpu_session* s) {
         return e ? atof(e) : 0.0;
     }();
     const bool sym_on = option(SEWALD_OPT_RS_SYM) != 0;
-    // pair-symmetric kernel (targets == sources): 28; separate targets: 40 (c4: 47.6 vs 49.3 ms)
-    const double ppc = ppc_env > 0.0 ? ppc_env : (s->same && sym_on ? 28.0 : 40.0);
     double target_w;
     if (refine > 0.0) {
         target_w = p.rc / refine;
@@ -340,6 +338,12 @@ void build_cell_grid(sewald_gpu_session* s) {
         double vol = 1.0;
         for (int a = 0; a < 3; ++a) vol *= std::max(a < p.d ? p.L[a] : hi[a] - lo[a], 1e-300);
         const double dens = s->N > 0 ? (double)s->N / vol : 1.0;
+        // pair-symmetric kernel (targets == sources): 28, or 40 with more than
+        // 5000 neighbours in the rc ball (c2 10.7k: 50.9 -> 50.3 ms, c3 19.7k:
+        // 102.3 -> 101.4; c5 2.5k: 51.5 vs 52.0 at 40); separate targets: 40 (c4:
+        // 47.6 vs 49.3 ms)
+        const double nbrs = dens * 4.18879020478639 * p.rc * p.rc * p.rc;
+        const double ppc = ppc_env > 0.0 ? ppc_env : (s->same && sym_on ? (nbrs > 5000.0 ? 40.0 : 28.0) : 40.0);
         target_w = std::cbrt(ppc / dens);
         target_w = std::min(std::max(target_w, p.rc / 8.0), p.rc / 2.0);
     }
