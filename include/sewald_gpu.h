@@ -16,6 +16,7 @@
 #ifndef SEWALD_GPU_H
 #define SEWALD_GPU_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -128,6 +129,13 @@ int sewald_gpu_set_stream(sewald_gpu_ctx* ctx, void* stream);
 int sewald_gpu_get_timings(const sewald_gpu_ctx* ctx, sewald_timings_c* out);
 /* 1 = record per-stage CUDA events (adds event overhead), 0 = off. */
 int sewald_gpu_set_profiling(sewald_gpu_ctx* ctx, int enabled);
+
+/* Pinned host memory of the context (>= bytes, valid until the next call
+ * with a larger size or sewald_gpu_destroy): passed as the u_out of the
+ * host-buffer entry points it receives the result by DMA without staging.
+ * The C++ drop-in uses it to overlap the allocation of its returned vector
+ * with the device work. */
+int sewald_gpu_host_buffer(sewald_gpu_ctx* ctx, size_t bytes, void** out);
 
 /* Cumulative number of engine kernels launched on this context. */
 int64_t sewald_gpu_launch_count(const sewald_gpu_ctx* ctx);

@@ -87,6 +87,7 @@ _SIGS = [
     ("sewald_gpu_set_stream", C.c_int, [VP, VP]),
     ("sewald_gpu_get_timings", C.c_int, [VP, C.POINTER(sewald_timings_c)]),
     ("sewald_gpu_set_profiling", C.c_int, [VP, C.c_int]),
+    ("sewald_gpu_host_buffer", C.c_int, [VP, C.c_size_t, C.POINTER(VP)]),
     ("sewald_gpu_fp64_peak", C.c_int, [VP, DP]),
     ("sewald_gpu_launch_count", I64, [VP]),
     ("sewald_gpu_set_option", C.c_int, [C.c_int, C.c_int]),

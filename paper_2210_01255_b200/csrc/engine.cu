@@ -1150,6 +1150,18 @@ int sewald_gpu_get_timings(const sewald_gpu_ctx* ctx, sewald_timings_c* out) {
     return SEWALD_OK;
 }
 
+int sewald_gpu_host_buffer(sewald_gpu_ctx* ctx, size_t bytes, void** out) {
+    if (!ctx || !out) return SEWALD_EINVAL;
+    try {
+        cuda_check(cudaSetDevice(ctx->device), "set device");
+        *out = ctx->pout.ensure(std::max<size_t>(bytes, 1));
+        return SEWALD_OK;
+    } catch (const std::exception& e) {
+        ctx->err = e.what();
+        return SEWALD_ECUDA;
+    }
+}
+
 int sewald_gpu_set_profiling(sewald_gpu_ctx* ctx, int enabled) {
     if (!ctx) return SEWALD_EINVAL;
     ctx->profiling = enabled != 0;

@@ -75,6 +75,7 @@ struct sewald_gpu_ctx {
     sewald_b200::DevBuf hx, hf, hnu, hxt, hu;
     // pinned staging of pageable host inputs / output (parallel host copies)
     sewald_b200::PinnedBuf px, pf, pnu, pxt, pu;
+    sewald_b200::PinnedBuf pout;  // sewald_gpu_host_buffer
 };
 
 struct sewald_gpu_session {
