@@ -36,6 +36,13 @@ constexpr int SM_THREADS = 32 * SM_WARPS;
 constexpr int SM_TG = 32;  // sources per table group (8 k-steps of 4)
 constexpr int SM_LS = 24;  // padded table width (z: 3 n-blocks of 8)
 
+// v >= 0 reduced mod n by subtraction (a region coordinate exceeds the grid
+// by less than the region edge): replaces an integer division per flushed row
+__device__ __forceinline__ int wrap_up(int v, int n) {
+    while (v >= n) v -= n;
+    return v;
+}
+
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
     asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(d0), "+d"(d1)
@@ -126,8 +133,8 @@ spread_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
             if (row >= ROWS) continue;
             const int a = row / L, b = row - a * L;
             int gx = X0 + a, gy = Y0 + b;
-            if (g.d > 0) gx %= g.n[0]; else if (gx >= g.n[0]) continue;
-            if (g.d > 1) gy %= g.n[1]; else if (gy >= g.n[1]) continue;
+            if (g.d > 0) gx = wrap_up(gx, g.n[0]); else if (gx >= g.n[0]) continue;
+            if (g.d > 1) gy = wrap_up(gy, g.n[1]); else if (gy >= g.n[1]) continue;
             double* col = oc + ((int64_t)gx * g.n[1] + gy) * g.n[2];
 #pragma unroll
             for (int nb = 0; nb < 3; ++nb)
@@ -136,7 +143,7 @@ spread_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
                     const int z = nb * 8 + 2 * (lane & 3) + h;
                     if (z >= L) continue;
                     int gz = Z0 + z;
-                    if (g.d > 2) gz %= g.n[2]; else if (gz >= g.n[2]) continue;
+                    if (g.d > 2) gz = wrap_up(gz, g.n[2]); else if (gz >= g.n[2]) continue;
                     const double v = acc[j][nb][h];
                     if (v != 0.0) atomicAdd(col + gz, v);
                 }
@@ -339,8 +346,8 @@ spread_tile_mma_cached_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz
                 if (row >= ROWS) continue;
                 const int a = row / L, b = row - a * L;
                 int gx = X0 + a, gy = Y0 + b;
-                if (g.d > 0) gx %= g.n[0]; else if (gx >= g.n[0]) continue;
-                if (g.d > 1) gy %= g.n[1]; else if (gy >= g.n[1]) continue;
+                if (g.d > 0) gx = wrap_up(gx, g.n[0]); else if (gx >= g.n[0]) continue;
+                if (g.d > 1) gy = wrap_up(gy, g.n[1]); else if (gy >= g.n[1]) continue;
                 double* col = oc + ((int64_t)gx * g.n[1] + gy) * g.n[2];
 #pragma unroll
                 for (int nb = 0; nb < 3; ++nb)
@@ -349,7 +356,7 @@ spread_tile_mma_cached_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz
                         const int z = nb * 8 + 2 * (lane & 3) + h;
                         if (z >= L) continue;
                         int gz = Z0 + z;
-                        if (g.d > 2) gz %= g.n[2]; else if (gz >= g.n[2]) continue;
+                        if (g.d > 2) gz = wrap_up(gz, g.n[2]); else if (gz >= g.n[2]) continue;
                         const double v = acc[j][nb][h];
                         if (v != 0.0) atomicAdd(col + gz, v);
                     }
@@ -473,8 +480,8 @@ spread_tile_mma_wide_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, 
                 }
                 if (row >= ROWS) continue;
                 int gx = X0 + a, gy = Y0 + b;
-                if (g.d > 0) gx %= g.n[0]; else if (gx >= g.n[0]) continue;
-                if (g.d > 1) gy %= g.n[1]; else if (gy >= g.n[1]) continue;
+                if (g.d > 0) gx = wrap_up(gx, g.n[0]); else if (gx >= g.n[0]) continue;
+                if (g.d > 1) gy = wrap_up(gy, g.n[1]); else if (gy >= g.n[1]) continue;
                 double* col = oc + ((int64_t)gx * g.n[1] + gy) * g.n[2];
 #pragma unroll
                 for (int nb = 0; nb < NB; ++nb)
@@ -483,7 +490,7 @@ spread_tile_mma_wide_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, 
                         const int z = nb * 8 + 2 * (lane & 3) + h;
                         if (z >= L) continue;
                         int gz = Z0 + z;
-                        if (g.d > 2) gz %= g.n[2]; else if (gz >= g.n[2]) continue;
+                        if (g.d > 2) gz = wrap_up(gz, g.n[2]); else if (gz >= g.n[2]) continue;
                         const double v = acc[nb][h];
                         if (v != 0.0) atomicAdd(col + gz, v);
                     }

@@ -1,1 +1,2 @@
-for c in 2 3 5; do echo "c$c $(timeout 300 python tools/rs_time.py $c 5 2>&1 | tail -1)"; done
+git_base=paper_2210_01255_b200/lib/var_base/libsewald_gpu.so
+for c in 2 3 4; do python tools/sg_time.py $c 5 ""; SEWALD_LIB=$git_base python tools/sg_time.py $c 5 ""; done
