@@ -346,8 +346,14 @@ spread_tile_mma_cached_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz
                 if (row >= ROWS) continue;
                 const int a = row / L, b = row - a * L;
                 int gx = X0 + a, gy = Y0 + b;
-                if (g.d > 0) gx = wrap_up(gx, g.n[0]); else if (gx >= g.n[0]) continue;
-                if (g.d > 1) gy = wrap_up(gy, g.n[1]); else if (gy >= g.n[1]) continue;
+                if (gx >= g.n[0]) {
+                    if (g.d <= 0) continue;
+                    gx = wrap_up(gx, g.n[0]);
+                }
+                if (gy >= g.n[1]) {
+                    if (g.d <= 1) continue;
+                    gy = wrap_up(gy, g.n[1]);
+                }
                 double* col = oc + ((int64_t)gx * g.n[1] + gy) * g.n[2];
 #pragma unroll
                 for (int nb = 0; nb < 3; ++nb)
@@ -356,7 +362,10 @@ spread_tile_mma_cached_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz
                         const int z = nb * 8 + 2 * (lane & 3) + h;
                         if (z >= L) continue;
                         int gz = Z0 + z;
-                        if (g.d > 2) gz = wrap_up(gz, g.n[2]); else if (gz >= g.n[2]) continue;
+                        if (gz >= g.n[2]) {  // rare: the region crosses the grid's end
+                            if (g.d <= 2) continue;
+                            gz = wrap_up(gz, g.n[2]);
+                        }
                         const double v = acc[j][nb][h];
                         if (v != 0.0) atomicAdd(col + gz, v);
                     }
