@@ -30,6 +30,7 @@ class Config:
     tol: float
     xi: float
     window: WindowKind
+    clustered: bool = False  # positions only in [0, 1/3)^3 and [2/3, 1)^3
 
 
 CONFIGS = {
@@ -38,6 +39,12 @@ CONFIGS = {
     3: Config(3, "c3_stresslet_d2_N1e6", Kernel.stresslet, 2, (1.0, 1.0, 1.0), 1_000_000, None, 1e-8, 33.5, WindowKind.pkb),
     4: Config(4, "c4_rotlet_d1_N5e5", Kernel.rotlet, 1, (1.0, 1.0, 1.0), 500_000, 500_000, 1e-10, 34.0, WindowKind.tg),
     5: Config(5, "c5_stokeslet_d0_N4e6", Kernel.stokeslet, 0, (2.0, 1.0, 1.0), 4_000_000, None, 1e-6, 68.5, WindowKind.pkb),
+    # not a BASELINE config: the paper's clustered random system (two dense
+    # cubes) at c2's size and parameters - a load-balance
+    # check (13.5x the local density: 13.5x the real-space pairs, tiles with
+    # 13.5x the points, most tiles and cell rows empty)
+    6: Config(6, "c6_stokeslet_d3_N1e6_clustered", Kernel.stokeslet, 3, (1.0, 1.0, 1.0), 1_000_000, None, 1e-8, 37.0,
+              WindowKind.pkb, clustered=True),
 }
 
 
@@ -49,6 +56,9 @@ def generate(cfg: Config, N: Optional[int] = None, Nt: Optional[int] = None, see
     rng = np.random.default_rng(1000 + cfg.index if seed is None else seed)
     L = np.asarray(cfg.L)
     x = rng.random((n, 3)) * L
+    if cfg.clustered:  # half the points in each of the two cubes of side L/3
+        x = x / 3.0
+        x[n // 2:] += 2.0 * L / 3.0
     f = rng.standard_normal((n, 3))
     nu = None
     if cfg.kind == Kernel.stresslet:
