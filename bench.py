@@ -257,6 +257,9 @@ def run_reference(args, cfg_index):
     if not R.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libsewald_ref.so not built"}))
         return
+    if cfg_index not in BI.CONFIGS:
+        print(json.dumps({"impl": "reference", "unavailable": f"config {cfg_index} is not a BASELINE config"}))
+        return
     wall0 = time.perf_counter()
     cfg = BI.CONFIGS[cfg_index]
     x, f, nu, xt = BI.generate(cfg_index)
