@@ -371,6 +371,43 @@ int64_t sewald_gpu_session_pair_count(sewald_gpu_session* s, int reset);
 /* Whole pipeline on one GPU: spread all, solve, evaluate all (parts = 7). */
 int sewald_gpu_session_run(sewald_gpu_session* s, int precompute_0p, double* u_dev);
 
+/* ---- analytic oracles (SPEC.md module `reference`) ----
+ * Slow, independently derived sums for validating the fast path (the
+ * reference ships this module as a stub, proj/src/reference.cpp:1). Host
+ * buffers in and out; sizes meant for validation (N * Nt * modes work).
+ * Periodic sums run over k_i = 2 pi j / L_i, -kmax_i <= j <= kmax_i - 1
+ * (PAPER.md:1117-1130), real part kept. */
+
+/* direct_sum_0p: plain O(N Nt) bare-kernel
+ * sum; starred skips n == t (Nt == N). A target on a source otherwise ->
+ * SEWALD_EDOMAIN. */
+int sewald_gpu_direct_sum_0p(sewald_gpu_ctx* ctx, int kind, const double* x, const double* f, const double* nu,
+                             int64_t N, const double* xt, int64_t Nt, int starred, double* u_out);
+/* direct_ewald_fourier_3p: the k != 0 Fourier
+ * sum over the (2 kmax)^3 cube plus the stresslet zero mode. */
+int sewald_gpu_ewald_fourier_3p(sewald_gpu_ctx* ctx, int kind, const double L[3], double xi, const int kmax[3],
+                                const double* x, const double* f, const double* nu, int64_t N, const double* xt,
+                                int64_t Nt, double* u_out);
+/* fourier_reference_potential: d = 2
+ * Appendix-A q-sums, d = 1 Appendix-B q-sums (gauge constants ell = 1), d = 3
+ * forwards to sewald_gpu_ewald_fourier_3p. kmax has d entries. */
+int sewald_gpu_fourier_reference_potential(sewald_gpu_ctx* ctx, int kind, int d, const double L[3], double xi,
+                                           const int* kmax, const double* x, const double* f, const double* nu,
+                                           int64_t N, const double* xt, int64_t Nt, double* u_out);
+/* q2p / q2p_zero / q1p / q1p_zero pointwise: args = 3 per
+ * point, (k1, k2, r3) for d = 2 or (k1, r2, r3) for d = 1; out = per point
+ * 3 x C complex (re, im) entries [j][c], c = l (C = 3) or 3 l + m (stresslet,
+ * C = 9). */
+int sewald_gpu_qtensor(sewald_gpu_ctx* ctx, int kind, int d, int zero_mode, int64_t n, const double* args,
+                       double xi, double* out);
+/* Incomplete Bessel K_nu(a, b), nu = -1, 0, 1, 2 (PAPER.md Knu-def), device
+ * quadrature used by the d = 1 oracle: out = 4 values per (a, b). */
+int sewald_gpu_incomplete_bessel_k4(sewald_gpu_ctx* ctx, int64_t n, const double* a, const double* b,
+                                    double* out);
+/* rms_error / rel_rms_error: n targets, 3 doubles each;
+ * SEWALD_EDOMAIN when rel_err is requested and u_ref is zero. */
+int sewald_rms_error(const double* u, const double* u_ref, int64_t n, double* abs_err, double* rel_err);
+
 #ifdef __cplusplus
 }
 #endif

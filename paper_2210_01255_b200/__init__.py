@@ -16,3 +16,4 @@ from .api import (Cell, DeviceError, DomainError, Engine, EstimateReport, EwaldP
                   set_kernel_option, kernel_options, MultiEngine)
 
 __all__ = [n for n in dir() if not n.startswith("_")]
+from . import analytic  # noqa: E402,F401  (GPU analytic oracles, SPEC module 'reference')

@@ -139,6 +139,13 @@ _SIGS = [
     ("sewald_gpu_session_d0_middle", C.c_int, [VP, C.c_int, VP, C.c_int, IP, C.c_int, C.c_int, VP]),
     ("sewald_gpu_session_d0_inverse", C.c_int, [VP, C.c_int, VP, C.c_int, C.c_int, C.c_int, IP, VP]),
     ("sewald_gpu_session_set_flow", C.c_int, [VP, VP]),
+    ("sewald_gpu_direct_sum_0p", C.c_int, [VP, C.c_int, DP, DP, DP, I64, DP, I64, C.c_int, DP]),
+    ("sewald_gpu_ewald_fourier_3p", C.c_int, [VP, C.c_int, DP, C.c_double, IP, DP, DP, DP, I64, DP, I64, DP]),
+    ("sewald_gpu_fourier_reference_potential", C.c_int, [VP, C.c_int, C.c_int, DP, C.c_double, IP, DP, DP, DP,
+                                                         I64, DP, I64, DP]),
+    ("sewald_gpu_qtensor", C.c_int, [VP, C.c_int, C.c_int, C.c_int, I64, DP, C.c_double, DP]),
+    ("sewald_gpu_incomplete_bessel_k4", C.c_int, [VP, I64, DP, DP, DP]),
+    ("sewald_rms_error", C.c_int, [DP, DP, I64, DP, DP]),
 ]
 
 EXPORTED = [s[0] for s in _SIGS]
