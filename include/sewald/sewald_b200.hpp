@@ -349,6 +349,21 @@ std::vector<Vec3> full_potential(const SourceSystem& system, const TargetSet& ta
                                  const EwaldParams& params, const SePipelineOptions& opt = {});
 
 // ---- B200 extension (not in the reference API) -------------------------------------
+
+// ---- analytic oracles (SPEC.md module `reference`; the
+// reference ships it as a stub, proj/src/reference.cpp:1). Slow direct sums
+// on the GPU for validating the fast path (include/sewald_gpu.h "analytic
+// oracles"); periodic sums over -kmax_i <= j <= kmax_i - 1 per periodic axis.
+std::vector<Vec3> direct_sum_0p(const SourceSystem& system, const TargetSet& targets, bool starred);
+std::vector<Vec3> direct_ewald_fourier_3p(const SourceSystem& system, const TargetSet& targets, double xi,
+                                          const std::array<int, 3>& kmax);
+std::vector<Vec3> fourier_reference_potential(const SourceSystem& system, const TargetSet& targets, double xi,
+                                              const std::array<int, 3>& kmax);
+// kmax per axis with the omitted modes below e^{-39} of the largest.
+std::array<int, 3> oracle_kmax(double xi, const Cell& cell);
+double rms_error(const std::vector<Vec3>& u, const std::vector<Vec3>& u_ref);
+double rel_rms_error(const std::vector<Vec3>& u, const std::vector<Vec3>& u_ref);
+
 namespace b200 {
 // full_potential / se_fourier_potential on these GPUs of this node (one
 // process, NVLink peer memory; include/sewald_gpu.h sewald_gpu_multi_*).

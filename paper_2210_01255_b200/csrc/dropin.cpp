@@ -733,4 +733,73 @@ std::vector<Vec3> realspace_potential(const SourceSystem& system, const TargetSe
     return u;
 }
 
+// ---- analytic oracles (C-ABI sewald_gpu_direct_sum_0p / _ewald_fourier_3p /
+// _fourier_reference_potential, csrc/analytic.cu)
+
+namespace {
+TargetSet oracle_targets(const SourceSystem& system, const TargetSet& targets) {
+    validate_system(system);
+    for (const Vec3& p : targets.x)
+        for (double c : p)
+            if (!std::isfinite(c)) throw std::invalid_argument("target coordinates must be finite");
+    return targets.same_as_sources ? TargetSet{system.x, true} : targets;
+}
+}  // namespace
+
+std::vector<Vec3> direct_sum_0p(const SourceSystem& system, const TargetSet& targets, bool starred) {
+    if (system.d != 0) throw std::invalid_argument("direct_sum_0p needs d = 0");
+    const TargetSet t = oracle_targets(system, targets);
+    if (starred && t.x.size() != system.size())
+        throw std::invalid_argument("starred evaluation needs one target per source");
+    std::vector<Vec3> u(t.x.size());
+    std::lock_guard<std::mutex> lk(g_mu);
+    check_ctx(sewald_gpu_direct_sum_0p(context(), kernel_id(system.kind), D(system.x), D(system.f),
+                                       system.kind == Kernel::stresslet ? D(system.nu) : nullptr,
+                                       static_cast<int64_t>(system.size()), D(t.x), static_cast<int64_t>(t.x.size()),
+                                       starred ? 1 : 0, reinterpret_cast<double*>(u.data())));
+    return u;
+}
+
+std::vector<Vec3> fourier_reference_potential(const SourceSystem& system, const TargetSet& targets, double xi,
+                                              const std::array<int, 3>& kmax) {
+    const TargetSet t = oracle_targets(system, targets);
+    std::vector<Vec3> u(t.x.size());
+    std::lock_guard<std::mutex> lk(g_mu);
+    check_ctx(sewald_gpu_fourier_reference_potential(
+        context(), kernel_id(system.kind), system.d, system.cell.L.data(), xi, kmax.data(), D(system.x),
+        D(system.f), system.kind == Kernel::stresslet ? D(system.nu) : nullptr, static_cast<int64_t>(system.size()),
+        D(t.x), static_cast<int64_t>(t.x.size()), reinterpret_cast<double*>(u.data())));
+    return u;
+}
+
+std::vector<Vec3> direct_ewald_fourier_3p(const SourceSystem& system, const TargetSet& targets, double xi,
+                                          const std::array<int, 3>& kmax) {
+    if (system.d != 3) throw std::invalid_argument("direct_ewald_fourier_3p needs d = 3");
+    return fourier_reference_potential(system, targets, xi, kmax);
+}
+
+std::array<int, 3> oracle_kmax(double xi, const Cell& cell) {
+    const double kc = 2.0 * xi * std::sqrt(39.0);
+    std::array<int, 3> k{};
+    for (int a = 0; a < 3; ++a) k[a] = static_cast<int>(std::ceil(kc * cell.L[a] / (2.0 * M_PI))) + 1;
+    return k;
+}
+
+double rms_error(const std::vector<Vec3>& u, const std::vector<Vec3>& u_ref) {
+    if (u.size() != u_ref.size()) throw std::invalid_argument("rms error needs equal lengths");
+    if (u.empty()) throw std::invalid_argument("rms error of an empty set");
+    double a = 0.0;
+    rethrow(sewald_rms_error(D(u), D(u_ref), static_cast<int64_t>(u.size()), &a, nullptr), "rms error");
+    return a;
+}
+
+double rel_rms_error(const std::vector<Vec3>& u, const std::vector<Vec3>& u_ref) {
+    if (u.size() != u_ref.size()) throw std::invalid_argument("rms error needs equal lengths");
+    if (u.empty()) throw std::invalid_argument("rms error of an empty set");
+    double a = 0.0, r = 0.0;
+    rethrow(sewald_rms_error(D(u), D(u_ref), static_cast<int64_t>(u.size()), &a, &r),
+            "relative rms error of a zero reference");
+    return r;
+}
+
 }  // namespace sewald
