@@ -63,6 +63,11 @@ def parse():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", type=int, default=2)
+    # split parameter override (not the BASELINE workload: BASELINE.md §3 pins xi
+    # per config): the paper's N_rc balancing of real-space vs Fourier work
+    # applied on the B200; parity is then reported as
+    # xi-invariance against the pinned-xi fixture (tau level, not 1e-12)
+    ap.add_argument("--xi", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-stages", action="store_true", default=True)
@@ -161,7 +166,7 @@ def cpu_model():
     return "unknown"
 
 
-def fixture_parity(u, cfg_index):
+def fixture_parity(u, cfg_index, xi_override=False):
     """rel-RMS of u against the reference's own full-size run stored in
     tests/golden/fullsize_c<k>.npz (sampled targets) and the worst
     all-target projection deviation (see tests/test_fullsize_parity.py)."""
@@ -177,8 +182,11 @@ def fixture_parity(u, cfg_index):
     rng = np.random.default_rng(int(g["proj_seed"]))
     pj = np.array([float(np.sum(rng.standard_normal(u.shape) * u)) for _ in range(len(g["proj_u"]))])
     pdev = float(np.max(np.abs(pj - g["proj_u"])) / np.sqrt(float(g["ss_u"])))
-    return {"fixture": os.path.relpath(path, ROOT), "rel_rms_sampled": rel, "n_sampled": int(len(idx)),
-            "proj_dev_all_targets": pdev, "bar": 1e-12}
+    out = {"fixture": os.path.relpath(path, ROOT), "rel_rms_sampled": rel, "n_sampled": int(len(idx)),
+           "proj_dev_all_targets": pdev, "bar": 1e-12}
+    if xi_override:  # another xi: same sum to the tolerance, not to rounding
+        out.update({"bar": 1e-7, "note": "xi differs from the fixture's pinned xi: xi-invariance at the tau level"})
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -470,7 +478,7 @@ def run_ours(args, cfg):
     # parity of the device-resident result against the reference's own run
     if rank == 0 and line is not None:
         torch.cuda.synchronize()
-        line["parity_vs_fixture"] = fixture_parity(u_step, cfg.index)
+        line["parity_vs_fixture"] = fixture_parity(u_step, cfg.index, args.xi is not None)
 
     # end-to-end through the public API with pinned host buffers: full_potential
     # on 1 GPU, parallel.full_potential_sharded on N (max over ranks)
@@ -506,7 +514,7 @@ def run_ours(args, cfg):
             line["e2e"] = {"value": Nt / e2e_s, "unit": "targets/s", "h2d_bytes_per_step": int(h2d) * ws,
                            "d2h_bytes_per_step": int(pout.nbytes), "ms_per_call": e2e_s * 1e3,
                            "api": api, "timing": "host wall clock per call, max over ranks, median of calls"}
-            par = fixture_parity(uo, cfg.index)
+            par = fixture_parity(uo, cfg.index, args.xi is not None)
             if par is not None:
                 line["e2e"]["parity_vs_fixture"] = par
 
@@ -563,7 +571,11 @@ def main():
         run_reference(args, args.config)
     else:
         from paper_2210_01255_b200.workloads import CONFIGS
-        run_ours(args, CONFIGS[args.config])
+        cfg = CONFIGS[args.config]
+        if args.xi is not None:
+            import dataclasses
+            cfg = dataclasses.replace(cfg, xi=float(args.xi), name=f"{cfg.name}_xi{args.xi:g}")
+        run_ours(args, cfg)
 
 
 if __name__ == "__main__":
