@@ -154,7 +154,7 @@ enum {
                                      1 auto (large target sets), 2 always */
     SEWALD_OPT_GATHER = 1,        /* -1 auto, 0 warp per target, 1 z-sweep, 2 tiles */
     SEWALD_OPT_GATHER_MMA = 2,    /* tiled gather: 1 tensor-core form (P <= 16), 0 CUDA-core form */
-    SEWALD_OPT_GATHER_L = 3,      /* tiled gather region edge: 0 auto, 15 or 19 */
+    SEWALD_OPT_GATHER_L = 3,      /* tiled gather region edge: 0 auto, 15, 19, 23 or 31 */
     SEWALD_OPT_SPREAD_SWEEP = 4,  /* -1 auto (P <= 24), 0 off, 1 on */
     SEWALD_OPT_SPREAD_MMA = 5,    /* 1 tensor-core spread for 15 <= P <= 32, 0 off */
     SEWALD_OPT_SPREAD_MMA_L = 6,  /* tensor-core spread region edge for P <= 20: 23 or 19 */

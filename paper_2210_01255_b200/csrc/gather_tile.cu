@@ -592,11 +592,29 @@ TileShape tile_shape(const DevGrid& g, int P, int64_t Nt) {
         const double tpt = cells > 0 ? (double)Nt / cells * b15 * b15 * b15 : 0.0;
         if (forced_l == 15 || (forced_l == 0 && tpt >= 12.0)) s.B = b15;
     }
+    // Sparse targets (register-A kernel): L = 23 tiles (B = 24 - P) when an L = 19
+    // tile would hold fewer than 24 targets on average - every chunk loads its
+    // whole region, so small chunks are load-bound. c2 workload at xi = 60
+    // (M = 204, 7.5 targets per L = 19 tile): 6.73 -> 3.63 ms; xi = 70: 10.8 ->
+    // 4.3 ms; xi = 45 (16.9 per tile) 3.76 -> 3.38 ms; at xi = 37 (30 per tile)
+    // L = 19 stays ahead (2.84 vs 3.38 ms).
+    // L = 31 (B = 32 - P, forced only) measured slower in all three.
+    if (P <= 16 && s.B == 20 - P && forced_l == 0 && option(SEWALD_OPT_GATHER_WIDE) == 2) {
+        const double b = s.B;
+        const double tpt19 = (double)Nt * b * b * b / ((double)g.n[0] * g.n[1] * g.n[2]);
+        if (tpt19 < 24.0) s.B = 24 - P;
+    }
+    if ((forced_l == 23 || forced_l == 31) && P <= 20 && option(SEWALD_OPT_GATHER_WIDE) == 2) s.B = forced_l + 1 - P;
     s.L = s.B + P - 1;
     for (int ax = 0; ax < 3; ++ax) s.nt[ax] = (g.n[ax] + s.B - 1) / s.B;
     s.ntiles = (int64_t)s.nt[0] * s.nt[1] * s.nt[2];
     s.tpt = s.ntiles > 0 ? (double)Nt / (double)s.ntiles : 0.0;
     if (s.ntiles >= (int64_t(1) << 31)) s.ok = false;
+    if (s.L == 31) {  // register-A tiles only (the L^3 region does not fit in shared memory)
+        s.smem = wide_smem_bytes(s.L);
+        if ((int64_t)g.n[0] * g.n[1] * g.n[2] >= (int64_t(1) << 31)) s.ok = false;
+        return s;
+    }
     const int pad = 2 * GT_PMAX * s.L + 2 * GT_PMAX;
     s.smem = sizeof(double) * ((size_t)s.L * s.L * s.L + pad + GT_WARPS * 3 * GT_PMAX) +
              sizeof(int) * ((size_t)s.L * s.L + s.L);

@@ -72,7 +72,7 @@ bool valid(int which, int v) {
         case SEWALD_OPT_RS_SYM: return v >= 0 && v <= 2;
         case SEWALD_OPT_GATHER: return v >= -1 && v <= 2;
         case SEWALD_OPT_GATHER_MMA: return v == 0 || v == 1;
-        case SEWALD_OPT_GATHER_L: return v == 0 || v == 15 || v == 19;
+        case SEWALD_OPT_GATHER_L: return v == 0 || v == 15 || v == 19 || v == 23 || v == 31;
         case SEWALD_OPT_SPREAD_SWEEP: return v >= -1 && v <= 1;
         case SEWALD_OPT_SPREAD_MMA: return v == 0 || v == 1;
         case SEWALD_OPT_SPREAD_MMA_L: return v == 19 || v == 23;

@@ -20,6 +20,9 @@ from paper_2210_01255_b200.workloads import CONFIGS, generate  # noqa: E402
 cfg = CONFIGS[int(sys.argv[1]) if len(sys.argv) > 1 else 2]
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
 variants = sys.argv[3:] or [""]
+if os.environ.get("SG_XI"):  # another split parameter (bench.py --xi)
+    import dataclasses
+    cfg = dataclasses.replace(cfg, xi=float(os.environ["SG_XI"]))
 x, f, nu, xt = generate(cfg)
 sysm = S.SourceSystem(cfg.kind, S.Cell(cfg.L), cfg.d, x, f, nu)
 p = S.select_parameters(cfg.kind, cfg.d, sysm.cell, S.source_quantity(sysm), cfg.xi, S.ToleranceSpec(cfg.tol),
