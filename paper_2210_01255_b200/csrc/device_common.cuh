@@ -57,6 +57,38 @@ __device__ __forceinline__ double window_eval(const DevWindow& w, double r) {
     return cyl_bessel_i0(w.beta * sqrt(arg)) / w.i0_beta;
 }
 
+// The P taps window_eval(w, ((j0 + p) - rel) * h), p < P, into out[0..P):
+// the same per-tap arithmetic (bit-identical values), four taps interleaved
+// so their division and Horner chains overlap (a thread evaluating its taps
+// one after another is latency-bound: the taps kernel of the c2 gather took
+// 0.41 ms for 1e6 targets).
+__device__ __forceinline__ void window_taps(const DevWindow& w, int j0, double rel, double h, double* out,
+                                            int stride = 1) {
+    const int P = w.P;
+    int p = 0;
+    if (w.kind == 1) {
+        for (; p + 4 <= P; p += 4) {
+            double r[4], u[4], acc[4];
+            const double* c[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                r[q] = ((double)(j0 + p + q) - rel) * h;
+                int l = (int)floor(r[q] / w.h);
+                l = l < -w.P / 2 ? -w.P / 2 : (l > w.P / 2 - 1 ? w.P / 2 - 1 : l);
+                u[q] = 2.0 * (r[q] - l * w.h) / w.h - 1.0;
+                c[q] = w.coef + (l + w.P / 2) * (w.nu + 1);
+                acc[q] = 0.0;
+            }
+            for (int i = w.nu; i >= 0; --i)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) acc[q] = c[q][i] + acc[q] * u[q];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) out[(p + q) * stride] = fabs(r[q]) > w.half_width ? 0.0 : acc[q];
+        }
+    }
+    for (; p < P; ++p) out[p * stride] = window_eval(w, ((double)(j0 + p) - rel) * h);
+}
+
 // Stencil start index and relative coordinate along one axis
 // (fourier.cpp:174-176): rel = (x - x0)/h, j0 = ceil(rel - P/2).
 __device__ __forceinline__ void stencil_origin(const DevGrid& g, int P, int ax, double x,

@@ -427,13 +427,8 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
                 const int sw = ax < g.d ? wrap_index(j0, g.n[ax]) : j0;
                 const int o = sw - (ax == 0 ? X0 : (ax == 1 ? Y0 : Z0));
                 if (ax == 0) ox[t] = o;
-                for (int p = 0; p < P; ++p) {
-                    const double v = window_eval(ftg->win, ((double)(j0 + p) - rel) * g.h);
-                    const int k = o + p;
-                    if (ax == 2) wz[t * LS + k] = v;
-                    else if (ax == 0) wx[k * WG_TMAX + t] = v;
-                    else wy[k * WG_TMAX + t] = v;
-                }
+                if (ax == 2) window_taps(ftg->win, j0, rel, g.h, wz + t * LS + o);
+                else window_taps(ftg->win, j0, rel, g.h, (ax == 0 ? wx : wy) + o * WG_TMAX + t, WG_TMAX);
             }
         } else
         for (int t = warp; t < nblk * 8; t += MM_WARPS) {

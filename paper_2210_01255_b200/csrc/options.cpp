@@ -78,7 +78,7 @@ bool valid(int which, int v) {
         case SEWALD_OPT_SPREAD_MMA_L: return v == 19 || v == 23;
         case SEWALD_OPT_SPREAD_CACHED: return v == 0 || v == 1;
         case SEWALD_OPT_SPREAD_ROWSWEEP: return v == 0 || v == 1;
-        case SEWALD_OPT_SPREAD_FUSED: return v == 0 || v == 1;
+        case SEWALD_OPT_SPREAD_FUSED: return v == 0 || v == 1 || v == 2;
         case SEWALD_OPT_GATHER_WIDE: return v >= 0 && v <= 2;
         case SEWALD_OPT_GATHER_FUSED: return v == 0 || v == 1;
         case SEWALD_OPT_SPREAD_SORT: return v == 0 || v == 1;

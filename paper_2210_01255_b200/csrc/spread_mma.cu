@@ -177,6 +177,9 @@ size_t cached_smem_bytes() {
 // thread per (axis, source), axis-major, so a warp's PKB coefficient reads
 // are uniform. Measured at c2 (C = 3): 4.31 vs 4.40 ms with the taps kernel;
 // c3 (C = 9): 12.7 vs 12.2 ms, so it is the default for 3 components only.
+// With the taps evaluated four at a time (window_taps) the staging got
+// cheaper: c2 3.52 -> 3.26 ms, xi = 63 5.57 -> 4.96; c3 fused (option 2)
+// 10.22 vs 10.01 ms unfused, still off for C = 9.
 struct FusedSrc {
     const double* x;        // positions of the spread slice (AoS)
     const double* f;        // strengths
@@ -260,7 +263,7 @@ spread_tile_mma_cached_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz
                 const int o = sw - (ax == 0 ? X0 : (ax == 1 ? Y0 : Z0));
                 if (ax == 0) ox[t] = o;
                 double* row = ax == 0 ? wx[t] : (ax == 1 ? wy[t] : wz[t]);
-                for (int p = 0; p < P; ++p) row[o + p] = window_eval(fsrc->win, ((double)(j0 + p) - rel) * g.h);
+                window_taps(fsrc->win, j0, rel, g.h, row + o);
             }
         } else {
             // tables of the chunk: warp per source, lane = region index
@@ -550,8 +553,10 @@ void launch_spread_mma_bucket(const DevGrid& g, int P, const SpreadMmaShape& s, 
 }
 
 bool spread_mma_fused_ok(const SpreadMmaShape& s, int C) {
-    return s.ok && s.L <= 23 && C == 3 && option(SEWALD_OPT_SPREAD_CACHED) != 0 &&
-           !option(SEWALD_OPT_SPREAD_ROWSWEEP) && option(SEWALD_OPT_SPREAD_FUSED) != 0;
+    // 1: three-component strengths only; 2: also the stresslet's nine
+    return s.ok && s.L <= 23 && (C == 3 || option(SEWALD_OPT_SPREAD_FUSED) == 2) &&
+           option(SEWALD_OPT_SPREAD_CACHED) != 0 && !option(SEWALD_OPT_SPREAD_ROWSWEEP) &&
+           option(SEWALD_OPT_SPREAD_FUSED) != 0;
 }
 
 int launch_spread_mma_fused(const DevGrid& g, const DevWindow& w, int P, const SpreadMmaShape& s, const double* x,

@@ -61,34 +61,35 @@ __global__ void sweep_bucket_kernel(DevGrid g, int P, const double* __restrict__
 // strength components (stresslet: q_l nu_m, fourier.cpp:253-258).
 constexpr int SWW_PTS = 64;  // points per block of the weights kernel
 
-__global__ void __launch_bounds__(SWW_PTS)
+// Thread per (axis, point), axis-major (a warp's taps share the PKB
+// coefficient rows): three times the independent work of a thread per point
+// (0.41 -> ~0.2 ms at c2's 1e6 targets, latency-bound before).
+__global__ void __launch_bounds__(3 * SWW_PTS)
 sweep_weights_kernel(DevGrid g, DevWindow win, const double* __restrict__ x, const double* __restrict__ f,
                      const double* __restrict__ nu, int stresslet, const uint32_t* __restrict__ order, int64_t N,
                      double* __restrict__ W, int4* __restrict__ SW, double* __restrict__ STR,
                      const int64_t* __restrict__ klo, const int64_t* __restrict__ khi) {
-    // thread per point (all lanes evaluate the same tap index: uniform
-    // window-coefficient reads), taps staged in shared memory and written
-    // back as one contiguous, coalesced block of rows
+    // taps staged in shared memory and written back as one contiguous,
+    // coalesced block of rows
     extern __shared__ double stage[];  // [SWW_PTS][3P + 1]
+    __shared__ int sws[3][SWW_PTS];
     const int P = win.P, row = 3 * P + 1;
     const int64_t k0 = (int64_t)blockIdx.x * SWW_PTS;
-    const int64_t k = k0 + threadIdx.x;
+    const int ax = threadIdx.x / SWW_PTS, pt = threadIdx.x - ax * SWW_PTS;
+    const int64_t k = k0 + pt;
     // optional sorted-index window (one rank's part of the targets)
     const int64_t lo = klo ? *klo : 0, hi = khi ? *khi : N;
     if (k0 + SWW_PTS <= lo || k0 >= hi) return;
-    if (k < N && k >= lo && k < hi) {
-        const int64_t i = order[k];
-        int sw[3];
-        for (int ax = 0; ax < 3; ++ax) {
-            int j0;
-            double rel;
-            stencil_origin(g, P, ax, x[3 * i + ax], j0, rel);
-            double* w = stage + threadIdx.x * row + ax * P;
-            for (int p = 0; p < P; ++p) w[p] = window_eval(win, ((double)(j0 + p) - rel) * g.h);
-            sw[ax] = ax < g.d ? wrapi(j0, g.n[ax]) : j0;
-        }
-        SW[k] = make_int4(sw[0], sw[1], sw[2], (int)i);
-        if (f) {
+    const bool live = k < N && k >= lo && k < hi;
+    int64_t i = 0;
+    if (live) {
+        i = order[k];
+        int j0;
+        double rel;
+        stencil_origin(g, P, ax, x[3 * i + ax], j0, rel);
+        window_taps(win, j0, rel, g.h, stage + pt * row + ax * P);
+        sws[ax][pt] = ax < g.d ? wrapi(j0, g.n[ax]) : j0;
+        if (f && ax == 0) {
             if (!stresslet) {
                 for (int c = 0; c < 3; ++c) STR[k * 3 + c] = f[3 * i + c];
             } else {
@@ -98,13 +99,14 @@ sweep_weights_kernel(DevGrid g, DevWindow win, const double* __restrict__ x, con
         }
     }
     __syncthreads();
+    if (live && ax == 0) SW[k] = make_int4(sws[0][pt], sws[1][pt], sws[2][pt], (int)i);
     const int64_t a = max(k0, lo), b = min(min(k0 + SWW_PTS, N), hi);
     const int tot = (int)(b - a) * 3 * P;
     double* dst = W + a * 3 * P;
     const int off0 = (int)(a - k0);
-    for (int e = threadIdx.x; e < tot; e += SWW_PTS) {
-        const int pt = e / (3 * P), q = e - pt * 3 * P;
-        dst[e] = stage[(off0 + pt) * row + q];
+    for (int e = threadIdx.x; e < tot; e += 3 * SWW_PTS) {
+        const int p2 = e / (3 * P), q = e - p2 * 3 * P;
+        dst[e] = stage[(off0 + p2) * row + q];
     }
 }
 
@@ -522,8 +524,8 @@ void launch_sweep_weights(const DevGrid& g, const DevWindow& w, const double* x,
     if (N == 0) return;
     const size_t smem = sizeof(double) * SWW_PTS * (3 * w.P + 1);
     if (smem > 48 * 1024) cudaFuncSetAttribute(sweep_weights_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    sweep_weights_kernel<<<(unsigned)((N + SWW_PTS - 1) / SWW_PTS), SWW_PTS, smem, st>>>(g, w, x, f, nu, stresslet,
-                                                                                         order, N, W, SW, STR, klo, khi);
+    sweep_weights_kernel<<<(unsigned)((N + SWW_PTS - 1) / SWW_PTS), 3 * SWW_PTS, smem, st>>>(
+        g, w, x, f, nu, stresslet, order, N, W, SW, STR, klo, khi);
 }
 
 int launch_spread_sweep(const DevGrid& g, int P, const double* W, const int4* SW, const double* STR, int C,
