@@ -63,9 +63,9 @@ __device__ __forceinline__ double window_eval(const DevWindow& w, double r) {
 // one after another is latency-bound: the taps kernel of the c2 gather took
 // 0.41 ms for 1e6 targets).
 __device__ __forceinline__ void window_taps(const DevWindow& w, int j0, double rel, double h, double* out,
-                                            int stride = 1) {
-    const int P = w.P;
-    int p = 0;
+                                            int stride = 1, int p_begin = 0, int p_end = -1) {
+    const int P = p_end < 0 ? w.P : p_end;
+    int p = p_begin;
     if (w.kind == 1) {
         for (; p + 4 <= P; p += 4) {
             double r[4], u[4], acc[4];

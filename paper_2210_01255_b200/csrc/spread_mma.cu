@@ -230,10 +230,10 @@ spread_tile_mma_cached_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz
             kmax[threadIdx.x] = -1;
         }
         if (FUSED) {
-            // zero the chunk's tables, then one thread per (axis, source) writes
-            // the P taps at the source's offset in the region
+            // zero the padding rows of the chunk's tables; the (axis, source,
+            // half) items below write whole rows (taps and the zeros around them)
             const int rows = ngroups * SM_TG;
-            for (int e = threadIdx.x; e < rows * SM_LS; e += SM_THREADS) {
+            for (int e = T * SM_LS + threadIdx.x; e < rows * SM_LS; e += SM_THREADS) {
                 (&wx[0][0])[e] = 0.0;
                 (&wy[0][0])[e] = 0.0;
                 (&wz[0][0])[e] = 0.0;
@@ -252,18 +252,25 @@ spread_tile_mma_cached_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz
                 }
                 fs[e] = v;
             }
-            __syncthreads();
-            for (int e = threadIdx.x; e < 3 * T; e += SM_THREADS) {
-                const int ax = e / T, t = e - ax * T;
+            // work item = (axis, source, half of the taps): more independent
+            // items than threads per chunk (c2: 1464 for 512 threads)
+            const int half = ((P + 1) / 2 + 3) & ~3;
+            for (int e = threadIdx.x; e < 6 * T; e += SM_THREADS) {
+                const int hh = e / (3 * T), e2 = e - hh * 3 * T;
+                const int ax = e2 / T, t = e2 - ax * T;
                 const int64_t i = fsrc->order[q0 + t];
                 int j0;
                 double rel;
                 stencil_origin(g, P, ax, fsrc->x[3 * i + ax], j0, rel);
                 const int sw = ax < g.d ? wrap_index(j0, g.n[ax]) : j0;
                 const int o = sw - (ax == 0 ? X0 : (ax == 1 ? Y0 : Z0));
-                if (ax == 0) ox[t] = o;
+                if (ax == 0 && hh == 0) ox[t] = o;
                 double* row = ax == 0 ? wx[t] : (ax == 1 ? wy[t] : wz[t]);
-                window_taps(fsrc->win, j0, rel, g.h, row + o);
+                const int pb = hh ? min(half, P) : 0, pe = hh ? P : min(half, P);
+                window_taps(fsrc->win, j0, rel, g.h, row + o, 1, pb, pe);
+                // zeros of this half's side of the row: [0, o) / [o + P, SM_LS)
+                if (hh == 0) for (int k = 0; k < o; ++k) row[k] = 0.0;
+                else for (int k = o + P; k < SM_LS; ++k) row[k] = 0.0;
             }
         } else {
             // tables of the chunk: warp per source, lane = region index
