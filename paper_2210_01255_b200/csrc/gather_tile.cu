@@ -167,7 +167,7 @@ constexpr int MM_WARPS = 8;
 constexpr int MM_THREADS = 32 * MM_WARPS;
 
 __device__ __forceinline__ void dmma_8x8x4(double& d0, double& d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                  : "+d"(d0), "+d"(d1)
                  : "d"(a), "d"(b));
 }
@@ -345,6 +345,9 @@ gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
 #ifndef SEWALD_WG_MINB
 #define SEWALD_WG_MINB 3
 #endif
+#ifndef SEWALD_WG_PAIR
+#define SEWALD_WG_PAIR 1
+#endif
 constexpr int WG_TMAX = SEWALD_WG_TMAX;
 
 // Targets' taps evaluated in the kernel (FUSED): positions + bucket order
@@ -474,6 +477,61 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
 #pragma unroll
             for (int nb = 0; nb < NBMAX; ++nb) acc[nb][0] = acc[nb][1] = 0.0;
             const int tcol = 2 * (lane & 3);
+            // two row blocks per pass for L = 23: each B fragment (z taps) read from
+            // shared memory feeds two DMMAs (the kernel is bound by the L1 / shared
+            // path): xi = 63 3.71 -> 3.55 ms; for L = 19 (46 row blocks over 8
+            // warps) it loses (c2 2.84 -> 3.10 ms)
+            if (SEWALD_WG_PAIR && MM_L == 23) {
+            for (int rb = warp; rb < RB; rb += 2 * MM_WARPS) {
+                const int rbq[2] = {rb, rb + MM_WARPS};
+                int lo[2], hi[2], aa[2], bb[2];
+                double af[2][KS];
+#pragma unroll
+                for (int q = 0; q < 2; ++q) {
+                    lo[q] = 1 << 20;
+                    hi[q] = -1;
+                    const int r = rbq[q];
+                    if (r < RB) {
+                        const int a_lo = (r * 8) / MM_L, a_hi = min(r * 8 + 7, ROWS - 1) / MM_L;
+                        lo[q] = min(nbmin[a_lo], nbmin[a_hi]);
+                        hi[q] = max(nbmax[a_lo], nbmax[a_hi]);
+                    }
+                    const int row_a = r * 8 + (lane >> 2);
+                    const int ro = (lo[q] <= hi[q] && row_a < ROWS) ? rowoff[row_a] : -1;
+#pragma unroll
+                    for (int ks = 0; ks < KS; ++ks) {
+                        const int zo = zoff[ks * 4 + (lane & 3)];
+                        af[q][ks] = (ro >= 0 && zo >= 0) ? __ldg(gc + ro + zo) : 0.0;
+                    }
+                    aa[q] = row_a / MM_L;
+                    bb[q] = row_a - aa[q] * MM_L;
+                }
+                if (lo[0] > hi[0] && lo[1] > hi[1]) continue;
+#pragma unroll
+                for (int nb = 0; nb < NBMAX; ++nb) {
+                    const bool in0 = nb >= lo[0] && nb <= hi[0], in1 = nb >= lo[1] && nb <= hi[1];
+                    if (in0 || in1) {
+                        double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+                        for (int ks = 0; ks < KS; ++ks) {
+                            const double bz = wz[(nb * 8 + (lane >> 2)) * LS + ks * 4 + (lane & 3)];
+                            if (in0) dmma_8x8x4(d[0][0], d[0][1], af[0][ks], bz);
+                            if (in1) dmma_8x8x4(d[1][0], d[1][1], af[1][ks], bz);
+                        }
+                        const int t = nb * 8 + tcol;
+#pragma unroll
+                        for (int q = 0; q < 2; ++q) {
+                            if ((q ? in1 : in0) && aa[q] < LS) {
+                                const double2 vx = *reinterpret_cast<const double2*>(wx + aa[q] * WG_TMAX + t);
+                                const double2 vy = *reinterpret_cast<const double2*>(wy + bb[q] * WG_TMAX + t);
+                                acc[nb][0] = fma(d[q][0], vx.x * vy.x, acc[nb][0]);
+                                acc[nb][1] = fma(d[q][1], vx.y * vy.y, acc[nb][1]);
+                            }
+                        }
+                    }
+                }
+            }
+            } else {
             for (int rb = warp; rb < RB; rb += MM_WARPS) {
                 const int a_lo = (rb * 8) / MM_L, a_hi = min(rb * 8 + 7, ROWS - 1) / MM_L;
                 const int nb_lo = min(nbmin[a_lo], nbmin[a_hi]), nb_hi = max(nbmax[a_lo], nbmax[a_hi]);
@@ -503,6 +561,7 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
                         }
                     }
                 }
+            }
             }
 #pragma unroll
             for (int nb = 0; nb < NBMAX; ++nb)
