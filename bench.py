@@ -70,6 +70,9 @@ def parse():
     ap.add_argument("--xi", type=float, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    # supplementary: the same workload at the split parameter balanced for the
+    # B200 (PAPER.md:3790-3800 applied on this GPU; not the BASELINE-pinned xi)
+    ap.add_argument("--no-balanced", action="store_true")
     ap.add_argument("--profile-stages", action="store_true", default=True)
     return ap.parse_args()
 
@@ -304,6 +307,71 @@ def run_reference(args, cfg_index):
 # our engine
 # ---------------------------------------------------------------------------
 
+BALANCED_XI = {2: 63.0}  # profiles/r2_xi_balance_c2.txt: 57.6 (xi 37) ... 24.3 ms (xi 63-71)
+
+
+def balanced_probe(S, cfg, x, f, nu, xt, engine, stream, dev, l2, steps=5, warmup=2):
+    """Same inputs, tolerance and window at the B200-balanced split parameter
+    (device-resident, L2 flushed, CUDA events): a supplementary figure, not the
+    headline (BASELINE.md §3 pins xi)."""
+    import dataclasses
+    import torch
+    cb = dataclasses.replace(cfg, xi=BALANCED_XI[cfg.index])
+    _, sel = select(S, cb, x, f, nu)
+    p = sel.params
+    same = xt is None
+    Nt = x.shape[0] if same else xt.shape[0]
+    sess = S.Session(p, S.Cell(cb.L), engine)
+    dx, df = torch.from_numpy(x).to(dev), torch.from_numpy(f).to(dev)
+    dnu = torch.from_numpy(nu).to(dev) if nu is not None else None
+    dxt = torch.from_numpy(xt).to(dev) if xt is not None else None
+    grid = torch.empty(sess.grid_size(), dtype=torch.float64, device=dev)
+    u = torch.zeros((Nt, 3), dtype=torch.float64, device=dev)
+
+    def step():
+        sess.set_sources(dx, df, dnu)
+        sess.set_targets(dxt, same)
+        sess.spread(0, x.shape[0], grid)
+        sess.solve(grid, True)
+        sess.evaluate(u, 0, 1, 7)
+
+    for _ in range(warmup):
+        l2.fill_(1.0)
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        l2.fill_(1.0)
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    ev[0].record(stream)
+    sess.spread(0, x.shape[0], grid)
+    ev[1].record(stream)
+    sess.solve(grid, True)
+    ev[2].record(stream)
+    sess.evaluate(u, 0, 1, 2)
+    ev[3].record(stream)
+    torch.cuda.synchronize()
+    st = {"spread(incl. bucket sort)": ev[0].elapsed_time(ev[1]), "fft+scale+ifft": ev[1].elapsed_time(ev[2]),
+          "realspace": ev[2].elapsed_time(ev[3])}
+    u.zero_()
+    step()
+    uu = u.cpu().numpy()
+    out = {"note": "supplementary, not the headline: same inputs / tolerance / window at the split parameter "
+                   "balanced for the B200 (PAPER.md:3790-3800); BASELINE.md pins xi = 37 for c2",
+           "xi": cb.xi, "M_ext": [int(v) for v in p.grid.M_ext], "P": int(p.window.P), "rc": float(p.rc),
+           "ms_per_step": ms, "value": Nt / (ms * 1e-3), "unit": "targets/s", "steps": steps, "warmup": warmup,
+           "stages_ms": {k: round(v, 4) for k, v in st.items()},
+           "parity_vs_fixture": fixture_parity(uu, cfg.index, True)}
+    del sess, grid, u
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args, cfg):
     import torch
     import torch.distributed as dist
@@ -479,6 +547,8 @@ def run_ours(args, cfg):
     if rank == 0 and line is not None:
         torch.cuda.synchronize()
         line["parity_vs_fixture"] = fixture_parity(u_step, cfg.index, args.xi is not None)
+        if ws == 1 and cfg.index == 2 and args.xi is None and not args.no_balanced:
+            line["balanced_xi"] = balanced_probe(S, cfg, x, f, nu, xt, engine, stream, dev, l2)
 
     # end-to-end through the public API with pinned host buffers: full_potential
     # on 1 GPU, parallel.full_potential_sharded on N (max over ranks)
