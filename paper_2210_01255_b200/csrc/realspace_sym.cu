@@ -39,6 +39,9 @@ constexpr int SYM_THREADS = 32 * SYM_WARPS;
 #ifndef SEWALD_SYM_MINB
 #define SEWALD_SYM_MINB 4
 #endif
+#ifndef SEWALD_SYM_BCAST
+#define SEWALD_SYM_BCAST 1
+#endif
 
 __device__ __forceinline__ int fdiv(int a, int b) {
     int q = a / b;
@@ -445,7 +448,8 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                         rec[1] = xy.y;
                         rec[2] = zi.x;
                         jid[lane] = __double_as_longlong(zi.y);
-                        jf[lane] = jf[lane + 32] = make_float4((float)xy.x, (float)xy.y, (float)zi.x, 0.0f);
+                        jf[lane] = make_float4((float)xy.x, (float)xy.y, (float)zi.x, 0.0f);
+                        if (!SEWALD_SYM_BCAST) jf[lane + 32] = jf[lane];
 #pragma unroll
                         for (int c = 0; c < NS; c += 2) {
                             const double2 v = __ldg(q2 + 2 + c / 2);
@@ -461,14 +465,16 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                         rec[1] = q[1];
                         rec[2] = q[2];
                         jid[lane] = __double_as_longlong(q[3]);
-                        jf[lane] = jf[lane + 32] = make_float4((float)q[0], (float)q[1], (float)q[2], 0.0f);
+                        jf[lane] = make_float4((float)q[0], (float)q[1], (float)q[2], 0.0f);
+                        if (!SEWALD_SYM_BCAST) jf[lane + 32] = jf[lane];
 #pragma unroll
                         for (int c = 0; c < NS; ++c) rec[3 + c] = q[4 + c];
                     } else {
 #endif
                         // unused slots: far away in fp32 (never candidates) and
                         // finite in fp64 (branch-free steps read them)
-                        jf[lane] = jf[lane + 32] = make_float4(1e30f, 1e30f, 1e30f, 0.0f);
+                        jf[lane] = make_float4(1e30f, 1e30f, 1e30f, 0.0f);
+                        if (!SEWALD_SYM_BCAST) jf[lane + 32] = jf[lane];
                         double* rec = jrec[lane];
                         rec[0] = rec[1] = rec[2] = 1e100;
 #pragma unroll
@@ -483,6 +489,35 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                     // iterations, FP32 pipe); (2) steps with any candidate (one
                     // warp OR-reduction); (3) fp64 work only on those steps.
                     unsigned m = 0u;
+#if SEWALD_SYM_BCAST
+                    // Candidate pass in j order with broadcast reads: every lane reads
+                    // the same jf[j] (one shared-memory wavefront instead of four for
+                    // a 16-byte access per lane at a different j), the lane's bits are
+                    // collected by j and rotated into step order at the end (bit s of
+                    // m <-> j = (lane + s) mod 32).
+                    if (valid) {
+                        unsigned mj = 0u;
+                        if (dlt <= -32) {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j) {
+                                const float4 p = jf[j];
+                                const float d0 = tf0 - p.x, d1 = tf1 - p.y, d2 = tf2 - p.z;
+                                if (fmaf(d2, d2, fmaf(d1, d1, d0 * d0)) < a.thresh_f) mj |= 1u << j;
+                            }
+                        } else {
+#pragma unroll 8
+                            for (int j = 0; j < 32; ++j) {
+                                const int dj = j - lane;
+                                const float4 p = jf[j];
+                                const float d0 = tf0 - p.x, d1 = tf1 - p.y, d2 = tf2 - p.z;
+                                const bool ok = j < cnt && (dj > dlt || (dj == dlt && pos_shift)) &&
+                                                fmaf(d2, d2, fmaf(d1, d1, d0 * d0)) < a.thresh_f;
+                                mj |= (ok ? 1u : 0u) << j;
+                            }
+                        }
+                        m = __funnelshift_r(mj, mj, lane);
+                    }
+#else
                     if (valid) {
                         if (dlt <= -32) {
                             // block entirely after the cluster: no half-rule test
@@ -508,6 +543,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                             }
                         }
                     }
+#endif
                     unsigned steps = __reduce_or_sync(0xffffffffu, m);
                     bool coincident = false;
 #if SEWALD_SYM_POOL > 0
