@@ -41,7 +41,7 @@ sys.path.insert(0, ROOT)
 
 # DRAM bytes (read + write) per launch of the dominant kernel from one
 # `ncu --set full` capture of the kernel at the same workload (profiles/r2_ncu_realspace_sym_v4.txt).
-TRAFFIC_BYTES = {"c2_stokeslet_d3_N1e6": 98_096_128 + 3_664_128}
+TRAFFIC_BYTES = {"c2_stokeslet_d3_N1e6": 97_504_768 + 4_602_624}
 
 # Algorithmic fp64 flops per accepted (directed) real-space pair of the
 # implemented evaluation, keyed (kernel, symmetric): ncu thread-level
