@@ -40,7 +40,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 # DRAM bytes (read + write) per launch of the dominant kernel from one
-# `ncu --set full` capture of the kernel at the same workload (profiles/r2_ncu_realspace_sym_v4.txt).
+# `ncu --set full` capture of the kernel at the same workload (profiles/r2_ncu_realspace_sym_v6.txt).
 TRAFFIC_BYTES = {"c2_stokeslet_d3_N1e6": 97_504_768 + 4_602_624}
 
 # Algorithmic fp64 flops per accepted (directed) real-space pair of the
