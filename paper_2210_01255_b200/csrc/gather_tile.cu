@@ -349,6 +349,20 @@ gather_tile_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
 #define SEWALD_WG_PAIR 1
 #endif
 constexpr int WG_TMAX = SEWALD_WG_TMAX;
+// Row stride of the Wx' / Wy' epilogue tables: WG_TMAX + 8 doubles puts the
+// two rows (b, b + 1) a quarter warp reads 16 banks apart (with a stride of
+// WG_TMAX = 64 doubles every row starts on the same bank: 2-way conflicts on
+// every epilogue load)
+#ifndef SEWALD_WG_PAD
+#define SEWALD_WG_PAD 8
+#endif
+constexpr int WXS = WG_TMAX + SEWALD_WG_PAD;
+// Row stride of the Wz' (B-fragment) table: the 8 rows a fragment load reads
+// must spread over the banks (stride = 4 or 12 mod 16 doubles); the GEMM K
+// stays LS. LS = 24 (L = 23) had every other row on the same banks.
+__host__ __device__ constexpr int wz_stride(int LS) {
+    return SEWALD_WG_PAD == 0 ? LS : ((LS % 16 == 4 || LS % 16 == 12) ? LS : LS + 4);
+}
 
 // Targets' taps evaluated in the kernel (FUSED): positions + bucket order
 // instead of the taps array of a separate kernel.
@@ -365,6 +379,7 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
                        const double* __restrict__ grid, double h3, int accumulate, double* __restrict__ u,
                        const FusedTgt* __restrict__ ftg) {
     constexpr int LS = (MM_L + 4) & ~3;  // K = LS = 4 x KS (columns >= L are zero taps)
+    constexpr int WZS = wz_stride(LS);   // row stride of the B-fragment table
     constexpr int KS = LS / 4;
     constexpr int ROWS = MM_L * MM_L;
     constexpr int RB = (ROWS + 7) / 8;
@@ -378,9 +393,9 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
     const int tx = (int)(tile / ((int64_t)ntz * nty));
     const int X0 = tx * B, Y0 = ty * B, Z0 = tz * B;
     double* wz = sm;                                   // [WG_TMAX][LS]   Wz'[t][c]
-    double* wx = wz + WG_TMAX * LS;                    // [LS][WG_TMAX]   Wx'[a][t]
-    double* wy = wx + LS * WG_TMAX;                    // [LS][WG_TMAX]   Wy'[b][t]
-    double* part = wy + LS * WG_TMAX;                  // [MM_WARPS][WG_TMAX]
+    double* wx = wz + WG_TMAX * WZS;                   // [LS][WXS]       Wx'[a][t]
+    double* wy = wx + LS * WXS;                        // [LS][WXS]       Wy'[b][t]
+    double* part = wy + LS * WXS;                      // [MM_WARPS][WG_TMAX]
     int* rowoff = reinterpret_cast<int*>(part + MM_WARPS * WG_TMAX);  // [ROWS]
     int* zoff = rowoff + ROWS;                                      // [LS]
     int* tid = zoff + LS;                                           // [WG_TMAX]
@@ -414,8 +429,8 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
             nbmax[threadIdx.x] = -1;
         }
         if (FUSED) {
-            for (int e = threadIdx.x; e < nblk * 8 * LS; e += MM_THREADS) wz[e] = 0.0;
-            for (int e = threadIdx.x; e < LS * WG_TMAX; e += MM_THREADS) {
+            for (int e = threadIdx.x; e < nblk * 8 * WZS; e += MM_THREADS) wz[e] = 0.0;
+            for (int e = threadIdx.x; e < LS * WXS; e += MM_THREADS) {
                 wx[e] = 0.0;
                 wy[e] = 0.0;
             }
@@ -430,8 +445,8 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
                 const int sw = ax < g.d ? wrap_index(j0, g.n[ax]) : j0;
                 const int o = sw - (ax == 0 ? X0 : (ax == 1 ? Y0 : Z0));
                 if (ax == 0) ox[t] = o;
-                if (ax == 2) window_taps(ftg->win, j0, rel, g.h, wz + t * LS + o);
-                else window_taps(ftg->win, j0, rel, g.h, (ax == 0 ? wx : wy) + o * WG_TMAX + t, WG_TMAX);
+                if (ax == 2) window_taps(ftg->win, j0, rel, g.h, wz + t * WZS + o);
+                else window_taps(ftg->win, j0, rel, g.h, (ax == 0 ? wx : wy) + o * WXS + t, WXS);
             }
         } else
         for (int t = warp; t < nblk * 8; t += MM_WARPS) {
@@ -446,9 +461,9 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
                     if (ky >= 0 && ky < P) vy = __ldg(wt + P + ky);
                     if (kz >= 0 && kz < P) vz = __ldg(wt + 2 * P + kz);
                 }
-                wz[t * LS + k] = vz;
-                wx[k * WG_TMAX + t] = vx;
-                wy[k * WG_TMAX + t] = vy;
+                wz[t * WZS + k] = vz;
+                wx[k * WXS + t] = vx;
+                wy[k * WXS + t] = vy;
             }
             if (lane == 0) {
                 tid[t] = sw.w;
@@ -514,7 +529,7 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
                         double d[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
                         for (int ks = 0; ks < KS; ++ks) {
-                            const double bz = wz[(nb * 8 + (lane >> 2)) * LS + ks * 4 + (lane & 3)];
+                            const double bz = wz[(nb * 8 + (lane >> 2)) * WZS + ks * 4 + (lane & 3)];
                             if (in0) dmma_8x8x4(d[0][0], d[0][1], af[0][ks], bz);
                             if (in1) dmma_8x8x4(d[1][0], d[1][1], af[1][ks], bz);
                         }
@@ -522,8 +537,8 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
 #pragma unroll
                         for (int q = 0; q < 2; ++q) {
                             if ((q ? in1 : in0) && aa[q] < LS) {
-                                const double2 vx = *reinterpret_cast<const double2*>(wx + aa[q] * WG_TMAX + t);
-                                const double2 vy = *reinterpret_cast<const double2*>(wy + bb[q] * WG_TMAX + t);
+                                const double2 vx = *reinterpret_cast<const double2*>(wx + aa[q] * WXS + t);
+                                const double2 vy = *reinterpret_cast<const double2*>(wy + bb[q] * WXS + t);
                                 acc[nb][0] = fma(d[q][0], vx.x * vy.x, acc[nb][0]);
                                 acc[nb][1] = fma(d[q][1], vx.y * vy.y, acc[nb][1]);
                             }
@@ -551,11 +566,11 @@ gather_wide_mma_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, int64
                         double d0 = 0.0, d1 = 0.0;
 #pragma unroll
                         for (int ks = 0; ks < KS; ++ks)
-                            dmma_8x8x4(d0, d1, af[ks], wz[(nb * 8 + (lane >> 2)) * LS + ks * 4 + (lane & 3)]);
+                            dmma_8x8x4(d0, d1, af[ks], wz[(nb * 8 + (lane >> 2)) * WZS + ks * 4 + (lane & 3)]);
                         if (a < LS) {
                             const int t = nb * 8 + tcol;
-                            const double2 vx = *reinterpret_cast<const double2*>(wx + a * WG_TMAX + t);
-                            const double2 vy = *reinterpret_cast<const double2*>(wy + b * WG_TMAX + t);
+                            const double2 vx = *reinterpret_cast<const double2*>(wx + a * WXS + t);
+                            const double2 vy = *reinterpret_cast<const double2*>(wy + b * WXS + t);
                             acc[nb][0] = fma(d0, vx.x * vy.x, acc[nb][0]);
                             acc[nb][1] = fma(d1, vx.y * vy.y, acc[nb][1]);
                         }
@@ -607,7 +622,7 @@ void launch_wide_fused(const DevGrid& g, int P, const TileShape& s, int64_t t0, 
 
 size_t wide_smem_bytes(int L) {
     const int LS = (L + 4) & ~3;
-    return sizeof(double) * ((size_t)3 * WG_TMAX * LS + MM_WARPS * WG_TMAX) +
+    return sizeof(double) * ((size_t)WG_TMAX * wz_stride(LS) + 2 * (size_t)WXS * LS + MM_WARPS * WG_TMAX) +
            sizeof(int) * ((size_t)L * L + 3 * LS + 2 * WG_TMAX);
 }
 
