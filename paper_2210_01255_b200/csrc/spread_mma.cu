@@ -35,6 +35,13 @@ constexpr int SM_THREADS = 32 * SM_WARPS;
 #endif
 constexpr int SM_TG = 32;  // sources per table group (8 k-steps of 4)
 constexpr int SM_LS = 24;  // padded table width (z: 3 n-blocks of 8)
+// Row stride of the cached kernel's tables: 28 doubles (= 12 mod 16) puts the
+// four source rows a half warp reads 24 banks apart; at 24 (= 8 mod 16) rows
+// t and t + 2 shared banks and every table load conflicted 2-way.
+#ifndef SEWALD_SM_LSP
+#define SEWALD_SM_LSP 28
+#endif
+constexpr int SM_LSP = SEWALD_SM_LSP;
 
 // v >= 0 reduced mod n by subtraction (a region coordinate exceeds the grid
 // by less than the region edge): replaces an integer division per flushed row
@@ -167,7 +174,7 @@ constexpr int CT_CMAX = 9;
 
 // + per-point x offsets and per-row k-step ranges
 size_t cached_smem_bytes() {
-    return sizeof(double) * (size_t)CT_TMAX * (3 * SM_LS + CT_CMAX) + sizeof(int) * (CT_TMAX + 2 * SM_LS);
+    return sizeof(double) * (size_t)CT_TMAX * (3 * SM_LSP + CT_CMAX) + sizeof(int) * (CT_TMAX + 2 * SM_LS);
 }
 
 // Fused taps (FUSED = true): the chunk's window taps are evaluated here from
@@ -198,10 +205,10 @@ spread_tile_mma_cached_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz
     constexpr int RB = (ROWS + 7) / 8;
     constexpr int RBW = (RB + SM_WARPS - 1) / SM_WARPS;  // row blocks per warp
     extern __shared__ __align__(16) double csm[];
-    double(*wx)[SM_LS] = reinterpret_cast<double(*)[SM_LS]>(csm);
-    double(*wy)[SM_LS] = reinterpret_cast<double(*)[SM_LS]>(csm + CT_TMAX * SM_LS);
-    double(*wz)[SM_LS] = reinterpret_cast<double(*)[SM_LS]>(csm + 2 * CT_TMAX * SM_LS);
-    double* fs = csm + 3 * CT_TMAX * SM_LS;  // [CT_TMAX][C]
+    double(*wx)[SM_LSP] = reinterpret_cast<double(*)[SM_LSP]>(csm);
+    double(*wy)[SM_LSP] = reinterpret_cast<double(*)[SM_LSP]>(csm + CT_TMAX * SM_LSP);
+    double(*wz)[SM_LSP] = reinterpret_cast<double(*)[SM_LSP]>(csm + 2 * CT_TMAX * SM_LSP);
+    double* fs = csm + 3 * CT_TMAX * SM_LSP;  // [CT_TMAX][C]
     int* ox = reinterpret_cast<int*>(fs + CT_TMAX * CT_CMAX);  // [CT_TMAX] x offset of each point in the region
     int* kmin = ox + CT_TMAX;                                  // [SM_LS] first / last k-step reaching row a
     int* kmax = kmin + SM_LS;
@@ -233,7 +240,7 @@ spread_tile_mma_cached_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz
             // zero the padding rows of the chunk's tables; the (axis, source,
             // half) items below write whole rows (taps and the zeros around them)
             const int rows = ngroups * SM_TG;
-            for (int e = T * SM_LS + threadIdx.x; e < rows * SM_LS; e += SM_THREADS) {
+            for (int e = T * SM_LSP + threadIdx.x; e < rows * SM_LSP; e += SM_THREADS) {
                 (&wx[0][0])[e] = 0.0;
                 (&wy[0][0])[e] = 0.0;
                 (&wz[0][0])[e] = 0.0;
