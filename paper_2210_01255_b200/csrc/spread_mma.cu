@@ -401,6 +401,12 @@ spread_tile_mma_cached_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz
 // WT_TMAX per tile are handled in further passes (more RED, same result).
 constexpr int WT_TMAX = 128;
 constexpr int WT_LS = 40;
+#ifndef SEWALD_WT_PAD
+#define SEWALD_WT_PAD 1
+#endif
+__host__ __device__ constexpr int wide_table_stride(int LS) {
+    return (!SEWALD_WT_PAD || LS % 16 == 4 || LS % 16 == 12) ? LS : LS + 4;
+}
 constexpr int WT_WARPS = 16;
 #ifndef SEWALD_SPREAD_RS_WARPS
 #define SEWALD_SPREAD_RS_WARPS 8
@@ -423,12 +429,15 @@ spread_tile_mma_wide_kernel(DevGrid g, int P, int B, int ntx, int nty, int ntz, 
     constexpr int ROWS = L * L;
     constexpr int RB = (ROWS + 7) / 8;
     constexpr int NB = WT_LS / 8;
+    // table row stride: 4 or 12 mod 16 doubles, so the four source rows a half
+    // warp reads lie on distinct banks (at LS = 40 / 24 rows t and t + 2 collide)
+    constexpr int LSP = wide_table_stride(LS);
     extern __shared__ __align__(16) double wsm[];
-    double(*wxf)[WT_LS] = reinterpret_cast<double(*)[WT_LS]>(wsm);                       // f_t wx_t(a)
-    double(*wx)[WT_LS] = reinterpret_cast<double(*)[WT_LS]>(wsm + WT_TMAX * WT_LS);      // wx_t(a)
-    double(*wy)[WT_LS] = reinterpret_cast<double(*)[WT_LS]>(wsm + 2 * WT_TMAX * WT_LS);  // wy_t(b)
-    double(*wz)[WT_LS] = reinterpret_cast<double(*)[WT_LS]>(wsm + 3 * WT_TMAX * WT_LS);  // wz_t(z)
-    int* ox = reinterpret_cast<int*>(wsm + 4 * WT_TMAX * WT_LS);  // [WT_TMAX] x offset of each point
+    double(*wxf)[LSP] = reinterpret_cast<double(*)[LSP]>(wsm);                     // f_t wx_t(a)
+    double(*wx)[LSP] = reinterpret_cast<double(*)[LSP]>(wsm + WT_TMAX * LSP);      // wx_t(a)
+    double(*wy)[LSP] = reinterpret_cast<double(*)[LSP]>(wsm + 2 * WT_TMAX * LSP);  // wy_t(b)
+    double(*wz)[LSP] = reinterpret_cast<double(*)[LSP]>(wsm + 3 * WT_TMAX * LSP);  // wz_t(z)
+    int* ox = reinterpret_cast<int*>(wsm + 4 * WT_TMAX * LSP);  // [WT_TMAX] x offset of each point
     int* kmin = ox + WT_TMAX;                                      // [WT_LS] first / last k-step reaching row a
     int* kmax = kmin + WT_LS;
 
@@ -599,14 +608,14 @@ int launch_spread_mma(const DevGrid& g, int P, const SpreadMmaShape& s, const do
     for (int64_t a = 0; a < s.ntiles; a += (int64_t)1 << 30) {
         const int64_t n = std::min<int64_t>(s.ntiles - a, (int64_t)1 << 30);
         if (s.L > 23) {
-            const size_t sm = sizeof(double) * 4 * WT_TMAX * WT_LS + sizeof(int) * (WT_TMAX + 2 * WT_LS);
+            const size_t sm = sizeof(double) * 4 * WT_TMAX * wide_table_stride(WT_LS) + sizeof(int) * (WT_TMAX + 2 * WT_LS);
             auto kern = s.L <= 31 ? spread_tile_mma_wide_kernel<31>
                                   : (s.L <= 35 ? spread_tile_mma_wide_kernel<35> : spread_tile_mma_wide_kernel<39>);
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
             kern<<<(unsigned)n, 32 * WT_WARPS, sm, st>>>(g, P, s.B, s.nt[0], s.nt[1], s.nt[2], a, W, SW, STR, C, off,
                                                         out);
         } else if (option(SEWALD_OPT_SPREAD_ROWSWEEP)) {
-            const size_t sm = sizeof(double) * 4 * WT_TMAX * 24 + sizeof(int) * (WT_TMAX + 2 * 24);
+            const size_t sm = sizeof(double) * 4 * WT_TMAX * wide_table_stride(24) + sizeof(int) * (WT_TMAX + 2 * 24);
             auto kern = s.L == 23 ? spread_tile_mma_wide_kernel<23, 24, SEWALD_SPREAD_RS_WARPS, SEWALD_SPREAD_RS_MINB>
                                   : spread_tile_mma_wide_kernel<19, 24, SEWALD_SPREAD_RS_WARPS, SEWALD_SPREAD_RS_MINB>;
             cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
