@@ -177,9 +177,11 @@ spread_sweep_kernel(DevGrid g, int P, const double* __restrict__ W, const int4* 
                     int nby, int nseg, double* __restrict__ out) {
     constexpr int WIN = PMAX + ZSTEP - 1;
     comp0 += blockIdx.z * NC;  // component groups run as independent CTAs
-    __shared__ double pwx[32][SX];
-    __shared__ double pwy[32][SY];
-    __shared__ double pwz[32][PMAX];
+    // rows padded to an odd number of doubles: each lane stages its own row, and
+    // even strides (32 / 64 / 112 bytes) put 2-8 lanes of a half warp on one bank
+    __shared__ double pwx[32][SX + 1];
+    __shared__ double pwy[32][SY + 1];
+    __shared__ double pwz[32][PMAX + 1];
     __shared__ double ps[32][NC];
     __shared__ int pdx[32], pdy[32], po[32];
     __shared__ uint32_t cidx[32];
@@ -337,9 +339,9 @@ gather_sweep_kernel(DevGrid g, int P, const double* __restrict__ W, const int4* 
                     const int64_t* __restrict__ off, int nbx, int nby, int nseg, int tile0,
                     const double* __restrict__ grid, double h3, double* __restrict__ u) {
     constexpr int WIN = PMAX + ZSTEP - 1;
-    __shared__ double pwx[32][SX];
-    __shared__ double pwy[32][SY];
-    __shared__ double pwz[32][PMAX];
+    __shared__ double pwx[32][SX + 1];
+    __shared__ double pwy[32][SY + 1];
+    __shared__ double pwz[32][PMAX + 1];
     __shared__ int pdx[32], pdy[32], po[32], pid[32];
     __shared__ uint32_t cidx[32];
     __shared__ double red[3][32][33];
