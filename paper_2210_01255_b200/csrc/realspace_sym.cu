@@ -42,6 +42,10 @@ constexpr int SYM_THREADS = 32 * SYM_WARPS;
 #ifndef SEWALD_SYM_BCAST
 #define SEWALD_SYM_BCAST 1
 #endif
+// packed fp32x2 candidate pass (needs SEWALD_SYM_BCAST)
+#ifndef SEWALD_SYM_F2
+#define SEWALD_SYM_F2 1
+#endif
 
 __device__ __forceinline__ int fdiv(int a, int b) {
     int q = a / b;
@@ -286,6 +290,12 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     // 14 (the kernel is issue-bound: c2 56.5 -> 53.2 ms, c3 108.0 -> 103.8, c5
     // 64.1 -> 59.8)
     __shared__ float4 jf_all[SYM_WARPS][64];
+#if SEWALD_SYM_F2
+    // the same fp32 positions negated and packed in pairs for the f32x2
+    // candidate pass: [-x_2p, -x_2p+1, -y_2p, -y_2p+1] and [-z_2p, -z_2p+1]
+    __shared__ float4 jq_all[SYM_WARPS][16];
+    __shared__ float2 jz_all[SYM_WARPS][16];
+#endif
     // 2^(j/32) table, replicated SEWALD_EXP_REP times (lane-interleaved: conflict-free lookups)
     __shared__ double exp_tab_rep[32 * SEWALD_EXP_REP];
 #if SEWALD_SYM_POOL > 0
@@ -304,6 +314,15 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     double(*jrec)[RS] = jrec_all[warp];
     long long* jid = jid_all[warp];
     float4* jf = jf_all[warp];
+#if SEWALD_SYM_F2
+    float* jqf = reinterpret_cast<float*>(jq_all[warp]);
+    float* jzf = reinterpret_cast<float*>(jz_all[warp]);
+    // this lane's slots in the pair tables
+    const int qx = (lane >> 1) * 4 + (lane & 1), qz = lane;
+#define SYM_F2_STORE(X, Y, Z) { jqf[qx] = -(X); jqf[qx + 2] = -(Y); jzf[qz] = -(Z); }
+#else
+#define SYM_F2_STORE(X, Y, Z) {}
+#endif
 #if SEWALD_SYM_POOL > 0
     double(*irec)[IS] = irec_all[warp];
     double(*ipool)[3] = ipool_all[warp];
@@ -449,6 +468,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                         rec[2] = zi.x;
                         jid[lane] = __double_as_longlong(zi.y);
                         jf[lane] = make_float4((float)xy.x, (float)xy.y, (float)zi.x, 0.0f);
+                        SYM_F2_STORE((float)xy.x, (float)xy.y, (float)zi.x)
                         if (!SEWALD_SYM_BCAST) jf[lane + 32] = jf[lane];
 #pragma unroll
                         for (int c = 0; c < NS; c += 2) {
@@ -466,6 +486,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                         rec[2] = q[2];
                         jid[lane] = __double_as_longlong(q[3]);
                         jf[lane] = make_float4((float)q[0], (float)q[1], (float)q[2], 0.0f);
+                        SYM_F2_STORE((float)q[0], (float)q[1], (float)q[2])
                         if (!SEWALD_SYM_BCAST) jf[lane + 32] = jf[lane];
 #pragma unroll
                         for (int c = 0; c < NS; ++c) rec[3 + c] = q[4 + c];
@@ -474,6 +495,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                         // unused slots: far away in fp32 (never candidates) and
                         // finite in fp64 (branch-free steps read them)
                         jf[lane] = make_float4(1e30f, 1e30f, 1e30f, 0.0f);
+                        SYM_F2_STORE(1e30f, 1e30f, 1e30f)
                         if (!SEWALD_SYM_BCAST) jf[lane + 32] = jf[lane];
                         double* rec = jrec[lane];
                         rec[0] = rec[1] = rec[2] = 1e100;
@@ -498,12 +520,32 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                     if (valid) {
                         unsigned mj = 0u;
                         if (dlt <= -32) {
+#if SEWALD_SYM_F2
+                            // two j per packed fp32x2 operation (FADD2 / FMUL2 / FFMA2):
+                            // the same IEEE fp32 operations as the scalar test, so the
+                            // same mask (x + (-y) == x - y exactly)
+                            const float2 t0 = make_float2(tf0, tf0), t1 = make_float2(tf1, tf1),
+                                         t2 = make_float2(tf2, tf2);
+                            const float4* jq = jq_all[warp];
+                            const float2* jz = jz_all[warp];
+#pragma unroll
+                            for (int jp = 0; jp < 16; ++jp) {
+                                const float4 q = jq[jp];
+                                const float2 d0 = __fadd2_rn(t0, make_float2(q.x, q.y));
+                                const float2 d1 = __fadd2_rn(t1, make_float2(q.z, q.w));
+                                const float2 d2 = __fadd2_rn(t2, jz[jp]);
+                                const float2 ss = __ffma2_rn(d2, d2, __ffma2_rn(d1, d1, __fmul2_rn(d0, d0)));
+                                if (ss.x < a.thresh_f) mj |= 1u << (2 * jp);
+                                if (ss.y < a.thresh_f) mj |= 2u << (2 * jp);
+                            }
+#else
 #pragma unroll
                             for (int j = 0; j < 32; ++j) {
                                 const float4 p = jf[j];
                                 const float d0 = tf0 - p.x, d1 = tf1 - p.y, d2 = tf2 - p.z;
                                 if (fmaf(d2, d2, fmaf(d1, d1, d0 * d0)) < a.thresh_f) mj |= 1u << j;
                             }
+#endif
                         } else {
 #pragma unroll 8
                             for (int j = 0; j < 32; ++j) {
