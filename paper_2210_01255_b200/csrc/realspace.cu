@@ -156,6 +156,10 @@ __device__ __forceinline__ void pair_accumulate(const Screened& sc, double xi2, 
 // One WARP = one independent work unit: 32 consecutive targets in cell
 // order (spatially compact), their bounding box, the cell rows within rc of
 // it, and a private shared-memory staging area. No block-wide barriers.
+#ifndef SEWALD_RS_F2
+#define SEWALD_RS_F2 1
+#endif
+
 template <int KIND, int S, bool SHORT>
 __global__ void __launch_bounds__(RS_THREADS, 4)
 realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed,
@@ -166,6 +170,12 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
     constexpr int CH = S > 8 ? 64 : WCHUNK;  // stresslet records: 64 (static shared-memory limit)
     __shared__ __align__(16) double src_all[RS_WARPS][CH * S];
     __shared__ float4 srcf_all[RS_WARPS][CH];
+#if SEWALD_RS_F2
+    // negated fp32 positions in pairs for the packed fp32x2 candidate pass:
+    // [-x_2p, -x_2p+1, -y_2p, -y_2p+1] and [-z_2p, -z_2p+1]
+    __shared__ float4 srcq_all[RS_WARPS][CH / 2];
+    __shared__ float2 srcz_all[RS_WARPS][CH / 2];
+#endif
 #if !SEWALD_RS_MASK
     __shared__ uint8_t queue_all[RS_WARPS][CH][32];
 #endif
@@ -294,8 +304,16 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
                         for (int e = lane; e < cnt * (S / 2); e += 32) s2[e] = __ldg(g2 + e);
 #if SEWALD_RS_MASK
                         // slots past the chunk: far away in fp32 (never candidates)
-                        for (int e = lane; e < CH; e += 32)
-                            srcf[e] = e < cnt ? __ldg(packedf + base + e) : make_float4(1e30f, 1e30f, 1e30f, 0.0f);
+                        for (int e = lane; e < CH; e += 32) {
+                            const float4 v = e < cnt ? __ldg(packedf + base + e) : make_float4(1e30f, 1e30f, 1e30f, 0.0f);
+                            srcf[e] = v;
+#if SEWALD_RS_F2
+                            float* sq = reinterpret_cast<float*>(srcq_all[warp]) + (e >> 1) * 4 + (e & 1);
+                            sq[0] = -v.x;
+                            sq[2] = -v.y;
+                            reinterpret_cast<float*>(srcz_all[warp])[e] = -v.z;
+#endif
+                        }
 #else
                         for (int e = lane; e < cnt; e += 32) srcf[e] = __ldg(packedf + base + e);
 #endif
@@ -312,6 +330,24 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
                     for (int h = 0; h < NM; ++h) {
                         cm[h] = 0ull;
                         const int kend = min(cnt8 - 64 * h, 64);
+#if SEWALD_RS_F2
+                        // two sources per packed fp32x2 operation, the same IEEE fp32
+                        // operations as the scalar test (x + (-y) == x - y)
+                        const float2 t0 = make_float2(tf0, tf0), t1 = make_float2(tf1, tf1),
+                                     t2 = make_float2(tf2, tf2);
+                        const float4* sq = srcq_all[warp] + 32 * h;
+                        const float2* sz = srcz_all[warp] + 32 * h;
+#pragma unroll 4
+                        for (int kp = 0; kp < kend / 2; ++kp) {
+                            const float4 q = sq[kp];
+                            const float2 d0 = __fadd2_rn(t0, make_float2(q.x, q.y));
+                            const float2 d1 = __fadd2_rn(t1, make_float2(q.z, q.w));
+                            const float2 d2 = __fadd2_rn(t2, sz[kp]);
+                            const float2 dd = __ffma2_rn(d2, d2, __ffma2_rn(d1, d1, __fmul2_rn(d0, d0)));
+                            cm[h] |= ((unsigned long long)(dd.x < a.thresh_f) | ((unsigned long long)(dd.y < a.thresh_f) << 1))
+                                     << (2 * kp);
+                        }
+#else
 #pragma unroll 8
                         for (int kk = 0; kk < kend; ++kk) {
                             const float4 q = srcf[64 * h + kk];
@@ -319,6 +355,7 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
                             const float dd = fmaf(d2, d2, fmaf(d1, d1, d0 * d0));
                             cm[h] |= (unsigned long long)(dd < a.thresh_f) << kk;
                         }
+#endif
                     }
                     // Pass 2 (fp64, exact reference test + kernel) on the candidates.
                     for (;;) {
