@@ -307,7 +307,10 @@ def run_reference(args, cfg_index):
 # our engine
 # ---------------------------------------------------------------------------
 
-BALANCED_XI = {2: 63.0}  # profiles/r2_xi_balance_c2.txt: 57.6 (xi 37) ... 24.3 ms (xi 63-71)
+# profiles/r2_xi_balance_c2.txt (c2: 57.6 ms at the pinned xi 37 ... 24.3 at 63-71) and
+# profiles/r2_xi_balance_c3_c4_c5.txt (c3: 117 -> 62.5 ms at 61; c4: 56.8 -> 41.6 at 46; c5's
+# pinned 68.5 is already the fastest measured)
+BALANCED_XI = {2: 63.0, 3: 61.0, 4: 46.0}
 
 
 def balanced_probe(S, cfg, x, f, nu, xt, engine, stream, dev, l2, steps=5, warmup=2):
@@ -362,7 +365,7 @@ def balanced_probe(S, cfg, x, f, nu, xt, engine, stream, dev, l2, steps=5, warmu
     step()
     uu = u.cpu().numpy()
     out = {"note": "supplementary, not the headline: same inputs / tolerance / window at the split parameter "
-                   "balanced for the B200 (PAPER.md:3790-3800); BASELINE.md pins xi = 37 for c2",
+                   "balanced for the B200 (PAPER.md:3790-3800); BASELINE.md pins xi per config",
            "xi": cb.xi, "M_ext": [int(v) for v in p.grid.M_ext], "P": int(p.window.P), "rc": float(p.rc),
            "ms_per_step": ms, "value": Nt / (ms * 1e-3), "unit": "targets/s", "steps": steps, "warmup": warmup,
            "stages_ms": {k: round(v, 4) for k, v in st.items()},
@@ -547,7 +550,7 @@ def run_ours(args, cfg):
     if rank == 0 and line is not None:
         torch.cuda.synchronize()
         line["parity_vs_fixture"] = fixture_parity(u_step, cfg.index, args.xi is not None)
-        if ws == 1 and cfg.index == 2 and args.xi is None and not args.no_balanced:
+        if ws == 1 and cfg.index in BALANCED_XI and args.xi is None and not args.no_balanced:
             line["balanced_xi"] = balanced_probe(S, cfg, x, f, nu, xt, engine, stream, dev, l2)
 
     # end-to-end through the public API with pinned host buffers: full_potential
