@@ -551,7 +551,10 @@ def run_ours(args, cfg):
         torch.cuda.synchronize()
         line["parity_vs_fixture"] = fixture_parity(u_step, cfg.index, args.xi is not None)
         if ws == 1 and cfg.index in BALANCED_XI and args.xi is None and not args.no_balanced:
-            line["balanced_xi"] = balanced_probe(S, cfg, x, f, nu, xt, engine, stream, dev, l2)
+            try:  # supplementary: never costs the headline line
+                line["balanced_xi"] = balanced_probe(S, cfg, x, f, nu, xt, engine, stream, dev, l2)
+            except Exception as ex:  # pragma: no cover - reported, not fatal
+                line["balanced_xi"] = {"error": f"{type(ex).__name__}: {ex}"[:300]}
 
     # end-to-end through the public API with pinned host buffers: full_potential
     # on 1 GPU, parallel.full_potential_sharded on N (max over ranks)
