@@ -199,3 +199,17 @@ def test_bench_fixed_nrc():
     assert [int(x[0]) for x in rows] == [20000, 40000, 80000]
     xi = [float(x[1]) for x in rows]
     assert xi[2] / xi[0] == pytest.approx(4 ** (1 / 3), rel=0.05)  # xi ~ N^(1/3) at fixed N_rc
+
+
+@pytest.mark.gpu
+def test_kinf_sweep_tracks_fourier_estimate():
+    """SPEC cmd_sweep example: k_inf sweep, stokeslet, xi = 10, d = 3: measured / estimated
+    Fourier truncation error within [0.2, 5] over the un-saturated range."""
+    r = run("sweep", "--kernel", "stokeslet", "--periodicity", 3, "--n", 300, "--xi", 10, "--axis", "kinf")
+    assert r.returncode == 0, r.stderr
+    rows = np.array([[float(v) for v in ln.split(",")] for ln in r.stdout.splitlines()[1:]])
+    live = rows[rows[:, 1] > 1e-11]
+    assert len(live) >= 4
+    ratio = live[:, 1] / live[:, 2]
+    assert np.all((ratio > 0.2) & (ratio < 5.0)), ratio
+    assert np.all(np.diff(rows[:, 1]) < 0)
