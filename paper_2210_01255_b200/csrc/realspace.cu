@@ -180,7 +180,7 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
     __shared__ uint8_t queue_all[RS_WARPS][CH][32];
 #endif
     __shared__ double exp_tab[32];
-    if (threadIdx.x < 32) exp_tab[threadIdx.x] = c_exp2_tab32[threadIdx.x];
+    if (threadIdx.x < 32) exp_tab[threadIdx.x] = exp_tab_entry<SHORT>(threadIdx.x);
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;

@@ -306,7 +306,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
     __shared__ double ipool_all[SYM_WARPS][32][3];
     __shared__ unsigned short queue_all[SYM_WARPS][SEWALD_SYM_QMAX];
 #endif
-    for (int t = threadIdx.x; t < 32 * SEWALD_EXP_REP; t += SYM_THREADS) exp_tab_rep[t] = c_exp2_tab32[t / SEWALD_EXP_REP];
+    for (int t = threadIdx.x; t < 32 * SEWALD_EXP_REP; t += SYM_THREADS) exp_tab_rep[t] = exp_tab_entry<SHORT>(t / SEWALD_EXP_REP);
     __syncthreads();
 
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
