@@ -765,7 +765,8 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                             const double n2 = __dadd_rn(__dadd_rn(__dmul_rn(r0, r0), __dmul_rn(r1, r1)), __dmul_rn(r2, r2));
                             bool acc = in && n2 < rc2;
                             // coincident distinct points (kernels.cpp:19-22): flagged per block
-                            coincident |= acc && n2 == 0.0;
+                            // (predicated stores: one instruction each on the rare path)
+                            if (acc && n2 == 0.0) coincident = true;
                             acc = acc && n2 != 0.0;
                             const double n2e = acc ? n2 : 0.25 * rc2;
                             double sj[NS];
@@ -795,7 +796,7 @@ realspace_sym_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ pa
                             *reinterpret_cast<double2*>(rec + RO) = make_double2(ub[0], ub[1]);
                             rec[RO + 2] = ub[2];
 #endif
-                            npairs32 += acc ? 2u : 0u;
+                            if (acc) npairs32 += 2u;
                         } else {
                             bool acc = (m >> s) & 1u;
                             double r0 = 0, r1 = 0, r2 = 0, n2 = 0;
