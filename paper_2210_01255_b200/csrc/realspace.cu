@@ -238,7 +238,10 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
     }
 
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-    unsigned long long npairs = 0;
+    // per-target pair count in 32 bits inside the pair loop (one instruction
+    // instead of a 64-bit add pair; a target's pairs <= 27 N fit for
+    // N < 1.5e8), widened to 64 bits for the warp sum below
+    unsigned npairs32 = 0;
     int row_id = -1;
 
     for (int cz = clo[2]; cz <= chi[2]; ++cz) {
@@ -396,7 +399,7 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
                         }
                         const Screened sc = screened<SHORT>(n2, a.xi, xi2, exp_tab);
                         pair_accumulate<KIND>(sc, xi2, n2, r0, r1, r2, q + 4, acc0, acc1, acc2);
-                        ++npairs;
+                        ++npairs32;
                     }
                 }
             }
@@ -420,6 +423,7 @@ realspace_kernel(CellGrid cg, RealspaceArgs a, const double* __restrict__ packed
         }
     }
     if (pair_count) {
+        unsigned long long npairs = npairs32;
 #pragma unroll
         for (int s = 16; s > 0; s >>= 1) npairs += __shfl_xor_sync(0xffffffffu, npairs, s);
         if (lane == 0 && npairs) atomicAdd(pair_count, npairs);
